@@ -1,0 +1,202 @@
+"""Oracle: metadata-mode trace driver (C3) -- CFS reschedule + paging calls.
+
+TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).
+
+Paper, Sec. 7: "For simplicity, we measure time slices as the
+number of inference iterations, as each iteration of a given batch size
+takes the same time. Aqua reschedules the batch every k iterations or when a
+request completes, paging out prompts that are not a part of the next batch
+and paging in prompts that were not on the GPU."
+SPEC reschedule S:279-287; iteration cost t = 20 ms + 40 us * tokens
+ drives a VIRTUAL clock used only for admission, so the
+schedule never depends on measured swap speed.
+
+Readings: R8 k = 8 by default; R11 an extra reschedule trigger
+when the current plan's next iteration no longer fits in NB (and when the
+plan has no work left); R13 page_out = every resident prompt not in the
+plan (literal); R14 a prompt preempted mid-prefill keeps its partial KV.
+
+Iteration semantics (R15): a prefill prompt scheduled for t tokens stores t
+KV tokens (ctx += t, f += t); when f reaches P it emits its first token
+(g = 1) and idles until the next plan.  A decode prompt stores the
+KV of its last token and emits one more (ctx += 1, g += 1); it finishes when
+g == O.  Before an iteration each scheduled prompt is grown to
+ceil((ctx + t) / bs) blocks with alloc_blocks, in plan order.
+
+The driver emits the exact call log the GPU run must reproduce:
+  ("swap_out", pids, [(loc, slots), ...])   ("swap_in", pids, [ids, ...])
+  ("alloc", pid, ids)    ("free", pid)    ("iter", i, [(pid, ctx0, t), ...])
+  ("plan", i, decode_ids, [(pid, tokens), ...])
+"""
+from __future__ import annotations
+
+import dataclasses
+from typing import Dict, List, Sequence, Tuple
+
+from . import cfs
+from .cfs import DECODE, PREFILL, Req
+from .kvpool import LOC_HOST, LOC_PEER, RESIDENT, SWAPPED, Layout, Pool
+
+
+@dataclasses.dataclass
+class SimConfig:
+    NB: int
+    bs: int = 16
+    b: int = 512
+    k: int = 8
+    policy: str = "cfs"            # "cfs" or "fcfs"
+    lender_slots: int = 0          # 0 -> no peer lender (DRAM only)
+    host_slots: int = 1 << 14
+    t_base: float = 0.020
+    t_token: float = 40e-6
+    max_iters: int = 10_000_000
+
+
+@dataclasses.dataclass
+class SimResult:
+    log: List[tuple]
+    ttft: Dict[int, float]
+    finish: Dict[int, float]
+    iters: int
+    blocks_out: int
+    blocks_in: int
+    vclock: float
+    timeline: List[Tuple[float, int]]      # (virtual time at iteration start, blocks owned)
+
+
+def run(trace: Sequence[Tuple[int, float, int, int]], cfg: SimConfig) -> SimResult:
+    """trace = [(id, arrival_s, prompt_tokens, output_tokens)] sorted by
+    (arrival, id)."""
+    lay = Layout(L=1, bs=cfg.bs, H=1, D=8, e=2, NB=cfg.NB)   # metadata only
+    pool = Pool(lay)
+    if cfg.lender_slots > 0:
+        pool.lend(LOC_PEER, cfg.lender_slots * lay.U)
+    if cfg.host_slots > 0:
+        pool.lend(LOC_HOST, cfg.host_slots * lay.U)
+
+    pending = sorted(trace, key=lambda x: (x[1], x[0]))
+    pi = 0
+    run_set: Dict[int, Req] = {}
+    log: List[tuple] = []
+    ttft: Dict[int, float] = {}
+    finish: Dict[int, float] = {}
+    admitted_fcfs: List[int] = []           # FCFS: admitted in arrival order
+    t = 0.0
+    i = 0
+    plan = None
+    last = 0
+    finished_prev = False
+    blocks_out = blocks_in = 0
+    timeline: List[Tuple[float, int]] = []
+
+    def resident(pid):
+        p = pool.prompts.get(pid)
+        return p is not None and p.state == RESIDENT
+
+    def this_iter_tokens(plan_):
+        D, PF = plan_
+        out = []
+        for pid in D:
+            r = run_set.get(pid)
+            if r is not None and r.phase == DECODE:
+                out.append((pid, 1))
+        for pid, a in PF:
+            r = run_set.get(pid)
+            if r is not None and r.phase == PREFILL:
+                out.append((pid, min(a, r.P - r.f)))
+        return out
+
+    def fits(work):
+        tok = dict(work)
+        tot = 0
+        for pid, p in pool.prompts.items():
+            if p.state == RESIDENT:
+                tot += cfs.need(run_set[pid], tok.get(pid, 0), lay.bs)
+        for pid, tt in work:
+            if not resident(pid):
+                tot += cfs.need(run_set[pid], tt, lay.bs)
+        return tot <= lay.NB
+
+    while (pi < len(pending) or run_set) and i < cfg.max_iters:
+        while pi < len(pending) and pending[pi][1] <= t:
+            rid, a, P, O = pending[pi]
+            run_set[rid] = Req(id=rid, arrival=a, P=P, O=O)
+            pi += 1
+        if not run_set:
+            t = pending[pi][1]          # idle: jump to the next arrival
+            plan = None
+            continue
+
+        if cfg.policy == "fcfs":
+            # admission: full projection must fit, head-of-line
+            proj = sum(cfs.need(run_set[x], run_set[x].P + run_set[x].O - run_set[x].ctx, lay.bs)
+                       for x in admitted_fcfs)
+            for r in sorted(run_set.values(), key=lambda r: (r.arrival, r.id)):
+                if r.id in admitted_fcfs:
+                    continue
+                n = -(-(r.P + r.O) // lay.bs)
+                if proj + n > lay.NB:
+                    break
+                proj += n
+                admitted_fcfs.append(r.id)
+            plan = cfs.fcfs_plan([run_set[x] for x in admitted_fcfs], cfg.b)
+            work = this_iter_tokens(plan)
+        else:
+            work = this_iter_tokens(plan) if plan is not None else []
+            if (plan is None or i - last >= cfg.k or finished_prev or not work
+                    or not fits(work)):
+                plan = cfs.plan(list(run_set.values()), cfg.b, lay.NB, lay.bs)
+                last = i
+                log.append(("plan", i, tuple(plan[0]), tuple(plan[1])))
+                in_plan = set(plan[0]) | {pid for pid, _ in plan[1]}
+                key = lambda pid: (run_set[pid].arrival, pid)
+                page_out = sorted((pid for pid in run_set if resident(pid) and pid not in in_plan), key=key)
+                page_in = sorted((pid for pid in in_plan
+                                  if pid in pool.prompts and pool.prompts[pid].state == SWAPPED), key=key)
+                if page_out:
+                    res = pool.swap_out(page_out)
+                    blocks_out += sum(len(s) for _, _, s in res)
+                    log.append(("swap_out", tuple(page_out), tuple((loc, tuple(s)) for _, loc, s in res)))
+                if page_in:
+                    res = pool.swap_in(page_in)
+                    blocks_in += sum(len(x) for x in res)
+                    log.append(("swap_in", tuple(page_in), tuple(tuple(x) for x in res)))
+                work = this_iter_tokens(plan)
+                if not work:
+                    raise RuntimeError("empty plan with runnable prompts (pool too small)")
+
+        # grow block tables in plan order, then run the iteration
+        for pid, tt in work:
+            r = run_set[pid]
+            have = len(pool.prompts[pid].blocks) if pid in pool.prompts else 0
+            n = cfs.need(r, tt, lay.bs) - have
+            if n > 0:
+                ids = pool.alloc_blocks(pid, n)
+                log.append(("alloc", pid, tuple(ids)))
+        log.append(("iter", i, tuple((pid, run_set[pid].ctx, tt) for pid, tt in work)))
+        timeline.append((t, lay.NB - len(pool.free)))
+        total = sum(tt for _, tt in work)
+        t += cfg.t_base + cfg.t_token * total
+        finished_prev = False
+        for pid, tt in work:
+            r = run_set[pid]
+            if r.phase == PREFILL:
+                r.f += tt
+                r.ctx += tt
+                if r.f == r.P:
+                    r.phase, r.g = DECODE, 1
+                    ttft[pid] = t - r.arrival
+            else:
+                r.ctx += 1
+                r.g += 1
+            if r.phase == DECODE and r.g >= r.O:
+                finish[pid] = t - r.arrival
+                pool.free_prompt(pid)
+                log.append(("free", pid))
+                del run_set[pid]
+                if pid in admitted_fcfs:
+                    admitted_fcfs.remove(pid)
+                finished_prev = True
+        i += 1
+    pool.check_invariants()
+    return SimResult(log, ttft, finish, i, blocks_out, blocks_in, t, timeline)
