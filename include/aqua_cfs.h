@@ -1,0 +1,94 @@
+/*
+ * aqua_cfs.h -- native time-slice scheduler that drives libaqua's paging
+ * (hot-path row A0: CFS reschedule -> ordered page_out / page_in lists).
+ *
+ * Paper, Sec. 7: batch partitioning into p prefill and d
+ * decode tokens, d set to its upper bound (the number of prompts that fit
+ * in memory), prefill prompts with the least prefill done first, decode
+ * prompts with the least tokens generated, leftover d slots to the prefill
+ * prompts, stop when memory is exhausted; reschedule every k iterations or
+ * when a request completes, paging out the prompts not in the next batch and
+ * paging in the prompts not on the GPU.  Readings R8-R16:
+ * ties (arrival, id); memory test ceil((ctx + t) / bs) blocks per prompt
+ * summed <= num_blocks; prefill filled before decode; a non-fitting prompt
+ * stops its walk; extra reschedule when the plan's next iteration no longer
+ * fits or has no work; literal eviction of every resident prompt not in the
+ * plan; a preempted prefill keeps its partial KV.
+ * FCFS is the no-preemption baseline.
+ *
+ * Iteration protocol (the caller owns the KV pool, via libaqua):
+ *   aqua_cfs_add() every request whose arrival <= aqua_cfs_vclock();
+ *   aqua_cfs_next()  -> page_out, page_in (call aqua_swap_out / aqua_swap_in
+ *                       in that order), and the work list: per prompt, the
+ *                       KV length before the iteration (ctx0), the tokens
+ *                       it runs (t) and the blocks to append (grow) with
+ *                       aqua_alloc_blocks, in list order;
+ *   run the iteration (write the KV of tokens [ctx0, ctx0 + t));
+ *   aqua_cfs_commit() -> finished pids (free them with aqua_free, in order)
+ *                       and the virtual clock advanced by
+ *                       t_base + t_token * tokens.
+ * If aqua_cfs_next() returns no work the runnable set is empty: advance the
+ * clock to the next arrival with aqua_cfs_advance_to().
+ */
+#ifndef AQUA_CFS_H_
+#define AQUA_CFS_H_
+
+#include "aqua.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct aqua_cfs aqua_cfs;
+
+enum { AQUA_POLICY_CFS = 0, AQUA_POLICY_FCFS = 1 };
+enum { AQUA_PHASE_PREFILL = 0, AQUA_PHASE_DECODE = 1 };
+
+typedef struct {
+  int32_t policy;        /* AQUA_POLICY_* */
+  int32_t batch_tokens;  /* b (chunk size, 512 in the paper's setup P:485) */
+  int32_t k;             /* reschedule interval in iterations (R8: 8) */
+  int32_t block_tokens;  /* bs */
+  int32_t num_blocks;    /* NB of the borrower pool */
+  int32_t pad_;
+  double t_base;         /* virtual iteration cost t_base + t_token * tokens */
+  double t_token;
+} aqua_cfs_config;
+
+typedef struct {
+  uint64_t pid;
+  int32_t ctx0;          /* KV tokens stored before this iteration */
+  int32_t tokens;        /* tokens this iteration (prefill chunk or 1 decode) */
+  int32_t grow;          /* blocks to append before the iteration */
+  int32_t phase;         /* AQUA_PHASE_* at plan time */
+} aqua_cfs_work;
+
+AQUA_API aqua_status aqua_cfs_create(const aqua_cfs_config* cfg, aqua_cfs** out);
+AQUA_API aqua_status aqua_cfs_destroy(aqua_cfs* s);
+/* Make a request runnable (arrival in virtual seconds). */
+AQUA_API aqua_status aqua_cfs_add(aqua_cfs* s, uint64_t pid, double arrival, int32_t prompt_tokens,
+                                  int32_t output_tokens);
+/* Overwrite a runnable request's service counters (tests / restarts). */
+AQUA_API aqua_status aqua_cfs_set_state(aqua_cfs* s, uint64_t pid, int32_t phase, int32_t prefill_done,
+                                        int32_t generated, int32_t ctx);
+/* Plan one iteration.  Arrays have capacity `cap`; *rescheduled = 1 when a
+ * new plan was made (then page_out / page_in may be non-empty). */
+AQUA_API aqua_status aqua_cfs_next(aqua_cfs* s, int32_t* rescheduled, uint64_t* page_out, int32_t* n_out,
+                                   uint64_t* page_in, int32_t* n_in, aqua_cfs_work* work, int32_t* n_work,
+                                   int32_t cap);
+/* Apply the planned iteration; finished pids (capacity cap) in work order. */
+AQUA_API aqua_status aqua_cfs_commit(aqua_cfs* s, uint64_t* finished, int32_t* n_fin, int32_t cap,
+                                     double* vclock);
+/* The partition of the current runnable set (no side effects): decode ids in
+ * selection order, then prefill (id, tokens) in selection order. */
+AQUA_API aqua_status aqua_cfs_partition(aqua_cfs* s, uint64_t* decode, int32_t* n_decode, uint64_t* prefill,
+                                        int32_t* prefill_tokens, int32_t* n_prefill, int32_t cap);
+AQUA_API aqua_status aqua_cfs_vclock(aqua_cfs* s, double* vclock);
+AQUA_API aqua_status aqua_cfs_advance_to(aqua_cfs* s, double vclock);
+/* Runnable prompts, prompts with KV resident in the pool, iterations run. */
+AQUA_API aqua_status aqua_cfs_stats(aqua_cfs* s, int32_t* runnable, int32_t* resident, int64_t* iterations);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* AQUA_CFS_H_ */

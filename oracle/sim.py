@@ -141,6 +141,8 @@ def run(trace: Sequence[Tuple[int, float, int, int]], cfg: SimConfig) -> SimResu
                 admitted_fcfs.append(r.id)
             plan = cfs.fcfs_plan([run_set[x] for x in admitted_fcfs], cfg.b)
             work = this_iter_tokens(plan)
+            if not work:
+                raise RuntimeError("FCFS: the head-of-line prompt can never fit the pool")
         else:
             work = this_iter_tokens(plan) if plan is not None else []
             if (plan is None or i - last >= cfg.k or finished_prev or not work

@@ -1,0 +1,265 @@
+"""Thin ctypes binding of libaqua (include/aqua.h).  Argument marshalling
+only: every step of the paging path runs in the C++ library and its sm_100a
+kernels.  There is no CPU fallback -- if libaqua.so is missing this module
+raises at import time; on a box without a GPU only AQUA_DRYRUN contexts
+work.
+
+Functions keep the C names without the ``aqua_`` prefix (``Ctx.swap_out`` ->
+``aqua_swap_out``).  Streams are passed as integers (``torch.cuda.Stream
+.cuda_stream``; 0 = the legacy default stream), device memory as integer
+addresses (``tensor.data_ptr()``).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import List, Sequence, Tuple
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libaqua.so")
+
+OK, E_INVAL, E_NOBLOCKS, E_NOSPACE, E_STATE, E_CUDA, E_PEER = 0, -1, -2, -3, -4, -5, -6
+HOST, DRYRUN, MAPPED = -1, -2, -3
+RESIDENT, SWAPPED = 1, 2
+LOC_LOCAL, LOC_PEER, LOC_HOST = 0, 1, 2
+KERNEL_AUTO, KERNEL_TMA, KERNEL_LDST, BASE_PER_CHUNK, BASE_GATHER_TEMP, BASE_BATCH = 0, 1, 2, 3, 4, 5
+OPT_KERNEL, OPT_MAX_CTAS, OPT_TMA_PIECE = 1, 2, 3
+
+# Every symbol include/aqua.h declares (checked by tests/test_abi.py).
+SYMBOLS = [
+    "aqua_create", "aqua_destroy", "aqua_lend", "aqua_alloc_blocks", "aqua_adopt_blocks",
+    "aqua_swap_out", "aqua_swap_in", "aqua_free", "aqua_wait", "aqua_sync", "aqua_ticket_done",
+    "aqua_query", "aqua_counts", "aqua_arena_base", "aqua_set_option", "aqua_get_option",
+    "aqua_last_descriptors", "aqua_launch_count", "aqua_ipc_export", "aqua_ipc_import",
+    "aqua_ipc_close", "aqua_can_access_peer", "aqua_kv_fill_pattern", "aqua_kv_verify_pattern",
+    "aqua_strerror", "aqua_last_error", "aqua_version",
+]
+
+
+class AquaError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"aqua status {code}: {msg}")
+        self.code = code
+
+
+class KVLayout(C.Structure):
+    _fields_ = [("num_layers", C.c_int32), ("block_tokens", C.c_int32), ("num_kv_heads", C.c_int32),
+                ("head_dim", C.c_int32), ("elem_bytes", C.c_int32), ("num_blocks", C.c_int32),
+                ("layer_base", C.POINTER(C.c_void_p)), ("kv_plane_stride", C.c_int64),
+                ("block_stride", C.c_int64)]
+
+
+def _load() -> C.CDLL:
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_2407_21255_b200.build` "
+                          "(there is no CPU fallback)")
+    lib = C.CDLL(LIB_PATH)
+    P, I32, I64, U64, VP = C.POINTER, C.c_int32, C.c_int64, C.c_uint64, C.c_void_p
+    sig = {
+        "aqua_create": (C.c_int, [C.c_int, P(KVLayout), P(VP)]),
+        "aqua_destroy": (C.c_int, [VP]),
+        "aqua_lend": (C.c_int, [VP, C.c_int, VP, U64, P(I32)]),
+        "aqua_alloc_blocks": (C.c_int, [VP, U64, I32, VP, P(I32)]),
+        "aqua_adopt_blocks": (C.c_int, [VP, U64, I32, P(I32), VP]),
+        "aqua_swap_out": (C.c_int, [VP, I32, P(U64), VP, P(U64)]),
+        "aqua_swap_in": (C.c_int, [VP, I32, P(U64), VP, P(I32), I64, P(I32), P(U64)]),
+        "aqua_free": (C.c_int, [VP, U64, VP]),
+        "aqua_wait": (C.c_int, [VP, U64, VP]),
+        "aqua_sync": (C.c_int, [VP, U64]),
+        "aqua_ticket_done": (C.c_int, [VP, U64, P(I32)]),
+        "aqua_query": (C.c_int, [VP, U64, P(I32), P(I32), P(I32), P(I32), I32]),
+        "aqua_counts": (C.c_int, [VP, P(I32), P(I32), P(I32)]),
+        "aqua_arena_base": (C.c_int, [VP, I32, P(VP), P(I32)]),
+        "aqua_set_option": (C.c_int, [VP, I32, I64]),
+        "aqua_get_option": (C.c_int, [VP, I32, P(I64)]),
+        "aqua_last_descriptors": (C.c_int, [VP, P(I32), P(I32), P(I32), I64, P(I64)]),
+        "aqua_launch_count": (C.c_int, [VP, P(U64)]),
+        "aqua_ipc_export": (C.c_int, [VP, P(C.c_uint8)]),
+        "aqua_ipc_import": (C.c_int, [C.c_int, P(C.c_uint8), P(VP)]),
+        "aqua_ipc_close": (C.c_int, [C.c_int, VP]),
+        "aqua_can_access_peer": (C.c_int, [C.c_int, C.c_int, P(I32)]),
+        "aqua_kv_fill_pattern": (C.c_int, [VP, U64, I32, I32, U64, VP]),
+        "aqua_kv_verify_pattern": (C.c_int, [VP, U64, I32, U64, VP, VP]),
+        "aqua_strerror": (C.c_char_p, [C.c_int]),
+        "aqua_last_error": (C.c_char_p, [VP]),
+        "aqua_version": (C.c_char_p, []),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(lib, name)
+        f.restype, f.argtypes = res, args
+    return lib
+
+
+lib = _load()
+
+
+def _i32p(a: np.ndarray):
+    return a.ctypes.data_as(C.POINTER(C.c_int32))
+
+
+def _u64p(a: np.ndarray):
+    return a.ctypes.data_as(C.POINTER(C.c_uint64))
+
+
+def _check(st: int, ctx=None):
+    if st != OK:
+        msg = lib.aqua_last_error(ctx).decode() if ctx is not None else lib.aqua_last_error(None).decode()
+        raise AquaError(st, msg or lib.aqua_strerror(st).decode())
+
+
+class Ctx:
+    """One borrower context (aqua_ctx*).  ``layer_ptrs`` are the L device
+    addresses of the per-layer KV tensors (caller-owned)."""
+
+    def __init__(self, device: int, L: int, bs: int, H: int, D: int, e: int, NB: int,
+                 layer_ptrs: Sequence[int], kv_plane_stride: int = 0, block_stride: int = 0):
+        self._ptrs = (C.c_void_p * L)(*[int(p) for p in layer_ptrs])
+        lay = KVLayout(L, bs, H, D, e, NB, C.cast(self._ptrs, C.POINTER(C.c_void_p)),
+                       kv_plane_stride, block_stride)
+        h = C.c_void_p()
+        _check(lib.aqua_create(device, C.byref(lay), C.byref(h)))
+        self.h = h
+        self.L, self.bs, self.H, self.D, self.e, self.NB = L, bs, H, D, e, NB
+        self.S = bs * H * D * e
+        self.U = 2 * L * self.S
+
+    def close(self):
+        if self.h:
+            lib.aqua_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _c(self, st):
+        _check(st, self.h)
+
+    def lend(self, lender_device: int, base: int = 0, nbytes: int = 0) -> int:
+        n = C.c_int32()
+        self._c(lib.aqua_lend(self.h, lender_device, C.c_void_p(base or None), nbytes, C.byref(n)))
+        return n.value
+
+    def alloc_blocks(self, pid: int, n: int, stream: int = 0) -> List[int]:
+        out = np.empty(max(n, 1), np.int32)
+        self._c(lib.aqua_alloc_blocks(self.h, pid, n, C.c_void_p(stream or None), _i32p(out)))
+        return out[:n].tolist()
+
+    def adopt_blocks(self, pid: int, ids: Sequence[int], stream: int = 0) -> None:
+        a = np.ascontiguousarray(ids, dtype=np.int32)
+        self._c(lib.aqua_adopt_blocks(self.h, pid, len(a), _i32p(a), C.c_void_p(stream or None)))
+
+    def swap_out(self, pids: Sequence[int], stream: int = 0) -> int:
+        a = np.ascontiguousarray(pids, dtype=np.uint64)
+        t = C.c_uint64()
+        self._c(lib.aqua_swap_out(self.h, len(a), _u64p(a), C.c_void_p(stream or None), C.byref(t)))
+        return t.value
+
+    def swap_in(self, pids: Sequence[int], stream: int = 0, cap: int = -1) -> Tuple[List[List[int]], int]:
+        a = np.ascontiguousarray(pids, dtype=np.uint64)
+        if cap < 0:
+            cap = sum(self.query(int(p))[2] for p in a)
+        ids = np.empty(max(cap, 1), np.int32)
+        counts = np.empty(max(len(a), 1), np.int32)
+        t = C.c_uint64()
+        self._c(lib.aqua_swap_in(self.h, len(a), _u64p(a), C.c_void_p(stream or None), _i32p(ids), cap,
+                                 _i32p(counts), C.byref(t)))
+        out, k = [], 0
+        for i in range(len(a)):
+            out.append(ids[k:k + counts[i]].tolist())
+            k += counts[i]
+        return out, t.value
+
+    def free(self, pid: int, stream: int = 0) -> None:
+        self._c(lib.aqua_free(self.h, pid, C.c_void_p(stream or None)))
+
+    def wait(self, ticket: int, stream: int = 0) -> None:
+        self._c(lib.aqua_wait(self.h, ticket, C.c_void_p(stream or None)))
+
+    def sync(self, ticket: int) -> None:
+        self._c(lib.aqua_sync(self.h, ticket))
+
+    def ticket_done(self, ticket: int) -> bool:
+        d = C.c_int32()
+        self._c(lib.aqua_ticket_done(self.h, ticket, C.byref(d)))
+        return bool(d.value)
+
+    def query(self, pid: int, with_ids: bool = False):
+        st, loc, n = C.c_int32(), C.c_int32(), C.c_int32()
+        self._c(lib.aqua_query(self.h, pid, C.byref(st), C.byref(loc), C.byref(n), None, 0))
+        if not with_ids:
+            return st.value, loc.value, n.value
+        ids = np.empty(max(n.value, 1), np.int32)
+        self._c(lib.aqua_query(self.h, pid, None, None, None, _i32p(ids), n.value))
+        return st.value, loc.value, n.value, ids[:n.value].tolist()
+
+    def counts(self) -> Tuple[int, int, int]:
+        a, b, c = C.c_int32(), C.c_int32(), C.c_int32()
+        self._c(lib.aqua_counts(self.h, C.byref(a), C.byref(b), C.byref(c)))
+        return a.value, b.value, c.value
+
+    def arena_base(self, loc: int) -> Tuple[int, int]:
+        p, n = C.c_void_p(), C.c_int32()
+        self._c(lib.aqua_arena_base(self.h, loc, C.byref(p), C.byref(n)))
+        return p.value or 0, n.value
+
+    def set_option(self, opt: int, value: int) -> None:
+        self._c(lib.aqua_set_option(self.h, opt, value))
+
+    def get_option(self, opt: int) -> int:
+        v = C.c_int64()
+        self._c(lib.aqua_get_option(self.h, opt, C.byref(v)))
+        return v.value
+
+    def last_descriptors(self):
+        n = C.c_int64()
+        self._c(lib.aqua_last_descriptors(self.h, None, None, None, 0, C.byref(n)))
+        b = np.empty(max(n.value, 1), np.int32)
+        s = np.empty_like(b)
+        l = np.empty_like(b)
+        self._c(lib.aqua_last_descriptors(self.h, _i32p(b), _i32p(s), _i32p(l), n.value, C.byref(n)))
+        k = n.value
+        return b[:k].tolist(), s[:k].tolist(), l[:k].tolist()
+
+    def launch_count(self) -> int:
+        v = C.c_uint64()
+        self._c(lib.aqua_launch_count(self.h, C.byref(v)))
+        return v.value
+
+    def kv_fill_pattern(self, pid: int, t0: int, t1: int, seed: int, stream: int = 0) -> None:
+        self._c(lib.aqua_kv_fill_pattern(self.h, pid, t0, t1, seed, C.c_void_p(stream or None)))
+
+    def kv_verify_pattern(self, pid: int, ntok: int, seed: int, d_counter: int, stream: int = 0) -> None:
+        self._c(lib.aqua_kv_verify_pattern(self.h, pid, ntok, seed, C.c_void_p(stream or None),
+                                           C.c_void_p(d_counter)))
+
+
+def ipc_export(dev_ptr: int) -> bytes:
+    h = (C.c_uint8 * 64)()
+    _check(lib.aqua_ipc_export(C.c_void_p(dev_ptr), h))
+    return bytes(h)
+
+
+def ipc_import(device: int, handle: bytes) -> int:
+    h = (C.c_uint8 * 64)(*handle)
+    p = C.c_void_p()
+    _check(lib.aqua_ipc_import(device, h, C.byref(p)))
+    return p.value
+
+
+def ipc_close(device: int, ptr: int) -> None:
+    _check(lib.aqua_ipc_close(device, C.c_void_p(ptr)))
+
+
+def can_access_peer(device: int, peer: int) -> bool:
+    v = C.c_int32()
+    _check(lib.aqua_can_access_peer(device, peer, C.byref(v)))
+    return bool(v.value)
+
+
+def version() -> str:
+    return lib.aqua_version().decode()

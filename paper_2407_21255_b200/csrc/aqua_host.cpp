@@ -1,0 +1,1007 @@
+// libaqua host library: C ABI (include/aqua.h), bookkeeping of the paged
+// KV pool, block tables, lender / host swap arenas and tickets, descriptor
+// staging, and dispatch of the sm_100a copy kernels (aqua_kernels.cu).
+//
+// Paper anchors (arXiv 2407.21255): Sec. 6 "Allocating AquaTensors"
+// P:737-756 (producer first, DRAM fallback), Sec. 5 P:529-534 (one producer
+// per consumer), Sec. 7 P:836-853 (page out / page in, gather / scatter),
+// P:855-857 (location query), Sec. 8 P:864-866 (library surface, CUDA
+// gather kernel in vLLM v0.5.3, safe transfers).  Readings R1..R17:
+// DESIGN.md.  This file never does data movement on the CPU: with no usable
+// GPU every data call fails (only AQUA_DRYRUN contexts run without one).
+#include "aqua.h"
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <deque>
+#include <map>
+#include <set>
+#include <string>
+#include <unordered_map>
+#include <unordered_set>
+#include <vector>
+
+#include "aqua_internal.h"
+
+using aqua::Desc;
+using aqua::kArenaBit;
+
+namespace {
+
+struct Arena {
+  bool present = false;
+  int device = 0;              // lender ordinal, AQUA_HOST or AQUA_MAPPED
+  uint8_t* base = nullptr;     // device-visible base
+  void* host_ptr = nullptr;    // host arena: pointer for cudaFreeHost
+  uint64_t bytes = 0;
+  int32_t nslots = 0;
+  bool owned = false;
+  std::set<int32_t> free;      // lowest-first (R4)
+  std::vector<uint64_t> tick;  // last library ticket that touched each slot
+};
+
+struct Prompt {
+  int32_t state = AQUA_ST_RESIDENT;
+  int32_t loc = AQUA_LOC_LOCAL;
+  std::vector<int32_t> ids;    // block table (RESIDENT) or slots (SWAPPED)
+};
+
+struct TicketRec {
+  cudaEvent_t ev;
+  cudaStream_t st;
+};
+
+struct StageRegion {
+  size_t off, len;
+  uint64_t ticket;
+};
+
+}  // namespace
+
+struct aqua_ctx {
+  int device = 0;
+  bool dry = false;
+  int32_t L = 0, bs = 0, H = 0, D = 0, e = 0, NB = 0;
+  int64_t S = 0, U = 0, P_kv = 0, P_b = 0;
+  std::vector<uint64_t> layer_base;
+  std::set<int32_t> free_blocks;
+  std::vector<uint64_t> btick;  // last library ticket that touched each block
+  std::unordered_map<uint64_t, Prompt> prompts;
+  Arena gpu, host;              // AQUA_LOC_PEER, AQUA_LOC_HOST
+  int kernel = AQUA_KERNEL_AUTO;
+  int max_ctas = 0;
+  int tma_piece = 0;
+  int num_sms = 148;
+  uint64_t* d_layer_base = nullptr;
+  // pinned -> device descriptor staging ring
+  uint8_t* h_stage = nullptr;
+  uint8_t* d_stage = nullptr;
+  size_t stage_cap = 0, stage_head = 0;
+  std::deque<StageRegion> stage_live;
+  // tickets
+  uint64_t next_ticket = 1;
+  std::map<uint64_t, TicketRec> live;
+  std::vector<cudaEvent_t> ev_pool;
+  // gather-temp baseline buffer
+  uint8_t* d_temp = nullptr;
+  size_t temp_cap = 0;
+  bool poisoned = false;
+  std::string err;
+  std::vector<int32_t> last_b, last_s, last_l;
+  uint64_t launches = 0;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+// Makes `d` the current device for the scope of a call (no-op for dry runs).
+struct DevGuard {
+  int prev = -1, want;
+  bool skip;
+  explicit DevGuard(int d, bool skip_ = false) : want(d), skip(skip_) {
+    if (skip) return;
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != want) cudaSetDevice(want);
+  }
+  ~DevGuard() {
+    if (!skip && prev >= 0 && prev != want) cudaSetDevice(prev);
+  }
+};
+
+aqua_status fail(aqua_ctx* c, aqua_status s, const std::string& m) {
+  if (c) c->err = m;
+  g_err = m;
+  return s;
+}
+
+aqua_status cuda_fail(aqua_ctx* c, cudaError_t e, const char* what) {
+  std::string m = std::string(what) + ": " + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ")";
+  if (c) c->poisoned = true;
+  return fail(c, AQUA_E_CUDA, m);
+}
+
+#define CK(ctx, expr)                                     \
+  do {                                                    \
+    cudaError_t _e = (expr);                              \
+    if (_e != cudaSuccess) return cuda_fail(ctx, _e, #expr); \
+  } while (0)
+
+// ------------------------------------------------------------ tickets
+void retire(aqua_ctx* c) {
+  int scanned = 0;
+  for (auto it = c->live.begin(); it != c->live.end() && scanned < 64; ++scanned) {
+    cudaError_t q = cudaEventQuery(it->second.ev);
+    if (q == cudaSuccess) {
+      c->ev_pool.push_back(it->second.ev);
+      it = c->live.erase(it);
+    } else {
+      if (q != cudaErrorNotReady) cudaGetLastError();
+      ++it;
+    }
+  }
+  while (!c->stage_live.empty() && !c->live.count(c->stage_live.front().ticket))
+    c->stage_live.pop_front();
+}
+
+aqua_status record(aqua_ctx* c, cudaStream_t st, uint64_t* t) {
+  const uint64_t id = c->next_ticket++;
+  if (c->dry) {
+    *t = id;
+    return AQUA_OK;
+  }
+  cudaEvent_t ev;
+  if (!c->ev_pool.empty()) {
+    ev = c->ev_pool.back();
+    c->ev_pool.pop_back();
+  } else {
+    CK(c, cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  }
+  CK(c, cudaEventRecord(ev, st));
+  c->live[id] = TicketRec{ev, st};
+  *t = id;
+  return AQUA_OK;
+}
+
+// Make `st` wait for every live ticket in `ts` recorded on another stream.
+aqua_status wait_all(aqua_ctx* c, const std::vector<uint64_t>& ts, cudaStream_t st) {
+  if (c->dry) return AQUA_OK;
+  std::vector<uint64_t> u(ts);
+  std::sort(u.begin(), u.end());
+  u.erase(std::unique(u.begin(), u.end()), u.end());
+  for (uint64_t t : u) {
+    if (t == 0) continue;
+    auto it = c->live.find(t);
+    if (it == c->live.end() || it->second.st == st) continue;
+    CK(c, cudaStreamWaitEvent(st, it->second.ev, 0));
+  }
+  return AQUA_OK;
+}
+
+// ------------------------------------------------------------ staging ring
+// Copies `len` bytes from host `src` to a device region through pinned
+// memory, on stream `st`.  The region stays reserved until the ticket that
+// the caller stores in stage_live.back() completes.
+aqua_status stage_upload(aqua_ctx* c, const void* src, size_t nbytes, cudaStream_t st, void** dptr) {
+  const size_t len = (nbytes + 255) & ~size_t(255);
+  if (len > c->stage_cap) {
+    // grow: drain every user of the old ring, then reallocate
+    for (auto& r : c->stage_live) {
+      auto it = c->live.find(r.ticket);
+      if (it != c->live.end()) CK(c, cudaEventSynchronize(it->second.ev));
+    }
+    c->stage_live.clear();
+    if (c->h_stage) cudaFreeHost(c->h_stage);
+    if (c->d_stage) cudaFree(c->d_stage);
+    c->h_stage = nullptr;
+    c->d_stage = nullptr;
+    size_t cap = std::max<size_t>(len * 2, size_t(1) << 20);
+    CK(c, cudaHostAlloc(reinterpret_cast<void**>(&c->h_stage), cap, cudaHostAllocDefault));
+    CK(c, cudaMalloc(reinterpret_cast<void**>(&c->d_stage), cap));
+    c->stage_cap = cap;
+    c->stage_head = 0;
+  }
+  if (c->stage_head + len > c->stage_cap) c->stage_head = 0;
+  const size_t off = c->stage_head;
+  // wait (host) for any live region overlapping [off, off+len)
+  for (auto it = c->stage_live.begin(); it != c->stage_live.end();) {
+    const bool overlap = it->off < off + len && off < it->off + it->len;
+    if (overlap) {
+      auto lt = c->live.find(it->ticket);
+      if (lt != c->live.end()) CK(c, cudaEventSynchronize(lt->second.ev));
+      it = c->stage_live.erase(it);
+    } else {
+      ++it;
+    }
+  }
+  std::memcpy(c->h_stage + off, src, nbytes);
+  CK(c, cudaMemcpyAsync(c->d_stage + off, c->h_stage + off, nbytes, cudaMemcpyHostToDevice, st));
+  c->stage_head = off + len;
+  c->stage_live.push_back(StageRegion{off, len, 0});
+  *dptr = c->d_stage + off;
+  return AQUA_OK;
+}
+
+void stage_seal(aqua_ctx* c, size_t nregions, uint64_t ticket) {
+  for (size_t i = 0; i < nregions && i < c->stage_live.size(); ++i)
+    c->stage_live[c->stage_live.size() - 1 - i].ticket = ticket;
+}
+
+// ------------------------------------------------------------ copy engines
+aqua_status run_copy(aqua_ctx* c, const std::vector<Desc>& ds, aqua::Dir dir, cudaStream_t st,
+                     int* regions) {
+  *regions = 0;
+  if (ds.empty()) return AQUA_OK;
+  aqua::SwapParams p{};
+  p.layer_base = c->d_layer_base;
+  p.arena_base[0] = reinterpret_cast<uint64_t>(c->gpu.base);
+  p.arena_base[1] = reinterpret_cast<uint64_t>(c->host.base);
+  p.ndesc = static_cast<int64_t>(ds.size());
+  p.L = c->L;
+  p.S = c->S;
+  p.U = c->U;
+  p.P_kv = c->P_kv;
+  p.P_b = c->P_b;
+  const int engine = c->kernel == AQUA_KERNEL_AUTO ? AQUA_KERNEL_TMA : c->kernel;
+
+  auto chunk_ptrs = [&](const Desc& d, int cc, uint8_t** pool, uint8_t** img) {
+    const int l = cc >> 1, kv = cc & 1;
+    *pool = reinterpret_cast<uint8_t*>(c->layer_base[l]) + kv * c->P_kv + int64_t(d.block) * c->P_b;
+    uint8_t* ab = (d.slot_arena & kArenaBit) ? c->host.base : c->gpu.base;
+    *img = ab + int64_t(d.slot_arena & ~kArenaBit) * c->U + int64_t(cc) * c->S;
+  };
+
+  if (engine == AQUA_KERNEL_TMA || engine == AQUA_KERNEL_LDST) {
+    void* dd;
+    aqua_status s = stage_upload(c, ds.data(), ds.size() * sizeof(Desc), st, &dd);
+    if (s) return s;
+    *regions = 1;
+    p.desc = static_cast<const Desc*>(dd);
+    int ctas = 0;
+    cudaError_t e;
+    if (engine == AQUA_KERNEL_TMA) {
+      int piece = c->tma_piece > 0 ? c->tma_piece : 16384;
+      if (piece > c->S) piece = static_cast<int>(c->S);
+      p.piece = piece;
+      p.npieces = static_cast<int32_t>((c->S + piece - 1) / piece);
+      p.nitems = p.ndesc * 2 * p.L * p.npieces;
+      e = aqua::launch_swap_tma(p, dir, c->num_sms, c->max_ctas, st, &ctas);
+    } else {
+      p.piece = 4096;
+      p.npieces = static_cast<int32_t>((c->S + 4095) / 4096);
+      p.nitems = p.ndesc * 2 * p.L * p.npieces;
+      e = aqua::launch_swap_ldst(p, dir, c->num_sms, c->max_ctas, st, &ctas);
+    }
+    if (e != cudaSuccess) return cuda_fail(c, e, "swap kernel launch");
+    c->launches++;
+    return AQUA_OK;
+  }
+  if (engine == AQUA_BASE_PER_CHUNK) {
+    for (const Desc& d : ds)
+      for (int cc = 0; cc < 2 * c->L; ++cc) {
+        uint8_t *pool, *img;
+        chunk_ptrs(d, cc, &pool, &img);
+        if (dir == aqua::kOut)
+          CK(c, cudaMemcpyAsync(img, pool, c->S, cudaMemcpyDefault, st));
+        else
+          CK(c, cudaMemcpyAsync(pool, img, c->S, cudaMemcpyDefault, st));
+      }
+    return AQUA_OK;
+  }
+  if (engine == AQUA_BASE_BATCH) {
+    const size_t n = ds.size() * 2 * c->L;
+    std::vector<void*> dsts(n), srcs(n);
+    std::vector<size_t> sizes(n, static_cast<size_t>(c->S));
+    size_t k = 0;
+    for (const Desc& d : ds)
+      for (int cc = 0; cc < 2 * c->L; ++cc, ++k) {
+        uint8_t *pool, *img;
+        chunk_ptrs(d, cc, &pool, &img);
+        dsts[k] = dir == aqua::kOut ? img : pool;
+        srcs[k] = dir == aqua::kOut ? pool : img;
+      }
+    cudaMemcpyAttributes attr{};
+    attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
+    size_t idx0 = 0, fail_idx = 0;
+    CK(c, cudaMemcpyBatchAsync(dsts.data(), srcs.data(), sizes.data(), n, &attr, &idx0, 1, &fail_idx, st));
+    return AQUA_OK;
+  }
+  if (engine == AQUA_BASE_GATHER_TEMP) {
+    // The paper's two-step path: gather into a temporary tensor
+    // on this GPU, then one large copy per contiguous run of slots.
+    const size_t need = ds.size() * static_cast<size_t>(c->U);
+    if (need > c->temp_cap) {
+      CK(c, cudaDeviceSynchronize());
+      if (c->d_temp) cudaFree(c->d_temp);
+      c->d_temp = nullptr;
+      CK(c, cudaMalloc(reinterpret_cast<void**>(&c->d_temp), need));
+      c->temp_cap = need;
+    }
+    std::vector<Desc> td(ds.size());
+    for (size_t j = 0; j < ds.size(); ++j) td[j] = Desc{ds[j].block, static_cast<uint32_t>(j)};
+    void* dd;
+    aqua_status s = stage_upload(c, td.data(), td.size() * sizeof(Desc), st, &dd);
+    if (s) return s;
+    *regions = 1;
+    p.desc = static_cast<const Desc*>(dd);
+    p.arena_base[0] = reinterpret_cast<uint64_t>(c->d_temp);
+    p.piece = 4096;
+    p.npieces = static_cast<int32_t>((c->S + 4095) / 4096);
+    p.nitems = p.ndesc * 2 * p.L * p.npieces;
+    auto runs = [&](bool to_arena) -> aqua_status {
+      size_t j = 0;
+      while (j < ds.size()) {
+        size_t r = 1;
+        while (j + r < ds.size() && ds[j + r].slot_arena == ds[j].slot_arena + r) ++r;
+        uint8_t* ab = (ds[j].slot_arena & kArenaBit) ? c->host.base : c->gpu.base;
+        uint8_t* img = ab + int64_t(ds[j].slot_arena & ~kArenaBit) * c->U;
+        uint8_t* tmp = c->d_temp + j * static_cast<size_t>(c->U);
+        if (to_arena)
+          CK(c, cudaMemcpyAsync(img, tmp, r * c->U, cudaMemcpyDefault, st));
+        else
+          CK(c, cudaMemcpyAsync(tmp, img, r * c->U, cudaMemcpyDefault, st));
+        j += r;
+      }
+      return AQUA_OK;
+    };
+    int ctas = 0;
+    if (dir == aqua::kOut) {
+      cudaError_t e = aqua::launch_swap_ldst(p, aqua::kOut, c->num_sms, c->max_ctas, st, &ctas);
+      if (e != cudaSuccess) return cuda_fail(c, e, "gather kernel launch");
+      c->launches++;
+      return runs(true);
+    }
+    aqua_status rs = runs(false);
+    if (rs) return rs;
+    cudaError_t e = aqua::launch_swap_ldst(p, aqua::kIn, c->num_sms, c->max_ctas, st, &ctas);
+    if (e != cudaSuccess) return cuda_fail(c, e, "scatter kernel launch");
+    c->launches++;
+    return AQUA_OK;
+  }
+  return fail(c, AQUA_E_INVAL, "unknown copy engine");
+}
+
+aqua_status precheck(aqua_ctx* c) {
+  if (!c) return fail(nullptr, AQUA_E_INVAL, "null ctx");
+  if (c->poisoned) return fail(c, AQUA_E_CUDA, "ctx poisoned by an earlier CUDA error: " + c->err);
+  if (!c->dry) retire(c);
+  return AQUA_OK;
+}
+
+void set_last(aqua_ctx* c, const std::vector<Desc>& ds) {
+  c->last_b.resize(ds.size());
+  c->last_s.resize(ds.size());
+  c->last_l.resize(ds.size());
+  for (size_t i = 0; i < ds.size(); ++i) {
+    c->last_b[i] = ds[i].block;
+    c->last_s[i] = static_cast<int32_t>(ds[i].slot_arena & ~kArenaBit);
+    c->last_l[i] = (ds[i].slot_arena & kArenaBit) ? AQUA_LOC_HOST : AQUA_LOC_PEER;
+  }
+}
+
+Arena* arena_of(aqua_ctx* c, int loc) { return loc == AQUA_LOC_HOST ? &c->host : &c->gpu; }
+
+}  // namespace
+
+extern "C" {
+
+const char* aqua_version(void) { return "aqua-b200 0.1 (sm_100a)"; }
+
+const char* aqua_strerror(aqua_status s) {
+  switch (s) {
+    case AQUA_OK: return "ok";
+    case AQUA_E_INVAL: return "invalid argument";
+    case AQUA_E_NOBLOCKS: return "not enough free blocks in the pool";
+    case AQUA_E_NOSPACE: return "no swap space (lender and host full)";
+    case AQUA_E_STATE: return "unknown prompt or wrong state";
+    case AQUA_E_CUDA: return "CUDA error (context poisoned)";
+    case AQUA_E_PEER: return "lender unreachable by P2P";
+  }
+  return "unknown status";
+}
+
+const char* aqua_last_error(aqua_ctx* c) { return c ? c->err.c_str() : g_err.c_str(); }
+
+aqua_status aqua_create(int device, const aqua_kv_layout* lay, aqua_ctx** out) {
+  if (!out || !lay) return fail(nullptr, AQUA_E_INVAL, "null argument");
+  *out = nullptr;
+  if (device < 0 && device != AQUA_DRYRUN) return fail(nullptr, AQUA_E_INVAL, "bad device");
+  if (lay->num_layers <= 0 || lay->block_tokens <= 0 || lay->num_kv_heads <= 0 || lay->head_dim <= 0 ||
+      lay->elem_bytes <= 0 || lay->num_blocks <= 0 || !lay->layer_base)
+    return fail(nullptr, AQUA_E_INVAL, "layout sizes must be > 0 and layer_base non-null");
+  const int64_t S = int64_t(lay->block_tokens) * lay->num_kv_heads * lay->head_dim * lay->elem_bytes;
+  const int64_t NB = lay->num_blocks;
+  const int64_t P_kv = lay->kv_plane_stride ? lay->kv_plane_stride : NB * S;
+  const int64_t P_b = lay->block_stride ? lay->block_stride : S;
+  if (S % 16 || P_kv % 16 || P_b % 16 || P_kv < 0 || P_b < 0)
+    return fail(nullptr, AQUA_E_INVAL, "S and strides must be multiples of 16 bytes");
+  if (S > (int64_t(1) << 30) || int64_t(2) * lay->num_layers * S > (int64_t(1) << 40))
+    return fail(nullptr, AQUA_E_INVAL, "chunk too large");
+  // chunks of distinct (kv, b) must not overlap: plane-major (flash) or block-major
+  const bool plane_major = P_b >= S && P_kv >= (NB - 1) * P_b + S;
+  const bool block_major = P_b >= 2 * S && P_kv >= S && P_kv + S <= P_b;
+  if (!plane_major && !block_major) return fail(nullptr, AQUA_E_INVAL, "overlapping chunk layout");
+  for (int l = 0; l < lay->num_layers; ++l)
+    if (reinterpret_cast<uintptr_t>(lay->layer_base[l]) % 16)
+      return fail(nullptr, AQUA_E_INVAL, "layer_base must be 16-byte aligned");
+
+  aqua_ctx* c = new aqua_ctx();
+  c->device = device;
+  c->dry = device == AQUA_DRYRUN;
+  c->L = lay->num_layers;
+  c->bs = lay->block_tokens;
+  c->H = lay->num_kv_heads;
+  c->D = lay->head_dim;
+  c->e = lay->elem_bytes;
+  c->NB = lay->num_blocks;
+  c->S = S;
+  c->U = 2 * c->L * S;
+  c->P_kv = P_kv;
+  c->P_b = P_b;
+  c->layer_base.resize(c->L);
+  for (int l = 0; l < c->L; ++l) c->layer_base[l] = reinterpret_cast<uint64_t>(lay->layer_base[l]);
+  for (int32_t b = 0; b < c->NB; ++b) c->free_blocks.insert(c->free_blocks.end(), b);
+  c->btick.assign(c->NB, 0);
+  if (!c->dry) {
+    DevGuard g(device);
+    cudaError_t e = cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
+    if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void**>(&c->d_layer_base), c->L * sizeof(uint64_t));
+    if (e == cudaSuccess)
+      e = cudaMemcpy(c->d_layer_base, c->layer_base.data(), c->L * sizeof(uint64_t), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+      std::string m = std::string("aqua_create: ") + cudaGetErrorString(e);
+      cudaGetLastError();
+      delete c;
+      return fail(nullptr, AQUA_E_CUDA, m);
+    }
+  }
+  *out = c;
+  return AQUA_OK;
+}
+
+aqua_status aqua_destroy(aqua_ctx* c) {
+  if (!c) return AQUA_E_INVAL;
+  if (!c->dry) {
+    DevGuard g(c->device);
+    for (auto& kv : c->live) {
+      cudaEventSynchronize(kv.second.ev);
+      cudaEventDestroy(kv.second.ev);
+    }
+    for (auto ev : c->ev_pool) cudaEventDestroy(ev);
+    if (c->gpu.present && c->gpu.owned) {
+      DevGuard g2(c->gpu.device);
+      cudaFree(c->gpu.base);
+    }
+    if (c->host.present && c->host.owned) cudaFreeHost(c->host.host_ptr);
+    if (c->d_layer_base) cudaFree(c->d_layer_base);
+    if (c->h_stage) cudaFreeHost(c->h_stage);
+    if (c->d_stage) cudaFree(c->d_stage);
+    if (c->d_temp) cudaFree(c->d_temp);
+    cudaGetLastError();
+  }
+  delete c;
+  return AQUA_OK;
+}
+
+aqua_status aqua_lend(aqua_ctx* c, int lender, void* base, uint64_t bytes, int32_t* out_nslots) {
+  if (aqua_status s = precheck(c)) return s;
+  const bool is_host = lender == AQUA_HOST;
+  Arena& a = is_host ? c->host : c->gpu;
+  if (a.present) return fail(c, AQUA_E_INVAL, is_host ? "host arena already lent" : "one GPU lender per borrower (P:529-534)");
+  if (lender < 0 && lender != AQUA_HOST && lender != AQUA_MAPPED) return fail(c, AQUA_E_INVAL, "bad lender");
+  if (lender == AQUA_MAPPED && !base) return fail(c, AQUA_E_INVAL, "AQUA_MAPPED needs a base");
+  if (base && reinterpret_cast<uintptr_t>(base) % 16) return fail(c, AQUA_E_INVAL, "base must be 16-byte aligned");
+  const int64_t ns = static_cast<int64_t>(bytes / static_cast<uint64_t>(c->U));
+  if (ns > 0x7fffffff) return fail(c, AQUA_E_INVAL, "too many slots");
+  Arena na;
+  na.present = true;
+  na.device = lender;
+  na.bytes = bytes;
+  na.nslots = static_cast<int32_t>(ns);
+  if (c->dry) {
+    na.base = static_cast<uint8_t*>(base);
+  } else {
+    DevGuard g(c->device);
+    if (is_host) {
+      if (base) {
+        void* dp = nullptr;
+        cudaError_t e = cudaHostGetDevicePointer(&dp, base, 0);
+        if (e != cudaSuccess) {
+          cudaGetLastError();
+          return fail(c, AQUA_E_INVAL, "host base is not pinned/mapped memory");
+        }
+        na.base = static_cast<uint8_t*>(dp);
+      } else if (bytes) {
+        void* hp = nullptr;
+        CK(c, cudaHostAlloc(&hp, bytes, cudaHostAllocMapped | cudaHostAllocPortable));
+        void* dp = nullptr;
+        CK(c, cudaHostGetDevicePointer(&dp, hp, 0));
+        na.host_ptr = hp;
+        na.base = static_cast<uint8_t*>(dp);
+        na.owned = true;
+      }
+    } else if (lender == AQUA_MAPPED) {
+      na.base = static_cast<uint8_t*>(base);
+    } else {
+      int ndev = 0;
+      CK(c, cudaGetDeviceCount(&ndev));
+      if (lender >= ndev) return fail(c, AQUA_E_INVAL, "lender device out of range");
+      if (lender != c->device) {
+        int can = 0;
+        CK(c, cudaDeviceCanAccessPeer(&can, c->device, lender));
+        if (!can) return fail(c, AQUA_E_PEER, "borrower cannot access lender by P2P");
+        cudaError_t e = cudaDeviceEnablePeerAccess(lender, 0);
+        if (e == cudaErrorPeerAccessAlreadyEnabled) {
+          cudaGetLastError();
+        } else if (e != cudaSuccess) {
+          cudaGetLastError();
+          return fail(c, AQUA_E_PEER, std::string("cudaDeviceEnablePeerAccess: ") + cudaGetErrorString(e));
+        }
+      }
+      if (base) {
+        na.base = static_cast<uint8_t*>(base);
+      } else if (bytes) {
+        DevGuard g2(lender);
+        CK(c, cudaMalloc(reinterpret_cast<void**>(&na.base), bytes));
+        na.owned = true;
+      }
+    }
+  }
+  for (int32_t s = 0; s < na.nslots; ++s) na.free.insert(na.free.end(), s);
+  na.tick.assign(na.nslots, 0);
+  a = std::move(na);
+  if (out_nslots) *out_nslots = a.nslots;
+  return AQUA_OK;
+}
+
+aqua_status aqua_alloc_blocks(aqua_ctx* c, uint64_t pid, int32_t n, aqua_stream_t stream, int32_t* out_ids) {
+  if (aqua_status s = precheck(c)) return s;
+  if (n < 0 || (n > 0 && !out_ids)) return fail(c, AQUA_E_INVAL, "n < 0 or null out_ids");
+  auto it = c->prompts.find(pid);
+  if (it != c->prompts.end() && it->second.state != AQUA_ST_RESIDENT)
+    return fail(c, AQUA_E_STATE, "pid is swapped out");
+  if (static_cast<int64_t>(c->free_blocks.size()) < n) return fail(c, AQUA_E_NOBLOCKS, "pool exhausted");
+  DevGuard g(c->device, c->dry);
+  std::vector<int32_t> ids;
+  ids.reserve(n);
+  auto fb = c->free_blocks.begin();
+  for (int32_t i = 0; i < n; ++i) ids.push_back(*fb++);
+  std::vector<uint64_t> ts;
+  for (int32_t b : ids) ts.push_back(c->btick[b]);
+  if (aqua_status s = wait_all(c, ts, reinterpret_cast<cudaStream_t>(stream))) return s;
+  c->free_blocks.erase(c->free_blocks.begin(), fb);
+  Prompt& p = c->prompts[pid];
+  for (int32_t b : ids) c->btick[b] = 0;
+  p.ids.insert(p.ids.end(), ids.begin(), ids.end());
+  std::copy(ids.begin(), ids.end(), out_ids);
+  return AQUA_OK;
+}
+
+aqua_status aqua_adopt_blocks(aqua_ctx* c, uint64_t pid, int32_t n, const int32_t* ids, aqua_stream_t stream) {
+  if (aqua_status s = precheck(c)) return s;
+  if (n < 0 || (n > 0 && !ids)) return fail(c, AQUA_E_INVAL, "n < 0 or null ids");
+  std::unordered_set<int32_t> seen;
+  for (int32_t i = 0; i < n; ++i) {
+    const int32_t b = ids[i];
+    if (b < 0 || b >= c->NB || !seen.insert(b).second || !c->free_blocks.count(b))
+      return fail(c, AQUA_E_INVAL, "ids must be in range, free and distinct");
+  }
+  auto it = c->prompts.find(pid);
+  if (it != c->prompts.end() && it->second.state != AQUA_ST_RESIDENT)
+    return fail(c, AQUA_E_STATE, "pid is swapped out");
+  DevGuard g(c->device, c->dry);
+  std::vector<uint64_t> ts;
+  for (int32_t i = 0; i < n; ++i) ts.push_back(c->btick[ids[i]]);
+  if (aqua_status s = wait_all(c, ts, reinterpret_cast<cudaStream_t>(stream))) return s;
+  Prompt& p = c->prompts[pid];
+  for (int32_t i = 0; i < n; ++i) {
+    c->free_blocks.erase(ids[i]);
+    c->btick[ids[i]] = 0;
+    p.ids.push_back(ids[i]);
+  }
+  return AQUA_OK;
+}
+
+aqua_status aqua_swap_out(aqua_ctx* c, int32_t n, const uint64_t* pids, aqua_stream_t stream, uint64_t* out_ticket) {
+  if (aqua_status s = precheck(c)) return s;
+  if (out_ticket) *out_ticket = 0;
+  if (n < 0 || (n > 0 && !pids)) return fail(c, AQUA_E_INVAL, "n < 0 or null pids");
+  std::unordered_set<uint64_t> seen;
+  std::vector<Prompt*> ps;
+  for (int32_t i = 0; i < n; ++i) {
+    if (!seen.insert(pids[i]).second) return fail(c, AQUA_E_INVAL, "duplicate pid");
+  }
+  for (int32_t i = 0; i < n; ++i) {
+    auto it = c->prompts.find(pids[i]);
+    if (it == c->prompts.end() || it->second.state != AQUA_ST_RESIDENT)
+      return fail(c, AQUA_E_STATE, "pid not resident");
+    ps.push_back(&it->second);
+  }
+  // placement (R5): whole prompt on the GPU lender if it fits, else host
+  int64_t gpu_left = c->gpu.present ? static_cast<int64_t>(c->gpu.free.size()) : -1;
+  int64_t host_left = c->host.present ? static_cast<int64_t>(c->host.free.size()) : -1;
+  std::vector<int> loc(n);
+  for (int32_t i = 0; i < n; ++i) {
+    const int64_t np = static_cast<int64_t>(ps[i]->ids.size());
+    if (gpu_left >= np) {
+      loc[i] = AQUA_LOC_PEER;
+      gpu_left -= np;
+    } else if (host_left >= np) {
+      loc[i] = AQUA_LOC_HOST;
+      host_left -= np;
+    } else {
+      return fail(c, AQUA_E_NOSPACE, "no swap space for a prompt");
+    }
+  }
+  // slots lowest-first per arena, in call order
+  std::vector<Desc> ds;
+  std::vector<std::vector<int32_t>> slots(n);
+  auto git = c->gpu.free.begin();
+  auto hit = c->host.free.begin();
+  for (int32_t i = 0; i < n; ++i) {
+    auto& itr = loc[i] == AQUA_LOC_PEER ? git : hit;
+    const uint32_t bit = loc[i] == AQUA_LOC_HOST ? kArenaBit : 0u;
+    for (int32_t b : ps[i]->ids) {
+      const int32_t s = *itr++;
+      slots[i].push_back(s);
+      ds.push_back(Desc{b, static_cast<uint32_t>(s) | bit});
+    }
+  }
+  set_last(c, ds);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  uint64_t ticket = 0;
+  if (!c->dry && !ds.empty()) {
+    DevGuard g(c->device);
+    std::vector<uint64_t> ts;
+    for (const Desc& d : ds) {
+      ts.push_back(c->btick[d.block]);
+      ts.push_back(arena_of(c, (d.slot_arena & kArenaBit) ? AQUA_LOC_HOST : AQUA_LOC_PEER)
+                       ->tick[d.slot_arena & ~kArenaBit]);
+    }
+    if (aqua_status s = wait_all(c, ts, st)) return s;
+    int regions = 0;
+    if (aqua_status s = run_copy(c, ds, aqua::kOut, st, &regions)) return s;
+    if (aqua_status s = record(c, st, &ticket)) return s;
+    stage_seal(c, regions, ticket);
+  } else if (c->dry && !ds.empty()) {
+    record(c, st, &ticket);
+  }
+  // commit bookkeeping
+  for (int32_t i = 0; i < n; ++i) {
+    Arena* a = arena_of(c, loc[i]);
+    for (int32_t s : slots[i]) {
+      a->free.erase(s);
+      a->tick[s] = ticket;
+    }
+    for (int32_t b : ps[i]->ids) {
+      c->free_blocks.insert(b);
+      c->btick[b] = ticket;
+    }
+    ps[i]->state = AQUA_ST_SWAPPED;
+    ps[i]->loc = loc[i];
+    ps[i]->ids = std::move(slots[i]);
+  }
+  if (out_ticket) *out_ticket = ticket;
+  return AQUA_OK;
+}
+
+aqua_status aqua_swap_in(aqua_ctx* c, int32_t n, const uint64_t* pids, aqua_stream_t stream, int32_t* out_ids,
+                         int64_t out_ids_cap, int32_t* out_counts, uint64_t* out_ticket) {
+  if (aqua_status s = precheck(c)) return s;
+  if (out_ticket) *out_ticket = 0;
+  if (n < 0 || (n > 0 && !pids)) return fail(c, AQUA_E_INVAL, "n < 0 or null pids");
+  std::unordered_set<uint64_t> seen;
+  for (int32_t i = 0; i < n; ++i)
+    if (!seen.insert(pids[i]).second) return fail(c, AQUA_E_INVAL, "duplicate pid");
+  std::vector<Prompt*> ps;
+  int64_t need = 0;
+  for (int32_t i = 0; i < n; ++i) {
+    auto it = c->prompts.find(pids[i]);
+    if (it == c->prompts.end() || it->second.state != AQUA_ST_SWAPPED)
+      return fail(c, AQUA_E_STATE, "pid not swapped");
+    ps.push_back(&it->second);
+    need += static_cast<int64_t>(it->second.ids.size());
+  }
+  if (need > 0 && (!out_ids || out_ids_cap < need)) return fail(c, AQUA_E_INVAL, "out_ids too small");
+  if (n > 0 && !out_counts) return fail(c, AQUA_E_INVAL, "null out_counts");
+  if (need > static_cast<int64_t>(c->free_blocks.size())) return fail(c, AQUA_E_NOBLOCKS, "pool exhausted");
+  std::vector<Desc> ds;
+  std::vector<std::vector<int32_t>> fresh(n);
+  auto fb = c->free_blocks.begin();
+  for (int32_t i = 0; i < n; ++i) {
+    const uint32_t bit = ps[i]->loc == AQUA_LOC_HOST ? kArenaBit : 0u;
+    for (int32_t s : ps[i]->ids) {
+      const int32_t b = *fb++;
+      fresh[i].push_back(b);
+      ds.push_back(Desc{b, static_cast<uint32_t>(s) | bit});
+    }
+  }
+  set_last(c, ds);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  uint64_t ticket = 0;
+  if (!c->dry && !ds.empty()) {
+    DevGuard g(c->device);
+    std::vector<uint64_t> ts;
+    for (const Desc& d : ds) {
+      ts.push_back(c->btick[d.block]);
+      ts.push_back(arena_of(c, (d.slot_arena & kArenaBit) ? AQUA_LOC_HOST : AQUA_LOC_PEER)
+                       ->tick[d.slot_arena & ~kArenaBit]);
+    }
+    if (aqua_status s = wait_all(c, ts, st)) return s;
+    int regions = 0;
+    if (aqua_status s = run_copy(c, ds, aqua::kIn, st, &regions)) return s;
+    if (aqua_status s = record(c, st, &ticket)) return s;
+    stage_seal(c, regions, ticket);
+  } else if (c->dry && !ds.empty()) {
+    record(c, st, &ticket);
+  }
+  c->free_blocks.erase(c->free_blocks.begin(), fb);
+  int64_t k = 0;
+  for (int32_t i = 0; i < n; ++i) {
+    Arena* a = arena_of(c, ps[i]->loc);
+    for (int32_t s : ps[i]->ids) {
+      a->free.insert(s);
+      a->tick[s] = ticket;
+    }
+    for (int32_t b : fresh[i]) {
+      c->btick[b] = ticket;
+      out_ids[k++] = b;
+    }
+    out_counts[i] = static_cast<int32_t>(fresh[i].size());
+    ps[i]->state = AQUA_ST_RESIDENT;
+    ps[i]->loc = AQUA_LOC_LOCAL;
+    ps[i]->ids = std::move(fresh[i]);
+  }
+  if (out_ticket) *out_ticket = ticket;
+  return AQUA_OK;
+}
+
+aqua_status aqua_free(aqua_ctx* c, uint64_t pid, aqua_stream_t stream) {
+  if (aqua_status s = precheck(c)) return s;
+  auto it = c->prompts.find(pid);
+  if (it == c->prompts.end()) return fail(c, AQUA_E_STATE, "unknown pid");
+  Prompt& p = it->second;
+  if (p.state == AQUA_ST_RESIDENT) {
+    uint64_t t = 0;
+    if (!c->dry && !p.ids.empty()) {
+      DevGuard g(c->device);
+      cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+      std::vector<uint64_t> ts;
+      for (int32_t b : p.ids) ts.push_back(c->btick[b]);
+      if (aqua_status s = wait_all(c, ts, st)) return s;
+      if (aqua_status s = record(c, st, &t)) return s;
+    }
+    for (int32_t b : p.ids) {
+      c->free_blocks.insert(b);
+      c->btick[b] = t;
+    }
+  } else {
+    Arena* a = arena_of(c, p.loc);
+    for (int32_t s : p.ids) a->free.insert(s);
+  }
+  c->prompts.erase(it);
+  return AQUA_OK;
+}
+
+aqua_status aqua_wait(aqua_ctx* c, uint64_t ticket, aqua_stream_t stream) {
+  if (aqua_status s = precheck(c)) return s;
+  if (c->dry) return AQUA_OK;
+  DevGuard g(c->device);
+  auto it = c->live.find(ticket);
+  if (it == c->live.end()) return AQUA_OK;
+  CK(c, cudaStreamWaitEvent(reinterpret_cast<cudaStream_t>(stream), it->second.ev, 0));
+  return AQUA_OK;
+}
+
+aqua_status aqua_sync(aqua_ctx* c, uint64_t ticket) {
+  if (aqua_status s = precheck(c)) return s;
+  if (c->dry) return AQUA_OK;
+  auto it = c->live.find(ticket);
+  if (it == c->live.end()) return AQUA_OK;
+  CK(c, cudaEventSynchronize(it->second.ev));
+  return AQUA_OK;
+}
+
+aqua_status aqua_ticket_done(aqua_ctx* c, uint64_t ticket, int32_t* done) {
+  if (aqua_status s = precheck(c)) return s;
+  if (!done) return fail(c, AQUA_E_INVAL, "null done");
+  *done = 1;
+  if (c->dry) return AQUA_OK;
+  auto it = c->live.find(ticket);
+  if (it == c->live.end()) return AQUA_OK;
+  cudaError_t q = cudaEventQuery(it->second.ev);
+  if (q == cudaErrorNotReady) {
+    *done = 0;
+    return AQUA_OK;
+  }
+  if (q != cudaSuccess) return cuda_fail(c, q, "cudaEventQuery");
+  return AQUA_OK;
+}
+
+aqua_status aqua_query(aqua_ctx* c, uint64_t pid, int32_t* state, int32_t* location, int32_t* n,
+                       int32_t* ids, int32_t cap) {
+  if (!c) return fail(nullptr, AQUA_E_INVAL, "null ctx");
+  auto it = c->prompts.find(pid);
+  if (it == c->prompts.end()) return fail(c, AQUA_E_STATE, "unknown pid");
+  const Prompt& p = it->second;
+  if (state) *state = p.state;
+  if (location) *location = p.loc;
+  if (n) *n = static_cast<int32_t>(p.ids.size());
+  if (ids) {
+    if (cap < static_cast<int32_t>(p.ids.size())) return fail(c, AQUA_E_INVAL, "ids capacity too small");
+    std::copy(p.ids.begin(), p.ids.end(), ids);
+  }
+  return AQUA_OK;
+}
+
+aqua_status aqua_counts(aqua_ctx* c, int32_t* fb, int32_t* pf, int32_t* hf) {
+  if (!c) return fail(nullptr, AQUA_E_INVAL, "null ctx");
+  if (fb) *fb = static_cast<int32_t>(c->free_blocks.size());
+  if (pf) *pf = c->gpu.present ? static_cast<int32_t>(c->gpu.free.size()) : -1;
+  if (hf) *hf = c->host.present ? static_cast<int32_t>(c->host.free.size()) : -1;
+  return AQUA_OK;
+}
+
+aqua_status aqua_arena_base(aqua_ctx* c, int32_t loc, void** base, int32_t* nslots) {
+  if (!c) return fail(nullptr, AQUA_E_INVAL, "null ctx");
+  if (loc != AQUA_LOC_PEER && loc != AQUA_LOC_HOST) return fail(c, AQUA_E_INVAL, "loc");
+  Arena* a = arena_of(c, loc);
+  if (!a->present) return fail(c, AQUA_E_STATE, "no such arena");
+  if (base) *base = a->base;
+  if (nslots) *nslots = a->nslots;
+  return AQUA_OK;
+}
+
+aqua_status aqua_set_option(aqua_ctx* c, int32_t opt, int64_t v) {
+  if (!c) return fail(nullptr, AQUA_E_INVAL, "null ctx");
+  switch (opt) {
+    case AQUA_OPT_KERNEL:
+      if (v < AQUA_KERNEL_AUTO || v > AQUA_BASE_BATCH) return fail(c, AQUA_E_INVAL, "kernel");
+      c->kernel = static_cast<int>(v);
+      return AQUA_OK;
+    case AQUA_OPT_MAX_CTAS:
+      if (v < 0 || v > (1 << 20)) return fail(c, AQUA_E_INVAL, "max_ctas");
+      c->max_ctas = static_cast<int>(v);
+      return AQUA_OK;
+    case AQUA_OPT_TMA_PIECE:
+      if (v < 0 || v > 65536 || v % 16) return fail(c, AQUA_E_INVAL, "tma piece");
+      c->tma_piece = static_cast<int>(v);
+      return AQUA_OK;
+  }
+  return fail(c, AQUA_E_INVAL, "unknown option");
+}
+
+aqua_status aqua_get_option(aqua_ctx* c, int32_t opt, int64_t* v) {
+  if (!c || !v) return fail(c, AQUA_E_INVAL, "null argument");
+  switch (opt) {
+    case AQUA_OPT_KERNEL: *v = c->kernel; return AQUA_OK;
+    case AQUA_OPT_MAX_CTAS: *v = c->max_ctas; return AQUA_OK;
+    case AQUA_OPT_TMA_PIECE: *v = c->tma_piece; return AQUA_OK;
+  }
+  return fail(c, AQUA_E_INVAL, "unknown option");
+}
+
+aqua_status aqua_last_descriptors(aqua_ctx* c, int32_t* blocks, int32_t* slots, int32_t* locs, int64_t cap,
+                                  int64_t* n_out) {
+  if (!c) return fail(nullptr, AQUA_E_INVAL, "null ctx");
+  const int64_t n = static_cast<int64_t>(c->last_b.size());
+  if (n_out) *n_out = n;
+  const int64_t m = std::min(n, cap);
+  for (int64_t i = 0; i < m; ++i) {
+    if (blocks) blocks[i] = c->last_b[i];
+    if (slots) slots[i] = c->last_s[i];
+    if (locs) locs[i] = c->last_l[i];
+  }
+  return AQUA_OK;
+}
+
+aqua_status aqua_launch_count(aqua_ctx* c, uint64_t* n) {
+  if (!c || !n) return fail(c, AQUA_E_INVAL, "null argument");
+  *n = c->launches;
+  return AQUA_OK;
+}
+
+aqua_status aqua_ipc_export(void* dev_ptr, uint8_t handle[64]) {
+  if (!dev_ptr || !handle) return fail(nullptr, AQUA_E_INVAL, "null argument");
+  cudaIpcMemHandle_t h;
+  cudaError_t e = cudaIpcGetMemHandle(&h, dev_ptr);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(nullptr, AQUA_E_CUDA, std::string("cudaIpcGetMemHandle: ") + cudaGetErrorString(e));
+  }
+  static_assert(sizeof(h) == 64, "IPC handle is 64 bytes");
+  std::memcpy(handle, &h, 64);
+  return AQUA_OK;
+}
+
+aqua_status aqua_ipc_import(int device, const uint8_t handle[64], void** out) {
+  if (!handle || !out) return fail(nullptr, AQUA_E_INVAL, "null argument");
+  DevGuard g(device);
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, 64);
+  cudaError_t e = cudaIpcOpenMemHandle(out, h, cudaIpcMemLazyEnablePeerAccess);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(nullptr, AQUA_E_PEER, std::string("cudaIpcOpenMemHandle: ") + cudaGetErrorString(e));
+  }
+  return AQUA_OK;
+}
+
+aqua_status aqua_ipc_close(int device, void* ptr) {
+  DevGuard g(device);
+  cudaError_t e = cudaIpcCloseMemHandle(ptr);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(nullptr, AQUA_E_CUDA, std::string("cudaIpcCloseMemHandle: ") + cudaGetErrorString(e));
+  }
+  return AQUA_OK;
+}
+
+aqua_status aqua_can_access_peer(int device, int peer, int32_t* can) {
+  if (!can) return fail(nullptr, AQUA_E_INVAL, "null argument");
+  int v = 0;
+  cudaError_t e = device == peer ? cudaSuccess : cudaDeviceCanAccessPeer(&v, device, peer);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(nullptr, AQUA_E_CUDA, std::string("cudaDeviceCanAccessPeer: ") + cudaGetErrorString(e));
+  }
+  *can = device == peer ? 1 : v;
+  return AQUA_OK;
+}
+
+static aqua_status pattern_call(aqua_ctx* c, uint64_t pid, int32_t t0, int32_t t1, uint64_t seed,
+                                aqua_stream_t stream, uint64_t* d_mism, bool verify) {
+  if (aqua_status s = precheck(c)) return s;
+  auto it = c->prompts.find(pid);
+  if (it == c->prompts.end() || it->second.state != AQUA_ST_RESIDENT)
+    return fail(c, AQUA_E_STATE, "pid not resident");
+  if (c->e != 2 || c->D % 8) return fail(c, AQUA_E_INVAL, "pattern needs elem_bytes 2 and head_dim % 8 == 0");
+  const Prompt& p = it->second;
+  if (t0 < 0 || t1 < t0 || static_cast<int64_t>(t1) > static_cast<int64_t>(p.ids.size()) * c->bs)
+    return fail(c, AQUA_E_INVAL, "token range outside the prompt's blocks");
+  if (verify && !d_mism) return fail(c, AQUA_E_INVAL, "null mismatch counter");
+  if (c->dry) return fail(c, AQUA_E_INVAL, "pattern kernels need a GPU ctx");
+  if (t1 == t0 || p.ids.empty()) return AQUA_OK;
+  DevGuard g(c->device);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  std::vector<uint64_t> ts;
+  for (int32_t b : p.ids) ts.push_back(c->btick[b]);
+  if (aqua_status s = wait_all(c, ts, st)) return s;
+  void* dbt;
+  if (aqua_status s = stage_upload(c, p.ids.data(), p.ids.size() * sizeof(int32_t), st, &dbt)) return s;
+  aqua::PatternParams pp{};
+  pp.bt = static_cast<const int32_t*>(dbt);
+  pp.layer_base = c->d_layer_base;
+  pp.P_kv = c->P_kv;
+  pp.P_b = c->P_b;
+  pp.L = c->L;
+  pp.bs = c->bs;
+  pp.H = c->H;
+  pp.D = c->D;
+  pp.t0 = t0;
+  pp.t1 = t1;
+  pp.pid = pid;
+  pp.seed = seed;
+  pp.mismatches = reinterpret_cast<unsigned long long*>(d_mism);
+  cudaError_t e = verify ? aqua::launch_pattern_verify(pp, c->num_sms, st) : aqua::launch_pattern_fill(pp, c->num_sms, st);
+  if (e != cudaSuccess) return cuda_fail(c, e, "pattern kernel launch");
+  c->launches++;
+  uint64_t t = 0;
+  if (aqua_status s = record(c, st, &t)) return s;
+  stage_seal(c, 1, t);
+  for (int32_t b : p.ids) c->btick[b] = t;
+  return AQUA_OK;
+}
+
+aqua_status aqua_kv_fill_pattern(aqua_ctx* c, uint64_t pid, int32_t t0, int32_t t1, uint64_t seed,
+                                 aqua_stream_t stream) {
+  return pattern_call(c, pid, t0, t1, seed, stream, nullptr, false);
+}
+
+aqua_status aqua_kv_verify_pattern(aqua_ctx* c, uint64_t pid, int32_t ntok, uint64_t seed, aqua_stream_t stream,
+                                   uint64_t* d_mismatches) {
+  return pattern_call(c, pid, 0, ntok, seed, stream, d_mismatches, true);
+}
+
+}  // extern "C"

@@ -1,0 +1,54 @@
+// Internal interface between the host library (aqua_host.cpp) and the
+// sm_100a kernels (aqua_kernels.cu).  Not part of the public ABI.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace aqua {
+
+// One swap descriptor: a pool block and an arena slot.  The arena index
+// (0 = GPU lender / self-lender, 1 = pinned host) rides in bit 31 of slot.
+struct Desc {
+  int32_t block;
+  uint32_t slot_arena;
+};
+constexpr uint32_t kArenaBit = 0x80000000u;
+
+enum Dir : int { kOut = 0, kIn = 1 };   // swap_out: pool -> arena; swap_in: arena -> pool
+
+struct SwapParams {
+  const Desc* desc;            // device array [ndesc]
+  const uint64_t* layer_base;  // device array [L]
+  uint64_t arena_base[2];      // device-visible bases: [0] GPU lender, [1] host
+  int64_t ndesc;
+  int32_t L;
+  int32_t piece;               // bytes per work item (multiple of 16, divides nothing in particular)
+  int32_t npieces;             // ceil(S / piece)
+  int32_t pad_;
+  int64_t S, U, P_kv, P_b;
+  int64_t nitems;              // ndesc * 2L * npieces
+};
+
+struct PatternParams {
+  const int32_t* bt;           // device block table of the prompt
+  const uint64_t* layer_base;
+  int64_t P_kv, P_b;
+  int32_t L, bs, H, D;
+  int32_t t0, t1;              // fill: tokens [t0, t1); verify: [0, t1)
+  uint64_t pid, seed;
+  unsigned long long* mismatches;  // verify only
+};
+
+// Launchers: return the CUDA error of the launch (cudaSuccess on success).
+// grid_cap = max CTAs (0 = derived from the SM count).
+cudaError_t launch_swap_tma(const SwapParams& p, Dir dir, int num_sms, int grid_cap,
+                            cudaStream_t s, int* ctas_used);
+cudaError_t launch_swap_ldst(const SwapParams& p, Dir dir, int num_sms, int grid_cap,
+                             cudaStream_t s, int* ctas_used);
+cudaError_t launch_pattern_fill(const PatternParams& p, int num_sms, cudaStream_t s);
+cudaError_t launch_pattern_verify(const PatternParams& p, int num_sms, cudaStream_t s);
+
+// Max dynamic shared memory the TMA kernel will request (for attribute setup).
+int tma_smem_bytes(int piece, int stages);
+
+}  // namespace aqua

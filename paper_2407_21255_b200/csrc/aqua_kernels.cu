@@ -1,0 +1,354 @@
+// sm_100a kernels of libaqua: the fused block-table gather/scatter that
+// pages a prompt's KV blocks between the borrower's pool and a swap arena
+// (peer HBM over NVLink 5 / NVSwitch, the same HBM, or mapped pinned host
+// memory), plus the harness pattern kernels.
+//
+// Paper: Sec. 7 "Efficient context switching" gathers the
+// per-layer pieces into a temporary GPU tensor and then copies it to the
+// AquaTensor; the reverse for swap-in.  Here the temporary tensor is gone:
+// every (block, layer, K|V) chunk is moved straight from its pool address to
+// its final place in the lender's slot (and back), in one launch for all the
+// prompts of a call.  Pure byte movement: no arithmetic on values, no tensor
+// cores.
+//
+// Work item = one piece (<= `piece` bytes) of one chunk (l, kv) of one
+// descriptor j.  Items are numbered j-major, then c = 2l + kv, then piece,
+// so consecutive items are consecutive bytes of the slot-major image.
+#include "aqua_internal.h"
+
+#include <algorithm>
+
+namespace aqua {
+namespace {
+
+// ------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "AQUA_WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra AQUA_WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// TMA bulk copy global -> shared, completion counted on an mbarrier (UBLKCP).
+__device__ __forceinline__ void bulk_g2s(void* sdst, const void* gsrc, uint32_t bytes, uint64_t* bar,
+                                         uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(sdst)),
+      "l"(gsrc), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+// TMA bulk copy shared -> global (local HBM, a P2P-mapped peer address or
+// mapped host memory), tracked by bulk groups.
+__device__ __forceinline__ void bulk_s2g(void* gdst, const void* ssrc, uint32_t bytes, uint64_t pol) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(gdst),
+               "r"(smem_u32(ssrc)), "r"(bytes), "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait() {
+  asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ int4 ld_stream(const void* p) {
+  int4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.s32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void st_stream(void* p, const int4& v) {
+  asm volatile("st.global.L1::no_allocate.v4.s32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y),
+               "r"(v.z), "r"(v.w)
+               : "memory");
+}
+
+// ------------------------------------------------------------ addressing
+struct Cursor {
+  int64_t j;
+  int32_t c, q;
+  __device__ __forceinline__ void init(int64_t item, const SwapParams& p) {
+    const int64_t per_desc = int64_t(2) * p.L * p.npieces;
+    j = item / per_desc;
+    const int64_t r = item - j * per_desc;
+    c = static_cast<int32_t>(r / p.npieces);
+    q = static_cast<int32_t>(r - int64_t(c) * p.npieces);
+  }
+  __device__ __forceinline__ void next(const SwapParams& p) {
+    if (++q == p.npieces) {
+      q = 0;
+      if (++c == 2 * p.L) {
+        c = 0;
+        ++j;
+      }
+    }
+  }
+};
+
+// chunk(l, kv, b) = layer_base[l] + kv*P_kv + b*P_b            (R1)
+// image chunk    = arena + slot*U + (2l+kv)*S                   (R3)
+template <Dir D>
+__device__ __forceinline__ void item_addrs(const SwapParams& p, const Desc d, int c, int q,
+                                           const uint8_t*& src, uint8_t*& dst, uint32_t& bytes) {
+  const int l = c >> 1, kv = c & 1;
+  const int64_t off = int64_t(q) * p.piece;
+  uint8_t* pool = reinterpret_cast<uint8_t*>(__ldg(p.layer_base + l)) + kv * p.P_kv +
+                  int64_t(d.block) * p.P_b + off;
+  const uint32_t a = d.slot_arena >> 31;
+  const int64_t slot = d.slot_arena & ~kArenaBit;
+  const uint64_t base = a ? p.arena_base[1] : p.arena_base[0];   // no dynamic param indexing
+  uint8_t* img = reinterpret_cast<uint8_t*>(base) + slot * p.U + int64_t(c) * p.S + off;
+  const int64_t rem = p.S - off;
+  bytes = static_cast<uint32_t>(rem < p.piece ? rem : p.piece);
+  if (D == kOut) {
+    src = pool;
+    dst = img;
+  } else {
+    src = img;
+    dst = pool;
+  }
+}
+
+// ------------------------------------------------------------ TMA ring kernel
+// One CTA = one warp; lane 0 drives a `stages`-deep ring of `piece`-byte
+// shared-memory stages: cp.async.bulk loads (mbarrier complete_tx) run
+// stages-1 items ahead of the cp.async.bulk stores.  Each CTA owns a
+// contiguous range of items, so its stores form one long contiguous run in
+// the image (swap_out) / its loads do (swap_in).
+template <Dir D>
+__global__ void __launch_bounds__(32) swap_tma_kernel(const SwapParams p, const int stages) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  if (threadIdx.x != 0) return;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + size_t(stages) * p.piece);
+  const int64_t G = gridDim.x, b = blockIdx.x;
+  const int64_t i0 = p.nitems * b / G, i1 = p.nitems * (b + 1) / G;
+  const int64_t n = i1 - i0;
+  if (n <= 0) return;
+  for (int s = 0; s < stages; ++s) mbar_init(&bars[s], 1);
+  fence_mbar_init();
+  const uint64_t pol = policy_evict_first();
+
+  Cursor lc, sc;
+  lc.init(i0, p);
+  sc = lc;
+  int64_t nload = 0;
+  int lstage = 0;
+  auto issue_load = [&]() {
+    const uint8_t* src;
+    uint8_t* dst;
+    uint32_t bytes;
+    item_addrs<D>(p, p.desc[lc.j], lc.c, lc.q, src, dst, bytes);
+    uint8_t* buf = smem + size_t(lstage) * p.piece;
+    mbar_expect_tx(&bars[lstage], bytes);
+    bulk_g2s(buf, src, bytes, &bars[lstage], pol);
+    lc.next(p);
+    ++nload;
+    if (++lstage == stages) lstage = 0;
+  };
+  const int64_t pre = n < stages - 1 ? n : stages - 1;
+  while (nload < pre) issue_load();
+
+  int sstage = 0;
+  uint32_t parity = 0;
+  for (int64_t k = 0; k < n; ++k) {
+    mbar_wait(&bars[sstage], parity);
+    const uint8_t* src;
+    uint8_t* dst;
+    uint32_t bytes;
+    item_addrs<D>(p, p.desc[sc.j], sc.c, sc.q, src, dst, bytes);
+    bulk_s2g(dst, smem + size_t(sstage) * p.piece, bytes, pol);
+    bulk_commit();
+    sc.next(p);
+    if (++sstage == stages) {
+      sstage = 0;
+      parity ^= 1u;
+    }
+    if (nload < n) {
+      bulk_wait_read<1>();  // the store of item k-1 has finished reading its stage
+      issue_load();         // item k+stages-1 -> the stage of item k-1
+    }
+  }
+  bulk_wait<0>();
+}
+
+// ------------------------------------------------------------ LDG/STG kernel
+// Grid-stride over items of up to 512*UNROLL bytes; a warp moves one item
+// with UNROLL independent 16-byte loads per lane in flight.
+template <Dir D, int UNROLL>
+__global__ void __launch_bounds__(256) swap_ldst_kernel(const SwapParams p) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t it = warp; it < p.nitems; it += nwarps) {
+    Cursor cu;
+    cu.init(it, p);
+    const uint8_t* src;
+    uint8_t* dst;
+    uint32_t bytes;
+    item_addrs<D>(p, p.desc[cu.j], cu.c, cu.q, src, dst, bytes);
+    const int nvec = static_cast<int>(bytes >> 4);
+    int4 v[UNROLL];
+#pragma unroll
+    for (int u = 0; u < UNROLL; ++u) {
+      const int idx = u * 32 + lane;
+      if (idx < nvec) v[u] = ld_stream(src + size_t(idx) * 16);
+    }
+#pragma unroll
+    for (int u = 0; u < UNROLL; ++u) {
+      const int idx = u * 32 + lane;
+      if (idx < nvec) st_stream(dst + size_t(idx) * 16, v[u]);
+    }
+  }
+}
+
+// ------------------------------------------------------------ pattern (C-11)
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+  uint64_t z = x + 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+__device__ __forceinline__ uint32_t word(uint64_t seed, uint64_t pid, uint64_t t, uint64_t l, uint64_t kv,
+                                         uint64_t h, uint64_t d) {
+  const uint64_t pk = (pid << 46) | (t << 26) | (l << 18) | (kv << 17) | (h << 10) | d;
+  return static_cast<uint32_t>(splitmix64(seed ^ pk) & 0xFFFFu);
+}
+
+// Thread = 8 consecutive 16-bit words (16 bytes) of one token row.  Index
+// order d8, h, t, kv, l so that neighbouring threads write neighbouring bytes.
+template <bool VERIFY>
+__global__ void __launch_bounds__(256) pattern_kernel(const PatternParams p) {
+  const int D8 = p.D >> 3;
+  const int t_lo = VERIFY ? 0 : p.t0;
+  const int64_t nt = p.t1 - t_lo;
+  const int64_t total = int64_t(D8) * p.H * nt * 2 * p.L;
+  unsigned long long bad = 0;
+  for (int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; idx < total;
+       idx += int64_t(gridDim.x) * blockDim.x) {
+    int64_t r = idx;
+    const int d8 = static_cast<int>(r % D8);
+    r /= D8;
+    const int h = static_cast<int>(r % p.H);
+    r /= p.H;
+    const int t = t_lo + static_cast<int>(r % nt);
+    r /= nt;
+    const int kv = static_cast<int>(r & 1);
+    const int l = static_cast<int>(r >> 1);
+    const int blk = __ldg(p.bt + t / p.bs);
+    const int row = t % p.bs;
+    uint8_t* a = reinterpret_cast<uint8_t*>(__ldg(p.layer_base + l)) + kv * p.P_kv + int64_t(blk) * p.P_b +
+                 (int64_t(row * p.H + h) * p.D + d8 * 8) * 2;
+    uint32_t w[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const uint64_t d = uint64_t(d8) * 8 + 2 * e;
+      w[e] = word(p.seed, p.pid, t, l, kv, h, d) | (word(p.seed, p.pid, t, l, kv, h, d + 1) << 16);
+    }
+    if (VERIFY) {
+      const uint4 got = *reinterpret_cast<const uint4*>(a);
+      const uint32_t g[4] = {got.x, got.y, got.z, got.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        bad += ((g[e] & 0xFFFFu) != (w[e] & 0xFFFFu));
+        bad += ((g[e] >> 16) != (w[e] >> 16));
+      }
+    } else {
+      *reinterpret_cast<uint4*>(a) = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+  }
+  if (VERIFY) {
+    for (int o = 16; o > 0; o >>= 1) bad += __shfl_xor_sync(0xffffffffu, bad, o);
+    if ((threadIdx.x & 31) == 0 && bad) atomicAdd(p.mismatches, bad);
+  }
+}
+
+template <typename K>
+int grid_for(int64_t work_units, int per_cta, int num_sms, int ctas_per_sm, int grid_cap) {
+  int64_t g = (work_units + per_cta - 1) / per_cta;
+  int64_t cap = int64_t(num_sms) * ctas_per_sm;
+  if (grid_cap > 0 && grid_cap < cap) cap = grid_cap;
+  if (g > cap) g = cap;
+  if (g < 1) g = 1;
+  return static_cast<int>(g);
+}
+
+}  // namespace
+
+int tma_smem_bytes(int piece, int stages) { return piece * stages + 8 * stages; }
+
+cudaError_t launch_swap_tma(const SwapParams& p, Dir dir, int num_sms, int grid_cap, cudaStream_t s,
+                            int* ctas_used) {
+  if (p.nitems == 0) return cudaSuccess;
+  // ~100 KiB of stages per CTA so that two CTAs share an SM.
+  int stages = (100 * 1024) / p.piece;
+  stages = std::max(2, std::min(stages, 32));
+  const int smem = tma_smem_bytes(p.piece, stages);
+  const int grid = grid_for<void>(p.nitems, 1, num_sms, 2, grid_cap);
+  cudaError_t e;
+  if (dir == kOut) {
+    e = cudaFuncSetAttribute(swap_tma_kernel<kOut>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    swap_tma_kernel<kOut><<<grid, 32, smem, s>>>(p, stages);
+  } else {
+    e = cudaFuncSetAttribute(swap_tma_kernel<kIn>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    swap_tma_kernel<kIn><<<grid, 32, smem, s>>>(p, stages);
+  }
+  if (ctas_used) *ctas_used = grid;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_swap_ldst(const SwapParams& p, Dir dir, int num_sms, int grid_cap, cudaStream_t s,
+                             int* ctas_used) {
+  if (p.nitems == 0) return cudaSuccess;
+  const int grid = grid_for<void>(p.nitems, 8, num_sms, 4, grid_cap);
+  if (dir == kOut)
+    swap_ldst_kernel<kOut, 8><<<grid, 256, 0, s>>>(p);
+  else
+    swap_ldst_kernel<kIn, 8><<<grid, 256, 0, s>>>(p);
+  if (ctas_used) *ctas_used = grid;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pattern_fill(const PatternParams& p, int num_sms, cudaStream_t s) {
+  const int64_t total = int64_t(p.D / 8) * p.H * (p.t1 - p.t0) * 2 * p.L;
+  if (total <= 0) return cudaSuccess;
+  const int grid = grid_for<void>(total, 256, num_sms, 8, 0);
+  pattern_kernel<false><<<grid, 256, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pattern_verify(const PatternParams& p, int num_sms, cudaStream_t s) {
+  const int64_t total = int64_t(p.D / 8) * p.H * p.t1 * 2 * p.L;
+  if (total <= 0) return cudaSuccess;
+  const int grid = grid_for<void>(total, 256, num_sms, 8, 0);
+  pattern_kernel<true><<<grid, 256, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
+}  // namespace aqua

@@ -1,0 +1,228 @@
+"""Host-logic parity on CPU: libaqua in AQUA_DRYRUN mode (bookkeeping and
+descriptors, no CUDA) and the native CFS scheduler against the oracle.
+
+Bit-exact (integers): ids, slots, locations, descriptors, error codes,
+plans and whole call logs must be identical."""
+import itertools
+import json
+import os
+import random
+
+import numpy as np
+import pytest
+
+from oracle import cfs as ocfs
+from oracle import kvpool as kp
+from oracle import sim as osim
+from paper_2407_21255_b200 import aqua
+from paper_2407_21255_b200.cfs import PHASE_DECODE, PHASE_PREFILL, POLICY_CFS, POLICY_FCFS, Scheduler
+from paper_2407_21255_b200.driver import run_trace
+from workloads import burst_trace
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+FAKE = 1 << 40
+
+
+def dry_ctx(L=2, bs=16, H=2, D=64, e=2, NB=40):
+    S = bs * H * D * e
+    ptrs = [FAKE + l * (1 << 32) for l in range(L)]
+    return aqua.Ctx(aqua.DRYRUN, L, bs, H, D, e, NB, ptrs)
+
+
+@pytest.mark.parametrize("variant", ["lender12", "lender8"])
+def test_c1_script_dryrun(variant):
+    g = json.load(open(os.path.join(GOLD, "c1_script.json")))
+    v = g[variant]
+    lay = g["layout"]
+    c = dry_ctx(**lay)
+    assert c.lend(0, FAKE * 2, v["lender_slots"] * c.U) == v["lender_slots"]
+    if v.get("host_slots"):
+        c.lend(aqua.HOST, FAKE * 3, v["host_slots"] * c.U)
+    for p in range(g["prompts"]):
+        assert c.alloc_blocks(p, g["blocks_per_prompt"]) == g["initial_ids"][str(p)]
+    c.swap_out(g["swap_out"])
+    b, s, l = c.last_descriptors()
+    want_b, want_s, want_l = [], [], []
+    for pid in g["swap_out"]:
+        loc, slots = v["placement"][str(pid)]
+        st, qloc, n, ids = c.query(pid, with_ids=True)
+        assert st == aqua.SWAPPED and ids == slots
+        assert qloc == {"peer": aqua.LOC_PEER, "host": aqua.LOC_HOST}[loc]
+        want_b += g["initial_ids"][str(pid)]
+        want_s += slots
+        want_l += [qloc] * len(slots)
+    assert (b, s, l) == (want_b, want_s, want_l)
+    assert c.alloc_blocks(g["filler"]["pid"], g["filler"]["n"]) == g["filler"]["expected_ids"]
+    new, _ = c.swap_in(g["swap_in"])
+    for pid, ids in zip(g["swap_in"], new):
+        assert ids == g["expected_swap_in_ids"][str(pid)]
+    c.free(g["filler"]["pid"])
+    assert c.counts()[0] == 40 - 32
+
+
+def _apply(pool, c, op):
+    """Run one op on the oracle and on the dry-run ctx; return both results."""
+    name, arg = op
+    res = []
+    for side in ("oracle", "lib"):
+        try:
+            if name == "alloc":
+                r = pool.alloc_blocks(*arg) if side == "oracle" else c.alloc_blocks(*arg)
+            elif name == "adopt":
+                r = pool.adopt_blocks(*arg) if side == "oracle" else c.adopt_blocks(*arg)
+            elif name == "out":
+                if side == "oracle":
+                    r = [(loc, s) for _, loc, s in pool.swap_out(arg)]
+                else:
+                    c.swap_out(arg)
+                    r = [(c.query(p)[1], c.query(p, with_ids=True)[3]) for p in arg]
+            elif name == "in":
+                r = pool.swap_in(arg) if side == "oracle" else c.swap_in(arg, cap=1 << 12)[0]
+            elif name == "free":
+                r = pool.free_prompt(arg) if side == "oracle" else c.free(arg)
+        except kp.AquaError as e:
+            r = ("err", e.code)
+        except aqua.AquaError as e:
+            r = ("err", e.code)
+        res.append(r)
+    return res
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_random_op_sequences_match_oracle(seed):
+    rnd = random.Random(seed)
+    NB = rnd.randint(1, 24)
+    lay = kp.Layout(L=1, bs=16, H=1, D=8, e=2, NB=NB)
+    pool = kp.Pool(lay)
+    c = aqua.Ctx(aqua.DRYRUN, 1, 16, 1, 8, 2, NB, [FAKE])
+    assert c.U == lay.U
+    peer = rnd.choice([0, 1, 3, 8, 16])
+    host = rnd.choice([0, 2, 8])
+    if peer:
+        pool.lend(kp.LOC_PEER, peer * lay.U)
+        c.lend(0, FAKE * 2, peer * lay.U)
+    if host:
+        pool.lend(kp.LOC_HOST, host * lay.U)
+        c.lend(aqua.HOST, FAKE * 3, host * lay.U)
+    pids = list(range(6))
+    for _ in range(60):
+        k = rnd.random()
+        if k < 0.3:
+            op = ("alloc", (rnd.choice(pids), rnd.randint(-1, 4)))
+        elif k < 0.4:
+            op = ("adopt", (rnd.choice(pids), [rnd.randint(-1, NB) for _ in range(rnd.randint(0, 3))]))
+        elif k < 0.6:
+            op = ("out", rnd.sample(pids, rnd.randint(0, 3)) + ([pids[0]] if rnd.random() < 0.05 else []))
+        elif k < 0.8:
+            op = ("in", rnd.sample(pids, rnd.randint(0, 3)))
+        else:
+            op = ("free", rnd.choice(pids))
+        a, b = _apply(pool, c, op)
+        assert a == b, (seed, op, a, b)
+        pool.check_invariants()
+        assert c.counts()[0] == len(pool.free)
+        for p, pr in pool.prompts.items():
+            st, loc, n, ids = c.query(p, with_ids=True)
+            assert (st, loc, ids) == (pr.state, pr.location, pr.blocks if pr.state == kp.RESIDENT else pr.slots)
+
+
+# ------------------------------------------------------------------ CFS
+def _grid():
+    return [(PHASE_PREFILL, 0, 0, 0), (PHASE_PREFILL, 20, 0, 20), (PHASE_PREFILL, 40, 0, 40),
+            (PHASE_DECODE, 50, 1, 50), (PHASE_DECODE, 50, 5, 54), (PHASE_DECODE, 50, 9, 58)]
+
+
+@pytest.mark.parametrize("NB", [2, 4, 7, 100])
+@pytest.mark.parametrize("b", [1, 3, 33, 512])
+def test_partition_matches_oracle_exhaustive(NB, b):
+    grid = _grid()
+    for n in (1, 2, 3):
+        for combo in itertools.product(range(len(grid)), repeat=n):
+            s = Scheduler(NB=NB, bs=16, b=b, cap=64)
+            rs = []
+            for i, gi in enumerate(combo):
+                ph, f, g, cx = grid[gi]
+                arr = float((i * 7) % 3)
+                s.add(i, arr, 50, 20)
+                s.set_state(i, ph, f, g, cx)
+                rs.append(ocfs.Req(id=i, arrival=arr, P=50, O=20, f=f, g=g, ctx=cx,
+                                   phase=ocfs.DECODE if ph == PHASE_DECODE else ocfs.PREFILL))
+            D, PF = s.partition()
+            oD, oPF = ocfs.plan(rs, b, NB, 16)
+            assert (D, [tuple(x) for x in PF]) == (oD, [tuple(x) for x in oPF]), combo
+            s.close()
+
+
+def test_partition_random_states_match_oracle():
+    rnd = random.Random(7)
+    for trial in range(400):
+        n = rnd.randint(1, 12)
+        NB = rnd.randint(1, 60)
+        b = rnd.choice([1, 8, 64, 512])
+        bs = rnd.choice([1, 4, 16])
+        s = Scheduler(NB=NB, bs=bs, b=b, cap=64)
+        rs = []
+        for i in range(n):
+            P = rnd.randint(1, 300)
+            O = rnd.randint(1, 50)
+            if rnd.random() < 0.5:
+                f = rnd.randint(0, P - 1)
+                ph, g, cx = PHASE_PREFILL, 0, f
+            else:
+                f, g = P, rnd.randint(1, O)
+                ph, cx = PHASE_DECODE, P + g - 1
+            arr = float(rnd.randint(0, 5))
+            s.add(i, arr, P, O)
+            s.set_state(i, ph, f, g, cx)
+            rs.append(ocfs.Req(id=i, arrival=arr, P=P, O=O, f=f, g=g, ctx=cx,
+                               phase=ocfs.DECODE if ph == PHASE_DECODE else ocfs.PREFILL))
+        D, PF = s.partition()
+        oD, oPF = ocfs.plan(rs, b, NB, bs)
+        assert (D, [tuple(x) for x in PF]) == (oD, [tuple(x) for x in oPF]), trial
+        s.close()
+
+
+def _product_log(trace, NB, lender_slots, host_slots, policy=POLICY_CFS, k=8, b=512, bs=16):
+    c = aqua.Ctx(aqua.DRYRUN, 1, bs, 1, 8, 2, NB, [FAKE])
+    if lender_slots:
+        c.lend(0, FAKE * 2, lender_slots * c.U)
+    if host_slots:
+        c.lend(aqua.HOST, FAKE * 3, host_slots * c.U)
+    s = Scheduler(NB=NB, bs=bs, b=b, k=k, policy=policy)
+    log, st = run_trace(trace, c, s)
+    return log, st
+
+
+@pytest.mark.parametrize("policy", ["cfs", "fcfs"])
+@pytest.mark.parametrize("k", [1, 8])
+def test_small_trace_call_log_matches_oracle(policy, k):
+    tr = burst_trace(seed=3, burst_s=8.0, tail_s=3.0, prompt=(300, 0.8, 1, 900), output=(40, 0.7, 1, 200))
+    NB = 120
+    o = osim.run(tr, osim.SimConfig(NB=NB, k=k, policy=policy, lender_slots=200, host_slots=400))
+    log, st = _product_log(tr, NB, 200, 400, policy=POLICY_CFS if policy == "cfs" else POLICY_FCFS, k=k)
+    assert st["iters"] == o.iters
+    assert len(log) == len(o.log)
+    for a, b in zip(log, o.log):
+        assert a == b
+    if policy == "cfs":
+        assert o.blocks_out > 0 and st["blocks_out"] == o.blocks_out
+
+
+def test_lender_overflow_falls_back_to_host_in_trace():
+    tr = burst_trace(seed=5, burst_s=8.0, tail_s=3.0, prompt=(300, 0.8, 1, 900), output=(40, 0.7, 1, 200))
+    o = osim.run(tr, osim.SimConfig(NB=100, lender_slots=30, host_slots=1000))
+    log, _ = _product_log(tr, 100, 30, 1000)
+    assert log == o.log
+    locs = {loc for e in o.log if e[0] == "swap_out" for loc, _ in e[2]}
+    assert locs == {kp.LOC_PEER, kp.LOC_HOST}
+
+
+def test_full_c3_trace_call_log_matches_oracle():
+    """BASELINE configs[2] at full size, metadata mode (seed 1): the native
+    scheduler + libaqua bookkeeping reproduce the oracle's call log."""
+    tr = burst_trace(seed=1)
+    NB = 4152                       # scripts/c3_nb.py (oracle FCFS pre-burst peak x 1.2)
+    o = osim.run(tr, osim.SimConfig(NB=NB, lender_slots=32768, host_slots=32768))
+    log, st = _product_log(tr, NB, 32768, 32768)
+    assert st["iters"] == o.iters and st["blocks_out"] == o.blocks_out
+    assert log == o.log
