@@ -223,6 +223,11 @@ AQUA_API aqua_status aqua_launch_count(aqua_ctx* ctx, uint64_t* launches);
 AQUA_API aqua_status aqua_ipc_export(void* dev_ptr, uint8_t handle[64]);
 AQUA_API aqua_status aqua_ipc_import(int device, const uint8_t handle[64], void** out_ptr);
 AQUA_API aqua_status aqua_ipc_close(int device, void* ptr);
+/* A dedicated cudaMalloc on `device` (its own allocation, so an exported
+ * handle maps to offset 0) for memory a producer offers to a consumer
+ * process; freed with aqua_ipc_free after every importer has closed it. */
+AQUA_API aqua_status aqua_ipc_alloc(int device, uint64_t bytes, void** out_ptr);
+AQUA_API aqua_status aqua_ipc_free(int device, void* ptr);
 /* 1 if `device` can access `peer` by P2P (cudaDeviceCanAccessPeer). */
 AQUA_API aqua_status aqua_can_access_peer(int device, int peer, int32_t* can);
 

@@ -33,7 +33,7 @@ SYMBOLS = [
     "aqua_swap_out", "aqua_swap_in", "aqua_free", "aqua_wait", "aqua_sync", "aqua_ticket_done",
     "aqua_query", "aqua_counts", "aqua_arena_base", "aqua_set_option", "aqua_get_option",
     "aqua_last_descriptors", "aqua_launch_count", "aqua_ipc_export", "aqua_ipc_import",
-    "aqua_ipc_close", "aqua_can_access_peer", "aqua_kv_fill_pattern", "aqua_kv_verify_pattern",
+    "aqua_ipc_close", "aqua_ipc_alloc", "aqua_ipc_free", "aqua_can_access_peer", "aqua_kv_fill_pattern", "aqua_kv_verify_pattern",
     "aqua_strerror", "aqua_last_error", "aqua_version",
 ]
 
@@ -79,6 +79,8 @@ def _load() -> C.CDLL:
         "aqua_ipc_export": (C.c_int, [VP, P(C.c_uint8)]),
         "aqua_ipc_import": (C.c_int, [C.c_int, P(C.c_uint8), P(VP)]),
         "aqua_ipc_close": (C.c_int, [C.c_int, VP]),
+        "aqua_ipc_alloc": (C.c_int, [C.c_int, U64, P(VP)]),
+        "aqua_ipc_free": (C.c_int, [C.c_int, VP]),
         "aqua_can_access_peer": (C.c_int, [C.c_int, C.c_int, P(I32)]),
         "aqua_kv_fill_pattern": (C.c_int, [VP, U64, I32, I32, U64, VP]),
         "aqua_kv_verify_pattern": (C.c_int, [VP, U64, I32, U64, VP, VP]),
@@ -253,6 +255,16 @@ def ipc_import(device: int, handle: bytes) -> int:
 
 def ipc_close(device: int, ptr: int) -> None:
     _check(lib.aqua_ipc_close(device, C.c_void_p(ptr)))
+
+
+def ipc_alloc(device: int, nbytes: int) -> int:
+    p = C.c_void_p()
+    _check(lib.aqua_ipc_alloc(device, nbytes, C.byref(p)))
+    return p.value
+
+
+def ipc_free(device: int, ptr: int) -> None:
+    _check(lib.aqua_ipc_free(device, C.c_void_p(ptr)))
 
 
 def can_access_peer(device: int, peer: int) -> bool:

@@ -938,6 +938,27 @@ aqua_status aqua_ipc_close(int device, void* ptr) {
   return AQUA_OK;
 }
 
+aqua_status aqua_ipc_alloc(int device, uint64_t bytes, void** out) {
+  if (!out || !bytes) return fail(nullptr, AQUA_E_INVAL, "null out or zero bytes");
+  DevGuard g(device);
+  cudaError_t e = cudaMalloc(out, bytes);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(nullptr, AQUA_E_CUDA, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+  }
+  return AQUA_OK;
+}
+
+aqua_status aqua_ipc_free(int device, void* ptr) {
+  DevGuard g(device);
+  cudaError_t e = cudaFree(ptr);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(nullptr, AQUA_E_CUDA, std::string("cudaFree: ") + cudaGetErrorString(e));
+  }
+  return AQUA_OK;
+}
+
 aqua_status aqua_can_access_peer(int device, int peer, int32_t* can) {
   if (!can) return fail(nullptr, AQUA_E_INVAL, "null argument");
   int v = 0;

@@ -1,0 +1,248 @@
+"""GPU parity (-m gpu): libaqua's sm_100a kernels against the CPU oracle,
+byte for byte (tolerance 0), through the C ABI.
+
+Whole-buffer comparison (pool, GPU lender arena, host arena) after every
+call for C1 (BASELINE configs[0]) and randomised op sequences at sizes that
+span several TMA stages and a ragged tail; the full-size C2 configuration is
+checked on sampled chunks against the oracle's closed-form pattern words and
+by the any-size restore property (pattern verify kernel)."""
+import json
+import os
+import random
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import kvpool as kp
+from oracle import pattern as opat
+from paper_2407_21255_b200 import aqua
+from workloads import block_permutation
+
+from gpu_util import Rig
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+ENGINES = {"tma": aqua.KERNEL_TMA, "ldst": aqua.KERNEL_LDST, "per_chunk": aqua.BASE_PER_CHUNK,
+           "gather_temp": aqua.BASE_GATHER_TEMP, "batch": aqua.BASE_BATCH}
+
+
+def _ops(rig, ops, stream=0):
+    """Apply ops to both sides and compare everything after each."""
+    c, o = rig.ctx, rig.opool
+    for name, arg in ops:
+        if name == "alloc":
+            assert c.alloc_blocks(*arg, stream=stream) == o.alloc_blocks(*arg)
+        elif name == "adopt":
+            c.adopt_blocks(*arg, stream=stream)
+            o.adopt_blocks(*arg)
+        elif name == "out":
+            c.swap_out(arg, stream)
+            res = o.swap_out(arg)
+            for pid, loc, slots in res:
+                assert c.query(pid, with_ids=True)[1:] == (loc, len(slots), slots)
+        elif name == "in":
+            new, _ = c.swap_in(arg, stream)
+            assert new == o.swap_in(arg)
+        elif name == "free":
+            c.free(arg, stream)
+            o.free_prompt(arg)
+        rig.assert_bytes_equal(f"after {name} {arg}")
+
+
+@pytest.mark.parametrize("engine", list(ENGINES))
+@pytest.mark.parametrize("variant", ["lender12", "lender8"])
+def test_c1_bytes(engine, variant):
+    g = json.load(open(os.path.join(GOLD, "c1_script.json")))
+    v = g[variant]
+    rig = Rig(**g["layout"], lender_slots=v["lender_slots"], host_slots=v.get("host_slots", 0))
+    rig.ctx.set_option(aqua.OPT_KERNEL, ENGINES[engine])
+    s = torch.cuda.Stream()
+    ops = [("alloc", (p, 4)) for p in range(8)]
+    ops += [("out", g["swap_out"]), ("alloc", (100, 6)), ("in", g["swap_in"]), ("free", 100)]
+    _ops(rig, ops, stream=s.cuda_stream if engine != "tma" else 0)
+    for pid, ids in g["expected_swap_in_ids"].items():
+        assert rig.ctx.query(int(pid), with_ids=True)[3] == ids
+
+
+SHAPES = {
+    # (L, bs, H, D): S bytes -> TMA pieces at the default 16 KiB piece
+    "tiny_256B": (1, 16, 1, 8),          # S = 256 B (one small piece)
+    "ragged_10KiB": (3, 16, 5, 64),      # S = 10 KiB: TMA pieces 4K, 4K, 2K (piece option 4096)
+    "llama_bs32": (4, 32, 8, 128),       # S = 64 KiB (4 pieces)
+    "odd_48KiB": (2, 16, 12, 128),       # S = 48 KiB (3 pieces)
+    "c4_shape": (5, 16, 2, 128),         # S = 8 KiB (Llama-70B TP4 chunk)
+}
+
+
+@pytest.mark.parametrize("shape", list(SHAPES))
+@pytest.mark.parametrize("engine", ["tma", "ldst"])
+@pytest.mark.parametrize("seed", [0, 1])
+def test_random_sequences_bytes(shape, engine, seed):
+    L, bs, H, D = SHAPES[shape]
+    rnd = random.Random(seed * 31 + len(shape))
+    NB = 24
+    rig = Rig(L=L, bs=bs, H=H, D=D, e=2, NB=NB, lender_slots=10, host_slots=8, seed=seed)
+    rig.ctx.set_option(aqua.OPT_KERNEL, ENGINES[engine])
+    if engine == "tma" and shape == "ragged_10KiB":
+        rig.ctx.set_option(aqua.OPT_TMA_PIECE, 4096)     # S = 10 KiB -> pieces 4K, 4K, 2K
+    pids = list(range(5))
+    ops = []
+    state = {}
+    for _ in range(25):
+        k = rnd.random()
+        p = rnd.choice(pids)
+        if k < 0.35:
+            ops.append(("alloc", (p, rnd.randint(0, 4))))
+        elif k < 0.6:
+            ops.append(("out", rnd.sample(pids, rnd.randint(1, 3))))
+        elif k < 0.85:
+            ops.append(("in", rnd.sample(pids, rnd.randint(1, 3))))
+        else:
+            ops.append(("free", p))
+    c, o = rig.ctx, rig.opool
+    for op in ops:
+        try:
+            _ops(rig, [op])
+        except (kp.AquaError, aqua.AquaError) as e:
+            # errors must agree and change nothing on either side
+            code_o = code_c = None
+            name, arg = op
+            try:
+                {"alloc": lambda: o.alloc_blocks(*arg), "out": lambda: o.swap_out(arg),
+                 "in": lambda: o.swap_in(arg), "free": lambda: o.free_prompt(arg)}[name]()
+            except kp.AquaError as eo:
+                code_o = eo.code
+            try:
+                {"alloc": lambda: c.alloc_blocks(*arg), "out": lambda: c.swap_out(arg),
+                 "in": lambda: c.swap_in(arg, cap=4096), "free": lambda: c.free(arg)}[name]()
+            except aqua.AquaError as ec:
+                code_c = ec.code
+            assert code_o is not None and code_o == code_c == e.code, (op, code_o, code_c)
+            rig.assert_bytes_equal(f"after failed {op}")
+
+
+def test_block_major_layout_bytes():
+    L, bs, H, D, NB = 3, 16, 2, 64, 12
+    S = bs * H * D * 2
+    rig = Rig(L=L, bs=bs, H=H, D=D, NB=NB, lender_slots=6, host_slots=6, kv_plane_stride=S, block_stride=2 * S)
+    _ops(rig, [("adopt", (1, [5, 0, 3])), ("alloc", (2, 4)), ("out", [1, 2]), ("alloc", (3, 2)), ("in", [2, 1])])
+
+
+def test_adversarial_reuse_on_other_streams():
+    """R7: freed blocks / slots are handed out again at once and overwritten
+    on another stream while the swap that read them may still be in flight;
+    the library's stream waits keep the result equal to sequential
+    execution."""
+    L, bs, H, D, NB = 4, 16, 8, 128, 64          # S = 32 KiB, U = 256 KiB
+    rig = Rig(L=L, bs=bs, H=H, D=D, NB=NB, lender_slots=32, host_slots=0)
+    c, o = rig.ctx, rig.opool
+    s_swap, s_dec = torch.cuda.Stream(), torch.cuda.Stream()
+    for p in range(4):
+        assert c.alloc_blocks(p, 16, s_dec.cuda_stream) == o.alloc_blocks(p, 16)
+    torch.cuda.synchronize()
+    for rnd in range(6):
+        # big swap out on s_swap ...
+        s_swap.wait_stream(s_dec)
+        c.swap_out([0, 1], s_swap.cuda_stream)
+        o.swap_out([0, 1])
+        # ... its blocks are immediately reallocated and scribbled on s_dec
+        ids = c.alloc_blocks(10 + rnd, 32, s_dec.cuda_stream)
+        assert ids == o.alloc_blocks(10 + rnd, 32)
+        with torch.cuda.stream(s_dec):
+            val = (rnd * 37 + 11) % 256
+            for b in ids:
+                for l in range(L):
+                    for kv in (0, 1):
+                        off = kv * rig.lay.P_kv + b * rig.lay.P_b
+                        rig.layers[l][off:off + rig.lay.S].fill_(val)
+                        o.chunk(l, kv, b)[:] = val
+        c.free(10 + rnd, s_dec.cuda_stream)
+        o.free_prompt(10 + rnd)
+        # swap back in on the swap stream (must wait for the scribbles that
+        # last touched the reused blocks), then its slots are reused by a
+        # swap_out on the decode stream
+        new, t = c.swap_in([1, 0], s_swap.cuda_stream)
+        assert new == o.swap_in([1, 0])
+        c.swap_out([2], s_dec.cuda_stream)
+        o.swap_out([2])
+        new, t2 = c.swap_in([2], s_swap.cuda_stream)
+        assert new == o.swap_in([2])
+    rig.assert_bytes_equal("adversarial")
+
+
+def test_c2_full_size_sampled_and_restore():
+    """BASELINE configs[1] in the bench's launch configuration: one 32K-token
+    Llama-3-8B prompt (2048 blocks of U = 2 MiB) on a fragmented block table
+    (seeded permutation of 4096), self-lender arena 4 GiB; plus the host arena
+    for a second prompt.  Sampled chunks are compared with the oracle's
+    closed-form words; the whole prompt with the pattern verify kernel."""
+    L, bs, H, D, NB = 32, 16, 8, 128, 4096
+    S = bs * H * D * 2
+    lay = kp.Layout(L=L, bs=bs, H=H, D=D, e=2, NB=NB)
+    dev = torch.device("cuda", 0)
+    layers = [torch.zeros(lay.layer_bytes, dtype=torch.uint8, device=dev) for _ in range(L)]
+    arena = torch.zeros(2048 * lay.U, dtype=torch.uint8, device=dev)
+    c = aqua.Ctx(0, L, bs, H, D, 2, NB, [t.data_ptr() for t in layers])
+    c.lend(0, arena.data_ptr(), 2048 * lay.U)
+    c.lend(aqua.HOST, 0, 64 * lay.U)                      # library-owned pinned arena
+    bt = block_permutation(NB, 2048, seed=2).tolist()
+    c.adopt_blocks(7, bt)
+    ntok, seed = 32768, 1234
+    c.kv_fill_pattern(7, 0, ntok, seed)
+    c.alloc_blocks(8, 64)
+    c.kv_fill_pattern(8, 0, 64 * bs, seed)
+    cnt = torch.zeros(1, dtype=torch.int64, device=dev)
+    c.swap_out([7, 8])
+    assert c.query(7)[1] == aqua.LOC_PEER and c.query(8)[1] == aqua.LOC_HOST
+    slots = c.query(7, with_ids=True)[3]
+    assert slots == list(range(2048))
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(0)
+    img = arena.view(2048, L, 2, bs, H, D * 2)
+    for _ in range(24):   # sampled chunks vs the oracle's words, token by token
+        j = int(rng.integers(0, 2048))
+        l = int(rng.integers(0, L))
+        kv = int(rng.integers(0, 2))
+        i = int(rng.integers(0, bs))
+        t = j * bs + i
+        want = opat.token_words(seed, 7, t, l, kv, H, D).reshape(-1).view(np.uint8).reshape(H, D * 2)
+        assert np.array_equal(img[slots[j], l, kv, i].cpu().numpy(), want)
+    # scribble over the freed pool, then resume into fresh blocks
+    for t_ in layers:
+        t_.fill_(0xA5)
+    new, tk = c.swap_in([8, 7])
+    assert new[0] == list(range(64)) and new[1] == list(range(64, 2112))
+    c.kv_verify_pattern(7, ntok, seed, cnt.data_ptr())
+    c.kv_verify_pattern(8, 64 * bs, seed, cnt.data_ptr())
+    torch.cuda.synchronize()
+    assert int(cnt.item()) == 0
+    # a wrong seed is detected (the verifier is live)
+    c.kv_verify_pattern(7, 16, seed + 1, cnt.data_ptr())
+    torch.cuda.synchronize()
+    assert int(cnt.item()) > 0
+
+
+def test_pattern_kernel_matches_oracle_words():
+    rig = Rig(L=2, bs=16, H=2, D=64, NB=8, lender_slots=0)
+    rig.ctx.adopt_blocks(3, [6, 2])
+    rig.opool.adopt_blocks(3, [6, 2])
+    rig.ctx.kv_fill_pattern(3, 5, 27, 99)
+    opat.write_tokens(rig.opool, 3, 5, 27, 99)
+    rig.assert_bytes_equal("pattern")
+
+
+def test_errors_leave_state_unchanged_and_no_cpu_fallback():
+    rig = Rig(L=2, bs=16, H=2, D=64, NB=8, lender_slots=2)
+    c = rig.ctx
+    c.alloc_blocks(1, 3)
+    with pytest.raises(aqua.AquaError) as e:
+        c.swap_out([1])                       # 3 blocks, lender has 2 slots, no host
+    assert e.value.code == aqua.E_NOSPACE
+    assert c.query(1)[0] == aqua.RESIDENT
+    rig.opool.alloc_blocks(1, 3)
+    rig.assert_bytes_equal("after NOSPACE")
+    n0 = c.launch_count()
+    c.alloc_blocks(2, 1)
+    c.swap_out([2])
+    assert c.launch_count() == n0 + 1         # the copy ran as one of our kernels
