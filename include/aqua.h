@@ -112,7 +112,8 @@ enum {
 enum {
   AQUA_OPT_KERNEL = 1,        /* one of AQUA_KERNEL_* / AQUA_BASE_* */
   AQUA_OPT_MAX_CTAS = 2,      /* cap on CTAs per swap launch (0 = all SMs); SMs left for decode */
-  AQUA_OPT_TMA_PIECE = 3      /* bytes per TMA stage (multiple of 16, <= 65536; 0 = auto) */
+  AQUA_OPT_TMA_PIECE = 3,     /* bytes per TMA stage (multiple of 16, <= 65536; 0 = auto: 32 KiB) */
+  AQUA_OPT_TMA_STAGES = 4     /* TMA ring depth (2..32; 0 = auto: ~200 KiB of smem per CTA, 1 CTA/SM) */
 };
 
 typedef struct aqua_ctx aqua_ctx;   /* one per borrower device (per TP rank) */

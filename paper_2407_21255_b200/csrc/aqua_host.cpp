@@ -72,6 +72,7 @@ struct aqua_ctx {
   int kernel = AQUA_KERNEL_AUTO;
   int max_ctas = 0;
   int tma_piece = 0;
+  int tma_stages = 0;
   int num_sms = 148;
   uint64_t* d_layer_base = nullptr;
   // pinned -> device descriptor staging ring
@@ -253,20 +254,25 @@ aqua_status run_copy(aqua_ctx* c, const std::vector<Desc>& ds, aqua::Dir dir, cu
   };
 
   if (engine == AQUA_KERNEL_TMA || engine == AQUA_KERNEL_LDST) {
-    void* dd;
-    aqua_status s = stage_upload(c, ds.data(), ds.size() * sizeof(Desc), st, &dd);
-    if (s) return s;
-    *regions = 1;
-    p.desc = static_cast<const Desc*>(dd);
+    if (ds.size() <= static_cast<size_t>(aqua::kInlineDesc)) {
+      p.desc = nullptr;                       // descriptors ride in the kernel parameters
+      std::copy(ds.begin(), ds.end(), p.inl);
+    } else {
+      void* dd;
+      aqua_status s = stage_upload(c, ds.data(), ds.size() * sizeof(Desc), st, &dd);
+      if (s) return s;
+      *regions = 1;
+      p.desc = static_cast<const Desc*>(dd);
+    }
     int ctas = 0;
     cudaError_t e;
     if (engine == AQUA_KERNEL_TMA) {
-      int piece = c->tma_piece > 0 ? c->tma_piece : 16384;
+      int piece = c->tma_piece > 0 ? c->tma_piece : 32768;
       if (piece > c->S) piece = static_cast<int>(c->S);
       p.piece = piece;
       p.npieces = static_cast<int32_t>((c->S + piece - 1) / piece);
       p.nitems = p.ndesc * 2 * p.L * p.npieces;
-      e = aqua::launch_swap_tma(p, dir, c->num_sms, c->max_ctas, st, &ctas);
+      e = aqua::launch_swap_tma(p, dir, c->num_sms, c->max_ctas, c->tma_stages, st, &ctas);
     } else {
       p.piece = 4096;
       p.npieces = static_cast<int32_t>((c->S + 4095) / 4096);
@@ -868,6 +874,10 @@ aqua_status aqua_set_option(aqua_ctx* c, int32_t opt, int64_t v) {
       if (v < 0 || v > 65536 || v % 16) return fail(c, AQUA_E_INVAL, "tma piece");
       c->tma_piece = static_cast<int>(v);
       return AQUA_OK;
+    case AQUA_OPT_TMA_STAGES:
+      if (v < 0 || v > 32 || v == 1) return fail(c, AQUA_E_INVAL, "tma stages");
+      c->tma_stages = static_cast<int>(v);
+      return AQUA_OK;
   }
   return fail(c, AQUA_E_INVAL, "unknown option");
 }
@@ -878,6 +888,7 @@ aqua_status aqua_get_option(aqua_ctx* c, int32_t opt, int64_t* v) {
     case AQUA_OPT_KERNEL: *v = c->kernel; return AQUA_OK;
     case AQUA_OPT_MAX_CTAS: *v = c->max_ctas; return AQUA_OK;
     case AQUA_OPT_TMA_PIECE: *v = c->tma_piece; return AQUA_OK;
+    case AQUA_OPT_TMA_STAGES: *v = c->tma_stages; return AQUA_OK;
   }
   return fail(c, AQUA_E_INVAL, "unknown option");
 }

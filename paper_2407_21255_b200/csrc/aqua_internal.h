@@ -16,8 +16,12 @@ constexpr uint32_t kArenaBit = 0x80000000u;
 
 enum Dir : int { kOut = 0, kIn = 1 };   // swap_out: pool -> arena; swap_in: arena -> pool
 
+// Calls with at most kInlineDesc descriptors pass them inside the kernel
+// parameters (__grid_constant__): no staging copy on the critical path.
+constexpr int kInlineDesc = 256;
+
 struct SwapParams {
-  const Desc* desc;            // device array [ndesc]
+  const Desc* desc;            // device array [ndesc], or nullptr -> use inl
   const uint64_t* layer_base;  // device array [L]
   uint64_t arena_base[2];      // device-visible bases: [0] GPU lender, [1] host
   int64_t ndesc;
@@ -27,6 +31,7 @@ struct SwapParams {
   int32_t pad_;
   int64_t S, U, P_kv, P_b;
   int64_t nitems;              // ndesc * 2L * npieces
+  Desc inl[kInlineDesc];       // inline descriptors when desc == nullptr
 };
 
 struct PatternParams {
@@ -41,7 +46,7 @@ struct PatternParams {
 
 // Launchers: return the CUDA error of the launch (cudaSuccess on success).
 // grid_cap = max CTAs (0 = derived from the SM count).
-cudaError_t launch_swap_tma(const SwapParams& p, Dir dir, int num_sms, int grid_cap,
+cudaError_t launch_swap_tma(const SwapParams& p, Dir dir, int num_sms, int grid_cap, int stages,
                             cudaStream_t s, int* ctas_used);
 cudaError_t launch_swap_ldst(const SwapParams& p, Dir dir, int num_sms, int grid_cap,
                              cudaStream_t s, int* ctas_used);

@@ -110,6 +110,10 @@ struct Cursor {
   }
 };
 
+__device__ __forceinline__ Desc desc_at(const SwapParams& p, int64_t j) {
+  return p.desc ? p.desc[j] : p.inl[j];
+}
+
 // chunk(l, kv, b) = layer_base[l] + kv*P_kv + b*P_b            (R1)
 // image chunk    = arena + slot*U + (2l+kv)*S                   (R3)
 template <Dir D>
@@ -141,7 +145,7 @@ __device__ __forceinline__ void item_addrs(const SwapParams& p, const Desc d, in
 // contiguous range of items, so its stores form one long contiguous run in
 // the image (swap_out) / its loads do (swap_in).
 template <Dir D>
-__global__ void __launch_bounds__(32) swap_tma_kernel(const SwapParams p, const int stages) {
+__global__ void __launch_bounds__(32) swap_tma_kernel(const __grid_constant__ SwapParams p, const int stages) {
   extern __shared__ __align__(128) uint8_t smem[];
   if (threadIdx.x != 0) return;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + size_t(stages) * p.piece);
@@ -162,7 +166,7 @@ __global__ void __launch_bounds__(32) swap_tma_kernel(const SwapParams p, const 
     const uint8_t* src;
     uint8_t* dst;
     uint32_t bytes;
-    item_addrs<D>(p, p.desc[lc.j], lc.c, lc.q, src, dst, bytes);
+    item_addrs<D>(p, desc_at(p, lc.j), lc.c, lc.q, src, dst, bytes);
     uint8_t* buf = smem + size_t(lstage) * p.piece;
     mbar_expect_tx(&bars[lstage], bytes);
     bulk_g2s(buf, src, bytes, &bars[lstage], pol);
@@ -180,7 +184,7 @@ __global__ void __launch_bounds__(32) swap_tma_kernel(const SwapParams p, const 
     const uint8_t* src;
     uint8_t* dst;
     uint32_t bytes;
-    item_addrs<D>(p, p.desc[sc.j], sc.c, sc.q, src, dst, bytes);
+    item_addrs<D>(p, desc_at(p, sc.j), sc.c, sc.q, src, dst, bytes);
     bulk_s2g(dst, smem + size_t(sstage) * p.piece, bytes, pol);
     bulk_commit();
     sc.next(p);
@@ -200,7 +204,7 @@ __global__ void __launch_bounds__(32) swap_tma_kernel(const SwapParams p, const 
 // Grid-stride over items of up to 512*UNROLL bytes; a warp moves one item
 // with UNROLL independent 16-byte loads per lane in flight.
 template <Dir D, int UNROLL>
-__global__ void __launch_bounds__(256) swap_ldst_kernel(const SwapParams p) {
+__global__ void __launch_bounds__(256) swap_ldst_kernel(const __grid_constant__ SwapParams p) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
@@ -210,7 +214,7 @@ __global__ void __launch_bounds__(256) swap_ldst_kernel(const SwapParams p) {
     const uint8_t* src;
     uint8_t* dst;
     uint32_t bytes;
-    item_addrs<D>(p, p.desc[cu.j], cu.c, cu.q, src, dst, bytes);
+    item_addrs<D>(p, desc_at(p, cu.j), cu.c, cu.q, src, dst, bytes);
     const int nvec = static_cast<int>(bytes >> 4);
     int4 v[UNROLL];
 #pragma unroll
@@ -301,24 +305,31 @@ int grid_for(int64_t work_units, int per_cta, int num_sms, int ctas_per_sm, int 
 
 int tma_smem_bytes(int piece, int stages) { return piece * stages + 8 * stages; }
 
-cudaError_t launch_swap_tma(const SwapParams& p, Dir dir, int num_sms, int grid_cap, cudaStream_t s,
-                            int* ctas_used) {
+cudaError_t launch_swap_tma(const SwapParams& p, Dir dir, int num_sms, int grid_cap, int stages_opt,
+                            cudaStream_t s, int* ctas_used) {
   if (p.nitems == 0) return cudaSuccess;
-  // ~100 KiB of stages per CTA so that two CTAs share an SM.
-  int stages = (100 * 1024) / p.piece;
+  // One CTA per SM (measured best on B200: r01 sweep), ~200 KiB of stages.
+  int stages = stages_opt > 0 ? stages_opt : (200 * 1024) / p.piece;
   stages = std::max(2, std::min(stages, 32));
+  while (stages > 2 && tma_smem_bytes(p.piece, stages) > 227 * 1024) --stages;
   const int smem = tma_smem_bytes(p.piece, stages);
-  const int grid = grid_for<void>(p.nitems, 1, num_sms, 2, grid_cap);
-  cudaError_t e;
-  if (dir == kOut) {
-    e = cudaFuncSetAttribute(swap_tma_kernel<kOut>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  const int grid = grid_for<void>(p.nitems, 1, num_sms, 1, grid_cap);
+  // the opt-in smem attribute is per device; remember the largest set so far
+  static thread_local int set_smem[2][64] = {};
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  int& have = set_smem[dir][dev & 63];
+  if (smem > have) {
+    e = cudaFuncSetAttribute(dir == kOut ? swap_tma_kernel<kOut> : swap_tma_kernel<kIn>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e != cudaSuccess) return e;
-    swap_tma_kernel<kOut><<<grid, 32, smem, s>>>(p, stages);
-  } else {
-    e = cudaFuncSetAttribute(swap_tma_kernel<kIn>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    swap_tma_kernel<kIn><<<grid, 32, smem, s>>>(p, stages);
+    have = 227 * 1024;
   }
+  if (dir == kOut)
+    swap_tma_kernel<kOut><<<grid, 32, smem, s>>>(p, stages);
+  else
+    swap_tma_kernel<kIn><<<grid, 32, smem, s>>>(p, stages);
   if (ctas_used) *ctas_used = grid;
   return cudaGetLastError();
 }

@@ -1,0 +1,109 @@
+"""Engine / launch-shape sweep and the C5 bandwidth sweep on one GPU
+(self-lender: arena in the same HBM, or the pinned host arena).
+
+    python scripts/sweep.py engines   -> per (engine, piece, max_ctas): swap_out / swap_in GB/s for C2
+    python scripts/sweep.py c5        -> block size 8..128 x blocks per launch 1..1024 (BASELINE configs[4])
+
+Prints one JSON object per line; the oracle's bwfit is NOT used here (fits
+are done in tests/analysis with oracle.bwfit).
+"""
+import json
+import os
+import statistics
+import sys
+
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from paper_2407_21255_b200 import aqua  # noqa: E402
+from workloads import block_permutation  # noqa: E402
+
+ENG = {"tma": aqua.KERNEL_TMA, "ldst": aqua.KERNEL_LDST, "gather_temp": aqua.BASE_GATHER_TEMP,
+       "batch": aqua.BASE_BATCH, "per_chunk": aqua.BASE_PER_CHUNK}
+
+
+def setup(L, bs, H, D, NB, nblk, host=False):
+    S = bs * H * D * 2
+    U = 2 * L * S
+    layers = [torch.zeros(2 * NB * S, dtype=torch.uint8, device="cuda") for _ in range(L)]
+    ctx = aqua.Ctx(0, L, bs, H, D, 2, NB, [t.data_ptr() for t in layers])
+    arena = None
+    if host:
+        ctx.lend(aqua.HOST, 0, nblk * U)
+    else:
+        arena = torch.empty(nblk * U, dtype=torch.uint8, device="cuda")
+        ctx.lend(0, arena.data_ptr(), nblk * U)
+    perm = block_permutation(NB, NB, seed=2).tolist()
+    ctx.adopt_blocks(1, perm[nblk:])
+    ctx.adopt_blocks(7, perm[:nblk])
+    return ctx, layers, arena, U
+
+
+def time_swaps(ctx, reps, stream):
+    outs, ins = [], []
+    for _ in range(2):
+        ctx.swap_out([7], stream.cuda_stream)
+        ctx.swap_in([7], stream.cuda_stream)
+    torch.cuda.synchronize()
+    for _ in range(reps):
+        a, b, c = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        a.record(stream)
+        ctx.swap_out([7], stream.cuda_stream)
+        b.record(stream)
+        ctx.swap_in([7], stream.cuda_stream)
+        c.record(stream)
+        torch.cuda.synchronize()
+        outs.append(a.elapsed_time(b))
+        ins.append(b.elapsed_time(c))
+    return statistics.median(outs), statistics.median(ins)
+
+
+def engines():
+    L, bs, H, D, NB, nblk = 32, 16, 8, 128, 4096, 2048
+    ctx, layers, arena, U = setup(L, bs, H, D, NB, nblk)
+    s = torch.cuda.Stream()
+    nbytes = nblk * U
+    grid = [("tma", p, c) for p in (4096, 8192, 16384, 32768) for c in (0, 148, 296, 444)]
+    grid += [("ldst", 0, c) for c in (0, 148, 296, 592)]
+    grid += [("gather_temp", 0, 0), ("batch", 0, 0)]
+    for eng, piece, ctas in grid:
+        ctx.set_option(aqua.OPT_KERNEL, ENG[eng])
+        ctx.set_option(aqua.OPT_TMA_PIECE, piece)
+        ctx.set_option(aqua.OPT_MAX_CTAS, ctas)
+        o, i = time_swaps(ctx, 10, s)
+        print(json.dumps({"engine": eng, "piece": piece, "max_ctas": ctas, "out_ms": round(o, 4),
+                          "in_ms": round(i, 4), "out_hbm_GBps": round(2 * nbytes / o / 1e6, 1),
+                          "in_hbm_GBps": round(2 * nbytes / i / 1e6, 1)}), flush=True)
+
+
+def c5(host=False):
+    L, H, D = 32, 8, 128
+    for bs in (8, 16, 32, 64, 128):
+        S = bs * H * D * 2
+        U = 2 * L * S
+        for nblk in (1, 2, 4, 8, 16, 32, 64, 128, 256, 512, 1024):
+            if nblk * U > (16 << 30) or (host and nblk * U > (4 << 30)):
+                continue
+            NB = 2 * nblk
+            ctx, layers, arena, _ = setup(L, bs, H, D, NB, nblk, host=host)
+            s = torch.cuda.Stream()
+            reps = 20 if nblk * U < (1 << 30) else 5
+            o, i = time_swaps(ctx, reps, s)
+            print(json.dumps({"c5": "host" if host else "self", "bs": bs, "U": U, "blocks": nblk,
+                              "bytes": nblk * U, "out_ms": round(o, 5), "in_ms": round(i, 5),
+                              "out_GBps": round(nblk * U / o / 1e6, 2), "in_GBps": round(nblk * U / i / 1e6, 2)}),
+                  flush=True)
+            ctx.close()
+            del layers, arena
+            torch.cuda.empty_cache()
+
+
+if __name__ == "__main__":
+    what = sys.argv[1] if len(sys.argv) > 1 else "engines"
+    if what == "engines":
+        engines()
+    elif what == "c5":
+        c5(host=False)
+    elif what == "c5host":
+        c5(host=True)

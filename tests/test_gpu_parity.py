@@ -246,3 +246,14 @@ def test_errors_leave_state_unchanged_and_no_cpu_fallback():
     c.alloc_blocks(2, 1)
     c.swap_out([2])
     assert c.launch_count() == n0 + 1         # the copy ran as one of our kernels
+
+
+@pytest.mark.parametrize("engine", ["tma", "ldst"])
+def test_staged_descriptor_path_bytes(engine):
+    """More than kInlineDesc (256) descriptors: the staging-ring upload path,
+    whole-buffer compare (both directions, fragmented table)."""
+    rig = Rig(L=2, bs=16, H=1, D=8, NB=700, lender_slots=300, host_slots=300)
+    rig.ctx.set_option(aqua.OPT_KERNEL, ENGINES[engine])
+    perm = block_permutation(700, 700, seed=5).tolist()
+    _ops(rig, [("adopt", (1, perm[:257])), ("adopt", (2, perm[257:600])), ("out", [1, 2]),
+               ("alloc", (3, 50)), ("in", [2, 1]), ("out", [3, 1]), ("in", [1])])
