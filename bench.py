@@ -200,10 +200,16 @@ def run_ours(args):
     from workloads import block_permutation
 
     ws, rank, local = _dist()
+    shared = os.environ.get("AQUA_BENCH_SHARED_GPU") == "1"   # test mode: all ranks on cuda:0, gloo
+    if shared:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if ws > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     L, bs, H, D, e = SHAPE["L"], SHAPE["bs"], SHAPE["H"], SHAPE["D"], SHAPE["e"]
     S = bs * H * D * e
     U = 2 * L * S
@@ -226,11 +232,10 @@ def run_ours(args):
         ctx.lend(local, arena.data_ptr(), arena_bytes)
         mode = "self-lender"
     else:
-        partner = rank ^ 1 if (rank ^ 1) < ws else rank
+        from paper_2407_21255_b200.pairing import exchange, partner as pair_of
+        partner = pair_of(rank, ws)
         ipc_ptr = aqua.ipc_alloc(local, arena_bytes)          # what this rank lends to its partner
-        handle = aqua.ipc_export(ipc_ptr)
-        handles = [None] * ws
-        dist.all_gather_object(handles, (rank, local, handle))
+        handles = exchange((rank, local, aqua.ipc_export(ipc_ptr)))
         if partner == rank:
             ctx.lend(local, ipc_ptr, arena_bytes)
             mode = "self-lender"
@@ -275,7 +280,7 @@ def run_ours(args):
     total_ms = start.elapsed_time(end)
     out_ms = [a.elapsed_time(b) for a, b, _ in ev]
     in_ms = [b.elapsed_time(c) for _, b, c in ev]
-    t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
+    t = torch.tensor([total_ms], device="cpu" if shared else dev, dtype=torch.float64)
     if ws > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms_max = float(t.item())

@@ -113,7 +113,8 @@ enum {
   AQUA_OPT_KERNEL = 1,        /* one of AQUA_KERNEL_* / AQUA_BASE_* */
   AQUA_OPT_MAX_CTAS = 2,      /* cap on CTAs per swap launch (0 = all SMs); SMs left for decode */
   AQUA_OPT_TMA_PIECE = 3,     /* bytes per TMA stage (multiple of 16, <= 65536; 0 = auto: 32 KiB) */
-  AQUA_OPT_TMA_STAGES = 4     /* TMA ring depth (2..32; 0 = auto: ~200 KiB of smem per CTA, 1 CTA/SM) */
+  AQUA_OPT_TMA_STAGES = 4,    /* TMA ring depth (2..32; 0 = auto: max(3, 64 KiB / piece), 1 CTA/SM) */
+  AQUA_OPT_TIMING = 5         /* 1: each swap also records a start event; aqua_ticket_elapsed gives its device time */
 };
 
 typedef struct aqua_ctx aqua_ctx;   /* one per borrower device (per TP rank) */
@@ -191,6 +192,11 @@ AQUA_API aqua_status aqua_free(aqua_ctx* ctx, uint64_t pid, aqua_stream_t stream
 AQUA_API aqua_status aqua_wait(aqua_ctx* ctx, uint64_t ticket, aqua_stream_t stream);
 /* Block the host until the ticket completes. */
 AQUA_API aqua_status aqua_sync(aqua_ctx* ctx, uint64_t ticket);
+/* Device time (ms) of the copy behind a swap ticket, from just before its
+ * descriptor upload / copy to its completion event.  Needs AQUA_OPT_TIMING = 1
+ * at swap time; AQUA_E_STATE if not timed or not complete yet.  The last
+ * 65536 retired timed tickets are remembered. */
+AQUA_API aqua_status aqua_ticket_elapsed(aqua_ctx* ctx, uint64_t ticket, float* ms);
 /* *done = 1 if the ticket has completed, else 0. */
 AQUA_API aqua_status aqua_ticket_done(aqua_ctx* ctx, uint64_t ticket, int32_t* done);
 

@@ -25,12 +25,12 @@ HOST, DRYRUN, MAPPED = -1, -2, -3
 RESIDENT, SWAPPED = 1, 2
 LOC_LOCAL, LOC_PEER, LOC_HOST = 0, 1, 2
 KERNEL_AUTO, KERNEL_TMA, KERNEL_LDST, BASE_PER_CHUNK, BASE_GATHER_TEMP, BASE_BATCH = 0, 1, 2, 3, 4, 5
-OPT_KERNEL, OPT_MAX_CTAS, OPT_TMA_PIECE, OPT_TMA_STAGES = 1, 2, 3, 4
+OPT_KERNEL, OPT_MAX_CTAS, OPT_TMA_PIECE, OPT_TMA_STAGES, OPT_TIMING = 1, 2, 3, 4, 5
 
 # Every symbol include/aqua.h declares (checked by tests/test_abi.py).
 SYMBOLS = [
     "aqua_create", "aqua_destroy", "aqua_lend", "aqua_alloc_blocks", "aqua_adopt_blocks",
-    "aqua_swap_out", "aqua_swap_in", "aqua_free", "aqua_wait", "aqua_sync", "aqua_ticket_done",
+    "aqua_swap_out", "aqua_swap_in", "aqua_free", "aqua_wait", "aqua_sync", "aqua_ticket_done", "aqua_ticket_elapsed",
     "aqua_query", "aqua_counts", "aqua_arena_base", "aqua_set_option", "aqua_get_option",
     "aqua_last_descriptors", "aqua_launch_count", "aqua_ipc_export", "aqua_ipc_import",
     "aqua_ipc_close", "aqua_ipc_alloc", "aqua_ipc_free", "aqua_can_access_peer", "aqua_kv_fill_pattern", "aqua_kv_verify_pattern",
@@ -69,6 +69,7 @@ def _load() -> C.CDLL:
         "aqua_wait": (C.c_int, [VP, U64, VP]),
         "aqua_sync": (C.c_int, [VP, U64]),
         "aqua_ticket_done": (C.c_int, [VP, U64, P(I32)]),
+        "aqua_ticket_elapsed": (C.c_int, [VP, U64, P(C.c_float)]),
         "aqua_query": (C.c_int, [VP, U64, P(I32), P(I32), P(I32), P(I32), I32]),
         "aqua_counts": (C.c_int, [VP, P(I32), P(I32), P(I32)]),
         "aqua_arena_base": (C.c_int, [VP, I32, P(VP), P(I32)]),
@@ -189,6 +190,11 @@ class Ctx:
         d = C.c_int32()
         self._c(lib.aqua_ticket_done(self.h, ticket, C.byref(d)))
         return bool(d.value)
+
+    def ticket_elapsed(self, ticket: int) -> float:
+        v = C.c_float()
+        self._c(lib.aqua_ticket_elapsed(self.h, ticket, C.byref(v)))
+        return v.value
 
     def query(self, pid: int, with_ids: bool = False):
         st, loc, n = C.c_int32(), C.c_int32(), C.c_int32()

@@ -22,6 +22,7 @@
 #include <unordered_set>
 #include <vector>
 
+#include "aqua_idset.h"
 #include "aqua_internal.h"
 
 using aqua::Desc;
@@ -37,7 +38,7 @@ struct Arena {
   uint64_t bytes = 0;
   int32_t nslots = 0;
   bool owned = false;
-  std::set<int32_t> free;      // lowest-first (R4)
+  aqua::IdSet free;            // lowest-first (R4)
   std::vector<uint64_t> tick;  // last library ticket that touched each slot
 };
 
@@ -50,6 +51,7 @@ struct Prompt {
 struct TicketRec {
   cudaEvent_t ev;
   cudaStream_t st;
+  cudaEvent_t start = nullptr;   // AQUA_OPT_TIMING: recorded before the copy
 };
 
 struct StageRegion {
@@ -65,7 +67,7 @@ struct aqua_ctx {
   int32_t L = 0, bs = 0, H = 0, D = 0, e = 0, NB = 0;
   int64_t S = 0, U = 0, P_kv = 0, P_b = 0;
   std::vector<uint64_t> layer_base;
-  std::set<int32_t> free_blocks;
+  aqua::IdSet free_blocks;
   std::vector<uint64_t> btick;  // last library ticket that touched each block
   std::unordered_map<uint64_t, Prompt> prompts;
   Arena gpu, host;              // AQUA_LOC_PEER, AQUA_LOC_HOST
@@ -84,6 +86,10 @@ struct aqua_ctx {
   uint64_t next_ticket = 1;
   std::map<uint64_t, TicketRec> live;
   std::vector<cudaEvent_t> ev_pool;
+  std::vector<cudaEvent_t> tev_pool;          // timing-enabled events
+  bool timing = false;
+  std::unordered_map<uint64_t, float> elapsed;  // retired timed tickets -> ms
+  std::deque<uint64_t> elapsed_order;
   // gather-temp baseline buffer
   uint8_t* d_temp = nullptr;
   size_t temp_cap = 0;
@@ -135,7 +141,20 @@ void retire(aqua_ctx* c) {
   for (auto it = c->live.begin(); it != c->live.end() && scanned < 64; ++scanned) {
     cudaError_t q = cudaEventQuery(it->second.ev);
     if (q == cudaSuccess) {
-      c->ev_pool.push_back(it->second.ev);
+      if (it->second.start) {
+        float ms = -1.f;
+        if (cudaEventElapsedTime(&ms, it->second.start, it->second.ev) != cudaSuccess) cudaGetLastError();
+        c->elapsed[it->first] = ms;
+        c->elapsed_order.push_back(it->first);
+        if (c->elapsed_order.size() > 65536) {
+          c->elapsed.erase(c->elapsed_order.front());
+          c->elapsed_order.pop_front();
+        }
+        c->tev_pool.push_back(it->second.start);
+        c->tev_pool.push_back(it->second.ev);
+      } else {
+        c->ev_pool.push_back(it->second.ev);
+      }
       it = c->live.erase(it);
     } else {
       if (q != cudaErrorNotReady) cudaGetLastError();
@@ -146,33 +165,53 @@ void retire(aqua_ctx* c) {
     c->stage_live.pop_front();
 }
 
-aqua_status record(aqua_ctx* c, cudaStream_t st, uint64_t* t) {
+aqua_status get_event(aqua_ctx* c, bool timing, cudaEvent_t* ev) {
+  auto& pool = timing ? c->tev_pool : c->ev_pool;
+  if (!pool.empty()) {
+    *ev = pool.back();
+    pool.pop_back();
+    return AQUA_OK;
+  }
+  CK(c, cudaEventCreateWithFlags(ev, timing ? cudaEventDefault : cudaEventDisableTiming));
+  return AQUA_OK;
+}
+
+// Records the ticket event on `st`.  `start` (nullable) is a timing event
+// recorded before the copy; the ticket then measures the copy's device time.
+aqua_status record(aqua_ctx* c, cudaStream_t st, uint64_t* t, cudaEvent_t start = nullptr) {
   const uint64_t id = c->next_ticket++;
   if (c->dry) {
     *t = id;
     return AQUA_OK;
   }
   cudaEvent_t ev;
-  if (!c->ev_pool.empty()) {
-    ev = c->ev_pool.back();
-    c->ev_pool.pop_back();
-  } else {
-    CK(c, cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-  }
+  if (aqua_status s = get_event(c, start != nullptr, &ev)) return s;
   CK(c, cudaEventRecord(ev, st));
-  c->live[id] = TicketRec{ev, st};
+  c->live[id] = TicketRec{ev, st, start};
   *t = id;
+  return AQUA_OK;
+}
+
+aqua_status timing_start(aqua_ctx* c, cudaStream_t st, cudaEvent_t* start) {
+  *start = nullptr;
+  if (!c->timing || c->dry) return AQUA_OK;
+  if (aqua_status s = get_event(c, true, start)) return s;
+  CK(c, cudaEventRecord(*start, st));
   return AQUA_OK;
 }
 
 // Make `st` wait for every live ticket in `ts` recorded on another stream.
 aqua_status wait_all(aqua_ctx* c, const std::vector<uint64_t>& ts, cudaStream_t st) {
   if (c->dry) return AQUA_OK;
-  std::vector<uint64_t> u(ts);
-  std::sort(u.begin(), u.end());
-  u.erase(std::unique(u.begin(), u.end()), u.end());
+  // few distinct tickets per call: dedupe linearly instead of sorting
+  std::vector<uint64_t> u;
+  uint64_t prev = 0;
+  for (uint64_t t : ts) {
+    if (t == 0 || t == prev) continue;
+    prev = t;
+    if (std::find(u.begin(), u.end(), t) == u.end()) u.push_back(t);
+  }
   for (uint64_t t : u) {
-    if (t == 0) continue;
     auto it = c->live.find(t);
     if (it == c->live.end() || it->second.st == st) continue;
     CK(c, cudaStreamWaitEvent(st, it->second.ev, 0));
@@ -447,7 +486,7 @@ aqua_status aqua_create(int device, const aqua_kv_layout* lay, aqua_ctx** out) {
   c->P_b = P_b;
   c->layer_base.resize(c->L);
   for (int l = 0; l < c->L; ++l) c->layer_base[l] = reinterpret_cast<uint64_t>(lay->layer_base[l]);
-  for (int32_t b = 0; b < c->NB; ++b) c->free_blocks.insert(c->free_blocks.end(), b);
+  c->free_blocks.init(c->NB, true);
   c->btick.assign(c->NB, 0);
   if (!c->dry) {
     DevGuard g(device);
@@ -473,8 +512,10 @@ aqua_status aqua_destroy(aqua_ctx* c) {
     for (auto& kv : c->live) {
       cudaEventSynchronize(kv.second.ev);
       cudaEventDestroy(kv.second.ev);
+      if (kv.second.start) cudaEventDestroy(kv.second.start);
     }
     for (auto ev : c->ev_pool) cudaEventDestroy(ev);
+    for (auto ev : c->tev_pool) cudaEventDestroy(ev);
     if (c->gpu.present && c->gpu.owned) {
       DevGuard g2(c->gpu.device);
       cudaFree(c->gpu.base);
@@ -554,7 +595,7 @@ aqua_status aqua_lend(aqua_ctx* c, int lender, void* base, uint64_t bytes, int32
       }
     }
   }
-  for (int32_t s = 0; s < na.nslots; ++s) na.free.insert(na.free.end(), s);
+  na.free.init(na.nslots, true);
   na.tick.assign(na.nslots, 0);
   a = std::move(na);
   if (out_nslots) *out_nslots = a.nslots;
@@ -576,7 +617,7 @@ aqua_status aqua_alloc_blocks(aqua_ctx* c, uint64_t pid, int32_t n, aqua_stream_
   std::vector<uint64_t> ts;
   for (int32_t b : ids) ts.push_back(c->btick[b]);
   if (aqua_status s = wait_all(c, ts, reinterpret_cast<cudaStream_t>(stream))) return s;
-  c->free_blocks.erase(c->free_blocks.begin(), fb);
+  c->free_blocks.erase_lowest(n);
   Prompt& p = c->prompts[pid];
   for (int32_t b : ids) c->btick[b] = 0;
   p.ids.insert(p.ids.end(), ids.begin(), ids.end());
@@ -666,9 +707,11 @@ aqua_status aqua_swap_out(aqua_ctx* c, int32_t n, const uint64_t* pids, aqua_str
                        ->tick[d.slot_arena & ~kArenaBit]);
     }
     if (aqua_status s = wait_all(c, ts, st)) return s;
+    cudaEvent_t t_start;
+    if (aqua_status s = timing_start(c, st, &t_start)) return s;
     int regions = 0;
     if (aqua_status s = run_copy(c, ds, aqua::kOut, st, &regions)) return s;
-    if (aqua_status s = record(c, st, &ticket)) return s;
+    if (aqua_status s = record(c, st, &ticket, t_start)) return s;
     stage_seal(c, regions, ticket);
   } else if (c->dry && !ds.empty()) {
     record(c, st, &ticket);
@@ -735,14 +778,16 @@ aqua_status aqua_swap_in(aqua_ctx* c, int32_t n, const uint64_t* pids, aqua_stre
                        ->tick[d.slot_arena & ~kArenaBit]);
     }
     if (aqua_status s = wait_all(c, ts, st)) return s;
+    cudaEvent_t t_start;
+    if (aqua_status s = timing_start(c, st, &t_start)) return s;
     int regions = 0;
     if (aqua_status s = run_copy(c, ds, aqua::kIn, st, &regions)) return s;
-    if (aqua_status s = record(c, st, &ticket)) return s;
+    if (aqua_status s = record(c, st, &ticket, t_start)) return s;
     stage_seal(c, regions, ticket);
   } else if (c->dry && !ds.empty()) {
     record(c, st, &ticket);
   }
-  c->free_blocks.erase(c->free_blocks.begin(), fb);
+  c->free_blocks.erase_lowest(static_cast<int32_t>(need));
   int64_t k = 0;
   for (int32_t i = 0; i < n; ++i) {
     Arena* a = arena_of(c, ps[i]->loc);
@@ -825,6 +870,24 @@ aqua_status aqua_ticket_done(aqua_ctx* c, uint64_t ticket, int32_t* done) {
   return AQUA_OK;
 }
 
+aqua_status aqua_ticket_elapsed(aqua_ctx* c, uint64_t ticket, float* ms) {
+  if (aqua_status s = precheck(c)) return s;
+  if (!ms) return fail(c, AQUA_E_INVAL, "null ms");
+  auto it = c->live.find(ticket);
+  if (it != c->live.end()) {
+    if (!it->second.start) return fail(c, AQUA_E_STATE, "ticket was not timed (AQUA_OPT_TIMING off)");
+    cudaError_t q = cudaEventQuery(it->second.ev);
+    if (q == cudaErrorNotReady) return fail(c, AQUA_E_STATE, "ticket not complete");
+    if (q != cudaSuccess) return cuda_fail(c, q, "cudaEventQuery");
+    CK(c, cudaEventElapsedTime(ms, it->second.start, it->second.ev));
+    return AQUA_OK;
+  }
+  auto e = c->elapsed.find(ticket);
+  if (e == c->elapsed.end()) return fail(c, AQUA_E_STATE, "no timing recorded for this ticket");
+  *ms = e->second;
+  return AQUA_OK;
+}
+
 aqua_status aqua_query(aqua_ctx* c, uint64_t pid, int32_t* state, int32_t* location, int32_t* n,
                        int32_t* ids, int32_t cap) {
   if (!c) return fail(nullptr, AQUA_E_INVAL, "null ctx");
@@ -878,6 +941,10 @@ aqua_status aqua_set_option(aqua_ctx* c, int32_t opt, int64_t v) {
       if (v < 0 || v > 32 || v == 1) return fail(c, AQUA_E_INVAL, "tma stages");
       c->tma_stages = static_cast<int>(v);
       return AQUA_OK;
+    case AQUA_OPT_TIMING:
+      if (v != 0 && v != 1) return fail(c, AQUA_E_INVAL, "timing");
+      c->timing = v != 0;
+      return AQUA_OK;
   }
   return fail(c, AQUA_E_INVAL, "unknown option");
 }
@@ -889,6 +956,7 @@ aqua_status aqua_get_option(aqua_ctx* c, int32_t opt, int64_t* v) {
     case AQUA_OPT_MAX_CTAS: *v = c->max_ctas; return AQUA_OK;
     case AQUA_OPT_TMA_PIECE: *v = c->tma_piece; return AQUA_OK;
     case AQUA_OPT_TMA_STAGES: *v = c->tma_stages; return AQUA_OK;
+    case AQUA_OPT_TIMING: *v = c->timing; return AQUA_OK;
   }
   return fail(c, AQUA_E_INVAL, "unknown option");
 }

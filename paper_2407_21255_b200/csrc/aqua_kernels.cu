@@ -308,8 +308,10 @@ int tma_smem_bytes(int piece, int stages) { return piece * stages + 8 * stages; 
 cudaError_t launch_swap_tma(const SwapParams& p, Dir dir, int num_sms, int grid_cap, int stages_opt,
                             cudaStream_t s, int* ctas_used) {
   if (p.nitems == 0) return cudaSuccess;
-  // One CTA per SM (measured best on B200: r01 sweep), ~200 KiB of stages.
-  int stages = stages_opt > 0 ? stages_opt : (200 * 1024) / p.piece;
+  // One CTA per SM and a shallow ring: 3 x 32 KiB or 64 KiB of loads in
+  // flight per SM measured best for HBM on B200 (profiles/r01_stages.jsonl);
+  // deeper rings lose 3-4 %.
+  int stages = stages_opt > 0 ? stages_opt : std::max(3, std::min(32, (64 * 1024) / p.piece));
   stages = std::max(2, std::min(stages, 32));
   while (stages > 2 && tma_smem_bytes(p.piece, stages) > 227 * 1024) --stages;
   const int smem = tma_smem_bytes(p.piece, stages);

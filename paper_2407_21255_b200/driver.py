@@ -23,13 +23,15 @@ from .cfs import Scheduler
 def run_trace(trace: Sequence[Tuple[int, float, int, int]], ctx: "aqua.Ctx", sched: Scheduler, *,
               fill_seed: Optional[int] = None, decode_stream: int = 0, swap_stream: int = 0,
               on_iteration: Optional[Callable] = None, record_log: bool = True,
-              stream_sync: Optional[Callable] = None):
+              stream_sync: Optional[Callable] = None, on_swap: Optional[Callable] = None):
     """Run the whole trace.  Returns (log, stats).
 
     ``stream_sync(kind, ticket)`` lets a GPU caller order streams:
       kind == "before_swap_out": swap stream must wait for decode;
+      kind == "before_swap_in":  (timing hook);
       kind == "after_swap_in":   decode must wait for the swap_in ticket.
     ``on_iteration(i, work)`` runs the per-iteration decode proxy (optional).
+    ``on_swap(kind, pids, ticket, nblocks)`` is called after each swap call.
     """
     pending = sorted(trace, key=lambda x: (x[1], x[0]))
     pi = 0
@@ -61,9 +63,13 @@ def run_trace(trace: Sequence[Tuple[int, float, int, int]], ctx: "aqua.Ctx", sch
             n = sum(x[2] for x in q)
             blocks_out += n
             swap_calls.append(("out", n, tk, t0))
+            if on_swap:
+                on_swap("out", outs, tk, n)
             if record_log:
                 log.append(("swap_out", tuple(outs), tuple((x[1], tuple(x[3])) for x in q)))
         if ins:
+            if stream_sync:
+                stream_sync("before_swap_in", 0)
             t0 = time.perf_counter()
             new, tk = ctx.swap_in(ins, swap_stream)
             n = sum(len(x) for x in new)
@@ -71,6 +77,8 @@ def run_trace(trace: Sequence[Tuple[int, float, int, int]], ctx: "aqua.Ctx", sch
             swap_calls.append(("in", n, tk, t0))
             if stream_sync:
                 stream_sync("after_swap_in", tk)
+            if on_swap:
+                on_swap("in", ins, tk, n)
             if record_log:
                 log.append(("swap_in", tuple(ins), tuple(tuple(x) for x in new)))
         for pid, ctx0, tok, grow, phase in work:

@@ -1,0 +1,145 @@
+"""C3 (BASELINE configs[2]) on the GPU: the bursty trace through the native
+CFS scheduler + libaqua paging + a synthetic decode, 1 borrower + 1 lender.
+
+    python scripts/c3_run.py --policy cfs-peer|cfs-host|fcfs [--proxy-gb G] [--check-oracle]
+
+At N=1 the "peer" lender arena lives in the same GPU (self-lender); the
+decode writes each new token's closed-form KV pattern (C-11) on a decode
+stream, swaps run on a swap stream, and every resumed prompt is verified
+against the pattern right after its swap_in (restore invariant at full
+scale).  --check-oracle also replays the oracle's metadata-mode run and
+requires an identical call log.  Prints one JSON line.
+"""
+import argparse
+import json
+import os
+import statistics
+import sys
+import time
+
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from paper_2407_21255_b200 import aqua  # noqa: E402
+from paper_2407_21255_b200.cfs import POLICY_CFS, POLICY_FCFS, Scheduler  # noqa: E402
+from paper_2407_21255_b200.driver import run_trace  # noqa: E402
+from workloads import burst_trace  # noqa: E402
+
+NB = 4152          # scripts/c3_nb.py
+L, bs, H, D, e = 32, 16, 8, 128, 2
+SEED = 77
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--policy", default="cfs-peer", choices=["cfs-peer", "cfs-host", "fcfs"])
+    ap.add_argument("--proxy-gb", type=float, default=0.0, help="decode proxy: GB of HBM streamed per iteration")
+    ap.add_argument("--lender-gib", type=int, default=64)
+    ap.add_argument("--host-gib", type=int, default=64)
+    ap.add_argument("--check-oracle", action="store_true")
+    ap.add_argument("--no-verify", action="store_true")
+    args = ap.parse_args()
+
+    dev = torch.device("cuda", 0)
+    S = bs * H * D * e
+    U = 2 * L * S
+    layers = [torch.zeros(2 * NB * S, dtype=torch.uint8, device=dev) for _ in range(L)]
+    ctx = aqua.Ctx(0, L, bs, H, D, e, NB, [t.data_ptr() for t in layers])
+    arena = None
+    if args.policy == "cfs-peer":
+        arena = torch.empty(args.lender_gib << 30, dtype=torch.uint8, device=dev)
+        ctx.lend(0, arena.data_ptr(), args.lender_gib << 30)
+    ctx.lend(aqua.HOST, 0, args.host_gib << 30)
+    ctx.set_option(aqua.OPT_TIMING, 1)               # per-swap device time via aqua_ticket_elapsed
+    pol = POLICY_FCFS if args.policy == "fcfs" else POLICY_CFS
+    sched = Scheduler(NB=NB, bs=bs, b=512, k=8, policy=pol)
+    trace = burst_trace(seed=1)
+    dec = torch.cuda.Stream(device=dev)
+    swp = torch.cuda.Stream(device=dev)
+    mism = torch.zeros(1, dtype=torch.int64, device=dev)
+    written = {}          # pid -> KV tokens written so far
+    swap_events = []      # (kind, nblocks, ticket, npids)
+    proxy = None
+    if args.proxy_gb > 0:
+        proxy = torch.empty(int(args.proxy_gb * 1e9) // 8, dtype=torch.int64, device=dev)
+        proxy_out = torch.empty(1, dtype=torch.int64, device=dev)
+
+    def stream_sync(kind, ticket):
+        if kind == "before_swap_out":
+            swp.wait_stream(dec)                      # the blocks' last writer is the decode
+        elif kind == "after_swap_in":
+            ctx.wait(ticket, dec.cuda_stream)         # decode waits only for what it needs
+
+    def on_swap(kind, pids, ticket, n):
+        swap_events.append((kind, n, ticket, len(pids)))
+        if kind == "in" and not args.no_verify:
+            for p in pids:
+                ctx.kv_verify_pattern(p, written.get(p, 0), SEED, mism.data_ptr(), dec.cuda_stream)
+
+    iters = {"n": 0}
+    first_tok = {}
+
+    def on_iteration(i, work):
+        for pid, ctx0, tok, grow, phase in work:
+            written[pid] = ctx0 + tok
+        if proxy is not None:
+            with torch.cuda.stream(dec):
+                torch.sum(proxy, out=proxy_out)
+        iters["n"] += 1
+
+    torch.cuda.synchronize()
+    n0 = ctx.launch_count()
+    t0 = time.perf_counter()
+    log, st = run_trace(trace, ctx, sched, fill_seed=SEED, decode_stream=dec.cuda_stream,
+                        swap_stream=swp.cuda_stream, on_iteration=on_iteration, stream_sync=stream_sync,
+                        on_swap=on_swap, record_log=args.check_oracle)
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    launches = ctx.launch_count() - n0
+    # per-call device time of the copies (library timing events)
+    per_block_ms = []
+    dev_ms = {"out": 0.0, "in": 0.0}
+    for kind, n, tk, npids in swap_events:
+        if n == 0:
+            continue
+        ms = ctx.ticket_elapsed(tk)
+        dev_ms[kind] += ms
+        per_block_ms.append((kind, ms, n, npids))
+    bytes_out, bytes_in = st["blocks_out"] * U, st["blocks_in"] * U
+    res = {
+        "config": "configs[2] bursty trace (seed 1, 373 requests, 25 @ 2.5/s then 5/s for 60 s then 2.5/s for 15 s), "
+                  "Llama-3-8B KV shape, NB=4152 (8.1 GiB), b=512, k=8",
+        "policy": args.policy, "mode": "self-lender (1 GPU)" if args.policy == "cfs-peer" else args.policy,
+        "iterations": st["iters"], "virtual_s": round(st["vclock"], 3), "wall_s": round(wall, 3),
+        "swap_out_calls": sum(1 for x in swap_events if x[0] == "out"),
+        "swap_in_calls": sum(1 for x in swap_events if x[0] == "in"),
+        "bytes_out": bytes_out, "bytes_in": bytes_in,
+        "swap_device_ms": {k: round(v, 3) for k, v in dev_ms.items()},
+        "swap_GBps": {k: round((bytes_out if k == "out" else bytes_in) / max(v, 1e-9) / 1e6, 1)
+                      for k, v in dev_ms.items() if v > 0},
+        "kernel_launches": launches,
+        "verify_mismatches": int(mism.item()),
+    }
+    outs = [ms / np_ for k, ms, n, np_ in per_block_ms if k == "out"]
+    ins = [ms / np_ for k, ms, n, np_ in per_block_ms if k == "in"]
+    if outs and ins:
+        so, si = sorted(outs), sorted(ins)
+        res["per_prompt_ms"] = {"preempt_p50": round(statistics.median(so), 4),
+                                "preempt_p99": round(so[min(len(so) - 1, int(0.99 * len(so)))], 4),
+                                "resume_p50": round(statistics.median(si), 4),
+                                "resume_p99": round(si[min(len(si) - 1, int(0.99 * len(si)))], 4)}
+    if args.check_oracle:
+        from oracle import sim as osim
+        o = osim.run(trace, osim.SimConfig(NB=NB, lender_slots=(args.lender_gib << 30) // U if arena is not None else 0,
+                                           host_slots=(args.host_gib << 30) // U,
+                                           policy="fcfs" if pol == POLICY_FCFS else "cfs"))
+        res["oracle_log_equal"] = (log == o.log)
+        res["oracle_calls"] = len(o.log)
+    print(json.dumps(res), flush=True)
+    if res["verify_mismatches"]:
+        raise SystemExit("KV pattern mismatch after resume")
+
+
+if __name__ == "__main__":
+    main()

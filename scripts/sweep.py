@@ -77,6 +77,23 @@ def engines():
                           "in_hbm_GBps": round(2 * nbytes / i / 1e6, 1)}), flush=True)
 
 
+def stages():
+    L, bs, H, D, NB, nblk = 32, 16, 8, 128, 4096, 2048
+    ctx, layers, arena, U = setup(L, bs, H, D, NB, nblk)
+    s = torch.cuda.Stream()
+    nbytes = nblk * U
+    for piece, st in [(16384, 4), (16384, 6), (16384, 8), (16384, 12), (32768, 2), (32768, 3), (32768, 4),
+                      (32768, 6), (65536, 2), (65536, 3), (8192, 12), (8192, 24)]:
+        for ctas in (148, 0):
+            ctx.set_option(aqua.OPT_TMA_PIECE, piece)
+            ctx.set_option(aqua.OPT_TMA_STAGES, st)
+            ctx.set_option(aqua.OPT_MAX_CTAS, ctas)
+            o, i = time_swaps(ctx, 10, s)
+            print(json.dumps({"piece": piece, "stages": st, "max_ctas": ctas, "out_ms": round(o, 4),
+                              "in_ms": round(i, 4), "out_hbm_GBps": round(2 * nbytes / o / 1e6, 1),
+                              "in_hbm_GBps": round(2 * nbytes / i / 1e6, 1)}), flush=True)
+
+
 def c5(host=False):
     L, H, D = 32, 8, 128
     for bs in (8, 16, 32, 64, 128):
@@ -107,3 +124,43 @@ if __name__ == "__main__":
         c5(host=False)
     elif what == "c5host":
         c5(host=True)
+    elif what == "stages":
+        stages()
+
+
+def latency():
+    """Host cost of one call (enqueue only) and device time of small calls."""
+    import time
+    L, bs, H, D = 32, 16, 8, 128
+    for nblk in (1, 8, 64, 256, 257, 2048):
+        ctx, layers, arena, U = setup(L, bs, H, D, 4096, nblk)
+        s = torch.cuda.Stream()
+        o, i = time_swaps(ctx, 20, s)
+        ctx.set_option(aqua.OPT_TIMING, 1)
+        dev = []
+        for _ in range(20):
+            t1 = ctx.swap_out([7], s.cuda_stream)
+            _, t2 = ctx.swap_in([7], s.cuda_stream)
+            torch.cuda.synchronize()
+            dev.append((ctx.ticket_elapsed(t1), ctx.ticket_elapsed(t2)))
+        ctx.set_option(aqua.OPT_TIMING, 0)
+        enq = []
+        for _ in range(50):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            ctx.swap_out([7], s.cuda_stream)
+            t1 = time.perf_counter()
+            ctx.swap_in([7], s.cuda_stream)
+            t2 = time.perf_counter()
+            enq.append((t1 - t0, t2 - t1))
+        torch.cuda.synchronize()
+        print(json.dumps({"latency": nblk, "bytes": nblk * U, "out_ms": round(o, 4), "in_ms": round(i, 4),
+                          "ticket_out_ms": round(statistics.median(d[0] for d in dev), 4),
+                          "ticket_in_ms": round(statistics.median(d[1] for d in dev), 4),
+                          "enqueue_out_us": round(1e6 * statistics.median(e[0] for e in enq), 1),
+                          "enqueue_in_us": round(1e6 * statistics.median(e[1] for e in enq), 1)}), flush=True)
+        ctx.close()
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "latency":
+    latency()

@@ -252,8 +252,25 @@ def test_errors_leave_state_unchanged_and_no_cpu_fallback():
 def test_staged_descriptor_path_bytes(engine):
     """More than kInlineDesc (256) descriptors: the staging-ring upload path,
     whole-buffer compare (both directions, fragmented table)."""
-    rig = Rig(L=2, bs=16, H=1, D=8, NB=700, lender_slots=300, host_slots=300)
+    rig = Rig(L=2, bs=16, H=1, D=8, NB=700, lender_slots=300, host_slots=400)
     rig.ctx.set_option(aqua.OPT_KERNEL, ENGINES[engine])
     perm = block_permutation(700, 700, seed=5).tolist()
     _ops(rig, [("adopt", (1, perm[:257])), ("adopt", (2, perm[257:600])), ("out", [1, 2]),
                ("alloc", (3, 50)), ("in", [2, 1]), ("out", [3, 1]), ("in", [1])])
+
+
+def test_ticket_timing():
+    rig = Rig(L=4, bs=16, H=8, D=128, NB=64, lender_slots=32)
+    c = rig.ctx
+    c.set_option(aqua.OPT_TIMING, 1)
+    c.alloc_blocks(1, 32)
+    t = c.swap_out([1])
+    c.sync(t)
+    ms = c.ticket_elapsed(t)
+    assert 0.0 < ms < 100.0
+    c.set_option(aqua.OPT_TIMING, 0)
+    _, t2 = c.swap_in([1])
+    c.sync(t2)
+    with pytest.raises(aqua.AquaError) as e:
+        c.ticket_elapsed(t2)
+    assert e.value.code == aqua.E_STATE

@@ -1,0 +1,57 @@
+"""N>1 host logic on CPU with gloo, world_size 2: pairing and the
+setup-time exchange of IPC handles (the data path itself needs GPUs)."""
+import os
+import socket
+
+import pytest
+import torch.multiprocessing as mp
+
+from paper_2407_21255_b200.pairing import partner
+
+
+def test_partner_matching():
+    assert [partner(r, 8) for r in range(8)] == [1, 0, 3, 2, 5, 4, 7, 6]
+    assert [partner(r, 3) for r in range(3)] == [1, 0, 2]
+    assert partner(0, 1) == 0
+    no = [[True, False], [False, True]]
+    assert partner(0, 2, no) == 0
+    # a perfect matching: partner(partner(r)) == r
+    for w in range(1, 9):
+        assert all(partner(partner(r, w), w) == r for r in range(w))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    import torch.distributed as dist
+    from paper_2407_21255_b200.pairing import exchange, partner
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    handle = bytes([rank]) * 64                       # stands in for cudaIpcMemHandle_t
+    got = exchange((rank, handle, 1 << 30))
+    p = partner(rank, world)
+    q.put((rank, p, got[p]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_gloo_handle_exchange_world2():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in ps)
+    for p in ps:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert res[0][1] == 1 and res[0][2] == (1, bytes([1]) * 64, 1 << 30)
+    assert res[1][1] == 0 and res[1][2] == (0, bytes([0]) * 64, 1 << 30)
