@@ -30,10 +30,32 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "KV swap GB/s per GPU pair vs 900 GB/s NVLink; preempt+resume latency/prompt"
-SHAPE = dict(L=32, bs=16, H=8, D=128, e=2)
-NB = 4096
-NBLK = 2048            # 32768 tokens / 16
+# Bench workloads (BASELINE.json configs).  c2 = configs[1], the default and
+# the one the metric is quoted on; c4 = one TP rank of configs[3] (Llama-3-70B
+# KV over TP4: 2 KV heads per rank, S = 8 KiB), 32 prompts x 2048 tokens
+# swapped in ONE batched call per direction.
+CONFIGS = {
+    "c2": dict(L=32, bs=16, H=8, D=128, e=2, NB=4096, nprompts=1, bpp=2048,
+               desc="configs[1]: Llama-3-8B-shaped KV (L=32, H=8, D=128, bf16, block 16), one 32K-token prompt = "
+                    "2048 blocks x 2 MiB on a fragmented block table"),
+    "c4": dict(L=80, bs=16, H=2, D=128, e=2, NB=8192, nprompts=32, bpp=128,
+               desc="configs[3] per rank: Llama-3-70B-shaped KV over TP4 (L=80, 2 KV heads, D=128, bf16, block 16), "
+                    "32 prompts x 2048 tokens = 4096 blocks x 1.25 MiB, one batched call per direction"),
+}
+SHAPE = NB = NBLK = PIDS = CFG = None
 SEED_PATTERN = 1234
+
+
+def select_config(name):
+    global SHAPE, NB, NBLK, PIDS, CFG
+    CFG = dict(CONFIGS[name], name=name)
+    SHAPE = {k: CFG[k] for k in ("L", "bs", "H", "D", "e")}
+    NB = CFG["NB"]
+    NBLK = CFG["nprompts"] * CFG["bpp"]
+    PIDS = list(range(100, 100 + CFG["nprompts"]))
+
+
+select_config("c2")
 
 
 def _peaks():
@@ -182,13 +204,14 @@ def run_reference(args):
 
 
 def _config(args, reference=False, n=1):
-    return {"workload": "configs[1]: Llama-3-8B-shaped KV (L=32, H=8, D=128, bf16, block 16), one 32K-token "
-                        "prompt = 2048 blocks x 2 MiB on a fragmented block table; step = preempt + resume "
+    U = 2 * SHAPE["L"] * SHAPE["bs"] * SHAPE["H"] * SHAPE["D"] * SHAPE["e"]
+    return {"workload": CFG["desc"] + "; step = preempt + resume "
                         + ("(self-lender: arena in the same HBM)" if n == 1 else "(peer lender rank^1 over NVLink)"),
-            "model": "llama3-8b-kv-shape", "global_batch": 1, "seq_len": 32768,
+            "name": CFG["name"], "model": "kv-shape-only (no weights)", "global_batch": CFG["nprompts"],
+            "seq_len": CFG["bpp"] * SHAPE["bs"],
             "parallelism": f"pairs{max(n // 2, 1)}" if n > 1 else "single",
-            "engine": args.engine, "bytes_per_step": 2 * NBLK * 2 * SHAPE["L"] * 16 * 8 * 128 * 2,
-            "l2": "inputs (4 GiB per direction) >> 126 MB L2; no flush needed"}
+            "engine": args.engine, "bytes_per_step": 2 * NBLK * U,
+            "l2": f"inputs ({NBLK * U / 2**30:.1f} GiB per direction) >> 126 MB L2; no flush needed"}
 
 
 def run_ours(args):
@@ -244,16 +267,18 @@ def run_ours(args):
             ctx.lend(aqua.MAPPED, imported, arena_bytes)
             mode = f"peer-lender rank{partner}"
     perm = block_permutation(NB, NB, seed=2).tolist()
-    ctx.adopt_blocks(1, perm[NBLK:])      # filler: keeps the prompt's blocks scattered over the pool
-    ctx.adopt_blocks(7, perm[:NBLK])
-    ctx.kv_fill_pattern(7, 0, NBLK * bs, SEED_PATTERN)
+    ctx.adopt_blocks(1, perm[NBLK:])      # filler: keeps the prompts' blocks scattered over the pool
+    bpp = CFG["bpp"]
+    for i, pid in enumerate(PIDS):
+        ctx.adopt_blocks(pid, perm[i * bpp:(i + 1) * bpp])
+        ctx.kv_fill_pattern(pid, 0, bpp * bs, SEED_PATTERN)
     torch.cuda.synchronize()
     swap = torch.cuda.Stream(device=dev)
     sw = swap.cuda_stream
 
     for _ in range(args.warmup):
-        ctx.swap_out([7], sw)
-        ctx.swap_in([7], sw)
+        ctx.swap_out(PIDS, sw)
+        ctx.swap_in(PIDS, sw)
     torch.cuda.synchronize()
 
     K = args.steps
@@ -268,9 +293,9 @@ def run_ours(args):
         start.record(swap)
         for k in range(K):
             ev[k][0].record(swap)
-            ctx.swap_out([7], sw)
+            ctx.swap_out(PIDS, sw)
             ev[k][1].record(swap)
-            ctx.swap_in([7], sw)
+            ctx.swap_in(PIDS, sw)
             ev[k][2].record(swap)
         end.record(swap)
         torch.cuda.synchronize()
@@ -287,7 +312,8 @@ def run_ours(args):
 
     # parity at full size: the resumed prompt still holds its pattern
     cnt = torch.zeros(1, dtype=torch.int64, device=dev)
-    ctx.kv_verify_pattern(7, NBLK * bs, SEED_PATTERN, cnt.data_ptr())
+    for pid in PIDS:
+        ctx.kv_verify_pattern(pid, bpp * bs, SEED_PATTERN, cnt.data_ptr())
     torch.cuda.synchronize()
     mism = int(cnt.item())
     if mism:
@@ -299,10 +325,10 @@ def run_ours(args):
     for _ in range(max(3, min(K, 10))):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        tk = ctx.swap_out([7], sw)
+        tk = ctx.swap_out(PIDS, sw)
         ctx.sync(tk)
         t1 = time.perf_counter()
-        new, tk2 = ctx.swap_in([7], sw)
+        new, tk2 = ctx.swap_in(PIDS, sw)
         ctx.sync(tk2)
         t2 = time.perf_counter()
         e2e_t.append(t2 - t0)
@@ -314,7 +340,7 @@ def run_ours(args):
     out_avg, in_avg = statistics.mean(out_ms), statistics.mean(in_ms)
 
     host = None
-    if ws == 1 and not args.no_host_baselines:
+    if ws == 1 and not args.no_host_baselines and CFG["name"] == "c2":
         host = host_baselines(ctx, layers, dev, aqua, args)
 
     if rank != 0:
@@ -363,8 +389,8 @@ def run_ours(args):
                         "table is produced on the host, the KV stays device-resident"},
         "gpu_launches": launches,
         "clocks": clk.summary(),
-        "parity": f"pattern verify: {mism} mismatching words over the whole 32K-token prompt after "
-                  f"{args.warmup + K} preempt/resume cycles",
+        "parity": f"pattern verify: {mism} mismatching words over all {len(PIDS)} prompt(s) "
+                  f"({NBLK * SHAPE['bs']} tokens) after {args.warmup + K} preempt/resume cycles",
         "host_baseline": host,
     }
     print(json.dumps(line), flush=True)
@@ -459,6 +485,7 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="c2")
     ap.add_argument("--engine", default="auto", choices=["auto", "tma", "ldst", "per_chunk", "gather_temp", "batch"])
     ap.add_argument("--max-ctas", type=int, default=0)
     ap.add_argument("--piece", type=int, default=0)
@@ -469,6 +496,7 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    select_config(args.config)
     if args.impl == "reference":
         run_reference(args)
     else:

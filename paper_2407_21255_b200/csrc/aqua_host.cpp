@@ -102,6 +102,7 @@ struct aqua_ctx {
 namespace {
 
 thread_local std::string g_err;
+constexpr int kHostCtas = 8;   // CTA cap for host-only swaps (PCIe-bound)
 
 // Makes `d` the current device for the scope of a call (no-op for dry runs).
 struct DevGuard {
@@ -305,18 +306,34 @@ aqua_status run_copy(aqua_ctx* c, const std::vector<Desc>& ds, aqua::Dir dir, cu
     }
     int ctas = 0;
     cudaError_t e;
+    // A call whose images all live in host DRAM is PCIe-bound: 4 SMs already
+    // saturate it (profiles/r01_host_ctas.jsonl), so cap it at 8 and leave
+    // the other SMs to decode (unless the caller set a smaller cap).
+    int cap = c->max_ctas;
+    bool all_host = true;
+    for (const Desc& d : ds) all_host = all_host && (d.slot_arena & kArenaBit);
+    if (all_host && (cap == 0 || cap > kHostCtas)) cap = kHostCtas;
     if (engine == AQUA_KERNEL_TMA) {
-      int piece = c->tma_piece > 0 ? c->tma_piece : 32768;
-      if (piece > c->S) piece = static_cast<int>(c->S);
+      // stage = 32 KiB (or the option): one piece of a large chunk, or a
+      // group of whole small chunks that are contiguous in the image
+      const int stage = c->tma_piece > 0 ? c->tma_piece : 32768;
+      int piece = stage;
+      if (piece >= c->S) {
+        piece = static_cast<int>(c->S);
+        p.group = std::max(1, std::min(stage / piece, 2 * c->L));
+      } else {
+        p.group = 1;
+      }
       p.piece = piece;
       p.npieces = static_cast<int32_t>((c->S + piece - 1) / piece);
       p.nitems = p.ndesc * 2 * p.L * p.npieces;
-      e = aqua::launch_swap_tma(p, dir, c->num_sms, c->max_ctas, c->tma_stages, st, &ctas);
+      e = aqua::launch_swap_tma(p, dir, c->num_sms, cap, c->tma_stages, st, &ctas);
     } else {
       p.piece = 4096;
+      p.group = 1;
       p.npieces = static_cast<int32_t>((c->S + 4095) / 4096);
       p.nitems = p.ndesc * 2 * p.L * p.npieces;
-      e = aqua::launch_swap_ldst(p, dir, c->num_sms, c->max_ctas, st, &ctas);
+      e = aqua::launch_swap_ldst(p, dir, c->num_sms, all_host && cap == kHostCtas ? 2 * kHostCtas : cap, st, &ctas);
     }
     if (e != cudaSuccess) return cuda_fail(c, e, "swap kernel launch");
     c->launches++;
@@ -372,6 +389,7 @@ aqua_status run_copy(aqua_ctx* c, const std::vector<Desc>& ds, aqua::Dir dir, cu
     p.desc = static_cast<const Desc*>(dd);
     p.arena_base[0] = reinterpret_cast<uint64_t>(c->d_temp);
     p.piece = 4096;
+    p.group = 1;
     p.npieces = static_cast<int32_t>((c->S + 4095) / 4096);
     p.nitems = p.ndesc * 2 * p.L * p.npieces;
     auto runs = [&](bool to_arena) -> aqua_status {

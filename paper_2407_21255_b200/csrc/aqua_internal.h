@@ -28,7 +28,7 @@ struct SwapParams {
   int32_t L;
   int32_t piece;               // bytes per work item (multiple of 16, divides nothing in particular)
   int32_t npieces;             // ceil(S / piece)
-  int32_t pad_;
+  int32_t group;               // TMA: chunks per stage when npieces == 1 (else 1)
   int64_t S, U, P_kv, P_b;
   int64_t nitems;              // ndesc * 2L * npieces
   Desc inl[kInlineDesc];       // inline descriptors when desc == nullptr

@@ -99,15 +99,6 @@ struct Cursor {
     c = static_cast<int32_t>(r / p.npieces);
     q = static_cast<int32_t>(r - int64_t(c) * p.npieces);
   }
-  __device__ __forceinline__ void next(const SwapParams& p) {
-    if (++q == p.npieces) {
-      q = 0;
-      if (++c == 2 * p.L) {
-        c = 0;
-        ++j;
-      }
-    }
-  }
 };
 
 __device__ __forceinline__ Desc desc_at(const SwapParams& p, int64_t j) {
@@ -139,62 +130,126 @@ __device__ __forceinline__ void item_addrs(const SwapParams& p, const Desc d, in
 }
 
 // ------------------------------------------------------------ TMA ring kernel
-// One CTA = one warp; lane 0 drives a `stages`-deep ring of `piece`-byte
-// shared-memory stages: cp.async.bulk loads (mbarrier complete_tx) run
-// stages-1 items ahead of the cp.async.bulk stores.  Each CTA owns a
-// contiguous range of items, so its stores form one long contiguous run in
-// the image (swap_out) / its loads do (swap_in).
+// One CTA = one warp; lane 0 drives a `stages`-deep ring of shared-memory
+// stages: cp.async.bulk loads (mbarrier complete_tx) run stages-1 units
+// ahead of the cp.async.bulk stores.  Each CTA owns a contiguous range of
+// items, so its image-side traffic is one long contiguous run.
+//
+// A unit is `group` consecutive chunks of one descriptor when a chunk fits a
+// piece (S <= piece): they are contiguous in the image, so the image side is
+// ONE bulk op of k*S bytes and the pool side k bulk ops of S bytes.  With
+// larger chunks a unit is one piece of one chunk (group == 1).
+struct Unit {
+  int64_t j;
+  int32_t c, q;
+  int64_t left;     // items of this CTA not yet covered
+};
+
+__device__ __forceinline__ int unit_len(const SwapParams& p, const Unit& u) {
+  if (p.group == 1) return 1;
+  int64_t k = 2 * p.L - u.c;
+  if (k > p.group) k = p.group;
+  if (k > u.left) k = u.left;
+  return static_cast<int>(k);
+}
+
+__device__ __forceinline__ void unit_next(const SwapParams& p, Unit& u, int k) {
+  u.left -= k;
+  if (p.group == 1) {
+    if (++u.q == p.npieces) {
+      u.q = 0;
+      if (++u.c == 2 * p.L) {
+        u.c = 0;
+        ++u.j;
+      }
+    }
+  } else {
+    u.c += k;
+    if (u.c == 2 * p.L) {
+      u.c = 0;
+      ++u.j;
+    }
+  }
+}
+
 template <Dir D>
 __global__ void __launch_bounds__(32) swap_tma_kernel(const __grid_constant__ SwapParams p, const int stages) {
   extern __shared__ __align__(128) uint8_t smem[];
   if (threadIdx.x != 0) return;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + size_t(stages) * p.piece);
+  const int64_t stage_bytes = int64_t(p.piece) * p.group;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + size_t(stages) * stage_bytes);
   const int64_t G = gridDim.x, b = blockIdx.x;
   const int64_t i0 = p.nitems * b / G, i1 = p.nitems * (b + 1) / G;
-  const int64_t n = i1 - i0;
-  if (n <= 0) return;
+  if (i1 <= i0) return;
   for (int s = 0; s < stages; ++s) mbar_init(&bars[s], 1);
   fence_mbar_init();
   const uint64_t pol = policy_evict_first();
 
-  Cursor lc, sc;
-  lc.init(i0, p);
-  sc = lc;
-  int64_t nload = 0;
-  int lstage = 0;
+  Unit lu, su;
+  {
+    Cursor cu;
+    cu.init(i0, p);
+    lu = Unit{cu.j, cu.c, cu.q, i1 - i0};
+    su = lu;
+  }
+  int lstage = 0, issued = 0;
   auto issue_load = [&]() {
+    const int k = unit_len(p, lu);
+    const Desc d = desc_at(p, lu.j);
+    uint8_t* buf = smem + size_t(lstage) * stage_bytes;
     const uint8_t* src;
     uint8_t* dst;
     uint32_t bytes;
-    item_addrs<D>(p, desc_at(p, lc.j), lc.c, lc.q, src, dst, bytes);
-    uint8_t* buf = smem + size_t(lstage) * p.piece;
-    mbar_expect_tx(&bars[lstage], bytes);
-    bulk_g2s(buf, src, bytes, &bars[lstage], pol);
-    lc.next(p);
-    ++nload;
+    item_addrs<D>(p, d, lu.c, lu.q, src, dst, bytes);
+    if (k == 1) {
+      mbar_expect_tx(&bars[lstage], bytes);
+      bulk_g2s(buf, src, bytes, &bars[lstage], pol);
+    } else if (D == kIn) {                 // image side: one contiguous load of k chunks
+      mbar_expect_tx(&bars[lstage], bytes * k);
+      bulk_g2s(buf, src, bytes * k, &bars[lstage], pol);
+    } else {                               // pool side: k scattered chunk loads
+      mbar_expect_tx(&bars[lstage], bytes * k);
+      for (int t = 0; t < k; ++t) {
+        item_addrs<D>(p, d, lu.c + t, 0, src, dst, bytes);
+        bulk_g2s(buf + size_t(t) * bytes, src, bytes, &bars[lstage], pol);
+      }
+    }
+    unit_next(p, lu, k);
+    ++issued;
     if (++lstage == stages) lstage = 0;
   };
-  const int64_t pre = n < stages - 1 ? n : stages - 1;
-  while (nload < pre) issue_load();
+  while (lu.left > 0 && issued < stages - 1) issue_load();
 
   int sstage = 0;
   uint32_t parity = 0;
-  for (int64_t k = 0; k < n; ++k) {
+  while (su.left > 0) {
     mbar_wait(&bars[sstage], parity);
+    const int k = unit_len(p, su);
+    const Desc d = desc_at(p, su.j);
+    uint8_t* buf = smem + size_t(sstage) * stage_bytes;
     const uint8_t* src;
     uint8_t* dst;
     uint32_t bytes;
-    item_addrs<D>(p, desc_at(p, sc.j), sc.c, sc.q, src, dst, bytes);
-    bulk_s2g(dst, smem + size_t(sstage) * p.piece, bytes, pol);
+    item_addrs<D>(p, d, su.c, su.q, src, dst, bytes);
+    if (k == 1) {
+      bulk_s2g(dst, buf, bytes, pol);
+    } else if (D == kOut) {                // image side: one contiguous store of k chunks
+      bulk_s2g(dst, buf, bytes * k, pol);
+    } else {                               // pool side: k scattered chunk stores
+      for (int t = 0; t < k; ++t) {
+        item_addrs<D>(p, d, su.c + t, 0, src, dst, bytes);
+        bulk_s2g(dst, buf + size_t(t) * bytes, bytes, pol);
+      }
+    }
     bulk_commit();
-    sc.next(p);
+    unit_next(p, su, k);
     if (++sstage == stages) {
       sstage = 0;
       parity ^= 1u;
     }
-    if (nload < n) {
-      bulk_wait_read<1>();  // the store of item k-1 has finished reading its stage
-      issue_load();         // item k+stages-1 -> the stage of item k-1
+    if (lu.left > 0) {
+      bulk_wait_read<1>();  // the stores of the previous unit have finished reading its stage
+      issue_load();         // -> the stage of the previous unit
     }
   }
   bulk_wait<0>();
@@ -311,10 +366,11 @@ cudaError_t launch_swap_tma(const SwapParams& p, Dir dir, int num_sms, int grid_
   // One CTA per SM and a shallow ring: 3 x 32 KiB or 64 KiB of loads in
   // flight per SM measured best for HBM on B200 (profiles/r01_stages.jsonl);
   // deeper rings lose 3-4 %.
-  int stages = stages_opt > 0 ? stages_opt : std::max(3, std::min(32, (64 * 1024) / p.piece));
+  const int stage_bytes = p.piece * p.group;
+  int stages = stages_opt > 0 ? stages_opt : std::max(3, std::min(32, (64 * 1024) / stage_bytes));
   stages = std::max(2, std::min(stages, 32));
-  while (stages > 2 && tma_smem_bytes(p.piece, stages) > 227 * 1024) --stages;
-  const int smem = tma_smem_bytes(p.piece, stages);
+  while (stages > 2 && tma_smem_bytes(stage_bytes, stages) > 227 * 1024) --stages;
+  const int smem = tma_smem_bytes(stage_bytes, stages);
   const int grid = grid_for<void>(p.nitems, 1, num_sms, 1, grid_cap);
   // the opt-in smem attribute is per device; remember the largest set so far
   static thread_local int set_smem[2][64] = {};

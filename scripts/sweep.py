@@ -40,6 +40,21 @@ def setup(L, bs, H, D, NB, nblk, host=False):
     return ctx, layers, arena, U
 
 
+def time_tickets(ctx, reps, stream):
+    """Device time of each copy from the library's timing events (excludes
+    host enqueue gaps)."""
+    ctx.set_option(aqua.OPT_TIMING, 1)
+    outs, ins = [], []
+    for _ in range(reps + 2):
+        t1 = ctx.swap_out([7], stream.cuda_stream)
+        _, t2 = ctx.swap_in([7], stream.cuda_stream)
+        torch.cuda.synchronize()
+        outs.append(ctx.ticket_elapsed(t1))
+        ins.append(ctx.ticket_elapsed(t2))
+    ctx.set_option(aqua.OPT_TIMING, 0)
+    return statistics.median(outs[2:]), statistics.median(ins[2:])
+
+
 def time_swaps(ctx, reps, stream):
     outs, ins = [], []
     for _ in range(2):
@@ -77,6 +92,32 @@ def engines():
                           "in_hbm_GBps": round(2 * nbytes / i / 1e6, 1)}), flush=True)
 
 
+def host_ctas():
+    """How many SMs the host (PCIe) path needs: SMs left for decode."""
+    L, bs, H, D, NB, nblk = 32, 16, 8, 128, 1024, 512
+    ctx, layers, arena, U = setup(L, bs, H, D, NB, nblk, host=True)
+    s = torch.cuda.Stream()
+    for eng in ("tma", "ldst"):
+        for ctas in (1, 2, 4, 8, 16, 32, 74, 148):
+            ctx.set_option(aqua.OPT_KERNEL, ENG[eng])
+            ctx.set_option(aqua.OPT_MAX_CTAS, ctas)
+            o, i = time_tickets(ctx, 3, s)
+            print(json.dumps({"host_ctas": ctas, "engine": eng, "out_GBps": round(nblk * U / o / 1e6, 2),
+                              "in_GBps": round(nblk * U / i / 1e6, 2)}), flush=True)
+
+
+def self_ctas():
+    """CTAs (SMs) needed to saturate HBM on the self-lender path."""
+    L, bs, H, D, NB, nblk = 32, 16, 8, 128, 4096, 2048
+    ctx, layers, arena, U = setup(L, bs, H, D, NB, nblk)
+    s = torch.cuda.Stream()
+    for ctas in (8, 16, 32, 48, 64, 96, 128, 148):
+        ctx.set_option(aqua.OPT_MAX_CTAS, ctas)
+        o, i = time_tickets(ctx, 5, s)
+        print(json.dumps({"self_ctas": ctas, "out_hbm_GBps": round(2 * nblk * U / o / 1e6, 1),
+                          "in_hbm_GBps": round(2 * nblk * U / i / 1e6, 1)}), flush=True)
+
+
 def stages():
     L, bs, H, D, NB, nblk = 32, 16, 8, 128, 4096, 2048
     ctx, layers, arena, U = setup(L, bs, H, D, NB, nblk)
@@ -106,7 +147,7 @@ def c5(host=False):
             ctx, layers, arena, _ = setup(L, bs, H, D, NB, nblk, host=host)
             s = torch.cuda.Stream()
             reps = 20 if nblk * U < (1 << 30) else 5
-            o, i = time_swaps(ctx, reps, s)
+            o, i = time_tickets(ctx, reps, s)
             print(json.dumps({"c5": "host" if host else "self", "bs": bs, "U": U, "blocks": nblk,
                               "bytes": nblk * U, "out_ms": round(o, 5), "in_ms": round(i, 5),
                               "out_GBps": round(nblk * U / o / 1e6, 2), "in_GBps": round(nblk * U / i / 1e6, 2)}),
@@ -126,6 +167,10 @@ if __name__ == "__main__":
         c5(host=True)
     elif what == "stages":
         stages()
+    elif what == "host_ctas":
+        host_ctas()
+    elif what == "self_ctas":
+        self_ctas()
 
 
 def latency():

@@ -71,19 +71,24 @@ SHAPES = {
     "ragged_10KiB": (3, 16, 5, 64),      # S = 10 KiB: TMA pieces 4K, 4K, 2K (piece option 4096)
     "llama_bs32": (4, 32, 8, 128),       # S = 64 KiB (4 pieces)
     "odd_48KiB": (2, 16, 12, 128),       # S = 48 KiB (3 pieces)
-    "c4_shape": (5, 16, 2, 128),         # S = 8 KiB (Llama-70B TP4 chunk)
+    "c4_shape": (5, 16, 2, 128),         # S = 8 KiB (Llama-70B TP4 chunk): TMA units of 4,4,2 chunks
+    "l3_8KiB": (3, 16, 2, 128),          # S = 8 KiB, 6 chunks per block: units of 4,2
 }
 
 
 @pytest.mark.parametrize("shape", list(SHAPES))
 @pytest.mark.parametrize("engine", ["tma", "ldst"])
 @pytest.mark.parametrize("seed", [0, 1])
-def test_random_sequences_bytes(shape, engine, seed):
+@pytest.mark.parametrize("ctas", [0, 3])
+def test_random_sequences_bytes(shape, engine, seed, ctas):
+    """ctas=3 forces many units per CTA (TMA: grouped chunks split at ragged
+    descriptor and CTA-range boundaries)."""
     L, bs, H, D = SHAPES[shape]
     rnd = random.Random(seed * 31 + len(shape))
     NB = 24
     rig = Rig(L=L, bs=bs, H=H, D=D, e=2, NB=NB, lender_slots=10, host_slots=8, seed=seed)
     rig.ctx.set_option(aqua.OPT_KERNEL, ENGINES[engine])
+    rig.ctx.set_option(aqua.OPT_MAX_CTAS, ctas)
     if engine == "tma" and shape == "ragged_10KiB":
         rig.ctx.set_option(aqua.OPT_TMA_PIECE, 4096)     # S = 10 KiB -> pieces 4K, 4K, 2K
     pids = list(range(5))
