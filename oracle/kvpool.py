@@ -158,7 +158,7 @@ class Pool:
             raise AquaError(E_INVAL, "kind")
         return nslots
 
-    def arena(self, loc: int) -> Arena:
+    def arena(self, loc: int) -> Optional[Arena]:
         return self.peer if loc == LOC_PEER else self.host
 
     # ---------------------------------------------------------------- C-2
@@ -287,6 +287,63 @@ class Pool:
             ar.free.update(p.slots)
             p.state, p.location, p.slots, p.blocks = RESIDENT, LOC_LOCAL, [], new
             out.append(list(new))
+        return out
+
+    # ---------------------------------------------------------- NEXT-1
+    def migrate(self, pids: Sequence[int], dst: int) -> List[tuple]:
+        """Move swap images between arenas (NEXT-1).  Paper Sec. 6
+        "Reclaiming AquaTensors": a producer whose load rises
+        takes its memory back and the consumer's tensors must move off it;
+        when the load falls the memory is offered again and AquaLib "moves
+        the offloaded tensors of the consumer back to the producer's GPU"
+        (fig:elastic_result).  SPEC migrate S:399-407.
+
+        All-or-nothing: pids listed once, each SWAPPED and not already in
+        `dst`, the dst arena present with room for all of them.  Per prompt
+        in call order: new = the n_p lowest free dst slots (R4); per j:
+            dst[new_j*U : +U] = src[old_j*U : +U]
+        then the old slots are freed.  Returns [(pid, new_slots)]."""
+        lay = self.lay
+        pids = [int(p) for p in pids]
+        if dst not in (LOC_PEER, LOC_HOST) or len(set(pids)) != len(pids):
+            raise AquaError(E_INVAL, "bad dst or duplicate pid")
+        for pid in pids:
+            p = self.prompts.get(pid)
+            if p is None or p.state != SWAPPED or p.location == dst:
+                raise AquaError(E_STATE, f"pid {pid} has no image outside dst")
+        ar_d = self.arena(dst)
+        if ar_d is None:
+            raise AquaError(E_NOSPACE, "no such arena")
+        need = sum(len(self.prompts[pid].slots) for pid in pids)
+        if need > len(ar_d.free):
+            raise AquaError(E_NOSPACE, "dst arena full")
+        out = []
+        for pid in pids:
+            p = self.prompts[pid]
+            ar_s = self.arena(p.location)
+            new = sorted(ar_d.free)[:len(p.slots)]
+            for s in new:
+                ar_d.free.remove(s)
+            if ar_s.data is not None and ar_d.data is not None:
+                for s_old, s_new in zip(p.slots, new):
+                    ar_d.data[s_new * lay.U:(s_new + 1) * lay.U] = ar_s.data[s_old * lay.U:(s_old + 1) * lay.U]
+            ar_s.free.update(p.slots)
+            p.location, p.slots = dst, list(new)
+            out.append((pid, list(new)))
+        return out
+
+    def reclaim(self) -> List[tuple]:
+        """The GPU lender takes its memory back: every image on
+        it moves to the host arena, ascending pid, then the lender is
+        detached (a later lend() is a re-offer).  All-or-nothing
+        (NOSPACE if the host cannot hold them); idempotent without a lender
+        ("double reclaim -> no-op")."""
+        if self.peer is None:
+            return []
+        pids = sorted(pid for pid, p in self.prompts.items()
+                      if p.state == SWAPPED and p.location == LOC_PEER)
+        out = self.migrate(pids, LOC_HOST) if pids else []
+        self.peer = None
         return out
 
     # ---------------------------------------------------------------- C-6

@@ -310,3 +310,200 @@ def test_bruteforce_op_sequences(NB, nslots, length):
             pool.check_invariants()
         n += 1
     assert n == len(ops) ** length
+
+
+# ------------------------------------------------------------------ NEXT-1
+def test_migrate_and_reclaim_bytes():
+    """Images keep their bytes through lender -> host -> lender moves, and a
+    resume from the new place restores the original blocks (I1 across
+    migration); SPEC S:384-392 reclaim examples."""
+    pool = make_pool(L=2, NB=16)
+    U = pool.lay.U
+    peer = np.zeros(8 * U, np.uint8)
+    host = np.zeros(8 * U, np.uint8)
+    pool.lend(kp.LOC_PEER, 8 * U, peer)
+    pool.lend(kp.LOC_HOST, 8 * U, host)
+    pool.adopt_blocks(1, [9, 2, 5])
+    pool.adopt_blocks(2, [0, 1])
+    before = planes(pool).copy()
+    pool.swap_out([1, 2])
+    img1 = peer.reshape(8, U)[[0, 1, 2]].copy()
+    # reclaim: both images move to the host, ascending pid, lowest host slots
+    moved = pool.reclaim()
+    assert moved == [(1, [0, 1, 2]), (2, [3, 4])]
+    assert pool.peer is None and pool.query(1)[1] == kp.LOC_HOST
+    assert np.array_equal(host.reshape(8, U)[[0, 1, 2]], img1)
+    assert pool.reclaim() == []                       # double reclaim: no-op
+    # re-offer and move pid 2 back (P:1086)
+    peer2 = np.zeros(4 * U, np.uint8)
+    pool.lend(kp.LOC_PEER, 4 * U, peer2)
+    assert pool.migrate([2], kp.LOC_PEER) == [(2, [0, 1])]
+    assert len(pool.host.free) == 8 - 3
+    new = pool.swap_in([2, 1])
+    after = planes(pool)
+    for pid, old in ((2, [0, 1]), (1, [9, 2, 5])):
+        ids = new[0] if pid == 2 else new[1]
+        for j, b in enumerate(ids):
+            assert np.array_equal(after[:, :, b, :], before[:, :, old[j], :])
+    pool.check_invariants()
+
+
+def test_migrate_errors_all_or_nothing():
+    pool = make_pool(L=1, NB=8)
+    U = pool.lay.U
+    pool.lend(kp.LOC_PEER, 4 * U)
+    pool.lend(kp.LOC_HOST, 2 * U)
+    pool.alloc_blocks(1, 2)
+    pool.alloc_blocks(2, 2)
+    pool.alloc_blocks(3, 1)
+    pool.swap_out([1, 2])
+    snap = (frozenset(pool.peer.free), frozenset(pool.host.free), pool.query(1), pool.query(2))
+    for fn, code in [(lambda: pool.migrate([1, 2], kp.LOC_HOST), kp.E_NOSPACE),   # host has 2 slots
+                     (lambda: pool.migrate([1], kp.LOC_PEER), kp.E_STATE),        # already there
+                     (lambda: pool.migrate([3], kp.LOC_HOST), kp.E_STATE),        # resident
+                     (lambda: pool.migrate([1, 1], kp.LOC_HOST), kp.E_INVAL),
+                     (lambda: pool.reclaim(), kp.E_NOSPACE)]:
+        with pytest.raises(kp.AquaError) as e:
+            fn()
+        assert e.value.code == code
+        assert (frozenset(pool.peer.free), frozenset(pool.host.free), pool.query(1), pool.query(2)) == snap
+    assert pool.peer is not None                      # failed reclaim keeps the lender
+
+
+class TwoArenaModel:
+    """Independent model with two arenas for the NEXT-1 brute force."""
+
+    def __init__(self, NB, np_, nh):
+        self.blk = [None] * NB
+        self.ar = {1: [None] * np_, 2: [None] * nh}
+        self.peer_on = True
+        self.st = {}          # pid -> ("R", ids) | ("S", loc, slots)
+
+    @staticmethod
+    def _free(arr, n):
+        out = [i for i, o in enumerate(arr) if o is None][:n]
+        return out if len(out) == n else None
+
+    def op(self, name, arg):
+        if name == "alloc":
+            pid, n = arg
+            if pid in self.st and self.st[pid][0] != "R":
+                return kp.E_STATE
+            ids = self._free(self.blk, n)
+            if ids is None:
+                return kp.E_NOBLOCKS
+            for i in ids:
+                self.blk[i] = pid
+            if pid not in self.st:
+                self.st[pid] = ("R", [])
+            self.st[pid][1].extend(ids)
+            return ids
+        if name == "out":
+            pid = arg
+            if self.st.get(pid, ("X",))[0] != "R":
+                return kp.E_STATE
+            ids = self.st[pid][1]
+            for loc in ((1, 2) if self.peer_on else (2,)):
+                sl = self._free(self.ar[loc], len(ids))
+                if sl is not None:
+                    break
+            else:
+                return kp.E_NOSPACE
+            for i in ids:
+                self.blk[i] = None
+            for x in sl:
+                self.ar[loc][x] = pid
+            self.st[pid] = ("S", loc, sl)
+            return (loc, sl)
+        if name == "in":
+            pid = arg
+            if self.st.get(pid, ("X",))[0] != "S":
+                return kp.E_STATE
+            _, loc, sl = self.st[pid]
+            ids = self._free(self.blk, len(sl))
+            if ids is None:
+                return kp.E_NOBLOCKS
+            for i in ids:
+                self.blk[i] = pid
+            for x in sl:
+                self.ar[loc][x] = None
+            self.st[pid] = ("R", ids)
+            return ids
+        if name == "mig":
+            pid, dst = arg
+            s = self.st.get(pid, ("X",))
+            if s[0] != "S" or s[1] == dst:
+                return kp.E_STATE
+            if dst == 1 and not self.peer_on:
+                return kp.E_NOSPACE
+            new = self._free(self.ar[dst], len(s[2]))
+            if new is None:
+                return kp.E_NOSPACE
+            for x in s[2]:
+                self.ar[s[1]][x] = None
+            for x in new:
+                self.ar[dst][x] = pid
+            self.st[pid] = ("S", dst, new)
+            return new
+        if name == "reclaim":
+            if not self.peer_on:
+                return []
+            pids = sorted(p for p, s in self.st.items() if s[0] == "S" and s[1] == 1)
+            need = sum(len(self.st[p][2]) for p in pids)
+            if need > sum(o is None for o in self.ar[2]):
+                return kp.E_NOSPACE
+            res = [(p, self.op("mig", (p, 2))) for p in pids]
+            self.peer_on = False
+            self.ar[1] = []
+            return res
+        if name == "relend":
+            if self.peer_on:
+                return kp.E_INVAL
+            self.peer_on = True
+            self.ar[1] = [None] * arg
+            return arg
+
+
+def _snap2(pool):
+    return (frozenset(pool.free), None if pool.peer is None else frozenset(pool.peer.free),
+            frozenset(pool.host.free),
+            {k: (v.state, v.location, tuple(v.blocks), tuple(v.slots)) for k, v in pool.prompts.items()})
+
+
+def test_bruteforce_with_migration():
+    ops = []
+    for pid in range(2):
+        ops += [("alloc", (pid, 1)), ("alloc", (pid, 2)), ("out", pid), ("in", pid),
+                ("mig", (pid, 1)), ("mig", (pid, 2))]
+    ops += [("reclaim", None), ("relend", 3)]
+    n = 0
+    for seq in itertools.product(ops, repeat=4):
+        lay = kp.Layout(L=1, bs=16, H=1, D=8, e=2, NB=4)
+        pool = kp.Pool(lay)
+        pool.lend(kp.LOC_PEER, 2 * lay.U)
+        pool.lend(kp.LOC_HOST, 3 * lay.U)
+        ref = TwoArenaModel(4, 2, 3)
+        for name, arg in seq:
+            want = ref.op(name, arg)
+            snap = _snap2(pool)
+            try:
+                if name == "alloc":
+                    got = pool.alloc_blocks(*arg)
+                elif name == "out":
+                    (_, loc, sl), = pool.swap_out([arg])
+                    got = (loc, sl)
+                elif name == "in":
+                    got = pool.swap_in([arg])[0]
+                elif name == "mig":
+                    got = pool.migrate([arg[0]], arg[1])[0][1]
+                elif name == "reclaim":
+                    got = pool.reclaim()
+                else:
+                    got = pool.lend(kp.LOC_PEER, arg * lay.U)
+            except kp.AquaError as e:
+                got = e.code
+                assert _snap2(pool) == snap
+            assert got == want, (seq, name, arg, got, want)
+            pool.check_invariants()
+        n += 1
+    assert n == len(ops) ** 4
