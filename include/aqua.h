@@ -188,6 +188,24 @@ AQUA_API aqua_status aqua_swap_in(aqua_ctx* ctx, int32_t n, const uint64_t* pids
  * are freed. */
 AQUA_API aqua_status aqua_free(aqua_ctx* ctx, uint64_t pid, aqua_stream_t stream);
 
+/* NEXT-1, elastic lending (Sec. 6 "Reclaiming AquaTensors" P:758-768;
+ * fig:elastic_result P:1073-1099).  Move the swap images of SWAPPED prompts
+ * (listed once, none already in dst) to arena dst_loc (AQUA_LOC_PEER or
+ * AQUA_LOC_HOST), lowest free slots in call order (R4):
+ *   dst[new_j*U : +U] = src[old_j*U : +U];  the old slots are freed.
+ * All-or-nothing: AQUA_E_NOSPACE if dst is missing or too small.  One fused
+ * kernel launch (arena -> arena) on `stream`. */
+AQUA_API aqua_status aqua_migrate(aqua_ctx* ctx, int32_t n, const uint64_t* pids, int32_t dst_loc,
+                                  aqua_stream_t stream, uint64_t* out_ticket);
+/* The GPU lender takes its memory back: every image on it moves to the host
+ * arena (ascending pid), then the lender is detached, so later swap_outs go
+ * to the host until aqua_lend is called again (a re-offer).  The
+ * ticket covers every library access to the lender: after it completes the
+ * lender's memory is unused (a library-owned arena is freed then).
+ * All-or-nothing (AQUA_E_NOSPACE if the host cannot hold the images);
+ * without a GPU lender it is a no-op with ticket 0. */
+AQUA_API aqua_status aqua_reclaim(aqua_ctx* ctx, aqua_stream_t stream, uint64_t* out_ticket);
+
 /* Make `stream` wait for a ticket (cudaStreamWaitEvent; no-op if done). */
 AQUA_API aqua_status aqua_wait(aqua_ctx* ctx, uint64_t ticket, aqua_stream_t stream);
 /* Block the host until the ticket completes. */

@@ -30,7 +30,7 @@ OPT_KERNEL, OPT_MAX_CTAS, OPT_TMA_PIECE, OPT_TMA_STAGES, OPT_TIMING = 1, 2, 3, 4
 # Every symbol include/aqua.h declares (checked by tests/test_abi.py).
 SYMBOLS = [
     "aqua_create", "aqua_destroy", "aqua_lend", "aqua_alloc_blocks", "aqua_adopt_blocks",
-    "aqua_swap_out", "aqua_swap_in", "aqua_free", "aqua_wait", "aqua_sync", "aqua_ticket_done", "aqua_ticket_elapsed",
+    "aqua_swap_out", "aqua_swap_in", "aqua_free", "aqua_migrate", "aqua_reclaim", "aqua_wait", "aqua_sync", "aqua_ticket_done", "aqua_ticket_elapsed",
     "aqua_query", "aqua_counts", "aqua_arena_base", "aqua_set_option", "aqua_get_option",
     "aqua_last_descriptors", "aqua_launch_count", "aqua_ipc_export", "aqua_ipc_import",
     "aqua_ipc_close", "aqua_ipc_alloc", "aqua_ipc_free", "aqua_can_access_peer", "aqua_kv_fill_pattern", "aqua_kv_verify_pattern",
@@ -66,6 +66,8 @@ def _load() -> C.CDLL:
         "aqua_swap_out": (C.c_int, [VP, I32, P(U64), VP, P(U64)]),
         "aqua_swap_in": (C.c_int, [VP, I32, P(U64), VP, P(I32), I64, P(I32), P(U64)]),
         "aqua_free": (C.c_int, [VP, U64, VP]),
+        "aqua_migrate": (C.c_int, [VP, I32, P(U64), I32, VP, P(U64)]),
+        "aqua_reclaim": (C.c_int, [VP, VP, P(U64)]),
         "aqua_wait": (C.c_int, [VP, U64, VP]),
         "aqua_sync": (C.c_int, [VP, U64]),
         "aqua_ticket_done": (C.c_int, [VP, U64, P(I32)]),
@@ -179,6 +181,17 @@ class Ctx:
 
     def free(self, pid: int, stream: int = 0) -> None:
         self._c(lib.aqua_free(self.h, pid, C.c_void_p(stream or None)))
+
+    def migrate(self, pids: Sequence[int], dst_loc: int, stream: int = 0) -> int:
+        a = np.ascontiguousarray(pids, dtype=np.uint64)
+        t = C.c_uint64()
+        self._c(lib.aqua_migrate(self.h, len(a), _u64p(a), dst_loc, C.c_void_p(stream or None), C.byref(t)))
+        return t.value
+
+    def reclaim(self, stream: int = 0) -> int:
+        t = C.c_uint64()
+        self._c(lib.aqua_reclaim(self.h, C.c_void_p(stream or None), C.byref(t)))
+        return t.value
 
     def wait(self, ticket: int, stream: int = 0) -> None:
         self._c(lib.aqua_wait(self.h, ticket, C.c_void_p(stream or None)))

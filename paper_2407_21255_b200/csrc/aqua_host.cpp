@@ -90,6 +90,13 @@ struct aqua_ctx {
   bool timing = false;
   std::unordered_map<uint64_t, float> elapsed;  // retired timed tickets -> ms
   std::deque<uint64_t> elapsed_order;
+  // reclaimed library-owned lender arenas, freed once their ticket completes
+  struct Zombie {
+    int device;
+    uint8_t* ptr;
+    uint64_t ticket;
+  };
+  std::vector<Zombie> zombies;
   // gather-temp baseline buffer
   uint8_t* d_temp = nullptr;
   size_t temp_cap = 0;
@@ -164,6 +171,18 @@ void retire(aqua_ctx* c) {
   }
   while (!c->stage_live.empty() && !c->live.count(c->stage_live.front().ticket))
     c->stage_live.pop_front();
+  for (auto it = c->zombies.begin(); it != c->zombies.end();) {
+    if (c->live.count(it->ticket)) {
+      ++it;
+      continue;
+    }
+    int prev = -1;
+    cudaGetDevice(&prev);
+    cudaSetDevice(it->device);
+    cudaFree(it->ptr);
+    if (prev >= 0) cudaSetDevice(prev);
+    it = c->zombies.erase(it);
+  }
 }
 
 aqua_status get_event(aqua_ctx* c, bool timing, cudaEvent_t* ev) {
@@ -284,7 +303,8 @@ aqua_status run_copy(aqua_ctx* c, const std::vector<Desc>& ds, aqua::Dir dir, cu
   p.U = c->U;
   p.P_kv = c->P_kv;
   p.P_b = c->P_b;
-  const int engine = c->kernel == AQUA_KERNEL_AUTO ? AQUA_KERNEL_TMA : c->kernel;
+  int engine = c->kernel == AQUA_KERNEL_AUTO ? AQUA_KERNEL_TMA : c->kernel;
+  if (dir == aqua::kMig && engine != AQUA_KERNEL_LDST) engine = AQUA_KERNEL_TMA;  // baselines do not migrate
 
   auto chunk_ptrs = [&](const Desc& d, int cc, uint8_t** pool, uint8_t** img) {
     const int l = cc >> 1, kv = cc & 1;
@@ -311,7 +331,9 @@ aqua_status run_copy(aqua_ctx* c, const std::vector<Desc>& ds, aqua::Dir dir, cu
     // the other SMs to decode (unless the caller set a smaller cap).
     int cap = c->max_ctas;
     bool all_host = true;
-    for (const Desc& d : ds) all_host = all_host && (d.slot_arena & kArenaBit);
+    for (const Desc& d : ds)
+      all_host = all_host && ((d.slot_arena & kArenaBit) ||
+                              (dir == aqua::kMig && (static_cast<uint32_t>(d.block) & kArenaBit)));
     if (all_host && (cap == 0 || cap > kHostCtas)) cap = kHostCtas;
     if (engine == AQUA_KERNEL_TMA) {
       // stage = 32 KiB (or the option): one piece of a large chunk, or a
@@ -537,6 +559,10 @@ aqua_status aqua_destroy(aqua_ctx* c) {
     if (c->gpu.present && c->gpu.owned) {
       DevGuard g2(c->gpu.device);
       cudaFree(c->gpu.base);
+    }
+    for (auto& z : c->zombies) {
+      DevGuard g2(z.device);
+      cudaFree(z.ptr);
     }
     if (c->host.present && c->host.owned) cudaFreeHost(c->host.host_ptr);
     if (c->d_layer_base) cudaFree(c->d_layer_base);
@@ -822,6 +848,114 @@ aqua_status aqua_swap_in(aqua_ctx* c, int32_t n, const uint64_t* pids, aqua_stre
     ps[i]->loc = AQUA_LOC_LOCAL;
     ps[i]->ids = std::move(fresh[i]);
   }
+  if (out_ticket) *out_ticket = ticket;
+  return AQUA_OK;
+}
+
+static aqua_status migrate_impl(aqua_ctx* c, const std::vector<uint64_t>& pids, int32_t dst, cudaStream_t st,
+                                uint64_t* out_ticket) {
+  if (dst != AQUA_LOC_PEER && dst != AQUA_LOC_HOST) return fail(c, AQUA_E_INVAL, "dst must be PEER or HOST");
+  std::unordered_set<uint64_t> seen;
+  for (uint64_t pid : pids)
+    if (!seen.insert(pid).second) return fail(c, AQUA_E_INVAL, "duplicate pid");
+  std::vector<Prompt*> ps;
+  int64_t need = 0;
+  for (uint64_t pid : pids) {
+    auto it = c->prompts.find(pid);
+    if (it == c->prompts.end() || it->second.state != AQUA_ST_SWAPPED || it->second.loc == dst)
+      return fail(c, AQUA_E_STATE, "pid has no image outside dst");
+    ps.push_back(&it->second);
+    need += static_cast<int64_t>(it->second.ids.size());
+  }
+  Arena* ad = arena_of(c, dst);
+  if (!ad->present || need > ad->free.size()) return fail(c, AQUA_E_NOSPACE, "dst arena missing or full");
+  std::vector<Desc> ds;
+  std::vector<std::vector<int32_t>> fresh(ps.size());
+  const uint32_t dbit = dst == AQUA_LOC_HOST ? kArenaBit : 0u;
+  auto it = ad->free.begin();
+  for (size_t i = 0; i < ps.size(); ++i) {
+    const uint32_t sbit = ps[i]->loc == AQUA_LOC_HOST ? kArenaBit : 0u;
+    for (int32_t so : ps[i]->ids) {
+      const int32_t sn = *it++;
+      fresh[i].push_back(sn);
+      ds.push_back(Desc{static_cast<int32_t>(static_cast<uint32_t>(so) | sbit), static_cast<uint32_t>(sn) | dbit});
+    }
+  }
+  c->last_b.clear();
+  c->last_s.clear();
+  c->last_l.clear();
+  for (const Desc& d : ds) {
+    c->last_b.push_back(static_cast<int32_t>(static_cast<uint32_t>(d.block) & ~kArenaBit));
+    c->last_s.push_back(static_cast<int32_t>(d.slot_arena & ~kArenaBit));
+    c->last_l.push_back(dst);
+  }
+  uint64_t ticket = 0;
+  if (!ds.empty()) {
+    if (!c->dry) {
+      DevGuard g(c->device);
+      std::vector<uint64_t> ts;
+      for (size_t i = 0; i < ps.size(); ++i) {
+        Arena* as = arena_of(c, ps[i]->loc);
+        for (int32_t so : ps[i]->ids) ts.push_back(as->tick[so]);
+        for (int32_t sn : fresh[i]) ts.push_back(ad->tick[sn]);
+      }
+      if (aqua_status s = wait_all(c, ts, st)) return s;
+      cudaEvent_t t_start;
+      if (aqua_status s = timing_start(c, st, &t_start)) return s;
+      int regions = 0;
+      if (aqua_status s = run_copy(c, ds, aqua::kMig, st, &regions)) return s;
+      if (aqua_status s = record(c, st, &ticket, t_start)) return s;
+      stage_seal(c, regions, ticket);
+    } else {
+      record(c, st, &ticket);
+    }
+  }
+  for (size_t i = 0; i < ps.size(); ++i) {
+    Arena* as = arena_of(c, ps[i]->loc);
+    for (int32_t so : ps[i]->ids) {
+      as->free.insert(so);
+      as->tick[so] = ticket;
+    }
+    for (int32_t sn : fresh[i]) {
+      ad->free.erase(sn);
+      ad->tick[sn] = ticket;
+    }
+    ps[i]->loc = dst;
+    ps[i]->ids = std::move(fresh[i]);
+  }
+  if (out_ticket) *out_ticket = ticket;
+  return AQUA_OK;
+}
+
+aqua_status aqua_migrate(aqua_ctx* c, int32_t n, const uint64_t* pids, int32_t dst_loc, aqua_stream_t stream,
+                         uint64_t* out_ticket) {
+  if (aqua_status s = precheck(c)) return s;
+  if (out_ticket) *out_ticket = 0;
+  if (n < 0 || (n > 0 && !pids)) return fail(c, AQUA_E_INVAL, "n < 0 or null pids");
+  std::vector<uint64_t> v(pids, pids + n);
+  return migrate_impl(c, v, dst_loc, reinterpret_cast<cudaStream_t>(stream), out_ticket);
+}
+
+aqua_status aqua_reclaim(aqua_ctx* c, aqua_stream_t stream, uint64_t* out_ticket) {
+  if (aqua_status s = precheck(c)) return s;
+  if (out_ticket) *out_ticket = 0;
+  if (!c->gpu.present) return AQUA_OK;                 // idempotent
+  std::vector<uint64_t> pids;
+  for (const auto& kv : c->prompts)
+    if (kv.second.state == AQUA_ST_SWAPPED && kv.second.loc == AQUA_LOC_PEER) pids.push_back(kv.first);
+  std::sort(pids.begin(), pids.end());
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  uint64_t ticket = 0;
+  if (!pids.empty())
+    if (aqua_status s = migrate_impl(c, pids, AQUA_LOC_HOST, st, &ticket)) return s;
+  // the returned ticket covers every library op that touched the lender
+  if (!c->dry) {
+    DevGuard g(c->device);
+    if (aqua_status s = wait_all(c, c->gpu.tick, st)) return s;
+    if (aqua_status s = record(c, st, &ticket)) return s;
+    if (c->gpu.owned) c->zombies.push_back(aqua_ctx::Zombie{c->gpu.device, c->gpu.base, ticket});
+  }
+  c->gpu = Arena();
   if (out_ticket) *out_ticket = ticket;
   return AQUA_OK;
 }

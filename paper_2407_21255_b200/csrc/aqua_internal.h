@@ -14,7 +14,10 @@ struct Desc {
 };
 constexpr uint32_t kArenaBit = 0x80000000u;
 
-enum Dir : int { kOut = 0, kIn = 1 };   // swap_out: pool -> arena; swap_in: arena -> pool
+// swap_out: pool -> arena; swap_in: arena -> pool; migrate: arena -> arena
+// (for kMig the descriptor's `block` field holds the SOURCE slot, with the
+// source arena in bit 31, reinterpreted as uint32).
+enum Dir : int { kOut = 0, kIn = 1, kMig = 2 };
 
 // Calls with at most kInlineDesc descriptors pass them inside the kernel
 // parameters (__grid_constant__): no staging copy on the critical path.

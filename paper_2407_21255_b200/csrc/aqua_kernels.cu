@@ -112,14 +112,22 @@ __device__ __forceinline__ void item_addrs(const SwapParams& p, const Desc d, in
                                            const uint8_t*& src, uint8_t*& dst, uint32_t& bytes) {
   const int l = c >> 1, kv = c & 1;
   const int64_t off = int64_t(q) * p.piece;
-  uint8_t* pool = reinterpret_cast<uint8_t*>(__ldg(p.layer_base + l)) + kv * p.P_kv +
-                  int64_t(d.block) * p.P_b + off;
   const uint32_t a = d.slot_arena >> 31;
   const int64_t slot = d.slot_arena & ~kArenaBit;
   const uint64_t base = a ? p.arena_base[1] : p.arena_base[0];   // no dynamic param indexing
   uint8_t* img = reinterpret_cast<uint8_t*>(base) + slot * p.U + int64_t(c) * p.S + off;
   const int64_t rem = p.S - off;
   bytes = static_cast<uint32_t>(rem < p.piece ? rem : p.piece);
+  if (D == kMig) {
+    // image -> image: the source slot rides in `block` (bit 31 = its arena)
+    const uint32_t sb = static_cast<uint32_t>(d.block);
+    const uint64_t sbase = (sb >> 31) ? p.arena_base[1] : p.arena_base[0];
+    src = reinterpret_cast<const uint8_t*>(sbase) + int64_t(sb & ~kArenaBit) * p.U + int64_t(c) * p.S + off;
+    dst = img;
+    return;
+  }
+  uint8_t* pool = reinterpret_cast<uint8_t*>(__ldg(p.layer_base + l)) + kv * p.P_kv +
+                  int64_t(d.block) * p.P_b + off;
   if (D == kOut) {
     src = pool;
     dst = img;
@@ -204,7 +212,7 @@ __global__ void __launch_bounds__(32) swap_tma_kernel(const __grid_constant__ Sw
     if (k == 1) {
       mbar_expect_tx(&bars[lstage], bytes);
       bulk_g2s(buf, src, bytes, &bars[lstage], pol);
-    } else if (D == kIn) {                 // image side: one contiguous load of k chunks
+    } else if (D != kOut) {                // image side: one contiguous load of k chunks
       mbar_expect_tx(&bars[lstage], bytes * k);
       bulk_g2s(buf, src, bytes * k, &bars[lstage], pol);
     } else {                               // pool side: k scattered chunk loads
@@ -233,7 +241,7 @@ __global__ void __launch_bounds__(32) swap_tma_kernel(const __grid_constant__ Sw
     item_addrs<D>(p, d, su.c, su.q, src, dst, bytes);
     if (k == 1) {
       bulk_s2g(dst, buf, bytes, pol);
-    } else if (D == kOut) {                // image side: one contiguous store of k chunks
+    } else if (D != kIn) {                 // image side: one contiguous store of k chunks
       bulk_s2g(dst, buf, bytes * k, pol);
     } else {                               // pool side: k scattered chunk stores
       for (int t = 0; t < k; ++t) {
@@ -373,21 +381,24 @@ cudaError_t launch_swap_tma(const SwapParams& p, Dir dir, int num_sms, int grid_
   const int smem = tma_smem_bytes(stage_bytes, stages);
   const int grid = grid_for<void>(p.nitems, 1, num_sms, 1, grid_cap);
   // the opt-in smem attribute is per device; remember the largest set so far
-  static thread_local int set_smem[2][64] = {};
+  static thread_local int set_smem[3][64] = {};
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
   int& have = set_smem[dir][dev & 63];
   if (smem > have) {
-    e = cudaFuncSetAttribute(dir == kOut ? swap_tma_kernel<kOut> : swap_tma_kernel<kIn>,
+    e = cudaFuncSetAttribute(dir == kOut ? swap_tma_kernel<kOut>
+                             : dir == kIn ? swap_tma_kernel<kIn> : swap_tma_kernel<kMig>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e != cudaSuccess) return e;
     have = 227 * 1024;
   }
   if (dir == kOut)
     swap_tma_kernel<kOut><<<grid, 32, smem, s>>>(p, stages);
-  else
+  else if (dir == kIn)
     swap_tma_kernel<kIn><<<grid, 32, smem, s>>>(p, stages);
+  else
+    swap_tma_kernel<kMig><<<grid, 32, smem, s>>>(p, stages);
   if (ctas_used) *ctas_used = grid;
   return cudaGetLastError();
 }
@@ -398,8 +409,10 @@ cudaError_t launch_swap_ldst(const SwapParams& p, Dir dir, int num_sms, int grid
   const int grid = grid_for<void>(p.nitems, 8, num_sms, 4, grid_cap);
   if (dir == kOut)
     swap_ldst_kernel<kOut, 8><<<grid, 256, 0, s>>>(p);
-  else
+  else if (dir == kIn)
     swap_ldst_kernel<kIn, 8><<<grid, 256, 0, s>>>(p);
+  else
+    swap_ldst_kernel<kMig, 8><<<grid, 256, 0, s>>>(p);
   if (ctas_used) *ctas_used = grid;
   return cudaGetLastError();
 }

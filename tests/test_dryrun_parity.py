@@ -80,12 +80,40 @@ def _apply(pool, c, op):
                 r = pool.swap_in(arg) if side == "oracle" else c.swap_in(arg, cap=1 << 12)[0]
             elif name == "free":
                 r = pool.free_prompt(arg) if side == "oracle" else c.free(arg)
+            elif name == "mig":
+                if side == "oracle":
+                    r = pool.migrate(*arg)
+                else:
+                    c.migrate(*arg)
+                    r = [(p, c.query(p, with_ids=True)[3]) for p in arg[0]]
+            elif name == "reclaim":
+                if side == "oracle":
+                    r = [p for p, _ in pool.reclaim()]
+                else:
+                    moved = sorted(p for p in range(6) if _loc(c, p) == aqua.LOC_PEER)
+                    c.reclaim()
+                    r = moved
+            elif name == "relend":
+                r = pool.lend(kp.LOC_PEER, arg * lay_U(pool)) if side == "oracle" else \
+                    c.lend(0, FAKE * 4, arg * c.U)
         except kp.AquaError as e:
             r = ("err", e.code)
         except aqua.AquaError as e:
             r = ("err", e.code)
         res.append(r)
     return res
+
+
+def _loc(c, p):
+    try:
+        st, loc, _ = c.query(p)
+        return loc if st == aqua.SWAPPED else None
+    except aqua.AquaError:
+        return None
+
+
+def lay_U(pool):
+    return pool.lay.U
 
 
 @pytest.mark.parametrize("seed", range(40))
@@ -113,14 +141,23 @@ def test_random_op_sequences_match_oracle(seed):
             op = ("adopt", (rnd.choice(pids), [rnd.randint(-1, NB) for _ in range(rnd.randint(0, 3))]))
         elif k < 0.6:
             op = ("out", rnd.sample(pids, rnd.randint(0, 3)) + ([pids[0]] if rnd.random() < 0.05 else []))
-        elif k < 0.8:
+        elif k < 0.75:
             op = ("in", rnd.sample(pids, rnd.randint(0, 3)))
-        else:
+        elif k < 0.85:
             op = ("free", rnd.choice(pids))
+        elif k < 0.93:
+            op = ("mig", (rnd.sample(pids, rnd.randint(1, 2)), rnd.choice([kp.LOC_PEER, kp.LOC_HOST])))
+        elif k < 0.97:
+            op = ("reclaim", None)
+        else:
+            op = ("relend", rnd.choice([1, 4, 8]))
         a, b = _apply(pool, c, op)
         assert a == b, (seed, op, a, b)
         pool.check_invariants()
-        assert c.counts()[0] == len(pool.free)
+        cnt = c.counts()
+        assert cnt[0] == len(pool.free)
+        assert cnt[1] == (len(pool.peer.free) if pool.peer is not None else -1)
+        assert cnt[2] == (len(pool.host.free) if pool.host is not None else -1)
         for p, pr in pool.prompts.items():
             st, loc, n, ids = c.query(p, with_ids=True)
             assert (st, loc, ids) == (pr.state, pr.location, pr.blocks if pr.state == kp.RESIDENT else pr.slots)

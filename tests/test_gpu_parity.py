@@ -279,3 +279,36 @@ def test_ticket_timing():
     with pytest.raises(aqua.AquaError) as e:
         c.ticket_elapsed(t2)
     assert e.value.code == aqua.E_STATE
+
+
+@pytest.mark.parametrize("engine", ["tma", "ldst"])
+def test_migrate_reclaim_relend_bytes(engine):
+    """NEXT-1 on the GPU: images move lender -> host (reclaim) and back
+    (re-offer) through the fused arena->arena kernel, byte for byte with the
+    oracle; resumes from either place restore the blocks."""
+    import torch
+    from workloads import kv_random_bytes
+    rig = Rig(L=3, bs=16, H=4, D=64, NB=40, lender_slots=12, host_slots=16)
+    c, o = rig.ctx, rig.opool
+    c.set_option(aqua.OPT_KERNEL, ENGINES[engine])
+    _ops(rig, [("alloc", (1, 5)), ("alloc", (2, 3)), ("alloc", (3, 4)), ("out", [1, 3]), ("out", [2])])
+    t = c.migrate([3], aqua.LOC_HOST)
+    o.migrate([3], kp.LOC_HOST)
+    rig.assert_bytes_equal("migrate 3 -> host")
+    t = c.reclaim()
+    moved = o.reclaim()
+    assert [p for p, _ in moved] == [1, 2]
+    c.sync(t)
+    assert c.counts()[1] == -1 and c.query(1)[1] == aqua.LOC_HOST
+    torch.cuda.synchronize()
+    assert np.array_equal(rig.host.numpy(), o.host.data)
+    # re-offer a new lender and move two images back
+    U = rig.lay.U
+    g = kv_random_bytes(8 * U, seed=77)
+    rig.peer = torch.from_numpy(g.copy()).cuda()
+    o.lend(kp.LOC_PEER, 8 * U, g.copy())
+    assert c.lend(0, rig.peer.data_ptr(), 8 * U) == 8
+    c.migrate([2, 1], aqua.LOC_PEER)
+    assert o.migrate([2, 1], kp.LOC_PEER) == [(2, [0, 1, 2]), (1, [3, 4, 5, 6, 7])]
+    rig.assert_bytes_equal("migrate back")
+    _ops(rig, [("in", [1, 2, 3]), ("out", [2])])
