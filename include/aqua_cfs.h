@@ -83,6 +83,12 @@ AQUA_API aqua_status aqua_cfs_commit(aqua_cfs* s, uint64_t* finished, int32_t* n
  * selection order, then prefill (id, tokens) in selection order. */
 AQUA_API aqua_status aqua_cfs_partition(aqua_cfs* s, uint64_t* decode, int32_t* n_decode, uint64_t* prefill,
                                         int32_t* prefill_tokens, int32_t* n_prefill, int32_t cap);
+/* Switch policy between iterations ("fall back to FCFS from CFS
+ * when tensors are on DRAM").  Entering FCFS admits the resident prompts (in
+ * arrival order); swapped prompts are paged in when FCFS admits them; if the
+ * inherited residents outgrow the pool the latest-arrived one is paged out
+ * (R18).  Returning to CFS replans at the next iteration. */
+AQUA_API aqua_status aqua_cfs_set_policy(aqua_cfs* s, int32_t policy);
 AQUA_API aqua_status aqua_cfs_vclock(aqua_cfs* s, double* vclock);
 AQUA_API aqua_status aqua_cfs_advance_to(aqua_cfs* s, double vclock);
 /* Runnable prompts, prompts with KV resident in the pool, iterations run. */

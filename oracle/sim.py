@@ -27,11 +27,21 @@ The driver emits the exact call log the GPU run must reproduce:
   ("swap_out", pids, [(loc, slots), ...])   ("swap_in", pids, [ids, ...])
   ("alloc", pid, ids)    ("free", pid)    ("iter", i, [(pid, ctx0, t), ...])
   ("plan", i, decode_ids, [(pid, tokens), ...])
+  ("reclaim", i, ((pid, slots), ...))   ("relend", i, nslots)
+  ("migrate", i, pids, (slots, ...))    ("policy", i, "fcfs"|"cfs")
+
+FCFS (R18; SPEC fcfs_step S:297-305, fallback S:306-313): requests are
+admitted in (arrival, id) order while the sum of their full projections
+ceil((P+O)/bs) fits NB; a swapped prompt is paged in when admitted; the
+plan decodes every admitted decode prompt, then prefills in arrival order.
+When FCFS takes over from CFS (fallback) the admitted set starts as the
+resident prompts; if their growth no longer fits, the latest-arrived
+admitted resident is paged out (the vLLM FCFS preemption order).
 """
 from __future__ import annotations
 
 import dataclasses
-from typing import Dict, List, Sequence, Tuple
+from typing import Dict, List, Optional, Sequence, Tuple
 
 from . import cfs
 from .cfs import DECODE, PREFILL, Req
@@ -50,6 +60,11 @@ class SimConfig:
     t_base: float = 0.020
     t_token: float = 40e-6
     max_iters: int = 10_000_000
+    # NEXT-1 elasticity: the lender reclaims its
+    # memory at virtual time elastic[0] and re-offers relend_slots at
+    # elastic[1]; while the images sit in DRAM the engine runs FCFS
+    elastic: Optional[Tuple[float, float]] = None
+    relend_slots: int = 0
 
 
 @dataclasses.dataclass
@@ -87,6 +102,8 @@ def run(trace: Sequence[Tuple[int, float, int, int]], cfg: SimConfig) -> SimResu
     last = 0
     finished_prev = False
     blocks_out = blocks_in = 0
+    mode = cfg.policy
+    reclaimed = relent = False
     timeline: List[Tuple[float, int]] = []
 
     def resident(pid):
@@ -127,10 +144,39 @@ def run(trace: Sequence[Tuple[int, float, int, int]], cfg: SimConfig) -> SimResu
             plan = None
             continue
 
-        if cfg.policy == "fcfs":
+        if cfg.elastic is not None:
+            if not reclaimed and t >= cfg.elastic[0]:
+                res = pool.reclaim()
+                log.append(("reclaim", i, tuple((pid, tuple(sl)) for pid, sl in res)))
+                reclaimed = True
+                mode = "fcfs"
+                admitted_fcfs[:] = [pid for pid in sorted(run_set, key=lambda x: (run_set[x].arrival, x))
+                                    if resident(pid)]
+                log.append(("policy", i, "fcfs"))
+            elif reclaimed and not relent and t >= cfg.elastic[1]:
+                n = pool.lend(LOC_PEER, cfg.relend_slots * lay.U)
+                log.append(("relend", i, n))
+                relent = True
+                back, room = [], n
+                for pid in sorted(pid for pid, p in pool.prompts.items()
+                                  if p.state == SWAPPED and p.location == LOC_HOST):
+                    k = len(pool.prompts[pid].slots)
+                    if k > room:
+                        break
+                    back.append(pid)
+                    room -= k
+                if back:
+                    res = pool.migrate(back, LOC_PEER)
+                    log.append(("migrate", i, tuple(back), tuple(tuple(sl) for _, sl in res)))
+                mode = cfg.policy
+                admitted_fcfs.clear()
+                plan = None
+                log.append(("policy", i, mode))
+
+        if mode == "fcfs":
             # admission: full projection must fit, head-of-line
-            proj = sum(cfs.need(run_set[x], run_set[x].P + run_set[x].O - run_set[x].ctx, lay.bs)
-                       for x in admitted_fcfs)
+            proj = sum(-(-(run_set[x].P + run_set[x].O) // lay.bs) for x in admitted_fcfs)
+            page_in = []
             for r in sorted(run_set.values(), key=lambda r: (r.arrival, r.id)):
                 if r.id in admitted_fcfs:
                     continue
@@ -139,8 +185,24 @@ def run(trace: Sequence[Tuple[int, float, int, int]], cfg: SimConfig) -> SimResu
                     break
                 proj += n
                 admitted_fcfs.append(r.id)
+                if r.id in pool.prompts and pool.prompts[r.id].state == SWAPPED:
+                    page_in.append(r.id)
+            if page_in:
+                res = pool.swap_in(page_in)
+                blocks_in += sum(len(x) for x in res)
+                log.append(("swap_in", tuple(page_in), tuple(tuple(x) for x in res)))
             plan = cfs.fcfs_plan([run_set[x] for x in admitted_fcfs], cfg.b)
             work = this_iter_tokens(plan)
+            while work and not fits(work):
+                # overflow after a fallback: preempt the latest-arrived resident
+                victims = [x for x in admitted_fcfs if resident(x)]
+                victim = max(victims, key=lambda x: (run_set[x].arrival, x))
+                admitted_fcfs.remove(victim)
+                res = pool.swap_out([victim])
+                blocks_out += sum(len(s_) for _, _, s_ in res)
+                log.append(("swap_out", (victim,), tuple((loc, tuple(s_)) for _, loc, s_ in res)))
+                plan = cfs.fcfs_plan([run_set[x] for x in admitted_fcfs], cfg.b)
+                work = this_iter_tokens(plan)
             if not work:
                 raise RuntimeError("FCFS: the head-of-line prompt can never fit the pool")
         else:

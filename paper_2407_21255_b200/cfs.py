@@ -10,7 +10,7 @@ POLICY_CFS, POLICY_FCFS = 0, 1
 PHASE_PREFILL, PHASE_DECODE = 0, 1
 
 SYMBOLS = ["aqua_cfs_create", "aqua_cfs_destroy", "aqua_cfs_add", "aqua_cfs_set_state", "aqua_cfs_next",
-           "aqua_cfs_commit", "aqua_cfs_partition", "aqua_cfs_vclock", "aqua_cfs_advance_to", "aqua_cfs_stats"]
+           "aqua_cfs_commit", "aqua_cfs_partition", "aqua_cfs_set_policy", "aqua_cfs_vclock", "aqua_cfs_advance_to", "aqua_cfs_stats"]
 
 
 class Config(C.Structure):
@@ -34,6 +34,7 @@ for _n, _a in {
     "aqua_cfs_commit": [_VP, _P(_U64), _P(_I32), _I32, _P(C.c_double)],
     "aqua_cfs_partition": [_VP, _P(_U64), _P(_I32), _P(_U64), _P(_I32), _P(_I32), _I32],
     "aqua_cfs_vclock": [_VP, _P(C.c_double)],
+    "aqua_cfs_set_policy": [_VP, _I32],
     "aqua_cfs_advance_to": [_VP, C.c_double],
     "aqua_cfs_stats": [_VP, _P(_I32), _P(_I32), _P(C.c_int64)],
 }.items():
@@ -97,6 +98,9 @@ class Scheduler:
         self._call("aqua_cfs_partition", self.h, self._dec, C.byref(nd), self._pre, self._pret, C.byref(npf),
                    self.cap)
         return list(self._dec[:nd.value]), list(zip(self._pre[:npf.value], self._pret[:npf.value]))
+
+    def set_policy(self, policy: int) -> None:
+        self._call("aqua_cfs_set_policy", self.h, policy)
 
     def vclock(self) -> float:
         v = C.c_double()

@@ -36,6 +36,7 @@ struct Plan {
 
 struct aqua_cfs {
   aqua_cfs_config cfg;
+  int32_t mode = AQUA_POLICY_CFS;    // current policy (cfg.policy, or FCFS during a fallback)
   std::unordered_map<uint64_t, Req> reqs;
   bool have_plan = false;
   Plan plan;
@@ -186,6 +187,7 @@ aqua_status aqua_cfs_create(const aqua_cfs_config* cfg, aqua_cfs** out) {
     return AQUA_E_INVAL;
   aqua_cfs* s = new aqua_cfs();
   s->cfg = *cfg;
+  s->mode = cfg->policy;
   *out = s;
   return AQUA_OK;
 }
@@ -244,7 +246,8 @@ aqua_status aqua_cfs_next(aqua_cfs* s, int32_t* rescheduled, uint64_t* page_out,
   }
   std::vector<uint64_t> outs, ins;
   std::vector<aqua_cfs_work> w;
-  if (s->cfg.policy == AQUA_POLICY_FCFS) {
+  if (s->mode == AQUA_POLICY_FCFS) {
+    // admission in arrival order while the full projections fit
     int64_t proj = 0;
     for (uint64_t id : s->admitted) {
       const Req& r = s->reqs.at(id);
@@ -259,25 +262,45 @@ aqua_status aqua_cfs_next(aqua_cfs* s, int32_t* rescheduled, uint64_t* page_out,
       if (proj + n > s->cfg.num_blocks) break;
       proj += n;
       s->admitted.push_back(r->id);
+      if (r->where == kSwapped) ins.push_back(r->id);      // paged in when admitted
     }
-    // decode for every admitted decode prompt, then prefill in arrival order
-    std::vector<const Req*> adm;
-    for (uint64_t id : s->admitted) adm.push_back(&s->reqs.at(id));
-    std::sort(adm.begin(), adm.end(), by_arrival);
-    Plan pl;
-    for (const Req* r : adm)
-      if (r->phase == AQUA_PHASE_DECODE && static_cast<int32_t>(pl.dec.size()) < s->cfg.batch_tokens)
-        pl.dec.push_back(r->id);
-    int32_t left = s->cfg.batch_tokens - static_cast<int32_t>(pl.dec.size());
-    for (const Req* r : adm) {
-      if (r->phase != AQUA_PHASE_PREFILL || left == 0) continue;
-      const int32_t t = std::min(left, r->P - r->f);
-      pl.pre.emplace_back(r->id, t);
-      left -= t;
-    }
-    s->plan = pl;
+    for (uint64_t id : ins) s->reqs.at(id).where = kResident;
+    auto fcfs_plan = [s]() {
+      std::vector<const Req*> adm;
+      for (uint64_t id : s->admitted) adm.push_back(&s->reqs.at(id));
+      std::sort(adm.begin(), adm.end(), by_arrival);
+      Plan pl;
+      for (const Req* r : adm)
+        if (r->phase == AQUA_PHASE_DECODE && static_cast<int32_t>(pl.dec.size()) < s->cfg.batch_tokens)
+          pl.dec.push_back(r->id);
+      int32_t left = s->cfg.batch_tokens - static_cast<int32_t>(pl.dec.size());
+      for (const Req* r : adm) {
+        if (r->phase != AQUA_PHASE_PREFILL || left == 0) continue;
+        const int32_t t = std::min(left, r->P - r->f);
+        pl.pre.emplace_back(r->id, t);
+        left -= t;
+      }
+      return pl;
+    };
+    s->plan = fcfs_plan();
     s->have_plan = true;
-    w = work_of(s, pl);
+    w = work_of(s, s->plan);
+    // after a fallback the inherited residents may outgrow the pool: page out
+    // the latest-arrived admitted resident until the iteration fits (R18)
+    while (!w.empty() && !fits(s, w)) {
+      const Req* victim = nullptr;
+      for (uint64_t id : s->admitted) {
+        const Req& r = s->reqs.at(id);
+        if (r.where == kResident && (!victim || by_arrival(victim, &r))) victim = &r;
+      }
+      if (!victim) break;
+      const uint64_t vid = victim->id;
+      s->admitted.erase(std::find(s->admitted.begin(), s->admitted.end(), vid));
+      s->reqs.at(vid).where = kSwapped;
+      outs.push_back(vid);
+      s->plan = fcfs_plan();
+      w = work_of(s, s->plan);
+    }
     if (w.empty()) return AQUA_E_NOBLOCKS;   // head-of-line prompt can never fit
   } else {
     if (s->have_plan) w = work_of(s, s->plan);
@@ -357,6 +380,25 @@ aqua_status aqua_cfs_commit(aqua_cfs* s, uint64_t* finished, int32_t* n_fin, int
   s->work.clear();
   s->work_pending = false;
   if (vclock) *vclock = s->vclock;
+  return AQUA_OK;
+}
+
+aqua_status aqua_cfs_set_policy(aqua_cfs* s, int32_t policy) {
+  if (!s || (policy != AQUA_POLICY_CFS && policy != AQUA_POLICY_FCFS)) return AQUA_E_INVAL;
+  if (s->work_pending) return AQUA_E_STATE;
+  if (policy == s->mode) return AQUA_OK;
+  s->mode = policy;
+  s->admitted.clear();
+  if (policy == AQUA_POLICY_FCFS) {
+    // the prompts already on the GPU are the admitted ones, in arrival order
+    std::vector<const Req*> res;
+    for (const auto& kv : s->reqs)
+      if (kv.second.where == kResident) res.push_back(&kv.second);
+    std::sort(res.begin(), res.end(), by_arrival);
+    for (const Req* r : res) s->admitted.push_back(r->id);
+  } else {
+    s->have_plan = false;    // replan at once
+  }
   return AQUA_OK;
 }
 

@@ -946,15 +946,19 @@ aqua_status aqua_reclaim(aqua_ctx* c, aqua_stream_t stream, uint64_t* out_ticket
   std::sort(pids.begin(), pids.end());
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   uint64_t ticket = 0;
-  if (!pids.empty())
-    if (aqua_status s = migrate_impl(c, pids, AQUA_LOC_HOST, st, &ticket)) return s;
-  // the returned ticket covers every library op that touched the lender
+  // the ticket must cover every library access to the lender: order the
+  // stream after all of them first, then move the images (or just record)
   if (!c->dry) {
     DevGuard g(c->device);
     if (aqua_status s = wait_all(c, c->gpu.tick, st)) return s;
-    if (aqua_status s = record(c, st, &ticket)) return s;
-    if (c->gpu.owned) c->zombies.push_back(aqua_ctx::Zombie{c->gpu.device, c->gpu.base, ticket});
   }
+  if (!pids.empty()) {
+    if (aqua_status s = migrate_impl(c, pids, AQUA_LOC_HOST, st, &ticket)) return s;
+  } else if (!c->dry) {
+    DevGuard g(c->device);
+    if (aqua_status s = record(c, st, &ticket)) return s;
+  }
+  if (!c->dry && c->gpu.owned) c->zombies.push_back(aqua_ctx::Zombie{c->gpu.device, c->gpu.base, ticket});
   c->gpu = Arena();
   if (out_ticket) *out_ticket = ticket;
   return AQUA_OK;

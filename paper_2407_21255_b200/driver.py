@@ -23,7 +23,8 @@ from .cfs import Scheduler
 def run_trace(trace: Sequence[Tuple[int, float, int, int]], ctx: "aqua.Ctx", sched: Scheduler, *,
               fill_seed: Optional[int] = None, decode_stream: int = 0, swap_stream: int = 0,
               on_iteration: Optional[Callable] = None, record_log: bool = True,
-              stream_sync: Optional[Callable] = None, on_swap: Optional[Callable] = None):
+              stream_sync: Optional[Callable] = None, on_swap: Optional[Callable] = None,
+              elastic: Optional[dict] = None, policy_after_relend: int = 0):
     """Run the whole trace.  Returns (log, stats).
 
     ``stream_sync(kind, ticket)`` lets a GPU caller order streams:
@@ -32,6 +33,12 @@ def run_trace(trace: Sequence[Tuple[int, float, int, int]], ctx: "aqua.Ctx", sch
       kind == "after_swap_in":   decode must wait for the swap_in ticket.
     ``on_iteration(i, work)`` runs the per-iteration decode proxy (optional).
     ``on_swap(kind, pids, ticket, nblocks)`` is called after each swap call.
+    ``elastic = {"t_reclaim": s, "t_relend": s, "relend": (device, base, bytes)}``
+    replays NEXT-1: at the first iteration at or after t_reclaim the lender
+    takes its memory back (aqua_reclaim: images move to host DRAM) and the
+    scheduler falls back to FCFS; at t_relend the memory is
+    offered again, the host images move back (ascending pid, as many as fit)
+    and CFS resumes.
     """
     pending = sorted(trace, key=lambda x: (x[1], x[0]))
     pi = 0
@@ -39,12 +46,55 @@ def run_trace(trace: Sequence[Tuple[int, float, int, int]], ctx: "aqua.Ctx", sch
     i = 0
     blocks_out = blocks_in = 0
     swap_calls = []
+    reclaimed = relent = False
+    swapped_at = {}          # pid -> arena of its image
     while True:
         t = sched.vclock()
         while pi < len(pending) and pending[pi][1] <= t:
             rid, a, P, O = pending[pi]
             sched.add(rid, a, P, O)
             pi += 1
+        if elastic is not None and sched.stats()[0] > 0:
+            if not reclaimed and t >= elastic["t_reclaim"]:
+                peer = sorted(p for p, loc in swapped_at.items() if loc == aqua.LOC_PEER)
+                tk = ctx.reclaim(swap_stream)
+                moved = []
+                for p in peer:
+                    q = ctx.query(p, with_ids=True)
+                    swapped_at[p] = q[1]
+                    moved.append((p, tuple(q[3])))
+                swap_calls.append(("reclaim", sum(len(x[1]) for x in moved), tk, time.perf_counter()))
+                sched.set_policy(1)
+                reclaimed = True
+                if record_log:
+                    log.append(("reclaim", i, tuple(moved)))
+                    log.append(("policy", i, "fcfs"))
+            elif reclaimed and not relent and t >= elastic["t_relend"]:
+                dev, base, nbytes = elastic["relend"]
+                n = ctx.lend(dev, base, nbytes)
+                relent = True
+                back, room = [], n
+                for p in sorted(p for p, loc in swapped_at.items() if loc == aqua.LOC_HOST):
+                    k = ctx.query(p)[2]
+                    if k > room:
+                        break
+                    back.append(p)
+                    room -= k
+                if record_log:
+                    log.append(("relend", i, n))
+                if back:
+                    tk = ctx.migrate(back, aqua.LOC_PEER, swap_stream)
+                    slots = []
+                    for p in back:
+                        q = ctx.query(p, with_ids=True)
+                        swapped_at[p] = q[1]
+                        slots.append(tuple(q[3]))
+                    swap_calls.append(("migrate", sum(len(x) for x in slots), tk, time.perf_counter()))
+                    if record_log:
+                        log.append(("migrate", i, tuple(back), tuple(slots)))
+                sched.set_policy(policy_after_relend)
+                if record_log:
+                    log.append(("policy", i, "cfs" if policy_after_relend == 0 else "fcfs"))
         res, outs, ins, work = sched.next()
         if not work:
             if pi >= len(pending):
@@ -60,6 +110,8 @@ def run_trace(trace: Sequence[Tuple[int, float, int, int]], ctx: "aqua.Ctx", sch
             t0 = time.perf_counter()
             tk = ctx.swap_out(outs, swap_stream)
             q = [ctx.query(p, with_ids=True) for p in outs]
+            for p, x in zip(outs, q):
+                swapped_at[p] = x[1]
             n = sum(x[2] for x in q)
             blocks_out += n
             swap_calls.append(("out", n, tk, t0))
@@ -72,6 +124,8 @@ def run_trace(trace: Sequence[Tuple[int, float, int, int]], ctx: "aqua.Ctx", sch
                 stream_sync("before_swap_in", 0)
             t0 = time.perf_counter()
             new, tk = ctx.swap_in(ins, swap_stream)
+            for p in ins:
+                swapped_at.pop(p, None)
             n = sum(len(x) for x in new)
             blocks_in += n
             swap_calls.append(("in", n, tk, t0))
@@ -95,6 +149,7 @@ def run_trace(trace: Sequence[Tuple[int, float, int, int]], ctx: "aqua.Ctx", sch
             on_iteration(i, work)
         fin, _ = sched.commit()
         for pid in fin:
+            swapped_at.pop(pid, None)
             ctx.free(pid, decode_stream)
             if record_log:
                 log.append(("free", pid))

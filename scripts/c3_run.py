@@ -39,6 +39,8 @@ def main():
     ap.add_argument("--host-gib", type=int, default=64)
     ap.add_argument("--check-oracle", action="store_true")
     ap.add_argument("--no-verify", action="store_true")
+    ap.add_argument("--elastic", default="", help="t_reclaim,t_relend (virtual s): NEXT-1 lender reclaim + FCFS "
+                                                   "fallback, then re-offer")
     args = ap.parse_args()
 
     dev = torch.device("cuda", 0)
@@ -91,9 +93,13 @@ def main():
     torch.cuda.synchronize()
     n0 = ctx.launch_count()
     t0 = time.perf_counter()
+    elastic = None
+    if args.elastic:
+        tr_, tl_ = (float(x) for x in args.elastic.split(","))
+        elastic = {"t_reclaim": tr_, "t_relend": tl_, "relend": (0, arena.data_ptr(), args.lender_gib << 30)}
     log, st = run_trace(trace, ctx, sched, fill_seed=SEED, decode_stream=dec.cuda_stream,
                         swap_stream=swp.cuda_stream, on_iteration=on_iteration, stream_sync=stream_sync,
-                        on_swap=on_swap, record_log=args.check_oracle)
+                        on_swap=on_swap, record_log=args.check_oracle, elastic=elastic)
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0
     launches = ctx.launch_count() - n0
@@ -106,6 +112,7 @@ def main():
         ms = ctx.ticket_elapsed(tk)
         dev_ms[kind] += ms
         per_block_ms.append((kind, ms, n, npids))
+    mig = [(k, n, ctx.ticket_elapsed(tk)) for k, n, tk, _ in st["swap_calls"] if k in ("reclaim", "migrate") and n]
     bytes_out, bytes_in = st["blocks_out"] * U, st["blocks_in"] * U
     res = {
         "config": "configs[2] bursty trace (seed 1, 373 requests, 25 @ 2.5/s then 5/s for 60 s then 2.5/s for 15 s), "
@@ -121,6 +128,10 @@ def main():
         "kernel_launches": launches,
         "verify_mismatches": int(mism.item()),
     }
+    if elastic:
+        res["elastic"] = {"t_reclaim": elastic["t_reclaim"], "t_relend": elastic["t_relend"],
+                          "moves": [{"kind": k, "blocks": n, "ms": round(ms, 3),
+                                     "GBps": round(n * U / ms / 1e6, 1)} for k, n, ms in mig]}
     outs = [ms / np_ for k, ms, n, np_ in per_block_ms if k == "out"]
     ins = [ms / np_ for k, ms, n, np_ in per_block_ms if k == "in"]
     if outs and ins:
@@ -133,7 +144,9 @@ def main():
         from oracle import sim as osim
         o = osim.run(trace, osim.SimConfig(NB=NB, lender_slots=(args.lender_gib << 30) // U if arena is not None else 0,
                                            host_slots=(args.host_gib << 30) // U,
-                                           policy="fcfs" if pol == POLICY_FCFS else "cfs"))
+                                           policy="fcfs" if pol == POLICY_FCFS else "cfs",
+                                           elastic=(elastic["t_reclaim"], elastic["t_relend"]) if elastic else None,
+                                           relend_slots=(args.lender_gib << 30) // U))
         res["oracle_log_equal"] = (log == o.log)
         res["oracle_calls"] = len(o.log)
     print(json.dumps(res), flush=True)

@@ -118,6 +118,37 @@ def self_ctas():
                           "in_hbm_GBps": round(2 * nblk * U / i / 1e6, 1)}), flush=True)
 
 
+def migrate():
+    """NEXT-1 data path: a 4 GiB image moved lender -> host (reclaim) and
+    host -> lender (re-offer), device time from the library's timing events."""
+    L, bs, H, D, NB, nblk = 32, 16, 8, 128, 4096, 2048
+    ctx, layers, arena, U = setup(L, bs, H, D, NB, nblk)
+    ctx.lend(aqua.HOST, 0, nblk * U)
+    ctx.set_option(aqua.OPT_TIMING, 1)
+    s = torch.cuda.Stream()
+    ctx.kv_fill_pattern(7, 0, nblk * bs, 5)
+    ctx.swap_out([7], s.cuda_stream)
+    res = []
+    for rep in range(3):
+        t1 = ctx.migrate([7], aqua.LOC_HOST, s.cuda_stream)
+        t2 = ctx.migrate([7], aqua.LOC_PEER, s.cuda_stream)
+        torch.cuda.synchronize()
+        res.append((ctx.ticket_elapsed(t1), ctx.ticket_elapsed(t2)))
+    t3 = ctx.reclaim(s.cuda_stream)
+    torch.cuda.synchronize()
+    rec = ctx.ticket_elapsed(t3)
+    _, t4 = ctx.swap_in([7], s.cuda_stream)
+    cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+    ctx.kv_verify_pattern(7, nblk * bs, 5, cnt.data_ptr(), s.cuda_stream)
+    torch.cuda.synchronize()
+    o = statistics.median(r[0] for r in res)
+    i = statistics.median(r[1] for r in res)
+    print(json.dumps({"migrate_bytes": nblk * U, "to_host_ms": round(o, 3), "to_lender_ms": round(i, 3),
+                      "to_host_GBps": round(nblk * U / o / 1e6, 2), "to_lender_GBps": round(nblk * U / i / 1e6, 2),
+                      "reclaim_ms": round(rec, 3), "resume_from_host_ms": round(ctx.ticket_elapsed(t4), 3),
+                      "verify_mismatches": int(cnt.item())}), flush=True)
+
+
 def stages():
     L, bs, H, D, NB, nblk = 32, 16, 8, 128, 4096, 2048
     ctx, layers, arena, U = setup(L, bs, H, D, NB, nblk)
@@ -167,6 +198,8 @@ if __name__ == "__main__":
         c5(host=True)
     elif what == "stages":
         stages()
+    elif what == "migrate":
+        migrate()
     elif what == "host_ctas":
         host_ctas()
     elif what == "self_ctas":

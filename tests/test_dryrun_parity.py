@@ -263,3 +263,51 @@ def test_full_c3_trace_call_log_matches_oracle():
     log, st = _product_log(tr, NB, 32768, 32768)
     assert st["iters"] == o.iters and st["blocks_out"] == o.blocks_out
     assert log == o.log
+
+
+@pytest.mark.parametrize("window", [(4.0, 9.0), (2.0, 30.0), (6.0, 6.5)])
+def test_elastic_trace_call_log_matches_oracle(window):
+    """NEXT-1 end to end in metadata mode: lender reclaim -> images to DRAM,
+    FCFS fallback, re-offer -> images back, CFS again; the
+    product's call log equals the oracle's."""
+    tr = burst_trace(seed=3, burst_s=8.0, tail_s=3.0, prompt=(300, 0.8, 1, 900), output=(40, 0.7, 1, 200))
+    NB, lender, host = 120, 400, 2000
+    o = osim.run(tr, osim.SimConfig(NB=NB, lender_slots=lender, host_slots=host, elastic=window,
+                                    relend_slots=lender))
+    c = aqua.Ctx(aqua.DRYRUN, 1, 16, 1, 8, 2, NB, [FAKE])
+    c.lend(0, FAKE * 2, lender * c.U)
+    c.lend(aqua.HOST, FAKE * 3, host * c.U)
+    s = Scheduler(NB=NB, bs=16, b=512, k=8)
+    log, st = run_trace(tr, c, s, elastic={"t_reclaim": window[0], "t_relend": window[1],
+                                          "relend": (0, FAKE * 5, lender * c.U)})
+    kinds = [e[0] for e in o.log]
+    assert "reclaim" in kinds and ("relend" in kinds) == (window[1] < o.vclock)
+    assert log == o.log
+    # while the images sit in DRAM no swap_out goes to the (absent) lender
+    fb = False
+    for e in o.log:
+        if e[0] == "policy":
+            fb = e[2] == "fcfs"
+        if fb and e[0] == "swap_out":
+            assert all(loc == kp.LOC_HOST for loc, _ in e[2])
+        if fb:
+            assert e[0] != "plan"
+
+
+def test_fallback_overflow_preemption_matches_oracle():
+    """FCFS fallback inheriting more residents than their projections allow:
+    growth overflows and the latest-arrived resident is paged out (R18);
+    swapped prompts are paged in when admitted."""
+    tr = [(i, 0.01 * i, 40, 300) for i in range(8)]
+    NB = 40
+    o = osim.run(tr, osim.SimConfig(NB=NB, b=64, lender_slots=400, host_slots=2000, elastic=(0.5, 1e9),
+                                    relend_slots=400))
+    fb = [e for e in o.log if e[0] in ("swap_out", "swap_in")
+          and o.log.index(e) > [x[0] for x in o.log].index("policy")]
+    assert any(e[0] == "swap_out" for e in fb) and any(e[0] == "swap_in" for e in fb)
+    c = aqua.Ctx(aqua.DRYRUN, 1, 16, 1, 8, 2, NB, [FAKE])
+    c.lend(0, FAKE * 2, 400 * c.U)
+    c.lend(aqua.HOST, FAKE * 3, 2000 * c.U)
+    s = Scheduler(NB=NB, bs=16, b=64, k=8)
+    log, _ = run_trace(tr, c, s, elastic={"t_reclaim": 0.5, "t_relend": 1e9, "relend": (0, FAKE * 5, 400 * c.U)})
+    assert log == o.log
