@@ -131,6 +131,7 @@ class Pool:
                 assert a.dtype == np.uint8 and a.size >= layout.layer_bytes
         self.free = set(range(layout.NB))          # C-2 free block set
         self.prompts: Dict[int, Prompt] = {}
+        self.prefixes: Dict[int, Prompt] = {}      # NEXT-2 persistent images
         self.peer: Optional[Arena] = None
         self.host: Optional[Arena] = None
 
@@ -303,7 +304,6 @@ class Pool:
         in call order: new = the n_p lowest free dst slots (R4); per j:
             dst[new_j*U : +U] = src[old_j*U : +U]
         then the old slots are freed.  Returns [(pid, new_slots)]."""
-        lay = self.lay
         pids = [int(p) for p in pids]
         if dst not in (LOC_PEER, LOC_HOST) or len(set(pids)) != len(pids):
             raise AquaError(E_INVAL, "bad dst or duplicate pid")
@@ -317,9 +317,15 @@ class Pool:
         need = sum(len(self.prompts[pid].slots) for pid in pids)
         if need > len(ar_d.free):
             raise AquaError(E_NOSPACE, "dst arena full")
+        return [(pid, slots) for pid, slots in zip(pids, self._move([self.prompts[p] for p in pids], dst))]
+
+    def _move(self, images: List[Prompt], dst: int) -> List[List[int]]:
+        """Copy each image to the lowest free dst slots, in order; free the
+        old slots.  (Capacity already checked by the caller.)"""
+        lay = self.lay
+        ar_d = self.arena(dst)
         out = []
-        for pid in pids:
-            p = self.prompts[pid]
+        for p in images:
             ar_s = self.arena(p.location)
             new = sorted(ar_d.free)[:len(p.slots)]
             for s in new:
@@ -329,22 +335,98 @@ class Pool:
                     ar_d.data[s_new * lay.U:(s_new + 1) * lay.U] = ar_s.data[s_old * lay.U:(s_old + 1) * lay.U]
             ar_s.free.update(p.slots)
             p.location, p.slots = dst, list(new)
-            out.append((pid, list(new)))
+            out.append(list(new))
         return out
 
     def reclaim(self) -> List[tuple]:
         """The GPU lender takes its memory back: every image on
-        it moves to the host arena, ascending pid, then the lender is
-        detached (a later lend() is a re-offer).  All-or-nothing
-        (NOSPACE if the host cannot hold them); idempotent without a lender
-        ("double reclaim -> no-op")."""
+        it moves to the host arena -- prompts in ascending pid, then cached
+        prefixes in ascending id -- and the lender is detached (a later
+        lend() is a re-offer).  All-or-nothing (NOSPACE if the host
+        cannot hold them); idempotent without a lender ("double
+        reclaim -> no-op").  Returns the moved prompts [(pid, slots)]."""
         if self.peer is None:
             return []
         pids = sorted(pid for pid, p in self.prompts.items()
                       if p.state == SWAPPED and p.location == LOC_PEER)
-        out = self.migrate(pids, LOC_HOST) if pids else []
+        fids = sorted(f for f, p in self.prefixes.items() if p.location == LOC_PEER)
+        need = sum(len(self.prompts[p].slots) for p in pids) + sum(len(self.prefixes[f].slots) for f in fids)
+        if need and (self.host is None or need > len(self.host.free)):
+            raise AquaError(E_NOSPACE, "host cannot hold the lender's images")
+        moved = self._move([self.prompts[p] for p in pids], LOC_HOST)
+        self._move([self.prefixes[f] for f in fids], LOC_HOST)
         self.peer = None
-        return out
+        return list(zip(pids, moved))
+
+    # ---------------------------------------------------------- NEXT-2
+    def prefix_store(self, fid: int, src_pid: int, n: int) -> tuple:
+        """Persist the first n blocks of a RESIDENT prompt as a cached prefix
+        image (Sec. 8: "a new prefill caching API with unique IDs, and
+        both CFS and prefill caching share the same swap space"; Sec. 9
+        P:895-896).  Copy, not move: the prompt keeps its
+        blocks.  Placement as swap_out (R5).  Per j < n, l, kv:
+            arena[s_j*U + (2l+kv)*S : +S] = chunk(l, kv, bt[j])
+        Errors: fid in use / bad n -> INVAL; src not resident -> STATE;
+        no room -> NOSPACE.  Returns (location, slots)."""
+        lay = self.lay
+        p = self.prompts.get(int(src_pid))
+        if int(fid) in self.prefixes:
+            raise AquaError(E_INVAL, "prefix id in use")
+        if p is None or p.state != RESIDENT:
+            raise AquaError(E_STATE, "src not resident")
+        if n < 0 or n > len(p.blocks):
+            raise AquaError(E_INVAL, "bad block count")
+        if self.peer is not None and len(self.peer.free) >= n:
+            loc = LOC_PEER
+        elif self.host is not None and len(self.host.free) >= n:
+            loc = LOC_HOST
+        else:
+            raise AquaError(E_NOSPACE, "no swap space for the prefix")
+        ar = self.arena(loc)
+        slots = sorted(ar.free)[:n]
+        for s in slots:
+            ar.free.remove(s)
+        if self.layers is not None and ar.data is not None:
+            for b, s in zip(p.blocks[:n], slots):
+                for l in range(lay.L):
+                    for kv in (0, 1):
+                        off = s * lay.U + (2 * l + kv) * lay.S
+                        ar.data[off:off + lay.S] = self.chunk(l, kv, b)
+        self.prefixes[int(fid)] = Prompt(SWAPPED, [], loc, list(slots))
+        return loc, list(slots)
+
+    def prefix_load(self, fid: int, dst_pid: int) -> List[int]:
+        """A prefix-cache hit: append n fresh blocks (lowest first, R4) to
+        dst_pid (created RESIDENT if new) and copy the cached image into
+        them; the image stays for the next hit.  Errors: unknown fid or dst
+        swapped -> STATE; pool too small -> NOBLOCKS."""
+        lay = self.lay
+        f = self.prefixes.get(int(fid))
+        if f is None:
+            raise AquaError(E_STATE, "unknown prefix")
+        p = self.prompts.get(int(dst_pid))
+        if p is not None and p.state != RESIDENT:
+            raise AquaError(E_STATE, "dst swapped")
+        if len(f.slots) > len(self.free):
+            raise AquaError(E_NOBLOCKS, "pool exhausted")
+        new = self._take_lowest(len(f.slots))
+        ar = self.arena(f.location)
+        if self.layers is not None and ar.data is not None:
+            for b, s in zip(new, f.slots):
+                for l in range(lay.L):
+                    for kv in (0, 1):
+                        off = s * lay.U + (2 * l + kv) * lay.S
+                        self.chunk(l, kv, b)[:] = ar.data[off:off + lay.S]
+        if p is None:
+            p = self.prompts[int(dst_pid)] = Prompt(RESIDENT, [], LOC_LOCAL, [])
+        p.blocks.extend(new)
+        return new
+
+    def prefix_drop(self, fid: int) -> None:
+        f = self.prefixes.pop(int(fid), None)
+        if f is None:
+            raise AquaError(E_STATE, "unknown prefix")
+        self.arena(f.location).free.update(f.slots)
 
     # ---------------------------------------------------------------- C-6
     def free_prompt(self, pid: int) -> None:
@@ -379,7 +461,7 @@ class Pool:
             ar = self.arena(loc)
             if ar is None:
                 continue
-            used = [s for p in self.prompts.values()
+            used = [s for p in list(self.prompts.values()) + list(self.prefixes.values())
                     if p.state == SWAPPED and p.location == loc for s in p.slots]
             assert len(used) == len(set(used)), "slot double-owned"
             assert not (set(used) & ar.free), "slot both free and owned"

@@ -507,3 +507,51 @@ def test_bruteforce_with_migration():
             pool.check_invariants()
         n += 1
     assert n == len(ops) ** 4
+
+
+# ------------------------------------------------------------------ NEXT-2
+def test_prefix_cache_bytes():
+    """A cached prefix is a copy: every hit gets the prefix blocks' bytes
+    (checked through the layout's meaning), the source prompt and the image
+    are untouched, and a reclaim moves the image with the prompts."""
+    pool = make_pool(L=2, NB=32)
+    U = pool.lay.U
+    peer = np.zeros(8 * U, np.uint8)
+    host = np.zeros(8 * U, np.uint8)
+    pool.lend(kp.LOC_PEER, 8 * U, peer)
+    pool.lend(kp.LOC_HOST, 8 * U, host)
+    pool.adopt_blocks(5, [7, 3, 11, 0, 9])
+    before = planes(pool).copy()
+    assert pool.prefix_store(42, 5, 3) == (kp.LOC_PEER, [0, 1, 2])
+    assert np.array_equal(planes(pool), before)                      # copy, not move
+    img = peer.reshape(8, pool.lay.L, 2, pool.lay.S)
+    for j, b in enumerate([7, 3, 11]):
+        assert np.array_equal(img[j], before[:, :, b, :])
+    hits = []
+    for dst in (100, 101, 102):
+        ids = pool.prefix_load(42, dst)
+        hits.append(ids)
+        pool.alloc_blocks(dst, 1)                                    # the suffix
+    now = planes(pool)
+    for ids in hits:
+        for j, b in enumerate(ids):
+            assert np.array_equal(now[:, :, b, :], before[:, :, [7, 3, 11][j], :])
+    assert hits[0] == [1, 2, 4]                                      # lowest free after 0,3,7,9,11 taken
+    pool.check_invariants()
+    with pytest.raises(kp.AquaError) as e:
+        pool.prefix_store(42, 5, 1)
+    assert e.value.code == kp.E_INVAL
+    with pytest.raises(kp.AquaError) as e:
+        pool.prefix_store(43, 5, 6)
+    assert e.value.code == kp.E_INVAL
+    pool.swap_out([5])
+    assert pool.reclaim() == [(5, [0, 1, 2, 3, 4])]
+    assert pool.prefixes[42].location == kp.LOC_HOST and pool.prefixes[42].slots == [5, 6, 7]
+    for j, b in enumerate([7, 3, 11]):
+        assert np.array_equal(host.reshape(8, pool.lay.L, 2, pool.lay.S)[5 + j], before[:, :, b, :])
+    pool.prefix_drop(42)
+    pool.check_invariants()
+    assert len(pool.host.free) == 3
+    with pytest.raises(kp.AquaError) as e:
+        pool.prefix_load(42, 200)
+    assert e.value.code == kp.E_STATE
