@@ -206,6 +206,28 @@ AQUA_API aqua_status aqua_migrate(aqua_ctx* ctx, int32_t n, const uint64_t* pids
  * without a GPU lender it is a no-op with ticket 0. */
 AQUA_API aqua_status aqua_reclaim(aqua_ctx* ctx, aqua_stream_t stream, uint64_t* out_ticket);
 
+/* NEXT-2, prefix caching (Sec. 8: "a new prefill caching API with
+ * unique IDs, and both CFS and prefill caching share the same swap space";
+ * Sec. 9).  Cached-prefix ids are their own
+ * namespace.
+ * aqua_prefix_store: persist the first n blocks of a RESIDENT prompt as
+ *   image `prefix_id` in swap space (placement as swap_out, R5).  Copy, not
+ *   move: the prompt keeps its blocks (its later writers must wait for the
+ *   ticket).  AQUA_E_INVAL if the id is in use or n is out of range.
+ * aqua_prefix_load: a cache hit -- append n fresh blocks (lowest first) to
+ *   dst_pid (created RESIDENT if new) and copy the image into them; the
+ *   image stays.  out_ids[cap] gets the new block ids.
+ * aqua_prefix_drop: free the image's slots.
+ * aqua_reclaim moves cached prefixes off the lender as well (after the
+ * prompts, ascending id). */
+AQUA_API aqua_status aqua_prefix_store(aqua_ctx* ctx, uint64_t prefix_id, uint64_t src_pid, int32_t n,
+                                       aqua_stream_t stream, uint64_t* out_ticket);
+AQUA_API aqua_status aqua_prefix_load(aqua_ctx* ctx, uint64_t prefix_id, uint64_t dst_pid, aqua_stream_t stream,
+                                      int32_t* out_ids, int32_t cap, uint64_t* out_ticket);
+AQUA_API aqua_status aqua_prefix_drop(aqua_ctx* ctx, uint64_t prefix_id);
+AQUA_API aqua_status aqua_prefix_query(aqua_ctx* ctx, uint64_t prefix_id, int32_t* location, int32_t* n,
+                                       int32_t* slots, int32_t cap);
+
 /* Make `stream` wait for a ticket (cudaStreamWaitEvent; no-op if done). */
 AQUA_API aqua_status aqua_wait(aqua_ctx* ctx, uint64_t ticket, aqua_stream_t stream);
 /* Block the host until the ticket completes. */

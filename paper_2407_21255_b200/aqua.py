@@ -30,7 +30,8 @@ OPT_KERNEL, OPT_MAX_CTAS, OPT_TMA_PIECE, OPT_TMA_STAGES, OPT_TIMING = 1, 2, 3, 4
 # Every symbol include/aqua.h declares (checked by tests/test_abi.py).
 SYMBOLS = [
     "aqua_create", "aqua_destroy", "aqua_lend", "aqua_alloc_blocks", "aqua_adopt_blocks",
-    "aqua_swap_out", "aqua_swap_in", "aqua_free", "aqua_migrate", "aqua_reclaim", "aqua_wait", "aqua_sync", "aqua_ticket_done", "aqua_ticket_elapsed",
+    "aqua_swap_out", "aqua_swap_in", "aqua_free", "aqua_migrate", "aqua_reclaim", "aqua_prefix_store", "aqua_prefix_load",
+    "aqua_prefix_drop", "aqua_prefix_query", "aqua_wait", "aqua_sync", "aqua_ticket_done", "aqua_ticket_elapsed",
     "aqua_query", "aqua_counts", "aqua_arena_base", "aqua_set_option", "aqua_get_option",
     "aqua_last_descriptors", "aqua_launch_count", "aqua_ipc_export", "aqua_ipc_import",
     "aqua_ipc_close", "aqua_ipc_alloc", "aqua_ipc_free", "aqua_can_access_peer", "aqua_kv_fill_pattern", "aqua_kv_verify_pattern",
@@ -68,6 +69,10 @@ def _load() -> C.CDLL:
         "aqua_free": (C.c_int, [VP, U64, VP]),
         "aqua_migrate": (C.c_int, [VP, I32, P(U64), I32, VP, P(U64)]),
         "aqua_reclaim": (C.c_int, [VP, VP, P(U64)]),
+        "aqua_prefix_store": (C.c_int, [VP, U64, U64, I32, VP, P(U64)]),
+        "aqua_prefix_load": (C.c_int, [VP, U64, U64, VP, P(I32), I32, P(U64)]),
+        "aqua_prefix_drop": (C.c_int, [VP, U64]),
+        "aqua_prefix_query": (C.c_int, [VP, U64, P(I32), P(I32), P(I32), I32]),
         "aqua_wait": (C.c_int, [VP, U64, VP]),
         "aqua_sync": (C.c_int, [VP, U64]),
         "aqua_ticket_done": (C.c_int, [VP, U64, P(I32)]),
@@ -192,6 +197,29 @@ class Ctx:
         t = C.c_uint64()
         self._c(lib.aqua_reclaim(self.h, C.c_void_p(stream or None), C.byref(t)))
         return t.value
+
+    def prefix_store(self, fid: int, src_pid: int, n: int, stream: int = 0) -> int:
+        t = C.c_uint64()
+        self._c(lib.aqua_prefix_store(self.h, fid, src_pid, n, C.c_void_p(stream or None), C.byref(t)))
+        return t.value
+
+    def prefix_query(self, fid: int):
+        loc, n = C.c_int32(), C.c_int32()
+        self._c(lib.aqua_prefix_query(self.h, fid, C.byref(loc), C.byref(n), None, 0))
+        sl = np.empty(max(n.value, 1), np.int32)
+        self._c(lib.aqua_prefix_query(self.h, fid, None, None, _i32p(sl), n.value))
+        return loc.value, sl[:n.value].tolist()
+
+    def prefix_load(self, fid: int, dst_pid: int, stream: int = 0) -> Tuple[List[int], int]:
+        n = self.prefix_query(fid)[1]
+        ids = np.empty(max(len(n), 1), np.int32)
+        t = C.c_uint64()
+        self._c(lib.aqua_prefix_load(self.h, fid, dst_pid, C.c_void_p(stream or None), _i32p(ids), len(n),
+                                     C.byref(t)))
+        return ids[:len(n)].tolist(), t.value
+
+    def prefix_drop(self, fid: int) -> None:
+        self._c(lib.aqua_prefix_drop(self.h, fid))
 
     def wait(self, ticket: int, stream: int = 0) -> None:
         self._c(lib.aqua_wait(self.h, ticket, C.c_void_p(stream or None)))

@@ -70,6 +70,7 @@ struct aqua_ctx {
   aqua::IdSet free_blocks;
   std::vector<uint64_t> btick;  // last library ticket that touched each block
   std::unordered_map<uint64_t, Prompt> prompts;
+  std::unordered_map<uint64_t, Prompt> prefixes;  // NEXT-2 cached-prefix images (ids: own namespace)
   Arena gpu, host;              // AQUA_LOC_PEER, AQUA_LOC_HOST
   int kernel = AQUA_KERNEL_AUTO;
   int max_ctas = 0;
@@ -852,23 +853,11 @@ aqua_status aqua_swap_in(aqua_ctx* c, int32_t n, const uint64_t* pids, aqua_stre
   return AQUA_OK;
 }
 
-static aqua_status migrate_impl(aqua_ctx* c, const std::vector<uint64_t>& pids, int32_t dst, cudaStream_t st,
-                                uint64_t* out_ticket) {
-  if (dst != AQUA_LOC_PEER && dst != AQUA_LOC_HOST) return fail(c, AQUA_E_INVAL, "dst must be PEER or HOST");
-  std::unordered_set<uint64_t> seen;
-  for (uint64_t pid : pids)
-    if (!seen.insert(pid).second) return fail(c, AQUA_E_INVAL, "duplicate pid");
-  std::vector<Prompt*> ps;
-  int64_t need = 0;
-  for (uint64_t pid : pids) {
-    auto it = c->prompts.find(pid);
-    if (it == c->prompts.end() || it->second.state != AQUA_ST_SWAPPED || it->second.loc == dst)
-      return fail(c, AQUA_E_STATE, "pid has no image outside dst");
-    ps.push_back(&it->second);
-    need += static_cast<int64_t>(it->second.ids.size());
-  }
+// Move the images `ps` (prompts or cached prefixes, capacity already checked)
+// to the lowest free slots of arena `dst`, in order, with one fused launch.
+static aqua_status move_images(aqua_ctx* c, const std::vector<Prompt*>& ps, int32_t dst, cudaStream_t st,
+                               uint64_t* out_ticket) {
   Arena* ad = arena_of(c, dst);
-  if (!ad->present || need > ad->free.size()) return fail(c, AQUA_E_NOSPACE, "dst arena missing or full");
   std::vector<Desc> ds;
   std::vector<std::vector<int32_t>> fresh(ps.size());
   const uint32_t dbit = dst == AQUA_LOC_HOST ? kArenaBit : 0u;
@@ -927,6 +916,26 @@ static aqua_status migrate_impl(aqua_ctx* c, const std::vector<uint64_t>& pids, 
   return AQUA_OK;
 }
 
+static aqua_status migrate_impl(aqua_ctx* c, const std::vector<uint64_t>& pids, int32_t dst, cudaStream_t st,
+                                uint64_t* out_ticket) {
+  if (dst != AQUA_LOC_PEER && dst != AQUA_LOC_HOST) return fail(c, AQUA_E_INVAL, "dst must be PEER or HOST");
+  std::unordered_set<uint64_t> seen;
+  for (uint64_t pid : pids)
+    if (!seen.insert(pid).second) return fail(c, AQUA_E_INVAL, "duplicate pid");
+  std::vector<Prompt*> ps;
+  int64_t need = 0;
+  for (uint64_t pid : pids) {
+    auto it = c->prompts.find(pid);
+    if (it == c->prompts.end() || it->second.state != AQUA_ST_SWAPPED || it->second.loc == dst)
+      return fail(c, AQUA_E_STATE, "pid has no image outside dst");
+    ps.push_back(&it->second);
+    need += static_cast<int64_t>(it->second.ids.size());
+  }
+  Arena* ad = arena_of(c, dst);
+  if (!ad->present || need > ad->free.size()) return fail(c, AQUA_E_NOSPACE, "dst arena missing or full");
+  return move_images(c, ps, dst, st, out_ticket);
+}
+
 aqua_status aqua_migrate(aqua_ctx* c, int32_t n, const uint64_t* pids, int32_t dst_loc, aqua_stream_t stream,
                          uint64_t* out_ticket) {
   if (aqua_status s = precheck(c)) return s;
@@ -940,10 +949,21 @@ aqua_status aqua_reclaim(aqua_ctx* c, aqua_stream_t stream, uint64_t* out_ticket
   if (aqua_status s = precheck(c)) return s;
   if (out_ticket) *out_ticket = 0;
   if (!c->gpu.present) return AQUA_OK;                 // idempotent
-  std::vector<uint64_t> pids;
+  // prompts in ascending pid, then cached prefixes in ascending id
+  std::vector<uint64_t> pids, fids;
   for (const auto& kv : c->prompts)
     if (kv.second.state == AQUA_ST_SWAPPED && kv.second.loc == AQUA_LOC_PEER) pids.push_back(kv.first);
+  for (const auto& kv : c->prefixes)
+    if (kv.second.loc == AQUA_LOC_PEER) fids.push_back(kv.first);
   std::sort(pids.begin(), pids.end());
+  std::sort(fids.begin(), fids.end());
+  std::vector<Prompt*> ps;
+  int64_t need = 0;
+  for (uint64_t p : pids) ps.push_back(&c->prompts[p]);
+  for (uint64_t f : fids) ps.push_back(&c->prefixes[f]);
+  for (Prompt* p : ps) need += static_cast<int64_t>(p->ids.size());
+  if (need > 0 && (!c->host.present || need > c->host.free.size()))
+    return fail(c, AQUA_E_NOSPACE, "host cannot hold the lender's images");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   uint64_t ticket = 0;
   // the ticket must cover every library access to the lender: order the
@@ -952,8 +972,8 @@ aqua_status aqua_reclaim(aqua_ctx* c, aqua_stream_t stream, uint64_t* out_ticket
     DevGuard g(c->device);
     if (aqua_status s = wait_all(c, c->gpu.tick, st)) return s;
   }
-  if (!pids.empty()) {
-    if (aqua_status s = migrate_impl(c, pids, AQUA_LOC_HOST, st, &ticket)) return s;
+  if (need > 0) {
+    if (aqua_status s = move_images(c, ps, AQUA_LOC_HOST, st, &ticket)) return s;
   } else if (!c->dry) {
     DevGuard g(c->device);
     if (aqua_status s = record(c, st, &ticket)) return s;
@@ -961,6 +981,144 @@ aqua_status aqua_reclaim(aqua_ctx* c, aqua_stream_t stream, uint64_t* out_ticket
   if (!c->dry && c->gpu.owned) c->zombies.push_back(aqua_ctx::Zombie{c->gpu.device, c->gpu.base, ticket});
   c->gpu = Arena();
   if (out_ticket) *out_ticket = ticket;
+  return AQUA_OK;
+}
+
+// ---------------------------------------------------------------- NEXT-2
+aqua_status aqua_prefix_store(aqua_ctx* c, uint64_t fid, uint64_t src_pid, int32_t n, aqua_stream_t stream,
+                              uint64_t* out_ticket) {
+  if (aqua_status s = precheck(c)) return s;
+  if (out_ticket) *out_ticket = 0;
+  if (c->prefixes.count(fid)) return fail(c, AQUA_E_INVAL, "prefix id in use");
+  auto it = c->prompts.find(src_pid);
+  if (it == c->prompts.end() || it->second.state != AQUA_ST_RESIDENT) return fail(c, AQUA_E_STATE, "src not resident");
+  Prompt& src = it->second;
+  if (n < 0 || n > static_cast<int32_t>(src.ids.size())) return fail(c, AQUA_E_INVAL, "bad block count");
+  int loc;
+  if (c->gpu.present && c->gpu.free.size() >= n)
+    loc = AQUA_LOC_PEER;
+  else if (c->host.present && c->host.free.size() >= n)
+    loc = AQUA_LOC_HOST;
+  else
+    return fail(c, AQUA_E_NOSPACE, "no swap space for the prefix");
+  Arena* a = arena_of(c, loc);
+  const uint32_t bit = loc == AQUA_LOC_HOST ? kArenaBit : 0u;
+  std::vector<Desc> ds;
+  std::vector<int32_t> slots;
+  auto fit = a->free.begin();
+  for (int32_t j = 0; j < n; ++j) {
+    const int32_t sl = *fit++;
+    slots.push_back(sl);
+    ds.push_back(Desc{src.ids[j], static_cast<uint32_t>(sl) | bit});
+  }
+  set_last(c, ds);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  uint64_t ticket = 0;
+  if (!c->dry && !ds.empty()) {
+    DevGuard g(c->device);
+    std::vector<uint64_t> ts;
+    for (const Desc& d : ds) {
+      ts.push_back(c->btick[d.block]);
+      ts.push_back(a->tick[d.slot_arena & ~kArenaBit]);
+    }
+    if (aqua_status s = wait_all(c, ts, st)) return s;
+    cudaEvent_t t_start;
+    if (aqua_status s = timing_start(c, st, &t_start)) return s;
+    int regions = 0;
+    if (aqua_status s = run_copy(c, ds, aqua::kOut, st, &regions)) return s;
+    if (aqua_status s = record(c, st, &ticket, t_start)) return s;
+    stage_seal(c, regions, ticket);
+  } else if (c->dry && !ds.empty()) {
+    record(c, st, &ticket);
+  }
+  for (size_t j = 0; j < slots.size(); ++j) {
+    a->free.erase(slots[j]);
+    a->tick[slots[j]] = ticket;
+    c->btick[src.ids[j]] = ticket;     // last reader of the prompt's blocks
+  }
+  Prompt img;
+  img.state = AQUA_ST_SWAPPED;
+  img.loc = loc;
+  img.ids = std::move(slots);
+  c->prefixes[fid] = std::move(img);
+  if (out_ticket) *out_ticket = ticket;
+  return AQUA_OK;
+}
+
+aqua_status aqua_prefix_load(aqua_ctx* c, uint64_t fid, uint64_t dst_pid, aqua_stream_t stream, int32_t* out_ids,
+                             int32_t cap, uint64_t* out_ticket) {
+  if (aqua_status s = precheck(c)) return s;
+  if (out_ticket) *out_ticket = 0;
+  auto fi = c->prefixes.find(fid);
+  if (fi == c->prefixes.end()) return fail(c, AQUA_E_STATE, "unknown prefix");
+  const Prompt& img = fi->second;
+  auto pi = c->prompts.find(dst_pid);
+  if (pi != c->prompts.end() && pi->second.state != AQUA_ST_RESIDENT) return fail(c, AQUA_E_STATE, "dst swapped");
+  const int32_t n = static_cast<int32_t>(img.ids.size());
+  if (n > 0 && (!out_ids || cap < n)) return fail(c, AQUA_E_INVAL, "out_ids too small");
+  if (n > c->free_blocks.size()) return fail(c, AQUA_E_NOBLOCKS, "pool exhausted");
+  Arena* a = arena_of(c, img.loc);
+  const uint32_t bit = img.loc == AQUA_LOC_HOST ? kArenaBit : 0u;
+  std::vector<Desc> ds;
+  std::vector<int32_t> fresh;
+  auto fb = c->free_blocks.begin();
+  for (int32_t j = 0; j < n; ++j) {
+    const int32_t b = *fb++;
+    fresh.push_back(b);
+    ds.push_back(Desc{b, static_cast<uint32_t>(img.ids[j]) | bit});
+  }
+  set_last(c, ds);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  uint64_t ticket = 0;
+  if (!c->dry && !ds.empty()) {
+    DevGuard g(c->device);
+    std::vector<uint64_t> ts;
+    for (const Desc& d : ds) {
+      ts.push_back(c->btick[d.block]);
+      ts.push_back(a->tick[d.slot_arena & ~kArenaBit]);
+    }
+    if (aqua_status s = wait_all(c, ts, st)) return s;
+    cudaEvent_t t_start;
+    if (aqua_status s = timing_start(c, st, &t_start)) return s;
+    int regions = 0;
+    if (aqua_status s = run_copy(c, ds, aqua::kIn, st, &regions)) return s;
+    if (aqua_status s = record(c, st, &ticket, t_start)) return s;
+    stage_seal(c, regions, ticket);
+  } else if (c->dry && !ds.empty()) {
+    record(c, st, &ticket);
+  }
+  c->free_blocks.erase_lowest(n);
+  Prompt& p = c->prompts[dst_pid];
+  for (int32_t j = 0; j < n; ++j) {
+    c->btick[fresh[j]] = ticket;
+    a->tick[img.ids[j]] = ticket;      // last reader of the image
+    p.ids.push_back(fresh[j]);
+    out_ids[j] = fresh[j];
+  }
+  if (out_ticket) *out_ticket = ticket;
+  return AQUA_OK;
+}
+
+aqua_status aqua_prefix_drop(aqua_ctx* c, uint64_t fid) {
+  if (aqua_status s = precheck(c)) return s;
+  auto fi = c->prefixes.find(fid);
+  if (fi == c->prefixes.end()) return fail(c, AQUA_E_STATE, "unknown prefix");
+  Arena* a = arena_of(c, fi->second.loc);
+  for (int32_t sl : fi->second.ids) a->free.insert(sl);   // slot ticks keep the last reader
+  c->prefixes.erase(fi);
+  return AQUA_OK;
+}
+
+aqua_status aqua_prefix_query(aqua_ctx* c, uint64_t fid, int32_t* location, int32_t* n, int32_t* slots, int32_t cap) {
+  if (!c) return fail(nullptr, AQUA_E_INVAL, "null ctx");
+  auto fi = c->prefixes.find(fid);
+  if (fi == c->prefixes.end()) return fail(c, AQUA_E_STATE, "unknown prefix");
+  if (location) *location = fi->second.loc;
+  if (n) *n = static_cast<int32_t>(fi->second.ids.size());
+  if (slots) {
+    if (cap < static_cast<int32_t>(fi->second.ids.size())) return fail(c, AQUA_E_INVAL, "capacity too small");
+    std::copy(fi->second.ids.begin(), fi->second.ids.end(), slots);
+  }
   return AQUA_OK;
 }
 

@@ -149,6 +149,49 @@ def migrate():
                       "verify_mismatches": int(cnt.item())}), flush=True)
 
 
+def prefix():
+    """NEXT-2, BASELINE-adjacent E7 shape: Yi-34B-200K over TP2 per
+    rank (60 layers, 4 KV heads, D=128, bf16, block 16 -> U = 1.875 MiB); a
+    100K-token cached prefix (6250 blocks, 11.4 GiB) stored once and loaded on
+    each hit, from the lender (self) and from host DRAM."""
+    L, bs, H, D = 60, 16, 4, 128
+    S = bs * H * D * 2
+    U = 2 * L * S
+    nblk = 6250
+    NB = 2 * nblk + 64
+    layers = [torch.zeros(2 * NB * S, dtype=torch.uint8, device="cuda") for _ in range(L)]
+    out = {}
+    for where in ("self", "host"):
+        ctx = aqua.Ctx(0, L, bs, H, D, 2, NB, [t.data_ptr() for t in layers])
+        arena = None
+        if where == "self":
+            arena = torch.empty(nblk * U, dtype=torch.uint8, device="cuda")
+            ctx.lend(0, arena.data_ptr(), nblk * U)
+        else:
+            ctx.lend(aqua.HOST, 0, nblk * U)
+        ctx.set_option(aqua.OPT_TIMING, 1)
+        s = torch.cuda.Stream()
+        ctx.adopt_blocks(1, block_permutation(NB, nblk, seed=4).tolist())
+        ctx.kv_fill_pattern(1, 0, nblk * bs, 11, s.cuda_stream)
+        t0 = ctx.prefix_store(77, 1, nblk, s.cuda_stream)
+        torch.cuda.synchronize()
+        store_ms = ctx.ticket_elapsed(t0)
+        ctx.free(1, s.cuda_stream)
+        loads = []
+        cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+        for hit in range(4):
+            ids, tk = ctx.prefix_load(77, 1000 + hit, s.cuda_stream)
+            torch.cuda.synchronize()
+            loads.append(ctx.ticket_elapsed(tk))
+            ctx.free(1000 + hit, s.cuda_stream)
+        out[where] = {"store_ms": round(store_ms, 3), "load_ms_p50": round(statistics.median(loads), 3),
+                      "load_GBps": round(nblk * U / statistics.median(loads) / 1e6, 1)}
+        ctx.close()
+        del arena
+        torch.cuda.empty_cache()
+    print(json.dumps({"prefix_tokens": nblk * bs, "bytes": nblk * U, **out}), flush=True)
+
+
 def stages():
     L, bs, H, D, NB, nblk = 32, 16, 8, 128, 4096, 2048
     ctx, layers, arena, U = setup(L, bs, H, D, NB, nblk)
@@ -198,6 +241,8 @@ if __name__ == "__main__":
         c5(host=True)
     elif what == "stages":
         stages()
+    elif what == "prefix":
+        prefix()
     elif what == "migrate":
         migrate()
     elif what == "host_ctas":

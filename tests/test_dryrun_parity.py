@@ -93,6 +93,16 @@ def _apply(pool, c, op):
                     moved = sorted(p for p in range(6) if _loc(c, p) == aqua.LOC_PEER)
                     c.reclaim()
                     r = moved
+            elif name == "pstore":
+                if side == "oracle":
+                    r = pool.prefix_store(*arg)
+                else:
+                    c.prefix_store(*arg)
+                    r = c.prefix_query(arg[0])
+            elif name == "pload":
+                r = pool.prefix_load(*arg) if side == "oracle" else c.prefix_load(*arg)[0]
+            elif name == "pdrop":
+                r = pool.prefix_drop(arg) if side == "oracle" else c.prefix_drop(arg)
             elif name == "relend":
                 r = pool.lend(kp.LOC_PEER, arg * lay_U(pool)) if side == "oracle" else \
                     c.lend(0, FAKE * 4, arg * c.U)
@@ -116,7 +126,7 @@ def lay_U(pool):
     return pool.lay.U
 
 
-@pytest.mark.parametrize("seed", range(40))
+@pytest.mark.parametrize("seed", range(60))
 def test_random_op_sequences_match_oracle(seed):
     rnd = random.Random(seed)
     NB = rnd.randint(1, 24)
@@ -147,10 +157,16 @@ def test_random_op_sequences_match_oracle(seed):
             op = ("free", rnd.choice(pids))
         elif k < 0.93:
             op = ("mig", (rnd.sample(pids, rnd.randint(1, 2)), rnd.choice([kp.LOC_PEER, kp.LOC_HOST])))
-        elif k < 0.97:
+        elif k < 0.95:
             op = ("reclaim", None)
-        else:
+        elif k < 0.96:
             op = ("relend", rnd.choice([1, 4, 8]))
+        elif k < 0.98:
+            op = ("pstore", (rnd.randint(0, 2), rnd.choice(pids), rnd.randint(-1, 3)))
+        elif k < 0.995:
+            op = ("pload", (rnd.randint(0, 2), rnd.choice(pids)))
+        else:
+            op = ("pdrop", rnd.randint(0, 2))
         a, b = _apply(pool, c, op)
         assert a == b, (seed, op, a, b)
         pool.check_invariants()
@@ -158,6 +174,8 @@ def test_random_op_sequences_match_oracle(seed):
         assert cnt[0] == len(pool.free)
         assert cnt[1] == (len(pool.peer.free) if pool.peer is not None else -1)
         assert cnt[2] == (len(pool.host.free) if pool.host is not None else -1)
+        for f, img in pool.prefixes.items():
+            assert c.prefix_query(f) == (img.location, img.slots)
         for p, pr in pool.prompts.items():
             st, loc, n, ids = c.query(p, with_ids=True)
             assert (st, loc, ids) == (pr.state, pr.location, pr.blocks if pr.state == kp.RESIDENT else pr.slots)

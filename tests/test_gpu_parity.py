@@ -312,3 +312,34 @@ def test_migrate_reclaim_relend_bytes(engine):
     assert o.migrate([2, 1], kp.LOC_PEER) == [(2, [0, 1, 2]), (1, [3, 4, 5, 6, 7])]
     rig.assert_bytes_equal("migrate back")
     _ops(rig, [("in", [1, 2, 3]), ("out", [2])])
+
+
+@pytest.mark.parametrize("engine", ["tma", "ldst"])
+def test_prefix_cache_bytes(engine):
+    """NEXT-2 on the GPU: store a cached prefix (copy), load it into three
+    new prompts, reclaim moves it to the host, load again -- whole buffers
+    byte-equal to the oracle after every call."""
+    rig = Rig(L=3, bs=16, H=4, D=64, NB=48, lender_slots=12, host_slots=12)
+    c, o = rig.ctx, rig.opool
+    c.set_option(aqua.OPT_KERNEL, ENGINES[engine])
+    _ops(rig, [("adopt", (5, [40, 3, 17, 8, 22]))])
+    c.prefix_store(9, 5, 4)
+    assert o.prefix_store(9, 5, 4) == (kp.LOC_PEER, [0, 1, 2, 3])
+    rig.assert_bytes_equal("prefix store")
+    for dst in (100, 101, 102):
+        ids, _ = c.prefix_load(9, dst)
+        assert ids == o.prefix_load(9, dst)
+        rig.assert_bytes_equal(f"prefix load {dst}")
+    _ops(rig, [("out", [101])])
+    c.reclaim()
+    o.reclaim()
+    assert c.prefix_query(9) == (aqua.LOC_HOST, o.prefixes[9].slots)
+    ids, _ = c.prefix_load(9, 103)
+    assert ids == o.prefix_load(9, 103)
+    torch.cuda.synchronize()
+    for l, t in enumerate(rig.layers):
+        assert np.array_equal(t.cpu().numpy(), o.layers[l])
+    assert np.array_equal(rig.host.numpy(), o.host.data)
+    c.prefix_drop(9)
+    o.prefix_drop(9)
+    assert c.counts()[2] == len(o.host.free)
