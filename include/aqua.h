@@ -183,6 +183,20 @@ AQUA_API aqua_status aqua_swap_in(aqua_ctx* ctx, int32_t n, const uint64_t* pids
                          int32_t* out_ids, int64_t out_ids_cap, int32_t* out_counts,
                          uint64_t* out_ticket);
 
+/* NEXT-3, layer-wise streaming (Sec. 9: FlexGen "pages the
+ * previous layer's context out and the next layer's in"): exactly
+ * aqua_swap_out / aqua_swap_in (same bookkeeping, same bytes), but the copy
+ * is issued as ceil(L / layer_group) launches in layer order, and
+ * out_tickets[g] completes when layers [g*layer_group, (g+1)*layer_group) are
+ * done -- decode can start on layer group 0 of a resumed prompt while the
+ * rest is still in flight.  The last ticket covers the whole copy.
+ * out_tickets has ceil(L / layer_group) entries; layer_group >= 1. */
+AQUA_API aqua_status aqua_swap_out_layers(aqua_ctx* ctx, int32_t n, const uint64_t* pids, aqua_stream_t stream,
+                                          int32_t layer_group, uint64_t* out_tickets);
+AQUA_API aqua_status aqua_swap_in_layers(aqua_ctx* ctx, int32_t n, const uint64_t* pids, aqua_stream_t stream,
+                                         int32_t layer_group, int32_t* out_ids, int64_t out_ids_cap,
+                                         int32_t* out_counts, uint64_t* out_tickets);
+
 /* Forget pid: RESIDENT -> its blocks are freed (their last use
  * is taken to be the work already queued on `stream`); SWAPPED -> its slots
  * are freed. */

@@ -30,7 +30,7 @@ OPT_KERNEL, OPT_MAX_CTAS, OPT_TMA_PIECE, OPT_TMA_STAGES, OPT_TIMING = 1, 2, 3, 4
 # Every symbol include/aqua.h declares (checked by tests/test_abi.py).
 SYMBOLS = [
     "aqua_create", "aqua_destroy", "aqua_lend", "aqua_alloc_blocks", "aqua_adopt_blocks",
-    "aqua_swap_out", "aqua_swap_in", "aqua_free", "aqua_migrate", "aqua_reclaim", "aqua_prefix_store", "aqua_prefix_load",
+    "aqua_swap_out", "aqua_swap_in", "aqua_swap_out_layers", "aqua_swap_in_layers", "aqua_free", "aqua_migrate", "aqua_reclaim", "aqua_prefix_store", "aqua_prefix_load",
     "aqua_prefix_drop", "aqua_prefix_query", "aqua_wait", "aqua_sync", "aqua_ticket_done", "aqua_ticket_elapsed",
     "aqua_query", "aqua_counts", "aqua_arena_base", "aqua_set_option", "aqua_get_option",
     "aqua_last_descriptors", "aqua_launch_count", "aqua_ipc_export", "aqua_ipc_import",
@@ -66,6 +66,8 @@ def _load() -> C.CDLL:
         "aqua_adopt_blocks": (C.c_int, [VP, U64, I32, P(I32), VP]),
         "aqua_swap_out": (C.c_int, [VP, I32, P(U64), VP, P(U64)]),
         "aqua_swap_in": (C.c_int, [VP, I32, P(U64), VP, P(I32), I64, P(I32), P(U64)]),
+        "aqua_swap_out_layers": (C.c_int, [VP, I32, P(U64), VP, I32, P(U64)]),
+        "aqua_swap_in_layers": (C.c_int, [VP, I32, P(U64), VP, I32, P(I32), I64, P(I32), P(U64)]),
         "aqua_free": (C.c_int, [VP, U64, VP]),
         "aqua_migrate": (C.c_int, [VP, I32, P(U64), I32, VP, P(U64)]),
         "aqua_reclaim": (C.c_int, [VP, VP, P(U64)]),
@@ -183,6 +185,29 @@ class Ctx:
             out.append(ids[k:k + counts[i]].tolist())
             k += counts[i]
         return out, t.value
+
+    def swap_out_layers(self, pids: Sequence[int], layer_group: int, stream: int = 0) -> List[int]:
+        a = np.ascontiguousarray(pids, dtype=np.uint64)
+        ng = -(-self.L // layer_group) if layer_group > 0 else 1
+        t = np.zeros(max(ng, 1), np.uint64)
+        self._c(lib.aqua_swap_out_layers(self.h, len(a), _u64p(a), C.c_void_p(stream or None), layer_group,
+                                         _u64p(t)))
+        return [int(x) for x in t[:ng]]
+
+    def swap_in_layers(self, pids: Sequence[int], layer_group: int, stream: int = 0):
+        a = np.ascontiguousarray(pids, dtype=np.uint64)
+        cap = sum(self.query(int(p))[2] for p in a)
+        ids = np.empty(max(cap, 1), np.int32)
+        counts = np.empty(max(len(a), 1), np.int32)
+        ng = -(-self.L // layer_group) if layer_group > 0 else 1
+        t = np.zeros(max(ng, 1), np.uint64)
+        self._c(lib.aqua_swap_in_layers(self.h, len(a), _u64p(a), C.c_void_p(stream or None), layer_group,
+                                        _i32p(ids), cap, _i32p(counts), _u64p(t)))
+        out, k = [], 0
+        for i in range(len(a)):
+            out.append(ids[k:k + counts[i]].tolist())
+            k += counts[i]
+        return out, [int(x) for x in t[:ng]]
 
     def free(self, pid: int, stream: int = 0) -> None:
         self._c(lib.aqua_free(self.h, pid, C.c_void_p(stream or None)))

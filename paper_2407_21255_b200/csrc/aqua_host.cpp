@@ -290,10 +290,13 @@ void stage_seal(aqua_ctx* c, size_t nregions, uint64_t ticket) {
 }
 
 // ------------------------------------------------------------ copy engines
+// Moves chunks [c0, c0 + nc) (c = 2l + kv; default: all 2L) of every
+// descriptor with the configured engine.
 aqua_status run_copy(aqua_ctx* c, const std::vector<Desc>& ds, aqua::Dir dir, cudaStream_t st,
-                     int* regions) {
+                     int* regions, int32_t c0 = 0, int32_t nc = -1, const Desc* dev_desc = nullptr) {
   *regions = 0;
   if (ds.empty()) return AQUA_OK;
+  if (nc < 0) nc = 2 * c->L;
   aqua::SwapParams p{};
   p.layer_base = c->d_layer_base;
   p.arena_base[0] = reinterpret_cast<uint64_t>(c->gpu.base);
@@ -304,8 +307,11 @@ aqua_status run_copy(aqua_ctx* c, const std::vector<Desc>& ds, aqua::Dir dir, cu
   p.U = c->U;
   p.P_kv = c->P_kv;
   p.P_b = c->P_b;
+  p.c0 = c0;
+  p.nc = nc;
   int engine = c->kernel == AQUA_KERNEL_AUTO ? AQUA_KERNEL_TMA : c->kernel;
   if (dir == aqua::kMig && engine != AQUA_KERNEL_LDST) engine = AQUA_KERNEL_TMA;  // baselines do not migrate
+  if (nc != 2 * c->L && engine == AQUA_BASE_GATHER_TEMP) engine = AQUA_KERNEL_TMA;  // whole blocks only
 
   auto chunk_ptrs = [&](const Desc& d, int cc, uint8_t** pool, uint8_t** img) {
     const int l = cc >> 1, kv = cc & 1;
@@ -315,7 +321,9 @@ aqua_status run_copy(aqua_ctx* c, const std::vector<Desc>& ds, aqua::Dir dir, cu
   };
 
   if (engine == AQUA_KERNEL_TMA || engine == AQUA_KERNEL_LDST) {
-    if (ds.size() <= static_cast<size_t>(aqua::kInlineDesc)) {
+    if (dev_desc) {
+      p.desc = dev_desc;                      // already uploaded by the caller
+    } else if (ds.size() <= static_cast<size_t>(aqua::kInlineDesc)) {
       p.desc = nullptr;                       // descriptors ride in the kernel parameters
       std::copy(ds.begin(), ds.end(), p.inl);
     } else {
@@ -343,19 +351,19 @@ aqua_status run_copy(aqua_ctx* c, const std::vector<Desc>& ds, aqua::Dir dir, cu
       int piece = stage;
       if (piece >= c->S) {
         piece = static_cast<int>(c->S);
-        p.group = std::max(1, std::min(stage / piece, 2 * c->L));
+        p.group = std::max(1, std::min(stage / piece, nc));
       } else {
         p.group = 1;
       }
       p.piece = piece;
       p.npieces = static_cast<int32_t>((c->S + piece - 1) / piece);
-      p.nitems = p.ndesc * 2 * p.L * p.npieces;
+      p.nitems = p.ndesc * nc * p.npieces;
       e = aqua::launch_swap_tma(p, dir, c->num_sms, cap, c->tma_stages, st, &ctas);
     } else {
       p.piece = 4096;
       p.group = 1;
       p.npieces = static_cast<int32_t>((c->S + 4095) / 4096);
-      p.nitems = p.ndesc * 2 * p.L * p.npieces;
+      p.nitems = p.ndesc * nc * p.npieces;
       e = aqua::launch_swap_ldst(p, dir, c->num_sms, all_host && cap == kHostCtas ? 2 * kHostCtas : cap, st, &ctas);
     }
     if (e != cudaSuccess) return cuda_fail(c, e, "swap kernel launch");
@@ -364,7 +372,7 @@ aqua_status run_copy(aqua_ctx* c, const std::vector<Desc>& ds, aqua::Dir dir, cu
   }
   if (engine == AQUA_BASE_PER_CHUNK) {
     for (const Desc& d : ds)
-      for (int cc = 0; cc < 2 * c->L; ++cc) {
+      for (int cc = c0; cc < c0 + nc; ++cc) {
         uint8_t *pool, *img;
         chunk_ptrs(d, cc, &pool, &img);
         if (dir == aqua::kOut)
@@ -375,12 +383,12 @@ aqua_status run_copy(aqua_ctx* c, const std::vector<Desc>& ds, aqua::Dir dir, cu
     return AQUA_OK;
   }
   if (engine == AQUA_BASE_BATCH) {
-    const size_t n = ds.size() * 2 * c->L;
+    const size_t n = ds.size() * nc;
     std::vector<void*> dsts(n), srcs(n);
     std::vector<size_t> sizes(n, static_cast<size_t>(c->S));
     size_t k = 0;
     for (const Desc& d : ds)
-      for (int cc = 0; cc < 2 * c->L; ++cc, ++k) {
+      for (int cc = c0; cc < c0 + nc; ++cc, ++k) {
         uint8_t *pool, *img;
         chunk_ptrs(d, cc, &pool, &img);
         dsts[k] = dir == aqua::kOut ? img : pool;
@@ -414,7 +422,7 @@ aqua_status run_copy(aqua_ctx* c, const std::vector<Desc>& ds, aqua::Dir dir, cu
     p.piece = 4096;
     p.group = 1;
     p.npieces = static_cast<int32_t>((c->S + 4095) / 4096);
-    p.nitems = p.ndesc * 2 * p.L * p.npieces;
+    p.nitems = p.ndesc * nc * p.npieces;
     auto runs = [&](bool to_arena) -> aqua_status {
       size_t j = 0;
       while (j < ds.size()) {
@@ -446,6 +454,50 @@ aqua_status run_copy(aqua_ctx* c, const std::vector<Desc>& ds, aqua::Dir dir, cu
     return AQUA_OK;
   }
   return fail(c, AQUA_E_INVAL, "unknown copy engine");
+}
+
+// Enqueue the copy of `ds` on `st`: one launch (layer_group <= 0 or >= L),
+// or one launch per group of layer_group layers in layer order, each with its
+// own ticket in group_tickets[] (layer-wise streaming, NEXT-3), so a consumer
+// can start on layer group g as soon as its ticket completes.  *ticket = the
+// last one, which covers the whole copy.
+aqua_status enqueue_copy(aqua_ctx* c, const std::vector<Desc>& ds, aqua::Dir dir, cudaStream_t st,
+                         int32_t layer_group, uint64_t* group_tickets, uint64_t* ticket) {
+  if (layer_group <= 0 || layer_group >= c->L) {
+    cudaEvent_t t_start;
+    if (aqua_status s = timing_start(c, st, &t_start)) return s;
+    int regions = 0;
+    if (aqua_status s = run_copy(c, ds, dir, st, &regions)) return s;
+    if (aqua_status s = record(c, st, ticket, t_start)) return s;
+    stage_seal(c, regions, *ticket);
+    if (group_tickets) group_tickets[0] = *ticket;
+    return AQUA_OK;
+  }
+  const Desc* dd = nullptr;
+  int up = 0;
+  const bool fused = c->kernel == AQUA_KERNEL_AUTO || c->kernel == AQUA_KERNEL_TMA || c->kernel == AQUA_KERNEL_LDST;
+  if (fused && ds.size() > static_cast<size_t>(aqua::kInlineDesc)) {
+    void* d;
+    if (aqua_status s = stage_upload(c, ds.data(), ds.size() * sizeof(Desc), st, &d)) return s;
+    dd = static_cast<const Desc*>(d);
+    up = 1;
+  }
+  const int32_t ng = (c->L + layer_group - 1) / layer_group;
+  for (int32_t g = 0; g < ng; ++g) {
+    const int32_t l0 = g * layer_group, l1 = std::min(c->L, l0 + layer_group);
+    cudaEvent_t t_start;
+    if (aqua_status s = timing_start(c, st, &t_start)) return s;
+    int regions = 0;
+    if (aqua_status s = run_copy(c, ds, dir, st, &regions, 2 * l0, 2 * (l1 - l0), dd)) return s;
+    if (aqua_status s = record(c, st, ticket, t_start)) return s;
+    stage_seal(c, regions, *ticket);
+    if (group_tickets) group_tickets[g] = *ticket;
+  }
+  if (up) {   // the shared descriptor upload lives until the last group is done
+    for (auto& r : c->stage_live)
+      if (r.ticket == 0) r.ticket = *ticket;
+  }
+  return AQUA_OK;
 }
 
 aqua_status precheck(aqua_ctx* c) {
@@ -695,7 +747,8 @@ aqua_status aqua_adopt_blocks(aqua_ctx* c, uint64_t pid, int32_t n, const int32_
   return AQUA_OK;
 }
 
-aqua_status aqua_swap_out(aqua_ctx* c, int32_t n, const uint64_t* pids, aqua_stream_t stream, uint64_t* out_ticket) {
+static aqua_status swap_out_impl(aqua_ctx* c, int32_t n, const uint64_t* pids, aqua_stream_t stream,
+                                 uint64_t* out_ticket, int32_t layer_group, uint64_t* group_tickets) {
   if (aqua_status s = precheck(c)) return s;
   if (out_ticket) *out_ticket = 0;
   if (n < 0 || (n > 0 && !pids)) return fail(c, AQUA_E_INVAL, "n < 0 or null pids");
@@ -752,12 +805,7 @@ aqua_status aqua_swap_out(aqua_ctx* c, int32_t n, const uint64_t* pids, aqua_str
                        ->tick[d.slot_arena & ~kArenaBit]);
     }
     if (aqua_status s = wait_all(c, ts, st)) return s;
-    cudaEvent_t t_start;
-    if (aqua_status s = timing_start(c, st, &t_start)) return s;
-    int regions = 0;
-    if (aqua_status s = run_copy(c, ds, aqua::kOut, st, &regions)) return s;
-    if (aqua_status s = record(c, st, &ticket, t_start)) return s;
-    stage_seal(c, regions, ticket);
+    if (aqua_status s = enqueue_copy(c, ds, aqua::kOut, st, layer_group, group_tickets, &ticket)) return s;
   } else if (c->dry && !ds.empty()) {
     record(c, st, &ticket);
   }
@@ -780,8 +828,9 @@ aqua_status aqua_swap_out(aqua_ctx* c, int32_t n, const uint64_t* pids, aqua_str
   return AQUA_OK;
 }
 
-aqua_status aqua_swap_in(aqua_ctx* c, int32_t n, const uint64_t* pids, aqua_stream_t stream, int32_t* out_ids,
-                         int64_t out_ids_cap, int32_t* out_counts, uint64_t* out_ticket) {
+static aqua_status swap_in_impl(aqua_ctx* c, int32_t n, const uint64_t* pids, aqua_stream_t stream,
+                                int32_t* out_ids, int64_t out_ids_cap, int32_t* out_counts, uint64_t* out_ticket,
+                                int32_t layer_group, uint64_t* group_tickets) {
   if (aqua_status s = precheck(c)) return s;
   if (out_ticket) *out_ticket = 0;
   if (n < 0 || (n > 0 && !pids)) return fail(c, AQUA_E_INVAL, "n < 0 or null pids");
@@ -823,12 +872,7 @@ aqua_status aqua_swap_in(aqua_ctx* c, int32_t n, const uint64_t* pids, aqua_stre
                        ->tick[d.slot_arena & ~kArenaBit]);
     }
     if (aqua_status s = wait_all(c, ts, st)) return s;
-    cudaEvent_t t_start;
-    if (aqua_status s = timing_start(c, st, &t_start)) return s;
-    int regions = 0;
-    if (aqua_status s = run_copy(c, ds, aqua::kIn, st, &regions)) return s;
-    if (aqua_status s = record(c, st, &ticket, t_start)) return s;
-    stage_seal(c, regions, ticket);
+    if (aqua_status s = enqueue_copy(c, ds, aqua::kIn, st, layer_group, group_tickets, &ticket)) return s;
   } else if (c->dry && !ds.empty()) {
     record(c, st, &ticket);
   }
@@ -851,6 +895,42 @@ aqua_status aqua_swap_in(aqua_ctx* c, int32_t n, const uint64_t* pids, aqua_stre
   }
   if (out_ticket) *out_ticket = ticket;
   return AQUA_OK;
+}
+
+aqua_status aqua_swap_out(aqua_ctx* c, int32_t n, const uint64_t* pids, aqua_stream_t stream, uint64_t* out_ticket) {
+  return swap_out_impl(c, n, pids, stream, out_ticket, 0, nullptr);
+}
+
+aqua_status aqua_swap_in(aqua_ctx* c, int32_t n, const uint64_t* pids, aqua_stream_t stream, int32_t* out_ids,
+                         int64_t out_ids_cap, int32_t* out_counts, uint64_t* out_ticket) {
+  return swap_in_impl(c, n, pids, stream, out_ids, out_ids_cap, out_counts, out_ticket, 0, nullptr);
+}
+
+aqua_status aqua_swap_out_layers(aqua_ctx* c, int32_t n, const uint64_t* pids, aqua_stream_t stream,
+                                 int32_t layer_group, uint64_t* out_tickets) {
+  if (!c) return fail(nullptr, AQUA_E_INVAL, "null ctx");
+  if (layer_group < 1 || !out_tickets) return fail(c, AQUA_E_INVAL, "layer_group >= 1 and out_tickets needed");
+  const int32_t ng = (c->L + layer_group - 1) / layer_group;
+  for (int32_t g = 0; g < ng; ++g) out_tickets[g] = 0;
+  uint64_t last = 0;
+  aqua_status s = swap_out_impl(c, n, pids, stream, &last, layer_group, out_tickets);
+  if (s == AQUA_OK && c->dry)
+    for (int32_t g = 0; g < ng; ++g) out_tickets[g] = last;
+  return s;
+}
+
+aqua_status aqua_swap_in_layers(aqua_ctx* c, int32_t n, const uint64_t* pids, aqua_stream_t stream,
+                                int32_t layer_group, int32_t* out_ids, int64_t out_ids_cap, int32_t* out_counts,
+                                uint64_t* out_tickets) {
+  if (!c) return fail(nullptr, AQUA_E_INVAL, "null ctx");
+  if (layer_group < 1 || !out_tickets) return fail(c, AQUA_E_INVAL, "layer_group >= 1 and out_tickets needed");
+  const int32_t ng = (c->L + layer_group - 1) / layer_group;
+  for (int32_t g = 0; g < ng; ++g) out_tickets[g] = 0;
+  uint64_t last = 0;
+  aqua_status s = swap_in_impl(c, n, pids, stream, out_ids, out_ids_cap, out_counts, &last, layer_group, out_tickets);
+  if (s == AQUA_OK && c->dry)
+    for (int32_t g = 0; g < ng; ++g) out_tickets[g] = last;
+  return s;
 }
 
 // Move the images `ps` (prompts or cached prefixes, capacity already checked)
@@ -1078,12 +1158,7 @@ aqua_status aqua_prefix_load(aqua_ctx* c, uint64_t fid, uint64_t dst_pid, aqua_s
       ts.push_back(a->tick[d.slot_arena & ~kArenaBit]);
     }
     if (aqua_status s = wait_all(c, ts, st)) return s;
-    cudaEvent_t t_start;
-    if (aqua_status s = timing_start(c, st, &t_start)) return s;
-    int regions = 0;
-    if (aqua_status s = run_copy(c, ds, aqua::kIn, st, &regions)) return s;
-    if (aqua_status s = record(c, st, &ticket, t_start)) return s;
-    stage_seal(c, regions, ticket);
+    if (aqua_status s = enqueue_copy(c, ds, aqua::kIn, st, 0, nullptr, &ticket)) return s;
   } else if (c->dry && !ds.empty()) {
     record(c, st, &ticket);
   }

@@ -32,8 +32,9 @@ struct SwapParams {
   int32_t piece;               // bytes per work item (multiple of 16, divides nothing in particular)
   int32_t npieces;             // ceil(S / piece)
   int32_t group;               // TMA: chunks per stage when npieces == 1 (else 1)
+  int32_t c0, nc;              // chunk range [c0, c0+nc) of each block (layer-wise: c = 2l + kv)
   int64_t S, U, P_kv, P_b;
-  int64_t nitems;              // ndesc * 2L * npieces
+  int64_t nitems;              // ndesc * nc * npieces
   Desc inl[kInlineDesc];       // inline descriptors when desc == nullptr
 };
 

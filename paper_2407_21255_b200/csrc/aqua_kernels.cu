@@ -93,11 +93,12 @@ struct Cursor {
   int64_t j;
   int32_t c, q;
   __device__ __forceinline__ void init(int64_t item, const SwapParams& p) {
-    const int64_t per_desc = int64_t(2) * p.L * p.npieces;
+    const int64_t per_desc = int64_t(p.nc) * p.npieces;
     j = item / per_desc;
     const int64_t r = item - j * per_desc;
-    c = static_cast<int32_t>(r / p.npieces);
-    q = static_cast<int32_t>(r - int64_t(c) * p.npieces);
+    const int32_t cl = static_cast<int32_t>(r / p.npieces);
+    q = static_cast<int32_t>(r - int64_t(cl) * p.npieces);
+    c = p.c0 + cl;
   }
 };
 
@@ -155,7 +156,7 @@ struct Unit {
 
 __device__ __forceinline__ int unit_len(const SwapParams& p, const Unit& u) {
   if (p.group == 1) return 1;
-  int64_t k = 2 * p.L - u.c;
+  int64_t k = p.c0 + p.nc - u.c;
   if (k > p.group) k = p.group;
   if (k > u.left) k = u.left;
   return static_cast<int>(k);
@@ -166,15 +167,15 @@ __device__ __forceinline__ void unit_next(const SwapParams& p, Unit& u, int k) {
   if (p.group == 1) {
     if (++u.q == p.npieces) {
       u.q = 0;
-      if (++u.c == 2 * p.L) {
-        u.c = 0;
+      if (++u.c == p.c0 + p.nc) {
+        u.c = p.c0;
         ++u.j;
       }
     }
   } else {
     u.c += k;
-    if (u.c == 2 * p.L) {
-      u.c = 0;
+    if (u.c == p.c0 + p.nc) {
+      u.c = p.c0;
       ++u.j;
     }
   }

@@ -192,6 +192,54 @@ def prefix():
     print(json.dumps({"prefix_tokens": nblk * bs, "bytes": nblk * U, **out}), flush=True)
 
 
+def layers():
+    """NEXT-3: layer-wise resume of an OPT-30B-like
+    8192-token prompt (48 layers, 56 KV heads, D=128, bf16, block 16 -> U = 21
+    MiB/block, 10.7 GiB: the paper's "10 GB swap space for an 8K prompt",
+    P:1077) and of the C2 prompt; per-layer tickets give the time until layer 0
+    is usable vs the whole resume, from the lender (self) and from host DRAM."""
+    import time
+    for name, (L, bs, H, D, nblk) in {"opt30b_8k": (48, 16, 56, 128, 512),
+                                      "llama8b_32k": (32, 16, 8, 128, 2048)}.items():
+        S = bs * H * D * 2
+        U = 2 * L * S
+        NB = 2 * nblk
+        lay = [torch.zeros(2 * NB * S, dtype=torch.uint8, device="cuda") for _ in range(L)]
+        for where in ("self", "host"):
+            ctx = aqua.Ctx(0, L, bs, H, D, 2, NB, [t.data_ptr() for t in lay])
+            arena = None
+            if where == "self":
+                arena = torch.empty(nblk * U, dtype=torch.uint8, device="cuda")
+                ctx.lend(0, arena.data_ptr(), nblk * U)
+            else:
+                ctx.lend(aqua.HOST, 0, nblk * U)
+            ctx.set_option(aqua.OPT_TIMING, 1)
+            s = torch.cuda.Stream()
+            perm = block_permutation(NB, NB, seed=2).tolist()
+            ctx.adopt_blocks(1, perm[nblk:])
+            ctx.adopt_blocks(7, perm[:nblk])
+            rows = []
+            for rep in range(3):
+                ctx.swap_out([7], s.cuda_stream)
+                torch.cuda.synchronize()
+                a = torch.cuda.Event(enable_timing=True)
+                a.record(s)
+                new, tks = ctx.swap_in_layers([7], 1, s.cuda_stream)
+                torch.cuda.synchronize()
+                per = [ctx.ticket_elapsed(t) for t in tks]
+                rows.append((per[0], sum(per)))
+            first = statistics.median(r[0] for r in rows)
+            total = statistics.median(r[1] for r in rows)
+            print(json.dumps({"layers": name, "where": where, "bytes": nblk * U, "L": L,
+                              "first_layer_ms": round(first, 3), "all_layers_ms": round(total, 3),
+                              "GBps": round(nblk * U / total / 1e6, 1)}), flush=True)
+            ctx.close()
+            del arena
+            torch.cuda.empty_cache()
+        del lay
+        torch.cuda.empty_cache()
+
+
 def stages():
     L, bs, H, D, NB, nblk = 32, 16, 8, 128, 4096, 2048
     ctx, layers, arena, U = setup(L, bs, H, D, NB, nblk)
@@ -241,6 +289,8 @@ if __name__ == "__main__":
         c5(host=True)
     elif what == "stages":
         stages()
+    elif what == "layers":
+        layers()
     elif what == "prefix":
         prefix()
     elif what == "migrate":

@@ -329,3 +329,16 @@ def test_fallback_overflow_preemption_matches_oracle():
     s = Scheduler(NB=NB, bs=16, b=64, k=8)
     log, _ = run_trace(tr, c, s, elastic={"t_reclaim": 0.5, "t_relend": 1e9, "relend": (0, FAKE * 5, 400 * c.U)})
     assert log == o.log
+
+
+def test_layered_calls_same_bookkeeping_dryrun():
+    c = dry_ctx(L=5, NB=20)
+    c.lend(0, FAKE * 2, 20 * c.U)
+    c.alloc_blocks(1, 4)
+    t = c.swap_out_layers([1], 2)
+    assert len(t) == 3 and len(set(t)) == 1
+    assert c.query(1, with_ids=True)[3] == [0, 1, 2, 3]
+    new, t = c.swap_in_layers([1], 5)
+    assert new == [[0, 1, 2, 3]] and len(t) == 1
+    with pytest.raises(aqua.AquaError):
+        c.swap_out_layers([1], 0)

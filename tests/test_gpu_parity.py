@@ -343,3 +343,27 @@ def test_prefix_cache_bytes(engine):
     c.prefix_drop(9)
     o.prefix_drop(9)
     assert c.counts()[2] == len(o.host.free)
+
+
+@pytest.mark.parametrize("layer_group", [1, 3, 4])
+@pytest.mark.parametrize("nblk", [6, 300])
+def test_layerwise_swaps_bytes(layer_group, nblk):
+    """NEXT-3: swap_out/in split into per-layer-group launches give exactly the
+    oracle's swap_out/swap_in bytes (inline and staged descriptors, ragged
+    last group); each group has its own ticket, in issue order."""
+    rig = Rig(L=4, bs=16, H=2, D=32, NB=2 * nblk + 8, lender_slots=nblk, host_slots=0)
+    c, o = rig.ctx, rig.opool
+    perm = block_permutation(2 * nblk + 8, nblk, seed=9).tolist()
+    c.adopt_blocks(3, perm)
+    o.adopt_blocks(3, perm)
+    tks = c.swap_out_layers([3], layer_group)
+    o.swap_out([3])
+    assert len(tks) == -(-4 // layer_group) and tks == sorted(tks) and len(set(tks)) == len(tks)
+    rig.assert_bytes_equal("layered swap_out")
+    c.alloc_blocks(4, 5)
+    o.alloc_blocks(4, 5)
+    new, tks = c.swap_in_layers([3], layer_group)
+    assert new == o.swap_in([3])
+    c.sync(tks[0])
+    assert c.ticket_done(tks[0])
+    rig.assert_bytes_equal("layered swap_in")
