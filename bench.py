@@ -250,13 +250,25 @@ def run_ours(args):
 
     arena_bytes = NBLK * U
     ipc_ptr = imported = None
+    matching = None
     if ws == 1:
         arena = torch.empty(arena_bytes, dtype=torch.uint8, device=dev)
         ctx.lend(local, arena.data_ptr(), arena_bytes)
         mode = "self-lender"
     else:
-        from paper_2407_21255_b200.pairing import exchange, partner as pair_of
-        partner = pair_of(rank, ws)
+        from paper_2407_21255_b200.pairing import best_matching, exchange, measure_p2p
+        # pairing from the measured topology: P2P reachability
+        # rows from every rank, or (--measure-topology) rank 0's bandwidth
+        # matrix; then the max-min perfect matching
+        if args.measure_topology and not shared:
+            bw = measure_p2p(ws) if rank == 0 else None
+            bw = exchange(bw)[0]
+        else:
+            row = [0.0 if j == local else (1.0 if shared or aqua.can_access_peer(local, j) else 0.0)
+                   for j in range(ws)]
+            bw = exchange(row)
+        matching = best_matching(bw)
+        partner = matching[rank]
         ipc_ptr = aqua.ipc_alloc(local, arena_bytes)          # what this rank lends to its partner
         handles = exchange((rank, local, aqua.ipc_export(ipc_ptr)))
         if partner == rank:
@@ -375,6 +387,7 @@ def run_ours(args):
         "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
         "config": _config(args, n=ws),
         "mode": mode,
+        "pairing": matching,
         "preempt_resume_ms": {"preempt_device_ms": round(out_avg, 4), "resume_device_ms": round(in_avg, 4),
                               "sum_device_ms": round(out_avg + in_avg, 4),
                               "preempt_host_p50_ms": round(1e3 * statistics.median(lat_out), 4),
@@ -492,6 +505,7 @@ def main():
     ap.add_argument("--no-host-baselines", action="store_true")
     ap.add_argument("--host-reps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--measure-topology", action="store_true", help="N>1: pair GPUs by measured P2P bandwidth")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     args = ap.parse_args()
     if args.warmup < 3:

@@ -55,3 +55,20 @@ def test_gloo_handle_exchange_world2():
         assert p.exitcode == 0
     assert res[0][1] == 1 and res[0][2] == (1, bytes([1]) * 64, 1 << 30)
     assert res[1][1] == 0 and res[1][2] == (0, bytes([0]) * 64, 1 << 30)
+
+
+def test_best_matching_from_measured_matrix():
+    from paper_2407_21255_b200.pairing import best_matching
+    n = 8
+    uniform = [[0 if i == j else 770.0 for j in range(n)] for i in range(n)]
+    assert best_matching(uniform) == [1, 0, 3, 2, 5, 4, 7, 6]        # NVSwitch: lowest-index matching
+    # a slow link between 0 and 1 (and 2-3) steers the matching elsewhere
+    bw = [row[:] for row in uniform]
+    bw[0][1] = bw[1][0] = 100.0
+    bw[2][3] = bw[3][2] = 100.0
+    m = best_matching(bw)
+    assert all(m[m[i]] == i for i in range(n)) and m[0] != 1 and m[2] != 3
+    assert min(bw[i][m[i]] for i in range(n)) == 770.0
+    # unreachable pairs are never chosen; odd counts self-lend one GPU
+    bw3 = [[0, 0, 500.0], [0, 0, 0], [500.0, 0, 0]]
+    assert best_matching(bw3) == [2, 1, 0]
