@@ -43,15 +43,42 @@ def main():
                                                    "fallback, then re-offer")
     args = ap.parse_args()
 
-    dev = torch.device("cuda", 0)
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    shared = os.environ.get("AQUA_BENCH_SHARED_GPU") == "1"
+    devi = 0 if (ws == 1 or shared) else rank
+    dev = torch.device("cuda", devi)
+    torch.cuda.set_device(devi)
     S = bs * H * D * e
     U = 2 * L * S
+    lend_bytes = args.lender_gib << 30
+    if ws == 2:
+        # 1 borrower (rank 0) + 1 lender (rank 1, another process -- another
+        # GPU, or the same one with AQUA_BENCH_SHARED_GPU=1): the lender offers
+        # HBM through a CUDA IPC handle; no data-path collective
+        import torch.distributed as dist
+        from paper_2407_21255_b200.pairing import exchange
+        dist.init_process_group("gloo")
+        if rank == 1:
+            ptr = aqua.ipc_alloc(devi, lend_bytes)
+            exchange((aqua.ipc_export(ptr), lend_bytes))
+            dist.barrier()                    # the borrower runs the trace
+            dist.barrier()                    # ... and has closed its mapping
+            aqua.ipc_free(devi, ptr)
+            dist.destroy_process_group()
+            return
+        handle = exchange(None)[1][0]
     layers = [torch.zeros(2 * NB * S, dtype=torch.uint8, device=dev) for _ in range(L)]
-    ctx = aqua.Ctx(0, L, bs, H, D, e, NB, [t.data_ptr() for t in layers])
+    ctx = aqua.Ctx(devi, L, bs, H, D, e, NB, [t.data_ptr() for t in layers])
     arena = None
+    lend_dev, lend_ptr = devi, 0
     if args.policy == "cfs-peer":
-        arena = torch.empty(args.lender_gib << 30, dtype=torch.uint8, device=dev)
-        ctx.lend(0, arena.data_ptr(), args.lender_gib << 30)
+        if ws == 2:
+            lend_dev, lend_ptr = aqua.MAPPED, aqua.ipc_import(devi, handle)
+        else:
+            arena = torch.empty(lend_bytes, dtype=torch.uint8, device=dev)
+            lend_ptr = arena.data_ptr()
+        ctx.lend(lend_dev, lend_ptr, lend_bytes)
     ctx.lend(aqua.HOST, 0, args.host_gib << 30)
     ctx.set_option(aqua.OPT_TIMING, 1)               # per-swap device time via aqua_ticket_elapsed
     pol = POLICY_FCFS if args.policy == "fcfs" else POLICY_CFS
@@ -96,7 +123,7 @@ def main():
     elastic = None
     if args.elastic:
         tr_, tl_ = (float(x) for x in args.elastic.split(","))
-        elastic = {"t_reclaim": tr_, "t_relend": tl_, "relend": (0, arena.data_ptr(), args.lender_gib << 30)}
+        elastic = {"t_reclaim": tr_, "t_relend": tl_, "relend": (lend_dev, lend_ptr, lend_bytes)}
     log, st = run_trace(trace, ctx, sched, fill_seed=SEED, decode_stream=dec.cuda_stream,
                         swap_stream=swp.cuda_stream, on_iteration=on_iteration, stream_sync=stream_sync,
                         on_swap=on_swap, record_log=args.check_oracle, elastic=elastic)
@@ -117,7 +144,9 @@ def main():
     res = {
         "config": "configs[2] bursty trace (seed 1, 373 requests, 25 @ 2.5/s then 5/s for 60 s then 2.5/s for 15 s), "
                   "Llama-3-8B KV shape, NB=4152 (8.1 GiB), b=512, k=8",
-        "policy": args.policy, "mode": "self-lender (1 GPU)" if args.policy == "cfs-peer" else args.policy,
+        "policy": args.policy,
+        "mode": args.policy if args.policy != "cfs-peer" else
+        ("self-lender (1 GPU)" if ws == 1 else ("IPC lender process, same GPU" if shared else "IPC peer lender GPU 1")),
         "iterations": st["iters"], "virtual_s": round(st["vclock"], 3), "wall_s": round(wall, 3),
         "swap_out_calls": sum(1 for x in swap_events if x[0] == "out"),
         "swap_in_calls": sum(1 for x in swap_events if x[0] == "in"),
@@ -142,7 +171,7 @@ def main():
                                 "resume_p99": round(si[min(len(si) - 1, int(0.99 * len(si)))], 4)}
     if args.check_oracle:
         from oracle import sim as osim
-        o = osim.run(trace, osim.SimConfig(NB=NB, lender_slots=(args.lender_gib << 30) // U if arena is not None else 0,
+        o = osim.run(trace, osim.SimConfig(NB=NB, lender_slots=lend_bytes // U if args.policy == "cfs-peer" else 0,
                                            host_slots=(args.host_gib << 30) // U,
                                            policy="fcfs" if pol == POLICY_FCFS else "cfs",
                                            elastic=(elastic["t_reclaim"], elastic["t_relend"]) if elastic else None,
@@ -150,6 +179,14 @@ def main():
         res["oracle_log_equal"] = (log == o.log)
         res["oracle_calls"] = len(o.log)
     print(json.dumps(res), flush=True)
+    if ws == 2:
+        import torch.distributed as dist
+        ctx.close()
+        if lend_dev == aqua.MAPPED:
+            aqua.ipc_close(devi, lend_ptr)
+        dist.barrier()
+        dist.barrier()
+        dist.destroy_process_group()
     if res["verify_mismatches"]:
         raise SystemExit("KV pattern mismatch after resume")
 
