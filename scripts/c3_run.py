@@ -101,17 +101,33 @@ def main():
             ctx.wait(ticket, dec.cuda_stream)         # decode waits only for what it needs
 
     def on_swap(kind, pids, ticket, n):
-        swap_events.append((kind, n, ticket, len(pids)))
+        swap_events.append((kind, n, ticket, len(pids), iters["n"]))
         if kind == "in" and not args.no_verify:
             for p in pids:
                 ctx.kv_verify_pattern(p, written.get(p, 0), SEED, mism.data_ptr(), dec.cuda_stream)
 
     iters = {"n": 0}
-    first_tok = {}
+    plen = {rid: (P, O) for rid, _, P, O in trace}
+    arrival = {rid: a for rid, a, _, _ in trace}
+    gen = {}
+    first_it, last_it = {}, {}
+    it_tokens = []
+
+    v_start = []
 
     def on_iteration(i, work):
+        it_tokens.append(sum(w[2] for w in work))
+        v_start.append(sched.vclock())
         for pid, ctx0, tok, grow, phase in work:
             written[pid] = ctx0 + tok
+            P, O = plen[pid]
+            if phase == 0 and ctx0 + tok == P:
+                first_it[pid] = i
+                gen[pid] = 1
+            elif phase == 1:
+                gen[pid] += 1
+            if gen.get(pid, 0) >= O:
+                last_it[pid] = i
         if proxy is not None:
             with torch.cuda.stream(dec):
                 torch.sum(proxy, out=proxy_out)
@@ -133,14 +149,34 @@ def main():
     # per-call device time of the copies (library timing events)
     per_block_ms = []
     dev_ms = {"out": 0.0, "in": 0.0}
-    for kind, n, tk, npids in swap_events:
+    swap_ms_at = [0.0] * (len(it_tokens) + 1)
+    for kind, n, tk, npids, at in swap_events:
         if n == 0:
             continue
         ms = ctx.ticket_elapsed(tk)
         dev_ms[kind] += ms
         per_block_ms.append((kind, ms, n, npids))
-    mig = [(k, n, ctx.ticket_elapsed(tk)) for k, n, tk, _ in st["swap_calls"] if k in ("reclaim", "migrate") and n]
+        swap_ms_at[at] += ms
+    # Responsiveness model (context for the paper's E6): the
+    # schedule is fixed by the virtual clock (R17); each swap's MEASURED
+    # device time is put on the critical path of the iteration that issued it
+    # (no overlap: "GPUs are idle while they wait for the paged data",
+    # P:305-308), and delays are absorbed by idle gaps:
+    #   E_start(i) = max(V_start(i), E_end(i-1)) + swaps(i);  E_end(i) = E_start(i) + cost(i)
+    e_end, prev = [], 0.0
+    for i, tok in enumerate(it_tokens):
+        e0 = max(v_start[i], prev) + swap_ms_at[i] / 1e3
+        prev = e0 + 0.020 + 40e-6 * tok
+        e_end.append(prev)
     bytes_out, bytes_in = st["blocks_out"] * U, st["blocks_in"] * U
+
+    def pct(xs, q):
+        xs = sorted(xs)
+        return round(xs[min(len(xs) - 1, int(q * len(xs)))], 4) if xs else None
+
+    ttft = [e_end[first_it[p]] - arrival[p] for p in first_it]
+    tpot = [(e_end[last_it[p]] - e_end[first_it[p]]) / (plen[p][1] - 1) for p in last_it
+            if p in first_it and plen[p][1] > 1]
     res = {
         "config": "configs[2] bursty trace (seed 1, 373 requests, 25 @ 2.5/s then 5/s for 60 s then 2.5/s for 15 s), "
                   "Llama-3-8B KV shape, NB=4152 (8.1 GiB), b=512, k=8",
@@ -156,6 +192,10 @@ def main():
                       for k, v in dev_ms.items() if v > 0},
         "kernel_launches": launches,
         "verify_mismatches": int(mism.item()),
+        "responsiveness_model_s": {"ttft_p50": pct(ttft, 0.5), "ttft_p99": pct(ttft, 0.99),
+                                   "ttft_max": pct(ttft, 1.0), "tpot_p50": pct(tpot, 0.5),
+                                   "tpot_p99": pct(tpot, 0.99), "makespan": round(e_end[-1], 3) if e_end else None,
+                                   "swap_on_critical_path_s": round(sum(swap_ms_at) / 1e3, 3)},
     }
     if elastic:
         res["elastic"] = {"t_reclaim": elastic["t_reclaim"], "t_relend": elastic["t_relend"],
