@@ -88,7 +88,7 @@ def main():
     swp = torch.cuda.Stream(device=dev)
     mism = torch.zeros(1, dtype=torch.int64, device=dev)
     written = {}          # pid -> KV tokens written so far
-    swap_events = []      # (kind, nblocks, ticket, npids)
+    swap_events = []      # (kind, nblocks, ticket, npids, iteration)
     proxy = None
     if args.proxy_gb > 0:
         proxy = torch.empty(int(args.proxy_gb * 1e9) // 8, dtype=torch.int64, device=dev)

@@ -367,3 +367,66 @@ def test_layerwise_swaps_bytes(layer_group, nblk):
     c.sync(tks[0])
     assert c.ticket_done(tks[0])
     rig.assert_bytes_equal("layered swap_in")
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_multistream_fuzz_equals_sequential(seed):
+    """R7 end to end: random library ops (fills, swaps, migrations, prefix
+    store/load, frees), each on a random one of three streams, must leave
+    exactly the bytes of the oracle's sequential execution -- every reuse
+    of a block or slot is ordered by the library's tickets."""
+    from oracle import pattern as opat
+    rnd = random.Random(100 + seed)
+    rig = Rig(L=3, bs=16, H=2, D=64, NB=64, lender_slots=24, host_slots=24, seed=seed)
+    c, o = rig.ctx, rig.opool
+    streams = [torch.cuda.Stream() for _ in range(3)]
+    ntok = {}
+    pids = list(range(6))
+    for step in range(120):
+        st = rnd.choice(streams).cuda_stream
+        k = rnd.random()
+        p = rnd.choice(pids)
+        try:
+            if k < 0.25:
+                n = rnd.randint(1, 4)
+                ids = o.alloc_blocks(p, n)
+                assert c.alloc_blocks(p, n, st) == ids
+                t0 = ntok.get(p, 0)
+                t1 = len(o.prompts[p].blocks) * 16
+                opat.write_tokens(o, p, t0, t1, 7)
+                c.kv_fill_pattern(p, t0, t1, 7, st)
+                ntok[p] = t1
+            elif k < 0.45:
+                sel = rnd.sample(pids, rnd.randint(1, 3))
+                o.swap_out(sel)
+                c.swap_out(sel, st)
+            elif k < 0.65:
+                sel = rnd.sample(pids, rnd.randint(1, 3))
+                want = o.swap_in(sel)
+                assert c.swap_in(sel, st)[0] == want
+            elif k < 0.72:
+                dst = rnd.choice([kp.LOC_PEER, kp.LOC_HOST])
+                o.migrate([p], dst)
+                c.migrate([p], dst, st)
+            elif k < 0.78:
+                f = rnd.randint(0, 1)
+                n = rnd.randint(0, 3)
+                o.prefix_store(f, p, n)
+                c.prefix_store(f, p, n, st)
+            elif k < 0.84:
+                f = rnd.randint(0, 1)
+                want = o.prefix_load(f, p)
+                assert c.prefix_load(f, p, st)[0] == want
+            elif k < 0.88:
+                f = rnd.randint(0, 1)
+                o.prefix_drop(f)
+                c.prefix_drop(f)
+            else:
+                o.free_prompt(p)
+                c.free(p, st)
+                ntok.pop(p, None)
+        except kp.AquaError:
+            continue      # the oracle refused: the library must not have been called
+        if step % 40 == 39:
+            rig.assert_bytes_equal(f"fuzz step {step}")
+    rig.assert_bytes_equal("fuzz end")
