@@ -334,7 +334,7 @@ def run_ours(args):
     # end to end through the public API: host pid list in, host block table
     # out, descriptor uploads inside, host-synchronised every step
     e2e_t, lat_out, lat_in = [], [], []
-    for _ in range(max(3, min(K, 10))):
+    for _ in range(max(10, min(K, 20))):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         tk = ctx.swap_out(PIDS, sw)
@@ -392,7 +392,17 @@ def run_ours(args):
                               "sum_device_ms": round(out_avg + in_avg, 4),
                               "preempt_host_p50_ms": round(1e3 * statistics.median(lat_out), 4),
                               "resume_host_p50_ms": round(1e3 * statistics.median(lat_in), 4),
-                              "sum_host_p50_ms": round(1e3 * statistics.median(e2e_t), 4)},
+                              "sum_host_p50_ms": round(1e3 * statistics.median(e2e_t), 4),
+                              "preempt_host_p99_ms": round(1e3 * _pct(lat_out, 0.99), 4),
+                              "resume_host_p99_ms": round(1e3 * _pct(lat_in, 0.99), 4),
+                              "what": "device = CUDA events on the swap stream around each call; host = wall time from "
+                                      "the C-ABI call to its ticket completing (aqua_sync)"},
+        "launch_ms": {"swap_out": {q: round(_pct(out_ms, v), 4) for q, v in (("p10", .1), ("p50", .5), ("p90", .9))},
+                      "swap_in": {q: round(_pct(in_ms, v), 4) for q, v in (("p10", .1), ("p50", .5), ("p90", .9))}},
+        "launch_shape": {"ctas": args.max_ctas or _sm_count(), "threads_per_cta": 32,
+                         "engine": args.engine, "blocks_per_launch": NBLK, "block_tokens": SHAPE["bs"],
+                         "chunk_bytes": SHAPE["bs"] * SHAPE["H"] * SHAPE["D"] * SHAPE["e"], "block_bytes_U": U},
+        "host": _host_info(),
         "roofline": roof,
         "cpu_baseline": cpu,
         "e2e": {"value": round(e2e_val, 2), "unit": "GB/s", "h2d_bytes_per_step": 2 * NBLK * 8,
@@ -408,6 +418,28 @@ def run_ours(args):
     }
     print(json.dumps(line), flush=True)
     _cleanup(aqua, local, ipc_ptr, imported, ws)
+
+
+def _pct(xs, q):
+    xs = sorted(xs)
+    return xs[min(len(xs) - 1, int(q * len(xs)))]
+
+
+def _sm_count():
+    import torch
+    return torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+
+
+def _host_info():
+    model = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count(), "cpu_model": model}
 
 
 def _cleanup(aqua, local, ipc_ptr, imported, ws):
