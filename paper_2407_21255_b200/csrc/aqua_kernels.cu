@@ -376,11 +376,21 @@ cudaError_t launch_swap_tma(const SwapParams& p, Dir dir, int num_sms, int grid_
   // flight per SM measured best for HBM on B200 (profiles/r01_stages.jsonl);
   // deeper rings lose 3-4 %.
   const int stage_bytes = p.piece * p.group;
-  int stages = stages_opt > 0 ? stages_opt : std::max(3, std::min(32, (64 * 1024) / stage_bytes));
+  const int grid = grid_for<void>(p.nitems, 1, num_sms, 1, grid_cap);
+  // Ring depth: keep ~9 MiB of loads in flight chip-wide.  With all 148 SMs
+  // that is 3 x 32 KiB stages (2 in flight), measured best; with an SM cap
+  // each CTA needs a deeper ring: 64 CTAs x 6 stages still reach 6.26 TB/s
+  // (profiles/r01_stages*.jsonl, r01_ctas_stages.jsonl).  At most ~200 KiB.
+  int stages = stages_opt;
+  if (stages <= 0) {
+    const int64_t want_inflight = int64_t(9) << 20;
+    const int64_t per_cta = (want_inflight + int64_t(grid) * stage_bytes - 1) / (int64_t(grid) * stage_bytes);
+    stages = static_cast<int>(std::min<int64_t>(per_cta + 1, std::max(3, (200 * 1024) / stage_bytes)));
+    stages = std::max(stages, 3);
+  }
   stages = std::max(2, std::min(stages, 32));
   while (stages > 2 && tma_smem_bytes(stage_bytes, stages) > 227 * 1024) --stages;
   const int smem = tma_smem_bytes(stage_bytes, stages);
-  const int grid = grid_for<void>(p.nitems, 1, num_sms, 1, grid_cap);
   // the opt-in smem attribute is per device; remember the largest set so far
   static thread_local int set_smem[3][64] = {};
   int dev = 0;

@@ -240,6 +240,22 @@ def layers():
         torch.cuda.empty_cache()
 
 
+def ctas_stages():
+    """Per-SM efficiency when the swap is capped to few SMs (to leave the
+    rest to decode): does a deeper ring recover throughput per SM?"""
+    L, bs, H, D, NB, nblk = 32, 16, 8, 128, 4096, 2048
+    ctx, layers, arena, U = setup(L, bs, H, D, NB, nblk)
+    s = torch.cuda.Stream()
+    for ctas in (8, 16, 32, 64):
+        for st in (3, 4, 6):
+            ctx.set_option(aqua.OPT_MAX_CTAS, ctas)
+            ctx.set_option(aqua.OPT_TMA_STAGES, st)
+            o, i = time_tickets(ctx, 3, s)
+            print(json.dumps({"ctas": ctas, "stages": st, "out_hbm_GBps": round(2 * nblk * U / o / 1e6, 1),
+                              "in_hbm_GBps": round(2 * nblk * U / i / 1e6, 1),
+                              "per_sm_GBps": round(2 * nblk * U / o / 1e6 / ctas, 1)}), flush=True)
+
+
 def stages():
     L, bs, H, D, NB, nblk = 32, 16, 8, 128, 4096, 2048
     ctx, layers, arena, U = setup(L, bs, H, D, NB, nblk)
@@ -295,6 +311,8 @@ if __name__ == "__main__":
         prefix()
     elif what == "migrate":
         migrate()
+    elif what == "ctas_stages":
+        ctas_stages()
     elif what == "host_ctas":
         host_ctas()
     elif what == "self_ctas":
