@@ -38,6 +38,7 @@ def main():
     ap.add_argument("--lender-gib", type=int, default=64)
     ap.add_argument("--host-gib", type=int, default=64)
     ap.add_argument("--check-oracle", action="store_true")
+    ap.add_argument("--serial", action="store_true", help="swaps on the decode stream (no overlap), for A8")
     ap.add_argument("--no-verify", action="store_true")
     ap.add_argument("--elastic", default="", help="t_reclaim,t_relend (virtual s): NEXT-1 lender reclaim + FCFS "
                                                    "fallback, then re-offer")
@@ -85,14 +86,14 @@ def main():
     sched = Scheduler(NB=NB, bs=bs, b=512, k=8, policy=pol)
     trace = burst_trace(seed=1)
     dec = torch.cuda.Stream(device=dev)
-    swp = torch.cuda.Stream(device=dev)
+    swp = dec if args.serial else torch.cuda.Stream(device=dev)
     mism = torch.zeros(1, dtype=torch.int64, device=dev)
     written = {}          # pid -> KV tokens written so far
     swap_events = []      # (kind, nblocks, ticket, npids, iteration)
     proxy = None
     if args.proxy_gb > 0:
         proxy = torch.empty(int(args.proxy_gb * 1e9) // 8, dtype=torch.int64, device=dev)
-        proxy_out = torch.empty(1, dtype=torch.int64, device=dev)
+        proxy_out = torch.empty((), dtype=torch.int64, device=dev)
 
     def stream_sync(kind, ticket):
         if kind == "before_swap_out":
@@ -130,7 +131,7 @@ def main():
                 last_it[pid] = i
         if proxy is not None:
             with torch.cuda.stream(dec):
-                torch.sum(proxy, out=proxy_out)
+                torch.sum(proxy, dim=0, out=proxy_out)
         iters["n"] += 1
 
     torch.cuda.synchronize()
@@ -191,6 +192,8 @@ def main():
         "swap_GBps": {k: round((bytes_out if k == "out" else bytes_in) / max(v, 1e-9) / 1e6, 1)
                       for k, v in dev_ms.items() if v > 0},
         "kernel_launches": launches,
+        "streams": "serial (one stream)" if args.serial else "decode + swap streams (tickets)",
+        "proxy_gb_per_iteration": args.proxy_gb,
         "verify_mismatches": int(mism.item()),
         "responsiveness_model_s": {"ttft_p50": pct(ttft, 0.5), "ttft_p99": pct(ttft, 0.99),
                                    "ttft_max": pct(ttft, 1.0), "tpot_p50": pct(tpot, 0.5),

@@ -39,7 +39,7 @@ def main():
     ctx.adopt_blocks(1, perm[nblk:])
     ctx.adopt_blocks(7, perm[:nblk])
     w = torch.ones(int(args.weights_gb * 1e9) // 8, dtype=torch.int64, device="cuda")
-    out = torch.empty(1, dtype=torch.int64, device="cuda")
+    out = torch.empty((), dtype=torch.int64, device="cuda")
 
     def timed(fn, stream):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
