@@ -210,3 +210,68 @@ def test_sim_determinism_and_paging_happens():
     assert a.log == b.log
     assert a.blocks_out > 0 and a.blocks_out == a.blocks_in
     assert set(a.finish) == {t[0] for t in tr}
+
+
+# ------------------------------------------------------------- FCFS (R18)
+def test_fcfs_admission_in_arrival_order_and_projection():
+    """Pure FCFS: first service follows arrival order and
+    the admitted projections never exceed the pool; it never pages."""
+    tr = [(i, 0.05 * i, 50 + 37 * (i % 5), 20 + 11 * (i % 3)) for i in range(12)]
+    NB = 40
+    r = sim.run(tr, sim.SimConfig(NB=NB, b=128, policy="fcfs", lender_slots=100))
+    assert not [e for e in r.log if e[0] in ("swap_out", "swap_in", "plan")]
+    first = []
+    for e in r.log:
+        if e[0] == "iter":
+            for pid, _, _ in e[2]:
+                if pid not in first:
+                    first.append(pid)
+    assert first == sorted(first)                       # arrival order == id order here
+    # projection bound: at any iteration the prompts holding KV fit their full need
+    live = set()
+    for e in r.log:
+        if e[0] == "alloc":
+            live.add(e[1])
+        elif e[0] == "free":
+            live.discard(e[1])
+        elif e[0] == "iter":
+            assert sum(-(-(tr[p][2] + tr[p][3]) // 16) for p in live) <= NB
+
+
+def test_fallback_keeps_residents_and_evicts_latest_arrival():
+    """CFS -> FCFS fallback (R18): the residents at the switch stay
+    admitted; when they outgrow the pool the latest-arrived resident is the
+    one paged out; while in fallback there is no CFS replanning and every
+    page-out goes to DRAM."""
+    tr = [(i, 0.01 * i, 40, 300) for i in range(8)]
+    r = sim.run(tr, sim.SimConfig(NB=40, b=64, lender_slots=400, host_slots=2000, elastic=(0.5, 1e9),
+                                  relend_slots=400))
+    i_sw = [k for k, e in enumerate(r.log) if e[0] == "policy"][0]
+    # residents just before the switch
+    res = set()
+    for e in r.log[:i_sw]:
+        if e[0] == "alloc":
+            res.add(e[1])
+        elif e[0] == "swap_out":
+            res -= set(e[1])
+        elif e[0] == "swap_in":
+            res |= set(e[1])
+        elif e[0] == "free":
+            res.discard(e[1])
+    outs = [e for e in r.log[i_sw:] if e[0] == "swap_out"]
+    assert outs, "the scenario must overflow"
+    # every fallback eviction is the latest-arrived resident at that moment
+    cur = set(res)
+    for e in r.log[i_sw:]:
+        if e[0] == "swap_out":
+            (victim,) = e[1]
+            assert victim == max(cur, key=lambda p: (tr[p][1], p))
+            assert all(loc == 2 for loc, _ in e[2])      # to DRAM: the lender is gone
+            cur.discard(victim)
+        elif e[0] == "swap_in":
+            cur |= set(e[1])
+        elif e[0] == "alloc":
+            cur.add(e[1])
+        elif e[0] == "free":
+            cur.discard(e[1])
+        assert e[0] != "plan"
