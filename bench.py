@@ -207,9 +207,8 @@ def _config(args, reference=False, n=1):
     U = 2 * SHAPE["L"] * SHAPE["bs"] * SHAPE["H"] * SHAPE["D"] * SHAPE["e"]
     return {"workload": CFG["desc"] + "; step = preempt + resume "
                         + ("(self-lender: arena in the same HBM)" if n == 1 else "(peer lender rank^1 over NVLink)"),
-            "name": CFG["name"], "model": "kv-shape-only (no weights)", "global_batch": CFG["nprompts"],
-            "seq_len": CFG["bpp"] * SHAPE["bs"],
-            "parallelism": f"pairs{max(n // 2, 1)}" if n > 1 else "single",
+            "name": CFG["name"], "prompts": CFG["nprompts"], "tokens_per_prompt": CFG["bpp"] * SHAPE["bs"],
+            "layout": dict(SHAPE, NB=NB), "lending": "self (same HBM)" if n == 1 else f"pairs over NVLink ({n} ranks)",
             "engine": args.engine, "bytes_per_step": 2 * NBLK * U,
             "l2": f"inputs ({NBLK * U / 2**30:.1f} GiB per direction) >> 126 MB L2; no flush needed"}
 
