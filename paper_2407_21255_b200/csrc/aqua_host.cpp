@@ -146,8 +146,12 @@ aqua_status cuda_fail(aqua_ctx* c, cudaError_t e, const char* what) {
 
 // ------------------------------------------------------------ tickets
 void retire(aqua_ctx* c) {
+  // Tickets mostly complete in issue order: retire from the oldest and stop
+  // at the first one still pending (a full scan only when many pile up, so a
+  // call costs O(completed) cudaEventQuery calls, not O(live)).
+  const bool full = c->live.size() > 4096;
   int scanned = 0;
-  for (auto it = c->live.begin(); it != c->live.end() && scanned < 64; ++scanned) {
+  for (auto it = c->live.begin(); it != c->live.end() && (full || scanned < 64); ++scanned) {
     cudaError_t q = cudaEventQuery(it->second.ev);
     if (q == cudaSuccess) {
       if (it->second.start) {
@@ -167,6 +171,7 @@ void retire(aqua_ctx* c) {
       it = c->live.erase(it);
     } else {
       if (q != cudaErrorNotReady) cudaGetLastError();
+      if (!full) break;
       ++it;
     }
   }

@@ -256,6 +256,99 @@ def ctas_stages():
                               "per_sm_GBps": round(2 * nblk * U / o / 1e6 / ctas, 1)}), flush=True)
 
 
+def c5_multi():
+    """C5 at N >= 2 (torchrun): every rank pages into HBM lent by its partner
+    over NVLink (IPC), all pairs at once; per point the device time of each
+    call is the max over ranks.  AQUA_BENCH_SHARED_GPU=1 runs all ranks on
+    cuda:0 (a functional check of the multi-rank path on one GPU)."""
+    import torch.distributed as dist
+    from paper_2407_21255_b200.pairing import best_matching, exchange
+    ws, rank = int(os.environ["WORLD_SIZE"]), int(os.environ["RANK"])
+    shared = os.environ.get("AQUA_BENCH_SHARED_GPU") == "1"
+    local = 0 if shared else int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dist.init_process_group("gloo")
+    row = [0.0 if j == local else (1.0 if shared or aqua.can_access_peer(local, j) else 0.0) for j in range(ws)]
+    partner = best_matching(exchange(row))[rank]
+    L, H, D = 32, 8, 128
+    for bs in (8, 16, 32, 64, 128):
+        S = bs * H * D * 2
+        U = 2 * L * S
+        for nblk in (1, 4, 16, 64, 256, 1024):
+            if nblk * U > (8 << 30):
+                continue
+            mine = aqua.ipc_alloc(local, nblk * U)
+            got = exchange((aqua.ipc_export(mine), nblk * U))
+            NB = 2 * nblk
+            layers = [torch.zeros(2 * NB * S, dtype=torch.uint8, device="cuda") for _ in range(L)]
+            ctx = aqua.Ctx(local, L, bs, H, D, 2, NB, [t.data_ptr() for t in layers])
+            mapped = None
+            if partner == rank:
+                ctx.lend(local, mine, nblk * U)
+            else:
+                mapped = aqua.ipc_import(local, got[partner][0])
+                ctx.lend(aqua.MAPPED, mapped, nblk * U)
+            perm = block_permutation(NB, NB, seed=2).tolist()
+            ctx.adopt_blocks(1, perm[nblk:])
+            ctx.adopt_blocks(7, perm[:nblk])
+            s = torch.cuda.Stream()
+            dist.barrier()
+            o, i = time_tickets(ctx, 5, s)
+            t = torch.tensor([o, i], dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            if rank == 0:
+                print(json.dumps({"c5_multi": ws, "partner0": partner, "bs": bs, "blocks": nblk, "bytes": nblk * U,
+                                  "out_ms_max": round(float(t[0]), 5), "in_ms_max": round(float(t[1]), 5),
+                                  "out_GBps": round(nblk * U / float(t[0]) / 1e6, 2),
+                                  "in_GBps": round(nblk * U / float(t[1]) / 1e6, 2)}), flush=True)
+            ctx.close()
+            if mapped:
+                aqua.ipc_close(local, mapped)
+            dist.barrier()
+            aqua.ipc_free(local, mine)
+            del layers
+            torch.cuda.empty_cache()
+    dist.destroy_process_group()
+
+
+def torch_baseline():
+    """What a PyTorch user would write for the same swap: per layer, index the
+    [2][NB][S] pool view with the block table and copy into the slot-major
+    arena view (L*2 gather/scatter ops), vs the fused kernel."""
+    L, bs, H, D, NB, nblk = 32, 16, 8, 128, 4096, 2048
+    ctx, layers, arena, U = setup(L, bs, H, D, NB, nblk)
+    S = bs * H * D * 2
+    bt = torch.tensor(block_permutation(NB, NB, seed=2)[:nblk].tolist(), device="cuda", dtype=torch.int64)
+    img = arena.view(nblk, L, 2, S)
+    views = [t.view(2, NB, S) for t in layers]
+
+    def out():
+        for l in range(L):
+            img[:, l] = views[l][:, bt].transpose(0, 1)
+
+    def inn():
+        for l in range(L):
+            views[l][:, bt] = img[:, l].transpose(0, 1)
+
+    res = {}
+    for name, fn in (("torch_swap_out", out), ("torch_swap_in", inn)):
+        fn()
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(5):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            fn()
+            b.record()
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b))
+        res[name] = {"ms": round(statistics.median(ts), 3),
+                     "hbm_GBps": round(2 * nblk * U / statistics.median(ts) / 1e6, 1)}
+    o, i = time_tickets(ctx, 5, torch.cuda.Stream())
+    res["aqua_tma"] = {"out_ms": round(o, 3), "in_ms": round(i, 3)}
+    print(json.dumps(res), flush=True)
+
+
 def stages():
     L, bs, H, D, NB, nblk = 32, 16, 8, 128, 4096, 2048
     ctx, layers, arena, U = setup(L, bs, H, D, NB, nblk)
@@ -311,6 +404,10 @@ if __name__ == "__main__":
         prefix()
     elif what == "migrate":
         migrate()
+    elif what == "torch_baseline":
+        torch_baseline()
+    elif what == "c5_multi":
+        c5_multi()
     elif what == "ctas_stages":
         ctas_stages()
     elif what == "host_ctas":
