@@ -72,3 +72,42 @@ def test_best_matching_from_measured_matrix():
     # unreachable pairs are never chosen; odd counts self-lend one GPU
     bw3 = [[0, 0, 500.0], [0, 0, 0], [500.0, 0, 0]]
     assert best_matching(bw3) == [2, 1, 0]
+
+
+def _tp_worker(rank, world, port, q):
+    """Two TP ranks in dry-run mode with their own KV-head shard: the
+    replicated native scheduler gives both the same call log."""
+    import hashlib
+    import torch.distributed as dist
+    from paper_2407_21255_b200 import aqua
+    from paper_2407_21255_b200.cfs import Scheduler
+    from paper_2407_21255_b200.driver import run_trace
+    from workloads import burst_trace
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    FAKE = 1 << 40
+    H = 8 // world
+    c = aqua.Ctx(aqua.DRYRUN, 4, 16, H, 128, 2, 120, [FAKE + l * (1 << 34) for l in range(4)])
+    c.lend(0, FAKE * 8, 3000 * c.U)
+    tr = burst_trace(seed=3, burst_s=6.0, tail_s=2.0, prompt=(300, 0.8, 1, 900), output=(40, 0.7, 1, 200))
+    log, _ = run_trace(tr, c, Scheduler(NB=120, bs=16))
+    hs = [None] * world
+    dist.all_gather_object(hs, hashlib.sha256(repr(log).encode()).hexdigest())
+    q.put((rank, hs, sum(1 for e in log if e[0] == "swap_out")))
+    dist.destroy_process_group()
+
+
+def test_tp_ranks_replicated_schedule():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_tp_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    res = [q.get(timeout=180) for _ in ps]
+    for p in ps:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, hs, nout in res:
+        assert len(set(hs)) == 1 and nout > 0
