@@ -183,6 +183,21 @@ AQUA_API aqua_status aqua_swap_in(aqua_ctx* ctx, int32_t n, const uint64_t* pids
                          int32_t* out_ids, int64_t out_ids_cap, int32_t* out_counts,
                          uint64_t* out_ticket);
 
+/* A reschedule with both lists ("paging out prompts that are not
+ * a part of the next batch and paging in prompts that were not on the GPU")
+ * in one call: exactly aqua_swap_out(out_pids) followed by
+ * aqua_swap_in(in_pids) -- same validation (all-or-nothing over both), ids,
+ * slots and bytes -- but the preemption runs on out_stream and the resume on
+ * in_stream, pipelined in `pieces` pieces: resume piece k waits only for the
+ * preemption piece that freed its blocks, so both directions of a
+ * full-duplex link (NVLink, PCIe) carry data at the same time.
+ * out_ticket / in_ticket cover the preemption / the resume. */
+AQUA_API aqua_status aqua_swap_exchange(aqua_ctx* ctx, int32_t n_out, const uint64_t* out_pids, int32_t n_in,
+                                        const uint64_t* in_pids, aqua_stream_t out_stream,
+                                        aqua_stream_t in_stream, int32_t pieces, int32_t* out_ids,
+                                        int64_t out_ids_cap, int32_t* out_counts, uint64_t* out_ticket,
+                                        uint64_t* in_ticket);
+
 /* NEXT-3, layer-wise streaming (Sec. 9: FlexGen "pages the
  * previous layer's context out and the next layer's in"): exactly
  * aqua_swap_out / aqua_swap_in (same bookkeeping, same bytes), but the copy

@@ -327,13 +327,14 @@ class Pool:
         out = []
         for p in images:
             ar_s = self.arena(p.location)
-            new = sorted(ar_d.free)[:len(p.slots)]
+            new = sorted(ar_d.free)[:len(p.slots)] if p.slots else []   # a 0-block image only relocates
             for s in new:
                 ar_d.free.remove(s)
-            if ar_s.data is not None and ar_d.data is not None:
+            if p.slots and ar_s.data is not None and ar_d.data is not None:
                 for s_old, s_new in zip(p.slots, new):
                     ar_d.data[s_new * lay.U:(s_new + 1) * lay.U] = ar_s.data[s_old * lay.U:(s_old + 1) * lay.U]
-            ar_s.free.update(p.slots)
+            if p.slots:
+                ar_s.free.update(p.slots)
             p.location, p.slots = dst, list(new)
             out.append(list(new))
         return out

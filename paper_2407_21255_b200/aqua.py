@@ -30,7 +30,7 @@ OPT_KERNEL, OPT_MAX_CTAS, OPT_TMA_PIECE, OPT_TMA_STAGES, OPT_TIMING = 1, 2, 3, 4
 # Every symbol include/aqua.h declares (checked by tests/test_abi.py).
 SYMBOLS = [
     "aqua_create", "aqua_destroy", "aqua_lend", "aqua_alloc_blocks", "aqua_adopt_blocks",
-    "aqua_swap_out", "aqua_swap_in", "aqua_swap_out_layers", "aqua_swap_in_layers", "aqua_free", "aqua_migrate", "aqua_reclaim", "aqua_prefix_store", "aqua_prefix_load",
+    "aqua_swap_out", "aqua_swap_in", "aqua_swap_exchange", "aqua_swap_out_layers", "aqua_swap_in_layers", "aqua_free", "aqua_migrate", "aqua_reclaim", "aqua_prefix_store", "aqua_prefix_load",
     "aqua_prefix_drop", "aqua_prefix_query", "aqua_wait", "aqua_sync", "aqua_ticket_done", "aqua_ticket_elapsed",
     "aqua_query", "aqua_counts", "aqua_arena_base", "aqua_set_option", "aqua_get_option",
     "aqua_last_descriptors", "aqua_launch_count", "aqua_ipc_export", "aqua_ipc_import",
@@ -66,6 +66,8 @@ def _load() -> C.CDLL:
         "aqua_adopt_blocks": (C.c_int, [VP, U64, I32, P(I32), VP]),
         "aqua_swap_out": (C.c_int, [VP, I32, P(U64), VP, P(U64)]),
         "aqua_swap_in": (C.c_int, [VP, I32, P(U64), VP, P(I32), I64, P(I32), P(U64)]),
+        "aqua_swap_exchange": (C.c_int, [VP, I32, P(U64), I32, P(U64), VP, VP, I32, P(I32), I64, P(I32), P(U64),
+                                         P(U64)]),
         "aqua_swap_out_layers": (C.c_int, [VP, I32, P(U64), VP, I32, P(U64)]),
         "aqua_swap_in_layers": (C.c_int, [VP, I32, P(U64), VP, I32, P(I32), I64, P(I32), P(U64)]),
         "aqua_free": (C.c_int, [VP, U64, VP]),
@@ -171,10 +173,20 @@ class Ctx:
         self._c(lib.aqua_swap_out(self.h, len(a), _u64p(a), C.c_void_p(stream or None), C.byref(t)))
         return t.value
 
+    def _cap(self, pids) -> int:
+        """Capacity for the new block ids of `pids` (0 for unknown pids: the
+        C call itself reports the error, in its own order)."""
+        n = 0
+        st, loc, k = C.c_int32(), C.c_int32(), C.c_int32()
+        for p in pids:
+            if lib.aqua_query(self.h, int(p), C.byref(st), C.byref(loc), C.byref(k), None, 0) == OK:
+                n += k.value
+        return n
+
     def swap_in(self, pids: Sequence[int], stream: int = 0, cap: int = -1) -> Tuple[List[List[int]], int]:
         a = np.ascontiguousarray(pids, dtype=np.uint64)
         if cap < 0:
-            cap = sum(self.query(int(p))[2] for p in a)
+            cap = self._cap(a)
         ids = np.empty(max(cap, 1), np.int32)
         counts = np.empty(max(len(a), 1), np.int32)
         t = C.c_uint64()
@@ -186,6 +198,24 @@ class Ctx:
             k += counts[i]
         return out, t.value
 
+    def swap_exchange(self, out_pids: Sequence[int], in_pids: Sequence[int], out_stream: int = 0,
+                      in_stream: int = 0, pieces: int = 8):
+        """-> (new block tables of in_pids, out_ticket, in_ticket)"""
+        a = np.ascontiguousarray(out_pids, dtype=np.uint64)
+        b = np.ascontiguousarray(in_pids, dtype=np.uint64)
+        cap = self._cap(b)
+        ids = np.empty(max(cap, 1), np.int32)
+        counts = np.empty(max(len(b), 1), np.int32)
+        to, ti = C.c_uint64(), C.c_uint64()
+        self._c(lib.aqua_swap_exchange(self.h, len(a), _u64p(a), len(b), _u64p(b), C.c_void_p(out_stream or None),
+                                       C.c_void_p(in_stream or None), pieces, _i32p(ids), cap, _i32p(counts),
+                                       C.byref(to), C.byref(ti)))
+        out, k = [], 0
+        for i in range(len(b)):
+            out.append(ids[k:k + counts[i]].tolist())
+            k += counts[i]
+        return out, to.value, ti.value
+
     def swap_out_layers(self, pids: Sequence[int], layer_group: int, stream: int = 0) -> List[int]:
         a = np.ascontiguousarray(pids, dtype=np.uint64)
         ng = -(-self.L // layer_group) if layer_group > 0 else 1
@@ -196,7 +226,7 @@ class Ctx:
 
     def swap_in_layers(self, pids: Sequence[int], layer_group: int, stream: int = 0):
         a = np.ascontiguousarray(pids, dtype=np.uint64)
-        cap = sum(self.query(int(p))[2] for p in a)
+        cap = self._cap(a)
         ids = np.empty(max(cap, 1), np.int32)
         counts = np.empty(max(len(a), 1), np.int32)
         ng = -(-self.L // layer_group) if layer_group > 0 else 1

@@ -938,6 +938,190 @@ aqua_status aqua_swap_in_layers(aqua_ctx* c, int32_t n, const uint64_t* pids, aq
   return s;
 }
 
+// Preempt + resume in one call (reschedule with both lists): the SAME
+// bookkeeping and bytes as aqua_swap_out(out) followed by aqua_swap_in(in),
+// but the copies run on two streams, pipelined in `pieces` pieces: resume
+// piece k waits only for the preemption piece that freed its blocks.  The two
+// directions of a full-duplex link (NVLink egress / ingress, PCIe D2H / H2D)
+// are then busy at the same time instead of one after the other.
+aqua_status aqua_swap_exchange(aqua_ctx* c, int32_t n_out, const uint64_t* out_pids, int32_t n_in,
+                               const uint64_t* in_pids, aqua_stream_t out_stream, aqua_stream_t in_stream,
+                               int32_t pieces, int32_t* out_ids, int64_t out_ids_cap, int32_t* out_counts,
+                               uint64_t* out_ticket, uint64_t* in_ticket) {
+  if (aqua_status s = precheck(c)) return s;
+  if (out_ticket) *out_ticket = 0;
+  if (in_ticket) *in_ticket = 0;
+  if (n_out < 0 || n_in < 0 || (n_out > 0 && !out_pids) || (n_in > 0 && !in_pids) || pieces < 1)
+    return fail(c, AQUA_E_INVAL, "bad counts, pointers or pieces");
+  // ---- validate everything first (all-or-nothing, as the two calls would)
+  std::unordered_set<uint64_t> seen;
+  for (int32_t i = 0; i < n_out; ++i)
+    if (!seen.insert(out_pids[i]).second) return fail(c, AQUA_E_INVAL, "duplicate pid");
+  std::vector<Prompt*> po;
+  int64_t freed = 0;
+  for (int32_t i = 0; i < n_out; ++i) {
+    auto it = c->prompts.find(out_pids[i]);
+    if (it == c->prompts.end() || it->second.state != AQUA_ST_RESIDENT)
+      return fail(c, AQUA_E_STATE, "pid not resident");
+    po.push_back(&it->second);
+    freed += static_cast<int64_t>(it->second.ids.size());
+  }
+  int64_t gpu_left = c->gpu.present ? static_cast<int64_t>(c->gpu.free.size()) : -1;
+  int64_t host_left = c->host.present ? static_cast<int64_t>(c->host.free.size()) : -1;
+  std::vector<int> loc(n_out);
+  for (int32_t i = 0; i < n_out; ++i) {
+    const int64_t np = static_cast<int64_t>(po[i]->ids.size());
+    if (gpu_left >= np) {
+      loc[i] = AQUA_LOC_PEER;
+      gpu_left -= np;
+    } else if (host_left >= np) {
+      loc[i] = AQUA_LOC_HOST;
+      host_left -= np;
+    } else {
+      return fail(c, AQUA_E_NOSPACE, "no swap space for a prompt");
+    }
+  }
+  std::unordered_set<uint64_t> seen_in;
+  std::vector<Prompt*> pi;
+  int64_t need = 0;
+  for (int32_t i = 0; i < n_in; ++i) {
+    if (!seen_in.insert(in_pids[i]).second) return fail(c, AQUA_E_INVAL, "duplicate pid");
+    auto it = c->prompts.find(in_pids[i]);
+    if (it == c->prompts.end() || it->second.state != AQUA_ST_SWAPPED)
+      return fail(c, AQUA_E_STATE, "pid not swapped");
+    pi.push_back(&it->second);
+    need += static_cast<int64_t>(it->second.ids.size());
+  }
+  if (need > 0 && (!out_ids || out_ids_cap < need)) return fail(c, AQUA_E_INVAL, "out_ids too small");
+  if (n_in > 0 && !out_counts) return fail(c, AQUA_E_INVAL, "null out_counts");
+  if (need > static_cast<int64_t>(c->free_blocks.size()) + freed)
+    return fail(c, AQUA_E_NOBLOCKS, "pool exhausted");
+
+  // ---- plan the preemption (slots lowest-first per arena, call order)
+  std::vector<Desc> dso;
+  std::vector<std::vector<int32_t>> slots(n_out);
+  {
+    auto git = c->gpu.free.begin();
+    auto hit = c->host.free.begin();
+    for (int32_t i = 0; i < n_out; ++i) {
+      auto& itr = loc[i] == AQUA_LOC_PEER ? git : hit;
+      const uint32_t bit = loc[i] == AQUA_LOC_HOST ? kArenaBit : 0u;
+      for (int32_t b : po[i]->ids) {
+        const int32_t sl = *itr++;
+        slots[i].push_back(sl);
+        dso.push_back(Desc{b, static_cast<uint32_t>(sl) | bit});
+      }
+    }
+  }
+  // piece of the preemption that reads each block (its end event frees it)
+  const int32_t npo = std::max<int32_t>(1, std::min<int32_t>(pieces, static_cast<int32_t>(dso.size())));
+  std::unordered_map<int32_t, int32_t> freed_by;
+  for (int32_t k = 0; k < npo; ++k) {
+    const size_t j0 = dso.size() * k / npo, j1 = dso.size() * (k + 1) / npo;   // the launch ranges below
+    for (size_t j = j0; j < j1; ++j) freed_by[dso[j].block] = k;
+  }
+  // old tickets, read before any bookkeeping changes them
+  std::vector<uint64_t> wait_out, wait_in;
+  for (const Desc& d : dso) {
+    wait_out.push_back(c->btick[d.block]);
+    wait_out.push_back(arena_of(c, (d.slot_arena & kArenaBit) ? AQUA_LOC_HOST : AQUA_LOC_PEER)
+                           ->tick[d.slot_arena & ~kArenaBit]);
+  }
+  // ---- preemption bookkeeping
+  for (int32_t i = 0; i < n_out; ++i) {
+    Arena* a = arena_of(c, loc[i]);
+    for (int32_t sl : slots[i]) a->free.erase(sl);
+    for (int32_t b : po[i]->ids) c->free_blocks.insert(b);
+  }
+  // ---- plan the resume on the updated free set (lowest-first)
+  std::vector<Desc> dsi;
+  std::vector<std::vector<int32_t>> fresh(n_in);
+  {
+    auto fb = c->free_blocks.begin();
+    for (int32_t i = 0; i < n_in; ++i) {
+      const uint32_t bit = pi[i]->loc == AQUA_LOC_HOST ? kArenaBit : 0u;
+      for (int32_t sl : pi[i]->ids) {
+        const int32_t b = *fb++;
+        fresh[i].push_back(b);
+        dsi.push_back(Desc{b, static_cast<uint32_t>(sl) | bit});
+      }
+    }
+  }
+  for (const Desc& d : dsi) {
+    wait_in.push_back(arena_of(c, (d.slot_arena & kArenaBit) ? AQUA_LOC_HOST : AQUA_LOC_PEER)
+                          ->tick[d.slot_arena & ~kArenaBit]);
+    if (!freed_by.count(d.block)) wait_in.push_back(c->btick[d.block]);
+  }
+  set_last(c, dsi);
+  // resume pieces: descriptors grouped by the preemption piece they wait for
+  std::vector<std::vector<Desc>> parts(npo);
+  for (const Desc& d : dsi) {
+    auto f = freed_by.find(d.block);
+    parts[f == freed_by.end() ? 0 : f->second].push_back(d);
+  }
+  // ---- launches
+  uint64_t t_out = 0, t_in = 0;
+  if (!c->dry) {
+    DevGuard g(c->device);
+    cudaStream_t so = reinterpret_cast<cudaStream_t>(out_stream);
+    cudaStream_t si = reinterpret_cast<cudaStream_t>(in_stream);
+    std::vector<uint64_t> piece_ticket(npo, 0);
+    if (!dso.empty()) {
+      if (aqua_status s = wait_all(c, wait_out, so)) return s;
+      for (int32_t k = 0; k < npo; ++k) {
+        const size_t j0 = dso.size() * k / npo, j1 = dso.size() * (k + 1) / npo;
+        std::vector<Desc> part(dso.begin() + j0, dso.begin() + j1);
+        if (aqua_status s = enqueue_copy(c, part, aqua::kOut, so, 0, nullptr, &piece_ticket[k])) return s;
+      }
+      t_out = piece_ticket[npo - 1];
+    }
+    if (!dsi.empty()) {
+      if (aqua_status s = wait_all(c, wait_in, si)) return s;
+      for (int32_t k = 0; k < npo; ++k) {
+        if (piece_ticket[k]) {
+          auto it = c->live.find(piece_ticket[k]);
+          if (it != c->live.end() && si != so) CK(c, cudaStreamWaitEvent(si, it->second.ev, 0));
+        }
+        if (parts[k].empty()) continue;
+        if (aqua_status s = enqueue_copy(c, parts[k], aqua::kIn, si, 0, nullptr, &t_in)) return s;
+      }
+      if (!t_in) record(c, si, &t_in);
+    }
+  } else {
+    if (!dso.empty()) record(c, nullptr, &t_out);
+    if (!dsi.empty()) record(c, nullptr, &t_in);
+  }
+  // ---- final bookkeeping and tickets
+  for (int32_t i = 0; i < n_out; ++i) {
+    Arena* a = arena_of(c, loc[i]);
+    for (int32_t sl : slots[i]) a->tick[sl] = t_out;
+    for (int32_t b : po[i]->ids) c->btick[b] = t_out;
+    po[i]->state = AQUA_ST_SWAPPED;
+    po[i]->loc = loc[i];
+    po[i]->ids = std::move(slots[i]);
+  }
+  c->free_blocks.erase_lowest(static_cast<int32_t>(need));
+  int64_t k = 0;
+  for (int32_t i = 0; i < n_in; ++i) {
+    Arena* a = arena_of(c, pi[i]->loc);
+    for (int32_t sl : pi[i]->ids) {
+      a->free.insert(sl);
+      a->tick[sl] = t_in;
+    }
+    for (int32_t b : fresh[i]) {
+      c->btick[b] = t_in;
+      out_ids[k++] = b;
+    }
+    out_counts[i] = static_cast<int32_t>(fresh[i].size());
+    pi[i]->state = AQUA_ST_RESIDENT;
+    pi[i]->loc = AQUA_LOC_LOCAL;
+    pi[i]->ids = std::move(fresh[i]);
+  }
+  if (out_ticket) *out_ticket = t_out;
+  if (in_ticket) *in_ticket = t_in;
+  return AQUA_OK;
+}
+
 // Move the images `ps` (prompts or cached prefixes, capacity already checked)
 // to the lowest free slots of arena `dst`, in order, with one fused launch.
 static aqua_status move_images(aqua_ctx* c, const std::vector<Prompt*>& ps, int32_t dst, cudaStream_t st,
@@ -1057,9 +1241,10 @@ aqua_status aqua_reclaim(aqua_ctx* c, aqua_stream_t stream, uint64_t* out_ticket
     DevGuard g(c->device);
     if (aqua_status s = wait_all(c, c->gpu.tick, st)) return s;
   }
-  if (need > 0) {
+  // every image moves -- zero-block ones too (only their location changes)
+  if (!ps.empty())
     if (aqua_status s = move_images(c, ps, AQUA_LOC_HOST, st, &ticket)) return s;
-  } else if (!c->dry) {
+  if (ticket == 0 && !c->dry) {
     DevGuard g(c->device);
     if (aqua_status s = record(c, st, &ticket)) return s;
   }

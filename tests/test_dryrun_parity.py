@@ -93,6 +93,16 @@ def _apply(pool, c, op):
                     moved = sorted(p for p in range(6) if _loc(c, p) == aqua.LOC_PEER)
                     c.reclaim()
                     r = moved
+            elif name == "xchg":
+                outs_, ins_ = arg
+                if side == "oracle":
+                    import copy as _copy
+                    trial = _copy.deepcopy(pool)       # all-or-nothing over both lists
+                    trial.swap_out(outs_)
+                    r = trial.swap_in(ins_)
+                    pool.__dict__.update(trial.__dict__)
+                else:
+                    r = c.swap_exchange(outs_, ins_, 0, 0, pieces=3)[0]
             elif name == "pstore":
                 if side == "oracle":
                     r = pool.prefix_store(*arg)
@@ -151,8 +161,12 @@ def test_random_op_sequences_match_oracle(seed):
             op = ("adopt", (rnd.choice(pids), [rnd.randint(-1, NB) for _ in range(rnd.randint(0, 3))]))
         elif k < 0.6:
             op = ("out", rnd.sample(pids, rnd.randint(0, 3)) + ([pids[0]] if rnd.random() < 0.05 else []))
-        elif k < 0.75:
+        elif k < 0.70:
             op = ("in", rnd.sample(pids, rnd.randint(0, 3)))
+        elif k < 0.75:
+            sel = rnd.sample(pids, rnd.randint(0, 4))
+            cut = rnd.randint(0, len(sel))
+            op = ("xchg", (sel[:cut], sel[cut:]))
         elif k < 0.85:
             op = ("free", rnd.choice(pids))
         elif k < 0.93:
