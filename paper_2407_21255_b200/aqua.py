@@ -199,7 +199,7 @@ class Ctx:
         return out, t.value
 
     def swap_exchange(self, out_pids: Sequence[int], in_pids: Sequence[int], out_stream: int = 0,
-                      in_stream: int = 0, pieces: int = 8):
+                      in_stream: int = 0, pieces: int = 16):
         """-> (new block tables of in_pids, out_ticket, in_ticket)"""
         a = np.ascontiguousarray(out_pids, dtype=np.uint64)
         b = np.ascontiguousarray(in_pids, dtype=np.uint64)

@@ -24,7 +24,8 @@ def run_trace(trace: Sequence[Tuple[int, float, int, int]], ctx: "aqua.Ctx", sch
               fill_seed: Optional[int] = None, decode_stream: int = 0, swap_stream: int = 0,
               on_iteration: Optional[Callable] = None, record_log: bool = True,
               stream_sync: Optional[Callable] = None, on_swap: Optional[Callable] = None,
-              elastic: Optional[dict] = None, policy_after_relend: int = 0):
+              elastic: Optional[dict] = None, policy_after_relend: int = 0,
+              exchange_stream: Optional[int] = None, exchange_pieces: int = 16):
     """Run the whole trace.  Returns (log, stats).
 
     ``stream_sync(kind, ticket)`` lets a GPU caller order streams:
@@ -34,6 +35,10 @@ def run_trace(trace: Sequence[Tuple[int, float, int, int]], ctx: "aqua.Ctx", sch
     ``on_iteration(i, work)`` runs the per-iteration decode proxy (optional).
     ``on_swap(kind, pids, ticket, nblocks)`` is called after each swap call.
     ``elastic = {"t_reclaim": s, "t_relend": s, "relend": (device, base, bytes)}``
+    ``exchange_stream`` (a second swap stream): a reschedule with both lists
+    uses aqua_swap_exchange -- the preemption on swap_stream, the resume on
+    exchange_stream, pipelined in exchange_pieces -- so both link directions
+    are busy together (same ids, slots and bytes as the two calls).
     replays NEXT-1: at the first iteration at or after t_reclaim the lender
     takes its memory back (aqua_reclaim: images move to host DRAM) and the
     scheduler falls back to FCFS; at t_relend the memory is
@@ -104,6 +109,32 @@ def run_trace(trace: Sequence[Tuple[int, float, int, int]], ctx: "aqua.Ctx", sch
         if res and record_log:
             D, PF = sched.partition()
             log.append(("plan", i, tuple(D), tuple((p, t) for p, t in PF)))
+        if outs and ins and exchange_stream is not None:
+            if stream_sync:
+                stream_sync("before_swap_out", 0)
+            t0 = time.perf_counter()
+            new, tko, tki = ctx.swap_exchange(outs, ins, swap_stream, exchange_stream, exchange_pieces)
+            q = [ctx.query(p, with_ids=True) for p in outs]
+            n_o = sum(x[2] for x in q)
+            n_i = sum(len(x) for x in new)
+            blocks_out += n_o
+            blocks_in += n_i
+            for p, x in zip(outs, q):
+                swapped_at[p] = x[1]
+            for p in ins:
+                swapped_at.pop(p, None)
+            swap_calls.append(("out", n_o, tko, t0))
+            swap_calls.append(("in", n_i, tki, t0))
+            if on_swap:
+                on_swap("out", outs, tko, n_o)
+            if stream_sync:
+                stream_sync("after_swap_in", tki)
+            if on_swap:
+                on_swap("in", ins, tki, n_i)
+            if record_log:
+                log.append(("swap_out", tuple(outs), tuple((x[1], tuple(x[3])) for x in q)))
+                log.append(("swap_in", tuple(ins), tuple(tuple(x) for x in new)))
+            outs = ins = []
         if outs:
             if stream_sync:
                 stream_sync("before_swap_out", 0)

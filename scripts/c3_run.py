@@ -39,6 +39,7 @@ def main():
     ap.add_argument("--host-gib", type=int, default=64)
     ap.add_argument("--check-oracle", action="store_true")
     ap.add_argument("--serial", action="store_true", help="swaps on the decode stream (no overlap), for A8")
+    ap.add_argument("--exchange", action="store_true", help="reschedules with both lists use aqua_swap_exchange")
     ap.add_argument("--no-verify", action="store_true")
     ap.add_argument("--elastic", default="", help="t_reclaim,t_relend (virtual s): NEXT-1 lender reclaim + FCFS "
                                                    "fallback, then re-offer")
@@ -87,6 +88,7 @@ def main():
     trace = burst_trace(seed=1)
     dec = torch.cuda.Stream(device=dev)
     swp = dec if args.serial else torch.cuda.Stream(device=dev)
+    swp2 = torch.cuda.Stream(device=dev) if args.exchange else None
     mism = torch.zeros(1, dtype=torch.int64, device=dev)
     written = {}          # pid -> KV tokens written so far
     swap_events = []      # (kind, nblocks, ticket, npids, iteration)
@@ -143,7 +145,8 @@ def main():
         elastic = {"t_reclaim": tr_, "t_relend": tl_, "relend": (lend_dev, lend_ptr, lend_bytes)}
     log, st = run_trace(trace, ctx, sched, fill_seed=SEED, decode_stream=dec.cuda_stream,
                         swap_stream=swp.cuda_stream, on_iteration=on_iteration, stream_sync=stream_sync,
-                        on_swap=on_swap, record_log=args.check_oracle, elastic=elastic)
+                        on_swap=on_swap, record_log=args.check_oracle, elastic=elastic,
+                        exchange_stream=swp2.cuda_stream if swp2 is not None else None)
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0
     launches = ctx.launch_count() - n0
@@ -192,7 +195,8 @@ def main():
         "swap_GBps": {k: round((bytes_out if k == "out" else bytes_in) / max(v, 1e-9) / 1e6, 1)
                       for k, v in dev_ms.items() if v > 0},
         "kernel_launches": launches,
-        "streams": "serial (one stream)" if args.serial else "decode + swap streams (tickets)",
+        "streams": ("serial (one stream)" if args.serial else "decode + swap streams (tickets)")
+                   + (" + exchange (preempt/resume on two streams)" if args.exchange else ""),
         "proxy_gb_per_iteration": args.proxy_gb,
         "verify_mismatches": int(mism.item()),
         "responsiveness_model_s": {"ttft_p50": pct(ttft, 0.5), "ttft_p99": pct(ttft, 0.99),

@@ -349,6 +349,118 @@ def torch_baseline():
     print(json.dumps(res), flush=True)
 
 
+def exchange():
+    """Preempt prompt A + resume prompt B (2048 blocks each, C2 shape) as two
+    sequential calls vs one aqua_swap_exchange on two streams, for the
+    lender-in-HBM and the host-DRAM arenas (full-duplex PCIe)."""
+    import time
+    L, bs, H, D, NB = 32, 16, 8, 128, 6144
+    nblk = 2048
+    S = bs * H * D * 2
+    U = 2 * L * S
+    layers = [torch.zeros(2 * NB * S, dtype=torch.uint8, device="cuda") for _ in range(L)]
+    for where in ("self", "host"):
+        ctx = aqua.Ctx(0, L, bs, H, D, 2, NB, [t.data_ptr() for t in layers])
+        arena = None
+        if where == "self":
+            arena = torch.empty(2 * nblk * U, dtype=torch.uint8, device="cuda")
+            ctx.lend(0, arena.data_ptr(), 2 * nblk * U)
+        else:
+            ctx.lend(aqua.HOST, 0, 2 * nblk * U)
+        perm = block_permutation(NB, NB, seed=2).tolist()
+        ctx.adopt_blocks(1, perm[2 * nblk:])
+        ctx.adopt_blocks(7, perm[:nblk])
+        ctx.adopt_blocks(8, perm[nblk:2 * nblk])
+        ctx.swap_out([8])
+        s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+        res = {}
+        for mode in ("sequential", "exchange"):
+            ts = []
+            for rep in range(4):
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                if mode == "sequential":
+                    ctx.swap_out([7], s1.cuda_stream)
+                    ctx.swap_in([8], s1.cuda_stream)
+                    ctx.swap_out([8], s1.cuda_stream)
+                    ctx.swap_in([7], s1.cuda_stream)
+                else:
+                    ctx.swap_exchange([7], [8], s1.cuda_stream, s2.cuda_stream, pieces=8)
+                    ctx.swap_exchange([8], [7], s2.cuda_stream, s1.cuda_stream, pieces=8)
+                torch.cuda.synchronize()
+                ts.append((time.perf_counter() - t0) / 2)
+            res[mode] = round(1e3 * statistics.median(ts[1:]), 3)
+        print(json.dumps({"exchange": where, "bytes_each_way": nblk * U, "ms_per_reschedule": res,
+                          "speedup": round(res["sequential"] / res["exchange"], 3)}), flush=True)
+        ctx.close()
+        del arena
+        torch.cuda.empty_cache()
+
+
+def duplex():
+    """Is the host link full duplex?  Copy-engine H2D + D2H concurrently vs
+    alone (1 GiB pinned each), and the zero-copy exchange at several piece
+    counts and CTA caps."""
+    n = 1 << 30
+    h1 = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+    h2 = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+    d1 = torch.empty(n, dtype=torch.uint8, device="cuda")
+    d2 = torch.empty(n, dtype=torch.uint8, device="cuda")
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+
+    def run(both):
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        s1.wait_event(a)
+        s2.wait_event(a)
+        with torch.cuda.stream(s1):
+            d1.copy_(h1, non_blocking=True)
+        if both:
+            with torch.cuda.stream(s2):
+                h2.copy_(d2, non_blocking=True)
+        e1, e2 = torch.cuda.Event(), torch.cuda.Event()
+        e1.record(s1)
+        e2.record(s2)
+        torch.cuda.current_stream().wait_event(e1)
+        torch.cuda.current_stream().wait_event(e2)
+        b.record()
+        torch.cuda.synchronize()
+        return a.elapsed_time(b)
+    run(True)
+    alone = min(run(False) for _ in range(3))
+    both = min(run(True) for _ in range(3))
+    print(json.dumps({"duplex_ce": {"h2d_alone_GBps": round(n / alone / 1e6, 1),
+                                    "h2d_plus_d2h_total_GBps": round(2 * n / both / 1e6, 1)}}), flush=True)
+    L, bs, H, D, NB = 32, 16, 8, 128, 6144
+    nblk = 2048
+    S = bs * H * D * 2
+    U = 2 * L * S
+    layers = [torch.zeros(2 * NB * S, dtype=torch.uint8, device="cuda") for _ in range(L)]
+    ctx = aqua.Ctx(0, L, bs, H, D, 2, NB, [t.data_ptr() for t in layers])
+    ctx.lend(aqua.HOST, 0, 2 * nblk * U)
+    perm = block_permutation(NB, NB, seed=2).tolist()
+    ctx.adopt_blocks(1, perm[2 * nblk:])
+    ctx.adopt_blocks(7, perm[:nblk])
+    ctx.adopt_blocks(8, perm[nblk:2 * nblk])
+    ctx.swap_out([8])
+    import time
+    for ctas in (8, 16, 32):
+        ctx.set_option(aqua.OPT_MAX_CTAS, ctas)
+        for pieces in (1, 4, 16):
+            ts = []
+            for rep in range(3):
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                ctx.swap_exchange([7], [8], s1.cuda_stream, s2.cuda_stream, pieces=pieces)
+                ctx.swap_exchange([8], [7], s2.cuda_stream, s1.cuda_stream, pieces=pieces)
+                torch.cuda.synchronize()
+                ts.append((time.perf_counter() - t0) / 2)
+            ms = 1e3 * statistics.median(ts)
+            print(json.dumps({"host_exchange_ctas": ctas, "pieces": pieces, "ms": round(ms, 2),
+                              "total_GBps": round(2 * nblk * U / ms / 1e6, 1)}), flush=True)
+
+
 def stages():
     L, bs, H, D, NB, nblk = 32, 16, 8, 128, 4096, 2048
     ctx, layers, arena, U = setup(L, bs, H, D, NB, nblk)
@@ -404,6 +516,10 @@ if __name__ == "__main__":
         prefix()
     elif what == "migrate":
         migrate()
+    elif what == "duplex":
+        duplex()
+    elif what == "exchange":
+        exchange()
     elif what == "torch_baseline":
         torch_baseline()
     elif what == "c5_multi":

@@ -356,3 +356,15 @@ def test_layered_calls_same_bookkeeping_dryrun():
     assert new == [[0, 1, 2, 3]] and len(t) == 1
     with pytest.raises(aqua.AquaError):
         c.swap_out_layers([1], 0)
+
+
+def test_exchange_driver_call_log_matches_oracle():
+    """Reschedules issued as aqua_swap_exchange keep the oracle's call log."""
+    tr = burst_trace(seed=3, burst_s=8.0, tail_s=3.0, prompt=(300, 0.8, 1, 900), output=(40, 0.7, 1, 200))
+    NB = 120
+    o = osim.run(tr, osim.SimConfig(NB=NB, lender_slots=200, host_slots=400))
+    c = aqua.Ctx(aqua.DRYRUN, 1, 16, 1, 8, 2, NB, [FAKE])
+    c.lend(0, FAKE * 2, 200 * c.U)
+    c.lend(aqua.HOST, FAKE * 3, 400 * c.U)
+    log, st = run_trace(tr, c, Scheduler(NB=NB, bs=16), exchange_stream=0)
+    assert log == o.log

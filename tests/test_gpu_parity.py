@@ -430,3 +430,29 @@ def test_multistream_fuzz_equals_sequential(seed):
         if step % 40 == 39:
             rig.assert_bytes_equal(f"fuzz step {step}")
     rig.assert_bytes_equal("fuzz end")
+
+
+@pytest.mark.parametrize("pieces", [1, 3, 8])
+@pytest.mark.parametrize("arena", ["lender", "host"])
+def test_swap_exchange_bytes(pieces, arena):
+    """aqua_swap_exchange == swap_out then swap_in (oracle), byte for byte,
+    with the resume on another stream pipelined behind the preemption pieces
+    whose blocks it reuses."""
+    rig = Rig(L=3, bs=16, H=4, D=64, NB=40, lender_slots=30 if arena == "lender" else 0, host_slots=40)
+    c, o = rig.ctx, rig.opool
+    perm = block_permutation(40, 40, seed=11).tolist()
+    for pid, k in ((1, 6), (2, 5), (3, 7), (4, 9)):
+        ids, perm = perm[:k], perm[k:]
+        c.adopt_blocks(pid, ids)
+        o.adopt_blocks(pid, ids)
+    _ops(rig, [("out", [2, 4])])
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    new, to, ti = c.swap_exchange([1, 3], [4, 2], s1.cuda_stream, s2.cuda_stream, pieces=pieces)
+    o.swap_out([1, 3])
+    assert new == o.swap_in([4, 2])
+    rig.assert_bytes_equal("exchange")
+    # and back again, same streams swapped
+    new, to, ti = c.swap_exchange([4], [1, 3], s2.cuda_stream, s1.cuda_stream, pieces=pieces)
+    o.swap_out([4])
+    assert new == o.swap_in([1, 3])
+    rig.assert_bytes_equal("exchange back")
