@@ -1060,7 +1060,7 @@ aqua_status aqua_swap_exchange(aqua_ctx* c, int32_t n_out, const uint64_t* out_p
     parts[f == freed_by.end() ? 0 : f->second].push_back(d);
   }
   // ---- launches
-  uint64_t t_out = 0, t_in = 0;
+  uint64_t t_out = 0, t_in = 0, first_in = 0;
   if (!c->dry) {
     DevGuard g(c->device);
     cudaStream_t so = reinterpret_cast<cudaStream_t>(out_stream);
@@ -1084,9 +1084,22 @@ aqua_status aqua_swap_exchange(aqua_ctx* c, int32_t n_out, const uint64_t* out_p
         }
         if (parts[k].empty()) continue;
         if (aqua_status s = enqueue_copy(c, parts[k], aqua::kIn, si, 0, nullptr, &t_in)) return s;
+        if (!first_in) first_in = t_in;
       }
       if (!t_in) record(c, si, &t_in);
     }
+    // AQUA_OPT_TIMING: the call tickets span all their pieces -- move the
+    // first piece's start event onto the last ticket of each direction
+    auto span = [c](uint64_t first, uint64_t last) {
+      if (!first || !last || first == last) return;
+      auto a = c->live.find(first), b = c->live.find(last);
+      if (a == c->live.end() || b == c->live.end() || !a->second.start || !b->second.start) return;
+      c->tev_pool.push_back(b->second.start);
+      b->second.start = a->second.start;
+      a->second.start = nullptr;   // its end event stays a live ticket (retired into the plain pool)
+    };
+    if (!dso.empty()) span(piece_ticket[0], t_out);
+    if (!dsi.empty()) span(first_in, t_in);
   } else {
     if (!dso.empty()) record(c, nullptr, &t_out);
     if (!dsi.empty()) record(c, nullptr, &t_in);

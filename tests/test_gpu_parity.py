@@ -456,3 +456,19 @@ def test_swap_exchange_bytes(pieces, arena):
     o.swap_out([4])
     assert new == o.swap_in([1, 3])
     rig.assert_bytes_equal("exchange back")
+
+
+def test_swap_exchange_timing_spans_pieces():
+    rig = Rig(L=4, bs=16, H=8, D=128, NB=96, lender_slots=96)
+    c = rig.ctx
+    c.alloc_blocks(1, 32)
+    c.alloc_blocks(2, 32)
+    c.swap_out([2])
+    c.set_option(aqua.OPT_TIMING, 1)
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    _, to, ti = c.swap_exchange([1], [2], s1.cuda_stream, s2.cuda_stream, pieces=4)
+    torch.cuda.synchronize()
+    t_one = c.swap_out([2], s1.cuda_stream)    # pid 2 is resident again; time a plain swap of the same size
+    torch.cuda.synchronize()
+    assert c.ticket_elapsed(to) > 0.5 * c.ticket_elapsed(t_one)
+    assert c.ticket_elapsed(ti) > 0
