@@ -154,13 +154,18 @@ def main():
     per_block_ms = []
     dev_ms = {"out": 0.0, "in": 0.0}
     swap_ms_at = [0.0] * (len(it_tokens) + 1)
+    by_iter = {}
     for kind, n, tk, npids, at in swap_events:
         if n == 0:
             continue
         ms = ctx.ticket_elapsed(tk)
         dev_ms[kind] += ms
         per_block_ms.append((kind, ms, n, npids))
-        swap_ms_at[at] += ms
+        by_iter.setdefault(at, []).append(ms)
+    for at, mss in by_iter.items():
+        # an exchange runs its two directions concurrently: its critical path
+        # is the longer one; separate calls are sequential on the swap stream
+        swap_ms_at[at] = max(mss) if args.exchange else sum(mss)
     # Responsiveness model (context for the paper's E6): the
     # schedule is fixed by the virtual clock (R17); each swap's MEASURED
     # device time is put on the critical path of the iteration that issued it
