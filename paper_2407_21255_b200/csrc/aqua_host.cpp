@@ -525,7 +525,33 @@ void set_last(aqua_ctx* c, const std::vector<Desc>& ds) {
 
 Arena* arena_of(aqua_ctx* c, int loc) { return loc == AQUA_LOC_HOST ? &c->host : &c->gpu; }
 
-}  // namespace
+}
+// Orders `st` after the last library use of every block and slot the
+// descriptors touch (R7), then enqueues the copy; a dry context only draws a
+// ticket.  For kMig the descriptor's `block` field is the source slot.
+aqua_status launch(aqua_ctx* c, const std::vector<Desc>& ds, aqua::Dir dir, cudaStream_t st, uint64_t* ticket,
+                   int32_t layer_group = 0, uint64_t* group_tickets = nullptr) {
+  *ticket = 0;
+  if (ds.empty()) return AQUA_OK;
+  if (c->dry) return record(c, st, ticket);
+  DevGuard g(c->device);
+  std::vector<uint64_t> ts;
+  ts.reserve(2 * ds.size());
+  for (const Desc& d : ds) {
+    if (dir == aqua::kMig) {
+      const uint32_t sb = static_cast<uint32_t>(d.block);
+      ts.push_back(arena_of(c, (sb & kArenaBit) ? AQUA_LOC_HOST : AQUA_LOC_PEER)->tick[sb & ~kArenaBit]);
+    } else {
+      ts.push_back(c->btick[d.block]);
+    }
+    ts.push_back(arena_of(c, (d.slot_arena & kArenaBit) ? AQUA_LOC_HOST : AQUA_LOC_PEER)
+                     ->tick[d.slot_arena & ~kArenaBit]);
+  }
+  if (aqua_status s = wait_all(c, ts, st)) return s;
+  return enqueue_copy(c, ds, dir, st, layer_group, group_tickets, ticket);
+}
+
+  // namespace
 
 extern "C" {
 
@@ -752,68 +778,65 @@ aqua_status aqua_adopt_blocks(aqua_ctx* c, uint64_t pid, int32_t n, const int32_
   return AQUA_OK;
 }
 
-static aqua_status swap_out_impl(aqua_ctx* c, int32_t n, const uint64_t* pids, aqua_stream_t stream,
-                                 uint64_t* out_ticket, int32_t layer_group, uint64_t* group_tickets) {
-  if (aqua_status s = precheck(c)) return s;
-  if (out_ticket) *out_ticket = 0;
+// Validation + placement of a preemption (R5: whole prompt on the GPU
+// lender if it fits, else the host arena; slots lowest-first per arena in
+// call order).  No state change.
+static aqua_status plan_out(aqua_ctx* c, int32_t n, const uint64_t* pids, std::vector<Prompt*>* ps,
+                            std::vector<int>* loc, std::vector<std::vector<int32_t>>* slots,
+                            std::vector<Desc>* ds) {
   if (n < 0 || (n > 0 && !pids)) return fail(c, AQUA_E_INVAL, "n < 0 or null pids");
   std::unordered_set<uint64_t> seen;
-  std::vector<Prompt*> ps;
-  for (int32_t i = 0; i < n; ++i) {
+  for (int32_t i = 0; i < n; ++i)
     if (!seen.insert(pids[i]).second) return fail(c, AQUA_E_INVAL, "duplicate pid");
-  }
   for (int32_t i = 0; i < n; ++i) {
     auto it = c->prompts.find(pids[i]);
     if (it == c->prompts.end() || it->second.state != AQUA_ST_RESIDENT)
       return fail(c, AQUA_E_STATE, "pid not resident");
-    ps.push_back(&it->second);
+    ps->push_back(&it->second);
   }
-  // placement (R5): whole prompt on the GPU lender if it fits, else host
   int64_t gpu_left = c->gpu.present ? static_cast<int64_t>(c->gpu.free.size()) : -1;
   int64_t host_left = c->host.present ? static_cast<int64_t>(c->host.free.size()) : -1;
-  std::vector<int> loc(n);
+  loc->assign(n, AQUA_LOC_PEER);
   for (int32_t i = 0; i < n; ++i) {
-    const int64_t np = static_cast<int64_t>(ps[i]->ids.size());
+    const int64_t np = static_cast<int64_t>((*ps)[i]->ids.size());
     if (gpu_left >= np) {
-      loc[i] = AQUA_LOC_PEER;
+      (*loc)[i] = AQUA_LOC_PEER;
       gpu_left -= np;
     } else if (host_left >= np) {
-      loc[i] = AQUA_LOC_HOST;
+      (*loc)[i] = AQUA_LOC_HOST;
       host_left -= np;
     } else {
       return fail(c, AQUA_E_NOSPACE, "no swap space for a prompt");
     }
   }
-  // slots lowest-first per arena, in call order
-  std::vector<Desc> ds;
-  std::vector<std::vector<int32_t>> slots(n);
+  slots->assign(n, {});
   auto git = c->gpu.free.begin();
   auto hit = c->host.free.begin();
   for (int32_t i = 0; i < n; ++i) {
-    auto& itr = loc[i] == AQUA_LOC_PEER ? git : hit;
-    const uint32_t bit = loc[i] == AQUA_LOC_HOST ? kArenaBit : 0u;
-    for (int32_t b : ps[i]->ids) {
-      const int32_t s = *itr++;
-      slots[i].push_back(s);
-      ds.push_back(Desc{b, static_cast<uint32_t>(s) | bit});
+    auto& itr = (*loc)[i] == AQUA_LOC_PEER ? git : hit;
+    const uint32_t bit = (*loc)[i] == AQUA_LOC_HOST ? kArenaBit : 0u;
+    for (int32_t b : (*ps)[i]->ids) {
+      const int32_t sl = *itr++;
+      (*slots)[i].push_back(sl);
+      ds->push_back(Desc{b, static_cast<uint32_t>(sl) | bit});
     }
   }
+  return AQUA_OK;
+}
+
+static aqua_status swap_out_impl(aqua_ctx* c, int32_t n, const uint64_t* pids, aqua_stream_t stream,
+                                 uint64_t* out_ticket, int32_t layer_group, uint64_t* group_tickets) {
+  if (aqua_status s = precheck(c)) return s;
+  if (out_ticket) *out_ticket = 0;
+  std::vector<Prompt*> ps;
+  std::vector<int> loc;
+  std::vector<std::vector<int32_t>> slots;
+  std::vector<Desc> ds;
+  if (aqua_status s = plan_out(c, n, pids, &ps, &loc, &slots, &ds)) return s;
   set_last(c, ds);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   uint64_t ticket = 0;
-  if (!c->dry && !ds.empty()) {
-    DevGuard g(c->device);
-    std::vector<uint64_t> ts;
-    for (const Desc& d : ds) {
-      ts.push_back(c->btick[d.block]);
-      ts.push_back(arena_of(c, (d.slot_arena & kArenaBit) ? AQUA_LOC_HOST : AQUA_LOC_PEER)
-                       ->tick[d.slot_arena & ~kArenaBit]);
-    }
-    if (aqua_status s = wait_all(c, ts, st)) return s;
-    if (aqua_status s = enqueue_copy(c, ds, aqua::kOut, st, layer_group, group_tickets, &ticket)) return s;
-  } else if (c->dry && !ds.empty()) {
-    record(c, st, &ticket);
-  }
+  if (aqua_status s = launch(c, ds, aqua::kOut, st, &ticket, layer_group, group_tickets)) return s;
   // commit bookkeeping
   for (int32_t i = 0; i < n; ++i) {
     Arena* a = arena_of(c, loc[i]);
@@ -868,19 +891,7 @@ static aqua_status swap_in_impl(aqua_ctx* c, int32_t n, const uint64_t* pids, aq
   set_last(c, ds);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   uint64_t ticket = 0;
-  if (!c->dry && !ds.empty()) {
-    DevGuard g(c->device);
-    std::vector<uint64_t> ts;
-    for (const Desc& d : ds) {
-      ts.push_back(c->btick[d.block]);
-      ts.push_back(arena_of(c, (d.slot_arena & kArenaBit) ? AQUA_LOC_HOST : AQUA_LOC_PEER)
-                       ->tick[d.slot_arena & ~kArenaBit]);
-    }
-    if (aqua_status s = wait_all(c, ts, st)) return s;
-    if (aqua_status s = enqueue_copy(c, ds, aqua::kIn, st, layer_group, group_tickets, &ticket)) return s;
-  } else if (c->dry && !ds.empty()) {
-    record(c, st, &ticket);
-  }
+  if (aqua_status s = launch(c, ds, aqua::kIn, st, &ticket, layer_group, group_tickets)) return s;
   c->free_blocks.erase_lowest(static_cast<int32_t>(need));
   int64_t k = 0;
   for (int32_t i = 0; i < n; ++i) {
@@ -954,33 +965,12 @@ aqua_status aqua_swap_exchange(aqua_ctx* c, int32_t n_out, const uint64_t* out_p
   if (n_out < 0 || n_in < 0 || (n_out > 0 && !out_pids) || (n_in > 0 && !in_pids) || pieces < 1)
     return fail(c, AQUA_E_INVAL, "bad counts, pointers or pieces");
   // ---- validate everything first (all-or-nothing, as the two calls would)
-  std::unordered_set<uint64_t> seen;
-  for (int32_t i = 0; i < n_out; ++i)
-    if (!seen.insert(out_pids[i]).second) return fail(c, AQUA_E_INVAL, "duplicate pid");
   std::vector<Prompt*> po;
-  int64_t freed = 0;
-  for (int32_t i = 0; i < n_out; ++i) {
-    auto it = c->prompts.find(out_pids[i]);
-    if (it == c->prompts.end() || it->second.state != AQUA_ST_RESIDENT)
-      return fail(c, AQUA_E_STATE, "pid not resident");
-    po.push_back(&it->second);
-    freed += static_cast<int64_t>(it->second.ids.size());
-  }
-  int64_t gpu_left = c->gpu.present ? static_cast<int64_t>(c->gpu.free.size()) : -1;
-  int64_t host_left = c->host.present ? static_cast<int64_t>(c->host.free.size()) : -1;
-  std::vector<int> loc(n_out);
-  for (int32_t i = 0; i < n_out; ++i) {
-    const int64_t np = static_cast<int64_t>(po[i]->ids.size());
-    if (gpu_left >= np) {
-      loc[i] = AQUA_LOC_PEER;
-      gpu_left -= np;
-    } else if (host_left >= np) {
-      loc[i] = AQUA_LOC_HOST;
-      host_left -= np;
-    } else {
-      return fail(c, AQUA_E_NOSPACE, "no swap space for a prompt");
-    }
-  }
+  std::vector<int> loc;
+  std::vector<std::vector<int32_t>> slots;
+  std::vector<Desc> dso;
+  if (aqua_status s = plan_out(c, n_out, out_pids, &po, &loc, &slots, &dso)) return s;
+  const int64_t freed = static_cast<int64_t>(dso.size());
   std::unordered_set<uint64_t> seen_in;
   std::vector<Prompt*> pi;
   int64_t need = 0;
@@ -997,22 +987,6 @@ aqua_status aqua_swap_exchange(aqua_ctx* c, int32_t n_out, const uint64_t* out_p
   if (need > static_cast<int64_t>(c->free_blocks.size()) + freed)
     return fail(c, AQUA_E_NOBLOCKS, "pool exhausted");
 
-  // ---- plan the preemption (slots lowest-first per arena, call order)
-  std::vector<Desc> dso;
-  std::vector<std::vector<int32_t>> slots(n_out);
-  {
-    auto git = c->gpu.free.begin();
-    auto hit = c->host.free.begin();
-    for (int32_t i = 0; i < n_out; ++i) {
-      auto& itr = loc[i] == AQUA_LOC_PEER ? git : hit;
-      const uint32_t bit = loc[i] == AQUA_LOC_HOST ? kArenaBit : 0u;
-      for (int32_t b : po[i]->ids) {
-        const int32_t sl = *itr++;
-        slots[i].push_back(sl);
-        dso.push_back(Desc{b, static_cast<uint32_t>(sl) | bit});
-      }
-    }
-  }
   // piece of the preemption that reads each block (its end event frees it)
   const int32_t npo = std::max<int32_t>(1, std::min<int32_t>(pieces, static_cast<int32_t>(dso.size())));
   std::unordered_map<int32_t, int32_t> freed_by;
@@ -1161,26 +1135,7 @@ static aqua_status move_images(aqua_ctx* c, const std::vector<Prompt*>& ps, int3
     c->last_l.push_back(dst);
   }
   uint64_t ticket = 0;
-  if (!ds.empty()) {
-    if (!c->dry) {
-      DevGuard g(c->device);
-      std::vector<uint64_t> ts;
-      for (size_t i = 0; i < ps.size(); ++i) {
-        Arena* as = arena_of(c, ps[i]->loc);
-        for (int32_t so : ps[i]->ids) ts.push_back(as->tick[so]);
-        for (int32_t sn : fresh[i]) ts.push_back(ad->tick[sn]);
-      }
-      if (aqua_status s = wait_all(c, ts, st)) return s;
-      cudaEvent_t t_start;
-      if (aqua_status s = timing_start(c, st, &t_start)) return s;
-      int regions = 0;
-      if (aqua_status s = run_copy(c, ds, aqua::kMig, st, &regions)) return s;
-      if (aqua_status s = record(c, st, &ticket, t_start)) return s;
-      stage_seal(c, regions, ticket);
-    } else {
-      record(c, st, &ticket);
-    }
-  }
+  if (aqua_status s = launch(c, ds, aqua::kMig, st, &ticket)) return s;
   for (size_t i = 0; i < ps.size(); ++i) {
     Arena* as = arena_of(c, ps[i]->loc);
     for (int32_t so : ps[i]->ids) {
@@ -1297,23 +1252,7 @@ aqua_status aqua_prefix_store(aqua_ctx* c, uint64_t fid, uint64_t src_pid, int32
   set_last(c, ds);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   uint64_t ticket = 0;
-  if (!c->dry && !ds.empty()) {
-    DevGuard g(c->device);
-    std::vector<uint64_t> ts;
-    for (const Desc& d : ds) {
-      ts.push_back(c->btick[d.block]);
-      ts.push_back(a->tick[d.slot_arena & ~kArenaBit]);
-    }
-    if (aqua_status s = wait_all(c, ts, st)) return s;
-    cudaEvent_t t_start;
-    if (aqua_status s = timing_start(c, st, &t_start)) return s;
-    int regions = 0;
-    if (aqua_status s = run_copy(c, ds, aqua::kOut, st, &regions)) return s;
-    if (aqua_status s = record(c, st, &ticket, t_start)) return s;
-    stage_seal(c, regions, ticket);
-  } else if (c->dry && !ds.empty()) {
-    record(c, st, &ticket);
-  }
+  if (aqua_status s = launch(c, ds, aqua::kOut, st, &ticket)) return s;
   for (size_t j = 0; j < slots.size(); ++j) {
     a->free.erase(slots[j]);
     a->tick[slots[j]] = ticket;
@@ -1353,18 +1292,7 @@ aqua_status aqua_prefix_load(aqua_ctx* c, uint64_t fid, uint64_t dst_pid, aqua_s
   set_last(c, ds);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   uint64_t ticket = 0;
-  if (!c->dry && !ds.empty()) {
-    DevGuard g(c->device);
-    std::vector<uint64_t> ts;
-    for (const Desc& d : ds) {
-      ts.push_back(c->btick[d.block]);
-      ts.push_back(a->tick[d.slot_arena & ~kArenaBit]);
-    }
-    if (aqua_status s = wait_all(c, ts, st)) return s;
-    if (aqua_status s = enqueue_copy(c, ds, aqua::kIn, st, 0, nullptr, &ticket)) return s;
-  } else if (c->dry && !ds.empty()) {
-    record(c, st, &ticket);
-  }
+  if (aqua_status s = launch(c, ds, aqua::kIn, st, &ticket)) return s;
   c->free_blocks.erase_lowest(n);
   Prompt& p = c->prompts[dst_pid];
   for (int32_t j = 0; j < n; ++j) {
