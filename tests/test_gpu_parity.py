@@ -472,3 +472,38 @@ def test_swap_exchange_timing_spans_pieces():
     torch.cuda.synchronize()
     assert c.ticket_elapsed(to) > 0.5 * c.ticket_elapsed(t_one)
     assert c.ticket_elapsed(ti) > 0
+
+
+def test_library_owned_lender_reclaim_frees_after_ticket():
+    """aqua_lend(base=NULL) allocates the lender arena itself; a reclaim
+    moves the images to the host and frees the arena once its ticket is
+    done (deferred free); the images stay byte-exact (verify after resume)."""
+    import torch
+    L, bs, H, D, NB = 4, 16, 8, 128, 64
+    S = bs * H * D * 2
+    layers = [torch.zeros(2 * NB * S, dtype=torch.uint8, device="cuda") for _ in range(L)]
+    c = aqua.Ctx(0, L, bs, H, D, 2, NB, [t.data_ptr() for t in layers])
+    U = c.U
+    assert c.lend(0, 0, 40 * U) == 40
+    assert c.lend(aqua.HOST, 0, 40 * U) == 40
+    base, n = c.arena_base(aqua.LOC_PEER)
+    assert base and n == 40
+    c.alloc_blocks(1, 16)
+    c.alloc_blocks(2, 8)
+    c.kv_fill_pattern(1, 0, 16 * bs, 5)
+    c.kv_fill_pattern(2, 0, 8 * bs, 5)
+    c.swap_out([1, 2])
+    t = c.reclaim()
+    c.sync(t)
+    assert c.counts()[1] == -1 and c.query(1)[1] == aqua.LOC_HOST
+    for x in layers:
+        x.fill_(0x33)
+    c.swap_in([2, 1])
+    cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+    c.kv_verify_pattern(1, 16 * bs, 5, cnt.data_ptr())
+    c.kv_verify_pattern(2, 8 * bs, 5, cnt.data_ptr())
+    torch.cuda.synchronize()
+    assert int(cnt.item()) == 0
+    c.alloc_blocks(3, 1)          # a later call retires the ticket and frees the zombie arena
+    assert c.lend(0, 0, 8 * U) == 8   # re-offer: a fresh library-owned arena
+    c.close()
