@@ -477,6 +477,7 @@ def host_baselines(ctx_dev, layers, dev, aqua, args):
     s = torch.cuda.Stream(device=dev)
     res = {}
     for name, eng in (("tma_zero_copy", aqua.KERNEL_TMA), ("ldst_zero_copy", aqua.KERNEL_LDST),
+                      ("ce_host_staged", aqua.KERNEL_CE_HOST),
                       ("per_chunk_memcpy", aqua.BASE_PER_CHUNK), ("gather_temp_memcpy", aqua.BASE_GATHER_TEMP),
                       ("memcpy_batch", aqua.BASE_BATCH)):
         ctx.set_option(aqua.OPT_KERNEL, eng)

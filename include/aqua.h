@@ -102,12 +102,15 @@ enum { AQUA_LOC_LOCAL = 0, AQUA_LOC_PEER = 1, AQUA_LOC_HOST = 2 };
 /* Copy engines for aqua_set_option(AQUA_OPT_KERNEL).  The first three are the
  * product; the last three are baselines kept for measurement only. */
 enum {
-  AQUA_KERNEL_AUTO = 0,       /* product default (picked from measurements) */
+  AQUA_KERNEL_AUTO = 0,       /* product default: CE_HOST when every image of the call is in host DRAM,
+                                 else TMA (picked from measurements) */
   AQUA_KERNEL_TMA = 1,        /* fused gather/scatter, cp.async.bulk smem ring (UBLKCP) */
   AQUA_KERNEL_LDST = 2,       /* fused gather/scatter, 16-byte LDG/STG register path */
   AQUA_BASE_PER_CHUNK = 3,    /* baseline: one cudaMemcpyAsync per chunk (vLLM-style) */
   AQUA_BASE_GATHER_TEMP = 4,  /* baseline: the paper's gather-to-temp + one copy */
-  AQUA_BASE_BATCH = 5         /* baseline: cudaMemcpyBatchAsync over all chunks */
+  AQUA_BASE_BATCH = 5,        /* baseline: cudaMemcpyBatchAsync over all chunks */
+  AQUA_KERNEL_CE_HOST = 6     /* host images via a GPU staging buffer + DMA copy engines (full-duplex PCIe);
+                                 GPU-lender images still use the TMA kernel */
 };
 enum {
   AQUA_OPT_KERNEL = 1,        /* one of AQUA_KERNEL_* / AQUA_BASE_* */

@@ -101,6 +101,10 @@ struct aqua_ctx {
   // gather-temp baseline buffer
   uint8_t* d_temp = nullptr;
   size_t temp_cap = 0;
+  // AQUA_KERNEL_CE_HOST staging buffers, one per direction (out, in), and
+  // the ticket of their last use
+  uint8_t* ce_temp[2] = {nullptr, nullptr};
+  uint64_t ce_tick[2] = {0, 0};
   bool poisoned = false;
   std::string err;
   std::vector<int32_t> last_b, last_s, last_l;
@@ -295,10 +299,84 @@ void stage_seal(aqua_ctx* c, size_t nregions, uint64_t ticket) {
 }
 
 // ------------------------------------------------------------ copy engines
+// AQUA_KERNEL_CE_HOST: host images through the DMA copy engines.  Per chunk
+// of descriptors (<= kCeChunk bytes) the TMA kernel gathers the blocks into a
+// device staging buffer laid out [j][chunk range] (swap_out) and one 2-D
+// cudaMemcpyAsync per run of consecutive slots moves it to pinned DRAM -- or
+// the reverse for swap_in.  The copy engines keep PCIe busy in both
+// directions at once (aqua_swap_exchange), where SM-issued zero-copy
+// accesses reach less (profiles/r01_duplex.jsonl).
+constexpr size_t kCeChunk = size_t(256) << 20;
+
+aqua_status run_copy(aqua_ctx* c, const std::vector<Desc>& ds, aqua::Dir dir, cudaStream_t st,
+                     int* regions, int32_t c0 = 0, int32_t nc = -1, const Desc* dev_desc = nullptr);
+
+aqua_status run_copy_ce_host(aqua_ctx* c, const std::vector<Desc>& ds, aqua::Dir dir, cudaStream_t st,
+                             int32_t c0, int32_t nc) {
+  const int di = dir == aqua::kOut ? 0 : 1;
+  const size_t per = static_cast<size_t>(nc) * c->S;           // bytes of one descriptor's range
+  const size_t chunk = std::max<size_t>(1, kCeChunk / per);     // descriptors per chunk
+  if (!c->ce_temp[di]) CK(c, cudaMalloc(reinterpret_cast<void**>(&c->ce_temp[di]), chunk * per));
+  if (aqua_status s = wait_all(c, {c->ce_tick[di]}, st)) return s;   // the buffer's last user
+  uint8_t* tmp = c->ce_temp[di];
+  const int kernel_engine = AQUA_KERNEL_TMA;
+  for (size_t j0 = 0; j0 < ds.size(); j0 += chunk) {
+    const size_t j1 = std::min(ds.size(), j0 + chunk);
+    std::vector<Desc> td;
+    td.reserve(j1 - j0);
+    for (size_t j = j0; j < j1; ++j) td.push_back(Desc{ds[j].block, static_cast<uint32_t>(j - j0)});
+    auto dma = [&](bool to_host) -> aqua_status {
+      size_t j = j0;
+      while (j < j1) {
+        size_t r = 1;
+        while (j + r < j1 && ds[j + r].slot_arena == ds[j].slot_arena + r) ++r;
+        uint8_t* img = c->host.base + int64_t(ds[j].slot_arena & ~kArenaBit) * c->U + int64_t(c0) * c->S;
+        uint8_t* t = tmp + (j - j0) * per;
+        if (to_host)
+          CK(c, cudaMemcpy2DAsync(img, c->U, t, per, per, r, cudaMemcpyDefault, st));
+        else
+          CK(c, cudaMemcpy2DAsync(t, per, img, c->U, per, r, cudaMemcpyDefault, st));
+        j += r;
+      }
+      return AQUA_OK;
+    };
+    // the staging buffer acts as a GPU "arena" of slots of `per` bytes whose
+    // chunk c sits at (c - c0)*S: base shifted by -c0*S, U = per
+    const int saved_kernel = c->kernel;
+    uint8_t* saved_base = c->gpu.base;
+    const int64_t saved_U = c->U;
+    c->kernel = kernel_engine;
+    c->gpu.base = tmp - int64_t(c0) * c->S;
+    c->U = static_cast<int64_t>(per);
+    int regions = 0;
+    aqua_status s = AQUA_OK;
+    if (dir == aqua::kOut) {
+      s = run_copy(c, td, aqua::kOut, st, &regions, c0, nc, nullptr);
+      c->kernel = saved_kernel, c->gpu.base = saved_base, c->U = saved_U;
+      if (!s) s = dma(true);
+    } else {
+      c->kernel = saved_kernel, c->gpu.base = saved_base, c->U = saved_U;
+      s = dma(false);
+      if (!s) {
+        c->kernel = kernel_engine, c->gpu.base = tmp - int64_t(c0) * c->S, c->U = static_cast<int64_t>(per);
+        s = run_copy(c, td, aqua::kIn, st, &regions, c0, nc, nullptr);
+        c->kernel = saved_kernel, c->gpu.base = saved_base, c->U = saved_U;
+      }
+    }
+    if (s) return s;
+    if (regions) {      // a staged descriptor upload: keep it until this stream passes here
+      uint64_t t;
+      if (aqua_status s2 = record(c, st, &t)) return s2;
+      stage_seal(c, regions, t);
+    }
+  }
+  return record(c, st, &c->ce_tick[di]);
+}
+
 // Moves chunks [c0, c0 + nc) (c = 2l + kv; default: all 2L) of every
 // descriptor with the configured engine.
 aqua_status run_copy(aqua_ctx* c, const std::vector<Desc>& ds, aqua::Dir dir, cudaStream_t st,
-                     int* regions, int32_t c0 = 0, int32_t nc = -1, const Desc* dev_desc = nullptr) {
+                     int* regions, int32_t c0, int32_t nc, const Desc* dev_desc) {
   *regions = 0;
   if (ds.empty()) return AQUA_OK;
   if (nc < 0) nc = 2 * c->L;
@@ -314,7 +392,15 @@ aqua_status run_copy(aqua_ctx* c, const std::vector<Desc>& ds, aqua::Dir dir, cu
   p.P_b = c->P_b;
   p.c0 = c0;
   p.nc = nc;
-  int engine = c->kernel == AQUA_KERNEL_AUTO ? AQUA_KERNEL_TMA : c->kernel;
+  // AUTO: images in host DRAM go through the copy engines (full-duplex PCIe,
+  // no SMs held for the transfer: profiles/r01_duplex2.jsonl); everything
+  // else through the fused TMA kernel
+  int engine = c->kernel;
+  if (engine == AQUA_KERNEL_AUTO) {
+    bool host_only = dir != aqua::kMig && !dev_desc;
+    for (const Desc& d : ds) host_only = host_only && (d.slot_arena & kArenaBit);
+    engine = host_only ? AQUA_KERNEL_CE_HOST : AQUA_KERNEL_TMA;
+  }
   if (dir == aqua::kMig && engine != AQUA_KERNEL_LDST) engine = AQUA_KERNEL_TMA;  // baselines do not migrate
   if (nc != 2 * c->L && engine == AQUA_BASE_GATHER_TEMP) engine = AQUA_KERNEL_TMA;  // whole blocks only
 
@@ -325,6 +411,12 @@ aqua_status run_copy(aqua_ctx* c, const std::vector<Desc>& ds, aqua::Dir dir, cu
     *img = ab + int64_t(d.slot_arena & ~kArenaBit) * c->U + int64_t(cc) * c->S;
   };
 
+  if (engine == AQUA_KERNEL_CE_HOST) {
+    bool all_host = dir != aqua::kMig;
+    for (const Desc& d : ds) all_host = all_host && (d.slot_arena & kArenaBit);
+    if (all_host && !dev_desc) return run_copy_ce_host(c, ds, dir, st, c0, nc);
+    engine = AQUA_KERNEL_TMA;   // only host images go through the copy engines
+  }
   if (engine == AQUA_KERNEL_TMA || engine == AQUA_KERNEL_LDST) {
     if (dev_desc) {
       p.desc = dev_desc;                      // already uploaded by the caller
@@ -412,6 +504,8 @@ aqua_status run_copy(aqua_ctx* c, const std::vector<Desc>& ds, aqua::Dir dir, cu
     if (need > c->temp_cap) {
       CK(c, cudaDeviceSynchronize());
       if (c->d_temp) cudaFree(c->d_temp);
+    for (uint8_t* t : c->ce_temp)
+      if (t) cudaFree(t);
       c->d_temp = nullptr;
       CK(c, cudaMalloc(reinterpret_cast<void**>(&c->d_temp), need));
       c->temp_cap = need;
@@ -1446,7 +1540,7 @@ aqua_status aqua_set_option(aqua_ctx* c, int32_t opt, int64_t v) {
   if (!c) return fail(nullptr, AQUA_E_INVAL, "null ctx");
   switch (opt) {
     case AQUA_OPT_KERNEL:
-      if (v < AQUA_KERNEL_AUTO || v > AQUA_BASE_BATCH) return fail(c, AQUA_E_INVAL, "kernel");
+      if (v < AQUA_KERNEL_AUTO || v > AQUA_KERNEL_CE_HOST) return fail(c, AQUA_E_INVAL, "kernel");
       c->kernel = static_cast<int>(v);
       return AQUA_OK;
     case AQUA_OPT_MAX_CTAS:

@@ -20,7 +20,7 @@ from paper_2407_21255_b200 import aqua  # noqa: E402
 from workloads import block_permutation  # noqa: E402
 
 ENG = {"tma": aqua.KERNEL_TMA, "ldst": aqua.KERNEL_LDST, "gather_temp": aqua.BASE_GATHER_TEMP,
-       "batch": aqua.BASE_BATCH, "per_chunk": aqua.BASE_PER_CHUNK}
+       "batch": aqua.BASE_BATCH, "per_chunk": aqua.BASE_PER_CHUNK, "ce_host": aqua.KERNEL_CE_HOST}
 
 
 def setup(L, bs, H, D, NB, nblk, host=False):
@@ -445,7 +445,8 @@ def duplex():
     ctx.adopt_blocks(8, perm[nblk:2 * nblk])
     ctx.swap_out([8])
     import time
-    for ctas in (8, 16, 32):
+    for eng, ctas in (("tma", 8), ("tma", 16), ("ce_host", 0)):
+        ctx.set_option(aqua.OPT_KERNEL, ENG[eng] if eng in ENG else aqua.KERNEL_CE_HOST)
         ctx.set_option(aqua.OPT_MAX_CTAS, ctas)
         for pieces in (1, 4, 16):
             ts = []
@@ -457,7 +458,7 @@ def duplex():
                 torch.cuda.synchronize()
                 ts.append((time.perf_counter() - t0) / 2)
             ms = 1e3 * statistics.median(ts)
-            print(json.dumps({"host_exchange_ctas": ctas, "pieces": pieces, "ms": round(ms, 2),
+            print(json.dumps({"host_exchange_engine": eng, "ctas": ctas, "pieces": pieces, "ms": round(ms, 2),
                               "total_GBps": round(2 * nblk * U / ms / 1e6, 1)}), flush=True)
 
 

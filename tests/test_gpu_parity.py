@@ -24,7 +24,7 @@ from gpu_util import Rig
 pytestmark = pytest.mark.gpu
 GOLD = os.path.join(os.path.dirname(__file__), "golden")
 ENGINES = {"tma": aqua.KERNEL_TMA, "ldst": aqua.KERNEL_LDST, "per_chunk": aqua.BASE_PER_CHUNK,
-           "gather_temp": aqua.BASE_GATHER_TEMP, "batch": aqua.BASE_BATCH}
+           "gather_temp": aqua.BASE_GATHER_TEMP, "batch": aqua.BASE_BATCH, "ce_host": aqua.KERNEL_CE_HOST}
 
 
 def _ops(rig, ops, stream=0):
@@ -347,12 +347,16 @@ def test_prefix_cache_bytes(engine):
 
 @pytest.mark.parametrize("layer_group", [1, 3, 4])
 @pytest.mark.parametrize("nblk", [6, 300])
-def test_layerwise_swaps_bytes(layer_group, nblk):
+@pytest.mark.parametrize("where", ["lender", "host_ce"])
+def test_layerwise_swaps_bytes(layer_group, nblk, where):
     """NEXT-3: swap_out/in split into per-layer-group launches give exactly the
     oracle's swap_out/swap_in bytes (inline and staged descriptors, ragged
     last group); each group has its own ticket, in issue order."""
-    rig = Rig(L=4, bs=16, H=2, D=32, NB=2 * nblk + 8, lender_slots=nblk, host_slots=0)
+    rig = Rig(L=4, bs=16, H=2, D=32, NB=2 * nblk + 8, lender_slots=nblk if where == "lender" else 0,
+              host_slots=0 if where == "lender" else nblk)
     c, o = rig.ctx, rig.opool
+    if where == "host_ce":
+        c.set_option(aqua.OPT_KERNEL, aqua.KERNEL_CE_HOST)
     perm = block_permutation(2 * nblk + 8, nblk, seed=9).tolist()
     c.adopt_blocks(3, perm)
     o.adopt_blocks(3, perm)
@@ -433,13 +437,15 @@ def test_multistream_fuzz_equals_sequential(seed):
 
 
 @pytest.mark.parametrize("pieces", [1, 3, 8])
-@pytest.mark.parametrize("arena", ["lender", "host"])
+@pytest.mark.parametrize("arena", ["lender", "host", "host_ce"])
 def test_swap_exchange_bytes(pieces, arena):
     """aqua_swap_exchange == swap_out then swap_in (oracle), byte for byte,
     with the resume on another stream pipelined behind the preemption pieces
     whose blocks it reuses."""
     rig = Rig(L=3, bs=16, H=4, D=64, NB=40, lender_slots=30 if arena == "lender" else 0, host_slots=40)
     c, o = rig.ctx, rig.opool
+    if arena == "host_ce":
+        c.set_option(aqua.OPT_KERNEL, aqua.KERNEL_CE_HOST)
     perm = block_permutation(40, 40, seed=11).tolist()
     for pid, k in ((1, 6), (2, 5), (3, 7), (4, 9)):
         ids, perm = perm[:k], perm[k:]
