@@ -317,6 +317,10 @@ AQUA_API aqua_status aqua_can_access_peer(int device, int peer, int32_t* can);
  * uint64, accumulated with atomicAdd).  Both are stream-ordered. */
 AQUA_API aqua_status aqua_kv_fill_pattern(aqua_ctx* ctx, uint64_t pid, int32_t t0, int32_t t1,
                                  uint64_t seed, aqua_stream_t stream);
+/* The same fill for many prompts in ONE launch (synthetic decode of a whole
+ * iteration): tokens [t0s[i], t1s[i]) of pids[i]. */
+AQUA_API aqua_status aqua_kv_fill_pattern_batch(aqua_ctx* ctx, int32_t n, const uint64_t* pids, const int32_t* t0s,
+                                                const int32_t* t1s, uint64_t seed, aqua_stream_t stream);
 AQUA_API aqua_status aqua_kv_verify_pattern(aqua_ctx* ctx, uint64_t pid, int32_t ntok, uint64_t seed,
                                    aqua_stream_t stream, uint64_t* d_mismatches);
 

@@ -34,7 +34,8 @@ SYMBOLS = [
     "aqua_prefix_drop", "aqua_prefix_query", "aqua_wait", "aqua_sync", "aqua_ticket_done", "aqua_ticket_elapsed",
     "aqua_query", "aqua_counts", "aqua_arena_base", "aqua_set_option", "aqua_get_option",
     "aqua_last_descriptors", "aqua_launch_count", "aqua_ipc_export", "aqua_ipc_import",
-    "aqua_ipc_close", "aqua_ipc_alloc", "aqua_ipc_free", "aqua_can_access_peer", "aqua_kv_fill_pattern", "aqua_kv_verify_pattern",
+    "aqua_ipc_close", "aqua_ipc_alloc", "aqua_ipc_free", "aqua_can_access_peer", "aqua_kv_fill_pattern", "aqua_kv_fill_pattern_batch",
+    "aqua_kv_verify_pattern",
     "aqua_strerror", "aqua_last_error", "aqua_version",
 ]
 
@@ -96,6 +97,7 @@ def _load() -> C.CDLL:
         "aqua_can_access_peer": (C.c_int, [C.c_int, C.c_int, P(I32)]),
         "aqua_kv_fill_pattern": (C.c_int, [VP, U64, I32, I32, U64, VP]),
         "aqua_kv_verify_pattern": (C.c_int, [VP, U64, I32, U64, VP, VP]),
+        "aqua_kv_fill_pattern_batch": (C.c_int, [VP, I32, P(U64), P(I32), P(I32), U64, VP]),
         "aqua_strerror": (C.c_char_p, [C.c_int]),
         "aqua_last_error": (C.c_char_p, [VP]),
         "aqua_version": (C.c_char_p, []),
@@ -336,6 +338,14 @@ class Ctx:
 
     def kv_fill_pattern(self, pid: int, t0: int, t1: int, seed: int, stream: int = 0) -> None:
         self._c(lib.aqua_kv_fill_pattern(self.h, pid, t0, t1, seed, C.c_void_p(stream or None)))
+
+    def kv_fill_pattern_batch(self, pids: Sequence[int], t0s: Sequence[int], t1s: Sequence[int], seed: int,
+                              stream: int = 0) -> None:
+        a = np.ascontiguousarray(pids, dtype=np.uint64)
+        b = np.ascontiguousarray(t0s, dtype=np.int32)
+        e = np.ascontiguousarray(t1s, dtype=np.int32)
+        self._c(lib.aqua_kv_fill_pattern_batch(self.h, len(a), _u64p(a), _i32p(b), _i32p(e), seed,
+                                               C.c_void_p(stream or None)))
 
     def kv_verify_pattern(self, pid: int, ntok: int, seed: int, d_counter: int, stream: int = 0) -> None:
         self._c(lib.aqua_kv_verify_pattern(self.h, pid, ntok, seed, C.c_void_p(stream or None),

@@ -1708,6 +1708,67 @@ static aqua_status pattern_call(aqua_ctx* c, uint64_t pid, int32_t t0, int32_t t
   return AQUA_OK;
 }
 
+aqua_status aqua_kv_fill_pattern_batch(aqua_ctx* c, int32_t n, const uint64_t* pids, const int32_t* t0s,
+                                       const int32_t* t1s, uint64_t seed, aqua_stream_t stream) {
+  if (aqua_status s = precheck(c)) return s;
+  if (n < 0 || (n > 0 && (!pids || !t0s || !t1s))) return fail(c, AQUA_E_INVAL, "bad arguments");
+  if (c->e != 2 || c->D % 8) return fail(c, AQUA_E_INVAL, "pattern needs elem_bytes 2 and head_dim % 8 == 0");
+  if (c->dry) return fail(c, AQUA_E_INVAL, "pattern kernels need a GPU ctx");
+  std::vector<aqua::FillItem> items;
+  std::vector<int32_t> bt_all;
+  std::vector<uint64_t> ts;
+  std::vector<const Prompt*> ps;
+  int64_t units = 0;
+  const int64_t per_tok = int64_t(2) * c->L * c->H * (c->D / 8);
+  for (int32_t i = 0; i < n; ++i) {
+    auto it = c->prompts.find(pids[i]);
+    if (it == c->prompts.end() || it->second.state != AQUA_ST_RESIDENT)
+      return fail(c, AQUA_E_STATE, "pid not resident");
+    const Prompt& p = it->second;
+    if (t0s[i] < 0 || t1s[i] < t0s[i] || static_cast<int64_t>(t1s[i]) > static_cast<int64_t>(p.ids.size()) * c->bs)
+      return fail(c, AQUA_E_INVAL, "token range outside the prompt's blocks");
+    if (t1s[i] == t0s[i]) continue;
+    items.push_back(aqua::FillItem{pids[i], units, static_cast<int32_t>(bt_all.size()), t0s[i], t1s[i]});
+    units += per_tok * (t1s[i] - t0s[i]);
+    bt_all.insert(bt_all.end(), p.ids.begin(), p.ids.end());
+    for (int32_t b : p.ids) ts.push_back(c->btick[b]);
+    ps.push_back(&p);
+  }
+  if (items.empty()) return AQUA_OK;
+  DevGuard g(c->device);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (aqua_status s = wait_all(c, ts, st)) return s;
+  // one upload: [items][block tables]
+  const size_t ib = items.size() * sizeof(aqua::FillItem);
+  std::vector<uint8_t> buf(ib + bt_all.size() * sizeof(int32_t));
+  std::memcpy(buf.data(), items.data(), ib);
+  std::memcpy(buf.data() + ib, bt_all.data(), bt_all.size() * sizeof(int32_t));
+  void* d;
+  if (aqua_status s = stage_upload(c, buf.data(), buf.size(), st, &d)) return s;
+  aqua::FillBatchParams fp{};
+  fp.items = static_cast<const aqua::FillItem*>(d);
+  fp.bt_all = reinterpret_cast<const int32_t*>(static_cast<uint8_t*>(d) + ib);
+  fp.layer_base = c->d_layer_base;
+  fp.P_kv = c->P_kv;
+  fp.P_b = c->P_b;
+  fp.total_units = units;
+  fp.n = static_cast<int32_t>(items.size());
+  fp.L = c->L;
+  fp.bs = c->bs;
+  fp.H = c->H;
+  fp.D = c->D;
+  fp.seed = seed;
+  cudaError_t e = aqua::launch_pattern_fill_batch(fp, c->num_sms, st);
+  if (e != cudaSuccess) return cuda_fail(c, e, "pattern batch launch");
+  c->launches++;
+  uint64_t t = 0;
+  if (aqua_status s = record(c, st, &t)) return s;
+  stage_seal(c, 1, t);
+  for (const Prompt* p : ps)
+    for (int32_t b : p->ids) c->btick[b] = t;
+  return AQUA_OK;
+}
+
 aqua_status aqua_kv_fill_pattern(aqua_ctx* c, uint64_t pid, int32_t t0, int32_t t1, uint64_t seed,
                                  aqua_stream_t stream) {
   return pattern_call(c, pid, t0, t1, seed, stream, nullptr, false);

@@ -48,6 +48,24 @@ struct PatternParams {
   unsigned long long* mismatches;  // verify only
 };
 
+// Batched fill: one launch writes token ranges of many prompts.
+struct FillItem {
+  uint64_t pid;
+  int64_t unit0;               // first work unit of this item (prefix sum)
+  int32_t bt_off;              // offset of its block table in the shared array
+  int32_t t0, t1;
+};
+struct FillBatchParams {
+  const FillItem* items;       // device [n]
+  const int32_t* bt_all;       // device concatenated block tables
+  const uint64_t* layer_base;
+  int64_t P_kv, P_b;
+  int64_t total_units;
+  int32_t n, L, bs, H, D;
+  uint64_t seed;
+};
+cudaError_t launch_pattern_fill_batch(const FillBatchParams& p, int num_sms, cudaStream_t s);
+
 // Launchers: return the CUDA error of the launch (cudaSuccess on success).
 // grid_cap = max CTAs (0 = derived from the SM count).
 cudaError_t launch_swap_tma(const SwapParams& p, Dir dir, int num_sms, int grid_cap, int stages,

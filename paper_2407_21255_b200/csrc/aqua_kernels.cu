@@ -355,6 +355,42 @@ __global__ void __launch_bounds__(256) pattern_kernel(const PatternParams p) {
   }
 }
 
+// Unit = 8 words of one token row, as in pattern_kernel; the item is found
+// by binary search over the items' unit prefix sums.
+__global__ void __launch_bounds__(256) pattern_fill_batch_kernel(const FillBatchParams p) {
+  const int D8 = p.D >> 3;
+  for (int64_t u = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; u < p.total_units;
+       u += int64_t(gridDim.x) * blockDim.x) {
+    int lo = 0, hi = p.n - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (p.items[mid].unit0 <= u) lo = mid; else hi = mid - 1;
+    }
+    const FillItem it = p.items[lo];
+    int64_t r = u - it.unit0;
+    const int d8 = static_cast<int>(r % D8);
+    r /= D8;
+    const int h = static_cast<int>(r % p.H);
+    r /= p.H;
+    const int64_t nt = it.t1 - it.t0;
+    const int t = it.t0 + static_cast<int>(r % nt);
+    r /= nt;
+    const int kv = static_cast<int>(r & 1);
+    const int l = static_cast<int>(r >> 1);
+    const int blk = __ldg(p.bt_all + it.bt_off + t / p.bs);
+    const int row = t % p.bs;
+    uint8_t* a = reinterpret_cast<uint8_t*>(__ldg(p.layer_base + l)) + kv * p.P_kv + int64_t(blk) * p.P_b +
+                 (int64_t(row * p.H + h) * p.D + d8 * 8) * 2;
+    uint32_t w[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const uint64_t d = uint64_t(d8) * 8 + 2 * e;
+      w[e] = word(p.seed, it.pid, t, l, kv, h, d) | (word(p.seed, it.pid, t, l, kv, h, d + 1) << 16);
+    }
+    *reinterpret_cast<uint4*>(a) = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+}
+
 template <typename K>
 int grid_for(int64_t work_units, int per_cta, int num_sms, int ctas_per_sm, int grid_cap) {
   int64_t g = (work_units + per_cta - 1) / per_cta;
@@ -433,6 +469,13 @@ cudaError_t launch_pattern_fill(const PatternParams& p, int num_sms, cudaStream_
   if (total <= 0) return cudaSuccess;
   const int grid = grid_for<void>(total, 256, num_sms, 8, 0);
   pattern_kernel<false><<<grid, 256, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pattern_fill_batch(const FillBatchParams& p, int num_sms, cudaStream_t s) {
+  if (p.total_units <= 0) return cudaSuccess;
+  const int grid = grid_for<void>(p.total_units, 256, num_sms, 8, 0);
+  pattern_fill_batch_kernel<<<grid, 256, 0, s>>>(p);
   return cudaGetLastError();
 }
 

@@ -173,9 +173,9 @@ def run_trace(trace: Sequence[Tuple[int, float, int, int]], ctx: "aqua.Ctx", sch
                     log.append(("alloc", pid, tuple(ids)))
         if record_log:
             log.append(("iter", i, tuple((pid, ctx0, tok) for pid, ctx0, tok, _, _ in work)))
-        if fill_seed is not None:
-            for pid, ctx0, tok, _, _ in work:
-                ctx.kv_fill_pattern(pid, ctx0, ctx0 + tok, fill_seed, decode_stream)
+        if fill_seed is not None and work:
+            ctx.kv_fill_pattern_batch([w[0] for w in work], [w[1] for w in work], [w[1] + w[2] for w in work],
+                                      fill_seed, decode_stream)
         if on_iteration:
             on_iteration(i, work)
         fin, _ = sched.commit()

@@ -513,3 +513,14 @@ def test_library_owned_lender_reclaim_frees_after_ticket():
     c.alloc_blocks(3, 1)          # a later call retires the ticket and frees the zombie arena
     assert c.lend(0, 0, 8 * U) == 8   # re-offer: a fresh library-owned arena
     c.close()
+
+
+def test_pattern_batch_kernel_matches_oracle_words():
+    rig = Rig(L=2, bs=16, H=2, D=64, NB=16, lender_slots=0)
+    for pid, ids in ((3, [6, 2]), (4, [9]), (5, [0, 12, 1])):
+        rig.ctx.adopt_blocks(pid, ids)
+        rig.opool.adopt_blocks(pid, ids)
+    rig.ctx.kv_fill_pattern_batch([3, 4, 5], [5, 0, 17], [27, 16, 40], 99)
+    for pid, t0, t1 in ((3, 5, 27), (4, 0, 16), (5, 17, 40)):
+        opat.write_tokens(rig.opool, pid, t0, t1, 99)
+    rig.assert_bytes_equal("pattern batch")
