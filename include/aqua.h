@@ -99,8 +99,10 @@ enum { AQUA_DRYRUN = -2 }; /* aqua_create device: bookkeeping + descriptors only
 enum { AQUA_ST_RESIDENT = 1, AQUA_ST_SWAPPED = 2 };
 enum { AQUA_LOC_LOCAL = 0, AQUA_LOC_PEER = 1, AQUA_LOC_HOST = 2 };
 
-/* Copy engines for aqua_set_option(AQUA_OPT_KERNEL).  The first three are the
- * product; the last three are baselines kept for measurement only. */
+/* Copy engines for aqua_set_option(AQUA_OPT_KERNEL).  AUTO, TMA, LDST and
+ * CE_HOST are the product; PER_CHUNK, GATHER_TEMP and BATCH are baselines
+ * kept for measurement only.  The environment variable AQUA_KERNEL
+ * (auto | tma | ldst | ce_host) sets a context's initial engine. */
 enum {
   AQUA_KERNEL_AUTO = 0,       /* product default: CE_HOST when every image of the call is in host DRAM,
                                  else TMA (picked from measurements) */

@@ -13,6 +13,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <deque>
 #include <map>
@@ -690,6 +691,14 @@ aqua_status aqua_create(int device, const aqua_kv_layout* lay, aqua_ctx** out) {
       return fail(nullptr, AQUA_E_INVAL, "layer_base must be 16-byte aligned");
 
   aqua_ctx* c = new aqua_ctx();
+  // AQUA_KERNEL=auto|tma|ldst|ce_host overrides the default copy engine
+  // (operational escape hatch; aqua_set_option still wins afterwards)
+  if (const char* k = std::getenv("AQUA_KERNEL")) {
+    const std::string v(k);
+    if (v == "tma") c->kernel = AQUA_KERNEL_TMA;
+    else if (v == "ldst") c->kernel = AQUA_KERNEL_LDST;
+    else if (v == "ce_host") c->kernel = AQUA_KERNEL_CE_HOST;
+  }
   c->device = device;
   c->dry = device == AQUA_DRYRUN;
   c->L = lay->num_layers;
