@@ -275,3 +275,49 @@ def test_fallback_keeps_residents_and_evicts_latest_arrival():
         elif e[0] == "free":
             cur.discard(e[1])
         assert e[0] != "plan"
+
+
+def test_relend_moves_back_lowest_pids_that_fit():
+    """NEXT-1 re-offer (P:1086 'moves the offloaded tensors of the consumer
+    back to the producer's GPU'): after the lender returns, host images move
+    back in ascending pid while they fit, into the lowest slots; CFS resumes
+    with a fresh plan."""
+    tr = [(i, 0.01 * i, 40, 300) for i in range(8)]
+    r = sim.run(tr, sim.SimConfig(NB=40, b=64, lender_slots=400, host_slots=2000, elastic=(2.0, 3.0),
+                                  relend_slots=7))
+    kinds = [e[0] for e in r.log]
+    assert len(r.log[kinds.index("reclaim")][2]) == 3       # three images were on the lender
+    i_rel = kinds.index("relend")
+    assert r.log[i_rel][2] == 7
+    # host images just before the re-offer
+    host, sizes = {}, {}
+    for e in r.log[:i_rel]:
+        if e[0] == "swap_out":
+            for pid, (loc, sl) in zip(e[1], e[2]):
+                host[pid] = loc == 2
+                sizes[pid] = len(sl)
+        elif e[0] == "reclaim":
+            for pid, sl in e[2]:
+                host[pid] = True
+        elif e[0] in ("swap_in",):
+            for pid in e[1]:
+                host.pop(pid, None)
+        elif e[0] == "free":
+            host.pop(e[1], None)
+    on_host = sorted(p for p, h in host.items() if h)
+    want, room = [], 7
+    for p in on_host:
+        if sizes[p] > room:
+            break
+        want.append(p)
+        room -= sizes[p]
+    mig = [e for e in r.log[i_rel:i_rel + 3] if e[0] == "migrate"]
+    assert want and on_host[len(want):], "scenario must move some images back and leave one"
+    if want:
+        assert list(mig[0][2]) == want
+        flat = [s for sl in mig[0][3] for s in sl]
+        assert flat == list(range(len(flat)))           # lowest slots of the fresh lender
+    else:
+        assert not mig
+    assert ("policy", r.log[i_rel][1], "cfs") in r.log[i_rel:i_rel + 4]
+    assert r.log[i_rel + (2 if mig else 1) + 1][0] == "plan"   # a fresh CFS plan right after
