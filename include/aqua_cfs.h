@@ -94,6 +94,47 @@ AQUA_API aqua_status aqua_cfs_advance_to(aqua_cfs* s, double vclock);
 /* Runnable prompts, prompts with KV resident in the pool, iterations run. */
 AQUA_API aqua_status aqua_cfs_stats(aqua_cfs* s, int32_t* runnable, int32_t* resident, int64_t* iterations);
 
+/* ---- Native trace runner (the engine loop of BASELINE configs[2]) --------
+ * Runs a whole request trace through the scheduler and libaqua: admission by
+ * the virtual clock, aqua_cfs_next, swap_out / swap_in (or aqua_swap_exchange
+ * when swap_stream2 is set), block growth, the synthetic decode (pattern
+ * fill of each iteration's tokens, one launch) and frees -- with the same
+ * semantics and call log as the Python driver and the oracle.  Streams: the
+ * swap stream waits for the decode stream before a preemption; the decode
+ * stream waits for each resume's ticket.  With d_mismatches every resumed
+ * prompt is checked against its pattern (restore invariant at full scale). */
+typedef struct {
+  uint64_t pid;
+  double arrival;             /* virtual seconds */
+  int32_t prompt_tokens, output_tokens;
+} aqua_trace_req;
+
+typedef struct {
+  aqua_stream_t decode_stream, swap_stream;
+  aqua_stream_t swap_stream2;  /* non-NULL: reschedules with both lists use aqua_swap_exchange */
+  int32_t exchange_pieces;
+  int32_t fill;                /* 1: write each iteration's KV pattern (needs a GPU ctx) */
+  uint64_t fill_seed;
+  uint64_t* d_mismatches;      /* device counter, or NULL: no verification */
+} aqua_trace_opts;
+
+typedef struct {
+  int64_t iterations, swap_out_calls, swap_in_calls, blocks_out, blocks_in;
+  double vclock;
+} aqua_trace_stats;
+
+/* Call log (optional): int64 records, in order --
+ *   1 plan:     it, nD, D..., nP, (pid, tokens)...
+ *   2 swap_out: n, pids..., then per pid: location, nslots, slots...
+ *   3 swap_in:  n, pids..., then per pid: nblocks, blocks...
+ *   4 alloc:    pid, n, ids...        5 iter: it, n, (pid, ctx0, tokens)...
+ *   6 free:     pid
+ * *log_len = records' total length; AQUA_E_INVAL if log_cap was too small
+ * (the run itself completed). */
+AQUA_API aqua_status aqua_trace_run(aqua_ctx* ctx, aqua_cfs* sched, int32_t n, const aqua_trace_req* reqs,
+                                    const aqua_trace_opts* opts, aqua_trace_stats* stats, int64_t* log_buf,
+                                    int64_t log_cap, int64_t* log_len);
+
 #ifdef __cplusplus
 }
 #endif

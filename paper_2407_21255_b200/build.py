@@ -15,7 +15,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(HERE, "libaqua.so")
-SOURCES = ["aqua_host.cpp", "aqua_kernels.cu", "aqua_cfs.cpp"]
+SOURCES = ["aqua_host.cpp", "aqua_kernels.cu", "aqua_cfs.cpp", "aqua_trace.cpp"]
 HEADERS = [os.path.join(CSRC, "aqua_internal.h"), os.path.join(CSRC, "aqua_idset.h"), os.path.join(INCLUDE, "aqua.h"),
            os.path.join(INCLUDE, "aqua_cfs.h")]
 

@@ -40,6 +40,7 @@ def main():
     ap.add_argument("--check-oracle", action="store_true")
     ap.add_argument("--serial", action="store_true", help="swaps on the decode stream (no overlap), for A8")
     ap.add_argument("--exchange", action="store_true", help="reschedules with both lists use aqua_swap_exchange")
+    ap.add_argument("--native", action="store_true", help="run the loop in C++ (aqua_trace_run)")
     ap.add_argument("--no-verify", action="store_true")
     ap.add_argument("--elastic", default="", help="t_reclaim,t_relend (virtual s): NEXT-1 lender reclaim + FCFS "
                                                    "fallback, then re-offer")
@@ -143,10 +144,20 @@ def main():
     if args.elastic:
         tr_, tl_ = (float(x) for x in args.elastic.split(","))
         elastic = {"t_reclaim": tr_, "t_relend": tl_, "relend": (lend_dev, lend_ptr, lend_bytes)}
-    log, st = run_trace(trace, ctx, sched, fill_seed=SEED, decode_stream=dec.cuda_stream,
-                        swap_stream=swp.cuda_stream, on_iteration=on_iteration, stream_sync=stream_sync,
-                        on_swap=on_swap, record_log=args.check_oracle, elastic=elastic,
-                        exchange_stream=swp2.cuda_stream if swp2 is not None else None)
+    if args.native:
+        from paper_2407_21255_b200.cfs import run_trace_native
+        if elastic or args.proxy_gb:
+            raise SystemExit("--native runs the plain trace (no elastic events, no decode proxy)")
+        log, st = run_trace_native(trace, ctx, sched, decode_stream=dec.cuda_stream, swap_stream=swp.cuda_stream,
+                                   swap_stream2=swp2.cuda_stream if swp2 is not None else 0, fill_seed=SEED,
+                                   d_mismatches=0 if args.no_verify else mism.data_ptr(),
+                                   record_log=args.check_oracle)
+        st["swap_calls"] = []
+    else:
+        log, st = run_trace(trace, ctx, sched, fill_seed=SEED, decode_stream=dec.cuda_stream,
+                            swap_stream=swp.cuda_stream, on_iteration=on_iteration, stream_sync=stream_sync,
+                            on_swap=on_swap, record_log=args.check_oracle, elastic=elastic,
+                            exchange_stream=swp2.cuda_stream if swp2 is not None else None)
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0
     launches = ctx.launch_count() - n0

@@ -368,3 +368,19 @@ def test_exchange_driver_call_log_matches_oracle():
     c.lend(aqua.HOST, FAKE * 3, 400 * c.U)
     log, st = run_trace(tr, c, Scheduler(NB=NB, bs=16), exchange_stream=0)
     assert log == o.log
+
+
+@pytest.mark.parametrize("exchange", [False, True])
+def test_native_trace_runner_matches_oracle(exchange):
+    """aqua_trace_run (the engine loop in C++) reproduces the oracle's call
+    log on the full C3 trace (dry-run ctx: bookkeeping only)."""
+    from paper_2407_21255_b200.cfs import run_trace_native
+    tr = burst_trace(seed=1)
+    NB = 4152
+    o = osim.run(tr, osim.SimConfig(NB=NB, lender_slots=32768, host_slots=32768))
+    c = aqua.Ctx(aqua.DRYRUN, 1, 16, 1, 8, 2, NB, [FAKE])
+    c.lend(0, FAKE * 2, 32768 * c.U)
+    c.lend(aqua.HOST, FAKE * 3, 32768 * c.U)
+    log, st = run_trace_native(tr, c, Scheduler(NB=NB, bs=16), swap_stream2=1 if exchange else 0)
+    assert st["iters"] == o.iters and st["blocks_out"] == o.blocks_out
+    assert log == o.log
