@@ -462,6 +462,57 @@ def duplex():
                               "total_GBps": round(2 * nblk * U / ms / 1e6, 1)}), flush=True)
 
 
+def layer_overlap():
+    """NEXT-3 in use: a decode that walks the layers of a resumed prompt.
+    (a) wait for the whole resume, then run 32 per-layer decode steps;
+    (b) resume with per-layer tickets and start layer l as soon as ticket l
+    completes.  Decode proxy per layer: a reduction over `per_layer_mb` of
+    HBM (a layer's weights).  Lender in HBM and host DRAM."""
+    L, bs, H, D, NB, nblk = 32, 16, 8, 128, 4096, 2048
+    per_layer_mb = 512
+    w = torch.ones(L * per_layer_mb * (1 << 20) // 8, dtype=torch.int64, device="cuda").view(L, -1)
+    out = torch.empty((), dtype=torch.int64, device="cuda")
+    for where in ("self", "host"):
+        ctx, layers, arena, U = setup(L, bs, H, D, NB, nblk, host=(where == "host"))
+        dec, swp = torch.cuda.Stream(), torch.cuda.Stream()
+
+        def decode_layer(l):
+            with torch.cuda.stream(dec):
+                torch.sum(w[l], dim=0, out=out)
+
+        res = {}
+        for mode in ("whole", "layerwise", "compute_only"):
+            ts = []
+            for rep in range(4):
+                ctx.swap_out([7], swp.cuda_stream)
+                torch.cuda.synchronize()
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(dec)
+                swp.wait_stream(dec)
+                if mode == "whole":
+                    _, tk = ctx.swap_in([7], swp.cuda_stream)
+                    ctx.wait(tk, dec.cuda_stream)
+                    for l in range(L):
+                        decode_layer(l)
+                elif mode == "layerwise":
+                    _, tks = ctx.swap_in_layers([7], 1, swp.cuda_stream)
+                    for l in range(L):
+                        ctx.wait(tks[l], dec.cuda_stream)
+                        decode_layer(l)
+                else:
+                    _, tk = ctx.swap_in([7], swp.cuda_stream)
+                    for l in range(L):
+                        decode_layer(l)
+                b.record(dec)
+                torch.cuda.synchronize()
+                ts.append(a.elapsed_time(b))
+            res[mode] = round(statistics.median(ts[1:]), 3)
+        print(json.dumps({"layer_overlap": where, "per_layer_decode_MB": per_layer_mb, "ms": res}), flush=True)
+        ctx.close()
+        del arena, layers
+        torch.cuda.empty_cache()
+
+
 def stages():
     L, bs, H, D, NB, nblk = 32, 16, 8, 128, 4096, 2048
     ctx, layers, arena, U = setup(L, bs, H, D, NB, nblk)
@@ -517,6 +568,8 @@ if __name__ == "__main__":
         prefix()
     elif what == "migrate":
         migrate()
+    elif what == "layer_overlap":
+        layer_overlap()
     elif what == "duplex":
         duplex()
     elif what == "exchange":
