@@ -5,7 +5,7 @@
  * data path of arXiv 2407.21255 ("Aqua").
  *
  * Citations: P:n = line n of the paper text, S:n = line n of
- * SPEC.md; the section is named beside each.  Readings R1..R17 are listed
+ * SPEC.md; the section is named beside each.  Readings R1..R18 are listed
  * in DESIGN.md.
  *
  * The operations (paper):
