@@ -8,7 +8,7 @@
  * prompts with the least tokens generated, leftover d slots to the prefill
  * prompts, stop when memory is exhausted; reschedule every k iterations or
  * when a request completes, paging out the prompts not in the next batch and
- * paging in the prompts not on the GPU.  Readings R8-R16:
+ * paging in the prompts not on the GPU.  Readings R8-R18:
  * ties (arrival, id); memory test ceil((ctx + t) / bs) blocks per prompt
  * summed <= num_blocks; prefill filled before decode; a non-fitting prompt
  * stops its walk; extra reschedule when the plan's next iteration no longer

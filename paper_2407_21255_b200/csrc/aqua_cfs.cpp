@@ -3,7 +3,7 @@
 //
 // Paper, Sec. 7 "Aqua's batch partitioning algorithm" and the
 // reschedule rule; FCFS baseline per SPEC S:297-305.  Readings
-// R8-R16 in DESIGN.md.  Written independently of the CPU oracle (oracle/cfs.py,
+// R8-R18 in DESIGN.md.  Written independently of the CPU oracle (oracle/cfs.py,
 // oracle/sim.py); tests compare the two call logs exactly.
 #include "aqua_cfs.h"
 

@@ -6,7 +6,7 @@
 // P:737-756 (producer first, DRAM fallback), Sec. 5 P:529-534 (one producer
 // per consumer), Sec. 7 P:836-853 (page out / page in, gather / scatter),
 // P:855-857 (location query), Sec. 8 P:864-866 (library surface, CUDA
-// gather kernel in vLLM v0.5.3, safe transfers).  Readings R1..R17:
+// gather kernel in vLLM v0.5.3, safe transfers).  Readings R1..R18:
 // DESIGN.md.  This file never does data movement on the CPU: with no usable
 // GPU every data call fails (only AQUA_DRYRUN contexts run without one).
 #include "aqua.h"
