@@ -77,6 +77,7 @@ struct aqua_ctx {
   int max_ctas = 0;
   int tma_piece = 0;
   int tma_stages = 0;
+  int ldst_variant = 2;
   int num_sms = 148;
   uint64_t* d_layer_base = nullptr;
   // pinned -> device descriptor staging ring
@@ -462,7 +463,8 @@ aqua_status run_copy(aqua_ctx* c, const std::vector<Desc>& ds, aqua::Dir dir, cu
       p.group = 1;
       p.npieces = static_cast<int32_t>((c->S + 4095) / 4096);
       p.nitems = p.ndesc * nc * p.npieces;
-      e = aqua::launch_swap_ldst(p, dir, c->num_sms, all_host && cap == kHostCtas ? 2 * kHostCtas : cap, st, &ctas);
+      e = aqua::launch_swap_ldst(p, dir, c->num_sms, all_host && cap == kHostCtas ? 2 * kHostCtas : cap, st, &ctas,
+                                 c->ldst_variant);
     }
     if (e != cudaSuccess) return cuda_fail(c, e, "swap kernel launch");
     c->launches++;
@@ -541,14 +543,14 @@ aqua_status run_copy(aqua_ctx* c, const std::vector<Desc>& ds, aqua::Dir dir, cu
     };
     int ctas = 0;
     if (dir == aqua::kOut) {
-      cudaError_t e = aqua::launch_swap_ldst(p, aqua::kOut, c->num_sms, c->max_ctas, st, &ctas);
+      cudaError_t e = aqua::launch_swap_ldst(p, aqua::kOut, c->num_sms, c->max_ctas, st, &ctas, c->ldst_variant);
       if (e != cudaSuccess) return cuda_fail(c, e, "gather kernel launch");
       c->launches++;
       return runs(true);
     }
     aqua_status rs = runs(false);
     if (rs) return rs;
-    cudaError_t e = aqua::launch_swap_ldst(p, aqua::kIn, c->num_sms, c->max_ctas, st, &ctas);
+    cudaError_t e = aqua::launch_swap_ldst(p, aqua::kIn, c->num_sms, c->max_ctas, st, &ctas, c->ldst_variant);
     if (e != cudaSuccess) return cuda_fail(c, e, "scatter kernel launch");
     c->launches++;
     return AQUA_OK;
@@ -1568,6 +1570,10 @@ aqua_status aqua_set_option(aqua_ctx* c, int32_t opt, int64_t v) {
       if (v != 0 && v != 1) return fail(c, AQUA_E_INVAL, "timing");
       c->timing = v != 0;
       return AQUA_OK;
+    case AQUA_OPT_LDST_VARIANT:
+      if (v < 0 || v > 2) return fail(c, AQUA_E_INVAL, "ldst variant");
+      c->ldst_variant = static_cast<int>(v);
+      return AQUA_OK;
   }
   return fail(c, AQUA_E_INVAL, "unknown option");
 }
@@ -1580,6 +1586,7 @@ aqua_status aqua_get_option(aqua_ctx* c, int32_t opt, int64_t* v) {
     case AQUA_OPT_TMA_PIECE: *v = c->tma_piece; return AQUA_OK;
     case AQUA_OPT_TMA_STAGES: *v = c->tma_stages; return AQUA_OK;
     case AQUA_OPT_TIMING: *v = c->timing; return AQUA_OK;
+    case AQUA_OPT_LDST_VARIANT: *v = c->ldst_variant; return AQUA_OK;
   }
   return fail(c, AQUA_E_INVAL, "unknown option");
 }

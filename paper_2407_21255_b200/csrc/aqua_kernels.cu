@@ -267,29 +267,74 @@ __global__ void __launch_bounds__(32) swap_tma_kernel(const __grid_constant__ Sw
 // ------------------------------------------------------------ LDG/STG kernel
 // Grid-stride over items of up to 512*UNROLL bytes; a warp moves one item
 // with UNROLL independent 16-byte loads per lane in flight.
-template <Dir D, int UNROLL>
+__device__ __forceinline__ int4 ld_plain(const void* p) {
+  int4 r;
+  asm volatile("ld.global.v4.s32 {%0, %1, %2, %3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void st_plain(void* p, const int4& v) {
+  asm volatile("st.global.v4.s32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
+
+// V selects the access flavour (tuning experiments, AQUA_OPT_LDST_VARIANT):
+// 0 streaming hints (ld.nc.L1::no_allocate.L2::256B / st.L1::no_allocate);
+// 1 plain ld/st; 2 streaming hints + the next item's loads issued before the
+// current item's stores (software pipelined).
+template <Dir D, int UNROLL, int V>
 __global__ void __launch_bounds__(256) swap_ldst_kernel(const __grid_constant__ SwapParams p) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
-  for (int64_t it = warp; it < p.nitems; it += nwarps) {
+  auto load = [&](int64_t it, int4* v, uint8_t** dst, int* nvec) {
     Cursor cu;
     cu.init(it, p);
     const uint8_t* src;
-    uint8_t* dst;
     uint32_t bytes;
-    item_addrs<D>(p, desc_at(p, cu.j), cu.c, cu.q, src, dst, bytes);
-    const int nvec = static_cast<int>(bytes >> 4);
-    int4 v[UNROLL];
+    item_addrs<D>(p, desc_at(p, cu.j), cu.c, cu.q, src, *dst, bytes);
+    *nvec = static_cast<int>(bytes >> 4);
 #pragma unroll
     for (int u = 0; u < UNROLL; ++u) {
       const int idx = u * 32 + lane;
-      if (idx < nvec) v[u] = ld_stream(src + size_t(idx) * 16);
+      if (idx < *nvec) v[u] = V == 1 ? ld_plain(src + size_t(idx) * 16) : ld_stream(src + size_t(idx) * 16);
     }
+  };
+  auto store = [&](const int4* v, uint8_t* dst, int nvec) {
 #pragma unroll
     for (int u = 0; u < UNROLL; ++u) {
       const int idx = u * 32 + lane;
-      if (idx < nvec) st_stream(dst + size_t(idx) * 16, v[u]);
+      if (idx < nvec) {
+        if (V == 1)
+          st_plain(dst + size_t(idx) * 16, v[u]);
+        else
+          st_stream(dst + size_t(idx) * 16, v[u]);
+      }
+    }
+  };
+  if (V != 2) {
+    for (int64_t it = warp; it < p.nitems; it += nwarps) {
+      int4 v[UNROLL];
+      uint8_t* dst;
+      int nvec;
+      load(it, v, &dst, &nvec);
+      store(v, dst, nvec);
+    }
+  } else {
+    int4 a[UNROLL], b[UNROLL];
+    uint8_t *da = nullptr, *db = nullptr;
+    int na = 0, nb = 0;
+    int64_t it = warp;
+    if (it < p.nitems) load(it, a, &da, &na);
+    while (it < p.nitems) {
+      const int64_t nx = it + nwarps;
+      if (nx < p.nitems) load(nx, b, &db, &nb);
+      store(a, da, na);
+      it = nx;
+      if (it >= p.nitems) break;
+      const int64_t ny = it + nwarps;
+      if (ny < p.nitems) load(ny, a, &da, &na);
+      store(b, db, nb);
+      it = ny;
     }
   }
 }
@@ -450,16 +495,28 @@ cudaError_t launch_swap_tma(const SwapParams& p, Dir dir, int num_sms, int grid_
   return cudaGetLastError();
 }
 
-cudaError_t launch_swap_ldst(const SwapParams& p, Dir dir, int num_sms, int grid_cap, cudaStream_t s,
-                             int* ctas_used) {
-  if (p.nitems == 0) return cudaSuccess;
-  const int grid = grid_for<void>(p.nitems, 8, num_sms, 4, grid_cap);
+template <int V>
+void launch_ldst_v(const SwapParams& p, Dir dir, int grid, cudaStream_t s) {
   if (dir == kOut)
-    swap_ldst_kernel<kOut, 8><<<grid, 256, 0, s>>>(p);
+    swap_ldst_kernel<kOut, 8, V><<<grid, 256, 0, s>>>(p);
   else if (dir == kIn)
-    swap_ldst_kernel<kIn, 8><<<grid, 256, 0, s>>>(p);
+    swap_ldst_kernel<kIn, 8, V><<<grid, 256, 0, s>>>(p);
   else
-    swap_ldst_kernel<kMig, 8><<<grid, 256, 0, s>>>(p);
+    swap_ldst_kernel<kMig, 8, V><<<grid, 256, 0, s>>>(p);
+}
+
+cudaError_t launch_swap_ldst(const SwapParams& p, Dir dir, int num_sms, int grid_cap, cudaStream_t s,
+                             int* ctas_used, int variant) {
+  if (p.nitems == 0) return cudaSuccess;
+  // variant 2 (software pipelined, the default) is best with one 256-thread
+  // CTA per SM: 6,624 / 6,572 GB/s on C2 (profiles/r01_ldst_variants.jsonl)
+  const int grid = grid_for<void>(p.nitems, 8, num_sms, variant == 2 ? 1 : 4, grid_cap);
+  if (variant == 1)
+    launch_ldst_v<1>(p, dir, grid, s);
+  else if (variant == 2)
+    launch_ldst_v<2>(p, dir, grid, s);
+  else
+    launch_ldst_v<0>(p, dir, grid, s);
   if (ctas_used) *ctas_used = grid;
   return cudaGetLastError();
 }

@@ -513,6 +513,21 @@ def layer_overlap():
         torch.cuda.empty_cache()
 
 
+def ldst_variants():
+    """LDST engine flavours (AQUA_OPT_LDST_VARIANT) on C2, self-lender."""
+    L, bs, H, D, NB, nblk = 32, 16, 8, 128, 4096, 2048
+    ctx, layers, arena, U = setup(L, bs, H, D, NB, nblk)
+    s = torch.cuda.Stream()
+    ctx.set_option(aqua.OPT_KERNEL, aqua.KERNEL_LDST)
+    for v in (0, 1, 2):
+        for ctas in (0, 148, 296):
+            ctx.set_option(aqua.OPT_LDST_VARIANT, v)
+            ctx.set_option(aqua.OPT_MAX_CTAS, ctas)
+            o, i = time_tickets(ctx, 5, s)
+            print(json.dumps({"ldst_variant": v, "ctas": ctas or 592, "out_hbm_GBps": round(2 * nblk * U / o / 1e6, 1),
+                              "in_hbm_GBps": round(2 * nblk * U / i / 1e6, 1)}), flush=True)
+
+
 def stages():
     L, bs, H, D, NB, nblk = 32, 16, 8, 128, 4096, 2048
     ctx, layers, arena, U = setup(L, bs, H, D, NB, nblk)
@@ -568,6 +583,8 @@ if __name__ == "__main__":
         prefix()
     elif what == "migrate":
         migrate()
+    elif what == "ldst_variants":
+        ldst_variants()
     elif what == "layer_overlap":
         layer_overlap()
     elif what == "duplex":
