@@ -384,3 +384,35 @@ def test_native_trace_runner_matches_oracle(exchange):
     log, st = run_trace_native(tr, c, Scheduler(NB=NB, bs=16), swap_stream2=1 if exchange else 0)
     assert st["iters"] == o.iters and st["blocks_out"] == o.blocks_out
     assert log == o.log
+
+
+def test_create_validates_layout():
+    """aqua_create rejects layouts the kernels cannot move exactly (S or a
+    stride not a multiple of 16, overlapping chunks, misaligned bases)."""
+    ok = aqua.Ctx(aqua.DRYRUN, 2, 16, 2, 64, 2, 8, [FAKE, FAKE + (1 << 30)])
+    ok.close()
+    bad = [
+        dict(L=1, bs=1, H=1, D=4, e=2, NB=4, ptrs=[FAKE]),                                   # S = 8 bytes
+        dict(L=1, bs=16, H=1, D=8, e=2, NB=4, ptrs=[FAKE + 8]),                              # misaligned base
+        dict(L=1, bs=16, H=1, D=8, e=2, NB=4, ptrs=[FAKE], kv=16, blk=256),                  # K/V planes overlap
+        dict(L=1, bs=16, H=1, D=8, e=2, NB=4, ptrs=[FAKE], kv=0, blk=128),                   # blocks overlap
+        dict(L=0, bs=16, H=1, D=8, e=2, NB=4, ptrs=[]),
+        dict(L=1, bs=16, H=1, D=8, e=2, NB=0, ptrs=[FAKE]),
+    ]
+    for b in bad:
+        with pytest.raises(aqua.AquaError) as e:
+            aqua.Ctx(aqua.DRYRUN, b["L"], b["bs"], b["H"], b["D"], b["e"], b["NB"], b["ptrs"],
+                     b.get("kv", 0), b.get("blk", 0))
+        assert e.value.code == aqua.E_INVAL
+    c = aqua.Ctx(aqua.DRYRUN, 1, 16, 1, 8, 2, 4, [FAKE])
+    for opt, val in ((aqua.OPT_KERNEL, 99), (aqua.OPT_TMA_PIECE, 17), (aqua.OPT_TMA_STAGES, 1),
+                     (aqua.OPT_MAX_CTAS, -1), (aqua.OPT_TIMING, 2), (aqua.OPT_LDST_VARIANT, 3), (77, 0)):
+        with pytest.raises(aqua.AquaError):
+            c.set_option(opt, val)
+    with pytest.raises(aqua.AquaError) as e:
+        c.lend(0, FAKE + 8, 4096)                                                             # misaligned arena
+    assert e.value.code == aqua.E_INVAL
+    c.lend(0, FAKE * 2, 10 * c.U)
+    with pytest.raises(aqua.AquaError) as e:
+        c.lend(0, FAKE * 3, 10 * c.U)                                                         # one GPU lender
+    assert e.value.code == aqua.E_INVAL

@@ -524,3 +524,17 @@ def test_pattern_batch_kernel_matches_oracle_words():
     for pid, t0, t1 in ((3, 5, 27), (4, 0, 16), (5, 17, 40)):
         opat.write_tokens(rig.opool, pid, t0, t1, 99)
     rig.assert_bytes_equal("pattern batch")
+
+
+@pytest.mark.parametrize("engine", ["tma", "ldst"])
+def test_many_small_blocks_whole_buffer(engine):
+    """Scale edge: 131,072 blocks of S = 256 B (100,000-block prompt, 800 KB of
+    staged descriptors, slot ids > 2^16), whole pool / arena compared with
+    the oracle after swap_out and after swap_in into a fragmented pool."""
+    NB = 131072
+    rig = Rig(L=1, bs=16, H=1, D=8, NB=NB, lender_slots=100000, host_slots=0)
+    c, o = rig.ctx, rig.opool
+    c.set_option(aqua.OPT_KERNEL, ENGINES[engine])
+    perm = block_permutation(NB, NB, seed=13).tolist()
+    _ops(rig, [("adopt", (1, perm[:100000])), ("adopt", (2, perm[100000:100500])), ("out", [1]),
+               ("alloc", (3, 20000)), ("in", [1])])
