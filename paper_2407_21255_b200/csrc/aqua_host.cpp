@@ -78,6 +78,7 @@ struct aqua_ctx {
   int tma_piece = 0;
   int tma_stages = 0;
   int ldst_variant = 2;
+  int tma_variant = 0;
   int num_sms = 148;
   uint64_t* d_layer_base = nullptr;
   // pinned -> device descriptor staging ring
@@ -457,7 +458,7 @@ aqua_status run_copy(aqua_ctx* c, const std::vector<Desc>& ds, aqua::Dir dir, cu
       p.piece = piece;
       p.npieces = static_cast<int32_t>((c->S + piece - 1) / piece);
       p.nitems = p.ndesc * nc * p.npieces;
-      e = aqua::launch_swap_tma(p, dir, c->num_sms, cap, c->tma_stages, st, &ctas);
+      e = aqua::launch_swap_tma(p, dir, c->num_sms, cap, c->tma_stages, st, &ctas, c->tma_variant);
     } else {
       p.piece = 4096;
       p.group = 1;
@@ -1574,6 +1575,10 @@ aqua_status aqua_set_option(aqua_ctx* c, int32_t opt, int64_t v) {
       if (v < 0 || v > 2) return fail(c, AQUA_E_INVAL, "ldst variant");
       c->ldst_variant = static_cast<int>(v);
       return AQUA_OK;
+    case AQUA_OPT_TMA_VARIANT:
+      if (v < 0 || v > 1) return fail(c, AQUA_E_INVAL, "tma variant");
+      c->tma_variant = static_cast<int>(v);
+      return AQUA_OK;
   }
   return fail(c, AQUA_E_INVAL, "unknown option");
 }
@@ -1587,6 +1592,7 @@ aqua_status aqua_get_option(aqua_ctx* c, int32_t opt, int64_t* v) {
     case AQUA_OPT_TMA_STAGES: *v = c->tma_stages; return AQUA_OK;
     case AQUA_OPT_TIMING: *v = c->timing; return AQUA_OK;
     case AQUA_OPT_LDST_VARIANT: *v = c->ldst_variant; return AQUA_OK;
+    case AQUA_OPT_TMA_VARIANT: *v = c->tma_variant; return AQUA_OK;
   }
   return fail(c, AQUA_E_INVAL, "unknown option");
 }

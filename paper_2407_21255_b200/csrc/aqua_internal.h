@@ -69,7 +69,7 @@ cudaError_t launch_pattern_fill_batch(const FillBatchParams& p, int num_sms, cud
 // Launchers: return the CUDA error of the launch (cudaSuccess on success).
 // grid_cap = max CTAs (0 = derived from the SM count).
 cudaError_t launch_swap_tma(const SwapParams& p, Dir dir, int num_sms, int grid_cap, int stages,
-                            cudaStream_t s, int* ctas_used);
+                            cudaStream_t s, int* ctas_used, int variant = 0);
 cudaError_t launch_swap_ldst(const SwapParams& p, Dir dir, int num_sms, int grid_cap,
                              cudaStream_t s, int* ctas_used, int variant = 0);
 cudaError_t launch_pattern_fill(const PatternParams& p, int num_sms, cudaStream_t s);

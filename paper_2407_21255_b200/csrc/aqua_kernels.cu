@@ -36,6 +36,9 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred p;\n"
@@ -264,6 +267,103 @@ __global__ void __launch_bounds__(32) swap_tma_kernel(const __grid_constant__ Sw
   bulk_wait<0>();
 }
 
+// Warp-specialised variant: warp 0 (one lane) only issues loads, warp 1 (one
+// lane) only issues stores; "full" mbarriers carry the bulk-load bytes and
+// "empty" mbarriers hand a stage back once its store has read it, so loads
+// never wait behind a store's completion check.
+template <Dir D>
+__global__ void __launch_bounds__(64) swap_tma_ws_kernel(const __grid_constant__ SwapParams p, const int stages) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int64_t stage_bytes = int64_t(p.piece) * p.group;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + size_t(stages) * stage_bytes);
+  uint64_t* empty = full + stages;
+  const int64_t G = gridDim.x, b = blockIdx.x;
+  const int64_t i0 = p.nitems * b / G, i1 = p.nitems * (b + 1) / G;
+  if (i1 <= i0) return;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if ((threadIdx.x & 31) != 0) return;
+  const uint64_t pol = policy_evict_first();
+  Unit u;
+  {
+    Cursor cu;
+    cu.init(i0, p);
+    u = Unit{cu.j, cu.c, cu.q, i1 - i0};
+  }
+  int stage = 0;
+  uint32_t ph = 0;
+  if (threadIdx.x == 0) {                    // producer: bulk loads
+    while (u.left > 0) {
+      mbar_wait(&empty[stage], ph ^ 1u);     // fresh barriers pass at once
+      const int k = unit_len(p, u);
+      const Desc d = desc_at(p, u.j);
+      uint8_t* buf = smem + size_t(stage) * stage_bytes;
+      const uint8_t* src;
+      uint8_t* dst;
+      uint32_t bytes;
+      item_addrs<D>(p, d, u.c, u.q, src, dst, bytes);
+      if (k == 1) {
+        mbar_expect_tx(&full[stage], bytes);
+        bulk_g2s(buf, src, bytes, &full[stage], pol);
+      } else if (D != kOut) {
+        mbar_expect_tx(&full[stage], bytes * k);
+        bulk_g2s(buf, src, bytes * k, &full[stage], pol);
+      } else {
+        mbar_expect_tx(&full[stage], bytes * k);
+        for (int t = 0; t < k; ++t) {
+          item_addrs<D>(p, d, u.c + t, 0, src, dst, bytes);
+          bulk_g2s(buf + size_t(t) * bytes, src, bytes, &full[stage], pol);
+        }
+      }
+      unit_next(p, u, k);
+      if (++stage == stages) {
+        stage = 0;
+        ph ^= 1u;
+      }
+    }
+  } else {                                    // consumer: bulk stores
+    int prev = -1;
+    while (u.left > 0) {
+      mbar_wait(&full[stage], ph);
+      const int k = unit_len(p, u);
+      const Desc d = desc_at(p, u.j);
+      uint8_t* buf = smem + size_t(stage) * stage_bytes;
+      const uint8_t* src;
+      uint8_t* dst;
+      uint32_t bytes;
+      item_addrs<D>(p, d, u.c, u.q, src, dst, bytes);
+      if (k == 1) {
+        bulk_s2g(dst, buf, bytes, pol);
+      } else if (D != kIn) {
+        bulk_s2g(dst, buf, bytes * k, pol);
+      } else {
+        for (int t = 0; t < k; ++t) {
+          item_addrs<D>(p, d, u.c + t, 0, src, dst, bytes);
+          bulk_s2g(dst, buf + size_t(t) * bytes, bytes, pol);
+        }
+      }
+      bulk_commit();
+      if (prev >= 0) {
+        bulk_wait_read<1>();                  // the previous unit's store has read its stage
+        mbar_arrive(&empty[prev]);
+      }
+      prev = stage;
+      unit_next(p, u, k);
+      if (++stage == stages) {
+        stage = 0;
+        ph ^= 1u;
+      }
+    }
+    bulk_wait<0>();
+  }
+}
+
 // ------------------------------------------------------------ LDG/STG kernel
 // Grid-stride over items of up to 512*UNROLL bytes; a warp moves one item
 // with UNROLL independent 16-byte loads per lane in flight.
@@ -451,7 +551,7 @@ int grid_for(int64_t work_units, int per_cta, int num_sms, int ctas_per_sm, int 
 int tma_smem_bytes(int piece, int stages) { return piece * stages + 8 * stages; }
 
 cudaError_t launch_swap_tma(const SwapParams& p, Dir dir, int num_sms, int grid_cap, int stages_opt,
-                            cudaStream_t s, int* ctas_used) {
+                            cudaStream_t s, int* ctas_used, int variant) {
   if (p.nitems == 0) return cudaSuccess;
   // One CTA per SM and a shallow ring: 3 x 32 KiB or 64 KiB of loads in
   // flight per SM measured best for HBM on B200 (profiles/r01_stages.jsonl);
@@ -470,27 +570,42 @@ cudaError_t launch_swap_tma(const SwapParams& p, Dir dir, int num_sms, int grid_
     stages = std::max(stages, 3);
   }
   stages = std::max(2, std::min(stages, 32));
-  while (stages > 2 && tma_smem_bytes(stage_bytes, stages) > 227 * 1024) --stages;
-  const int smem = tma_smem_bytes(stage_bytes, stages);
+  const int bar_extra = variant == 1 ? 8 : 0;   // the "empty" barriers of the warp-specialised variant
+  while (stages > 2 && tma_smem_bytes(stage_bytes, stages) + bar_extra * stages > 227 * 1024) --stages;
+  const int smem = tma_smem_bytes(stage_bytes, stages) + bar_extra * stages;
   // the opt-in smem attribute is per device; remember the largest set so far
-  static thread_local int set_smem[3][64] = {};
+  static thread_local int set_smem[2][3][64] = {};
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
-  int& have = set_smem[dir][dev & 63];
+  const int vi = variant == 1 ? 1 : 0;
+  int& have = set_smem[vi][dir][dev & 63];
   if (smem > have) {
-    e = cudaFuncSetAttribute(dir == kOut ? swap_tma_kernel<kOut>
-                             : dir == kIn ? swap_tma_kernel<kIn> : swap_tma_kernel<kMig>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (vi)
+      e = cudaFuncSetAttribute(dir == kOut ? swap_tma_ws_kernel<kOut>
+                               : dir == kIn ? swap_tma_ws_kernel<kIn> : swap_tma_ws_kernel<kMig>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    else
+      e = cudaFuncSetAttribute(dir == kOut ? swap_tma_kernel<kOut>
+                               : dir == kIn ? swap_tma_kernel<kIn> : swap_tma_kernel<kMig>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e != cudaSuccess) return e;
     have = 227 * 1024;
   }
-  if (dir == kOut)
+  if (vi) {
+    if (dir == kOut)
+      swap_tma_ws_kernel<kOut><<<grid, 64, smem, s>>>(p, stages);
+    else if (dir == kIn)
+      swap_tma_ws_kernel<kIn><<<grid, 64, smem, s>>>(p, stages);
+    else
+      swap_tma_ws_kernel<kMig><<<grid, 64, smem, s>>>(p, stages);
+  } else if (dir == kOut) {
     swap_tma_kernel<kOut><<<grid, 32, smem, s>>>(p, stages);
-  else if (dir == kIn)
+  } else if (dir == kIn) {
     swap_tma_kernel<kIn><<<grid, 32, smem, s>>>(p, stages);
-  else
+  } else {
     swap_tma_kernel<kMig><<<grid, 32, smem, s>>>(p, stages);
+  }
   if (ctas_used) *ctas_used = grid;
   return cudaGetLastError();
 }

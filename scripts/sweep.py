@@ -528,6 +528,32 @@ def ldst_variants():
                               "in_hbm_GBps": round(2 * nblk * U / i / 1e6, 1)}), flush=True)
 
 
+def tma_variants():
+    """TMA engine: one issuing thread (0) vs warp-specialised load/store warps (1),
+    C2 self-lender, across ring depths and SM caps; LDST v2 for reference."""
+    L, bs, H, D, NB, nblk = 32, 16, 8, 128, 4096, 2048
+    ctx, layers, arena, U = setup(L, bs, H, D, NB, nblk)
+    s = torch.cuda.Stream()
+    for v in (0, 1):
+        for st in (0, 2, 3, 4, 6):
+            for ctas in (0, 74, 32):
+                ctx.set_option(aqua.OPT_KERNEL, aqua.KERNEL_TMA)
+                ctx.set_option(aqua.OPT_TMA_VARIANT, v)
+                ctx.set_option(aqua.OPT_TMA_STAGES, st)
+                ctx.set_option(aqua.OPT_MAX_CTAS, ctas)
+                o, i = time_tickets(ctx, 5, s)
+                print(json.dumps({"tma_variant": v, "stages": st or "auto", "ctas": ctas or 148,
+                                  "out_hbm_GBps": round(2 * nblk * U / o / 1e6, 1),
+                                  "in_hbm_GBps": round(2 * nblk * U / i / 1e6, 1)}), flush=True)
+    ctx.set_option(aqua.OPT_TMA_STAGES, 0)
+    ctx.set_option(aqua.OPT_KERNEL, aqua.KERNEL_LDST)
+    for ctas in (0, 74, 32):
+        ctx.set_option(aqua.OPT_MAX_CTAS, ctas)
+        o, i = time_tickets(ctx, 5, s)
+        print(json.dumps({"ldst_variant": 2, "ctas": ctas or 148, "out_hbm_GBps": round(2 * nblk * U / o / 1e6, 1),
+                          "in_hbm_GBps": round(2 * nblk * U / i / 1e6, 1)}), flush=True)
+
+
 def stages():
     L, bs, H, D, NB, nblk = 32, 16, 8, 128, 4096, 2048
     ctx, layers, arena, U = setup(L, bs, H, D, NB, nblk)
@@ -585,6 +611,8 @@ if __name__ == "__main__":
         migrate()
     elif what == "ldst_variants":
         ldst_variants()
+    elif what == "tma_variants":
+        tma_variants()
     elif what == "layer_overlap":
         layer_overlap()
     elif what == "duplex":

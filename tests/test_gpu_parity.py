@@ -24,7 +24,14 @@ from gpu_util import Rig
 pytestmark = pytest.mark.gpu
 GOLD = os.path.join(os.path.dirname(__file__), "golden")
 ENGINES = {"tma": aqua.KERNEL_TMA, "ldst": aqua.KERNEL_LDST, "per_chunk": aqua.BASE_PER_CHUNK,
-           "gather_temp": aqua.BASE_GATHER_TEMP, "batch": aqua.BASE_BATCH, "ce_host": aqua.KERNEL_CE_HOST}
+           "gather_temp": aqua.BASE_GATHER_TEMP, "batch": aqua.BASE_BATCH, "ce_host": aqua.KERNEL_CE_HOST,
+           "tma_ws": aqua.KERNEL_TMA}
+
+
+def _engine(ctx, name):
+    """Select an engine; "tma_ws" is the TMA engine's warp-specialised variant."""
+    ctx.set_option(aqua.OPT_KERNEL, ENGINES[name])
+    ctx.set_option(aqua.OPT_TMA_VARIANT, 1 if name == "tma_ws" else 0)
 
 
 def _ops(rig, ops, stream=0):
@@ -56,7 +63,7 @@ def test_c1_bytes(engine, variant):
     g = json.load(open(os.path.join(GOLD, "c1_script.json")))
     v = g[variant]
     rig = Rig(**g["layout"], lender_slots=v["lender_slots"], host_slots=v.get("host_slots", 0))
-    rig.ctx.set_option(aqua.OPT_KERNEL, ENGINES[engine])
+    _engine(rig.ctx, engine)
     s = torch.cuda.Stream()
     ops = [("alloc", (p, 4)) for p in range(8)]
     ops += [("out", g["swap_out"]), ("alloc", (100, 6)), ("in", g["swap_in"]), ("free", 100)]
@@ -77,7 +84,7 @@ SHAPES = {
 
 
 @pytest.mark.parametrize("shape", list(SHAPES))
-@pytest.mark.parametrize("engine", ["tma", "ldst"])
+@pytest.mark.parametrize("engine", ["tma", "tma_ws", "ldst"])
 @pytest.mark.parametrize("seed", [0, 1])
 @pytest.mark.parametrize("ctas", [0, 3])
 def test_random_sequences_bytes(shape, engine, seed, ctas):
@@ -87,9 +94,9 @@ def test_random_sequences_bytes(shape, engine, seed, ctas):
     rnd = random.Random(seed * 31 + len(shape))
     NB = 24
     rig = Rig(L=L, bs=bs, H=H, D=D, e=2, NB=NB, lender_slots=10, host_slots=8, seed=seed)
-    rig.ctx.set_option(aqua.OPT_KERNEL, ENGINES[engine])
+    _engine(rig.ctx, engine)
     rig.ctx.set_option(aqua.OPT_MAX_CTAS, ctas)
-    if engine == "tma" and shape == "ragged_10KiB":
+    if engine.startswith("tma") and shape == "ragged_10KiB":
         rig.ctx.set_option(aqua.OPT_TMA_PIECE, 4096)     # S = 10 KiB -> pieces 4K, 4K, 2K
     pids = list(range(5))
     ops = []
@@ -253,12 +260,12 @@ def test_errors_leave_state_unchanged_and_no_cpu_fallback():
     assert c.launch_count() == n0 + 1         # the copy ran as one of our kernels
 
 
-@pytest.mark.parametrize("engine", ["tma", "ldst"])
+@pytest.mark.parametrize("engine", ["tma", "tma_ws", "ldst"])
 def test_staged_descriptor_path_bytes(engine):
     """More than kInlineDesc (256) descriptors: the staging-ring upload path,
     whole-buffer compare (both directions, fragmented table)."""
     rig = Rig(L=2, bs=16, H=1, D=8, NB=700, lender_slots=300, host_slots=400)
-    rig.ctx.set_option(aqua.OPT_KERNEL, ENGINES[engine])
+    _engine(rig.ctx, engine)
     perm = block_permutation(700, 700, seed=5).tolist()
     _ops(rig, [("adopt", (1, perm[:257])), ("adopt", (2, perm[257:600])), ("out", [1, 2]),
                ("alloc", (3, 50)), ("in", [2, 1]), ("out", [3, 1]), ("in", [1])])
@@ -281,7 +288,7 @@ def test_ticket_timing():
     assert e.value.code == aqua.E_STATE
 
 
-@pytest.mark.parametrize("engine", ["tma", "ldst"])
+@pytest.mark.parametrize("engine", ["tma", "tma_ws", "ldst"])
 def test_migrate_reclaim_relend_bytes(engine):
     """NEXT-1 on the GPU: images move lender -> host (reclaim) and back
     (re-offer) through the fused arena->arena kernel, byte for byte with the
@@ -290,7 +297,7 @@ def test_migrate_reclaim_relend_bytes(engine):
     from workloads import kv_random_bytes
     rig = Rig(L=3, bs=16, H=4, D=64, NB=40, lender_slots=12, host_slots=16)
     c, o = rig.ctx, rig.opool
-    c.set_option(aqua.OPT_KERNEL, ENGINES[engine])
+    _engine(c, engine)
     _ops(rig, [("alloc", (1, 5)), ("alloc", (2, 3)), ("alloc", (3, 4)), ("out", [1, 3]), ("out", [2])])
     t = c.migrate([3], aqua.LOC_HOST)
     o.migrate([3], kp.LOC_HOST)
@@ -314,14 +321,14 @@ def test_migrate_reclaim_relend_bytes(engine):
     _ops(rig, [("in", [1, 2, 3]), ("out", [2])])
 
 
-@pytest.mark.parametrize("engine", ["tma", "ldst"])
+@pytest.mark.parametrize("engine", ["tma", "tma_ws", "ldst"])
 def test_prefix_cache_bytes(engine):
     """NEXT-2 on the GPU: store a cached prefix (copy), load it into three
     new prompts, reclaim moves it to the host, load again -- whole buffers
     byte-equal to the oracle after every call."""
     rig = Rig(L=3, bs=16, H=4, D=64, NB=48, lender_slots=12, host_slots=12)
     c, o = rig.ctx, rig.opool
-    c.set_option(aqua.OPT_KERNEL, ENGINES[engine])
+    _engine(c, engine)
     _ops(rig, [("adopt", (5, [40, 3, 17, 8, 22]))])
     c.prefix_store(9, 5, 4)
     assert o.prefix_store(9, 5, 4) == (kp.LOC_PEER, [0, 1, 2, 3])
@@ -526,7 +533,7 @@ def test_pattern_batch_kernel_matches_oracle_words():
     rig.assert_bytes_equal("pattern batch")
 
 
-@pytest.mark.parametrize("engine", ["tma", "ldst"])
+@pytest.mark.parametrize("engine", ["tma", "tma_ws", "ldst"])
 def test_many_small_blocks_whole_buffer(engine):
     """Scale edge: 131,072 blocks of S = 256 B (100,000-block prompt, 800 KB of
     staged descriptors, slot ids > 2^16), whole pool / arena compared with
@@ -534,7 +541,7 @@ def test_many_small_blocks_whole_buffer(engine):
     NB = 131072
     rig = Rig(L=1, bs=16, H=1, D=8, NB=NB, lender_slots=100000, host_slots=0)
     c, o = rig.ctx, rig.opool
-    c.set_option(aqua.OPT_KERNEL, ENGINES[engine])
+    _engine(c, engine)
     perm = block_permutation(NB, NB, seed=13).tolist()
     _ops(rig, [("adopt", (1, perm[:100000])), ("adopt", (2, perm[100000:100500])), ("out", [1]),
                ("alloc", (3, 20000)), ("in", [1])])
