@@ -80,6 +80,9 @@ SHAPES = {
     "odd_48KiB": (2, 16, 12, 128),       # S = 48 KiB (3 pieces)
     "c4_shape": (5, 16, 2, 128),         # S = 8 KiB (Llama-70B TP4 chunk): TMA units of 4,4,2 chunks
     "l3_8KiB": (3, 16, 2, 128),          # S = 8 KiB, 6 chunks per block: units of 4,2
+    "fp8_kv": (2, 16, 8, 128, 1),        # e = 1 (FP8 KV cache): S = 16 KiB
+    "fp32_kv": (2, 16, 4, 128, 4),       # e = 4: S = 32 KiB (one full stage)
+    "bs128": (1, 128, 8, 128),           # S = 256 KiB: 8 pieces per chunk
 }
 
 
@@ -90,10 +93,10 @@ SHAPES = {
 def test_random_sequences_bytes(shape, engine, seed, ctas):
     """ctas=3 forces many units per CTA (TMA: grouped chunks split at ragged
     descriptor and CTA-range boundaries)."""
-    L, bs, H, D = SHAPES[shape]
+    L, bs, H, D, *e = SHAPES[shape]
     rnd = random.Random(seed * 31 + len(shape))
     NB = 24
-    rig = Rig(L=L, bs=bs, H=H, D=D, e=2, NB=NB, lender_slots=10, host_slots=8, seed=seed)
+    rig = Rig(L=L, bs=bs, H=H, D=D, e=(e or [2])[0], NB=NB, lender_slots=10, host_slots=8, seed=seed)
     _engine(rig.ctx, engine)
     rig.ctx.set_option(aqua.OPT_MAX_CTAS, ctas)
     if engine.startswith("tma") and shape == "ragged_10KiB":
