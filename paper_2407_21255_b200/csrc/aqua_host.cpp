@@ -1576,7 +1576,7 @@ aqua_status aqua_set_option(aqua_ctx* c, int32_t opt, int64_t v) {
       c->ldst_variant = static_cast<int>(v);
       return AQUA_OK;
     case AQUA_OPT_TMA_VARIANT:
-      if (v < 0 || v > 1) return fail(c, AQUA_E_INVAL, "tma variant");
+      if (v < 0 || v > 2) return fail(c, AQUA_E_INVAL, "tma variant");
       c->tma_variant = static_cast<int>(v);
       return AQUA_OK;
   }

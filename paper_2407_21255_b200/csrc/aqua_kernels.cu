@@ -184,13 +184,19 @@ __device__ __forceinline__ void unit_next(const SwapParams& p, Unit& u, int k) {
   }
 }
 
+// blockDim.x / 32 = R independent rings per CTA (AQUA_OPT_TMA_VARIANT 2 is
+// R = 2; R = 1 is the product default): lane 0 of warp w drives ring w over the
+// w-th R-th of the CTA's item range, with its own stages and barriers.
 template <Dir D>
-__global__ void __launch_bounds__(32) swap_tma_kernel(const __grid_constant__ SwapParams p, const int stages) {
-  extern __shared__ __align__(128) uint8_t smem[];
-  if (threadIdx.x != 0) return;
+__global__ void __launch_bounds__(128) swap_tma_kernel(const __grid_constant__ SwapParams p, const int stages) {
+  extern __shared__ __align__(128) uint8_t smem_all[];
+  if ((threadIdx.x & 31) != 0) return;
   const int64_t stage_bytes = int64_t(p.piece) * p.group;
+  const int64_t R = blockDim.x >> 5, w = threadIdx.x >> 5;
+  const int64_t ring_bytes = (stage_bytes * stages + 8 * stages + 127) & ~int64_t(127);
+  uint8_t* smem = smem_all + w * ring_bytes;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + size_t(stages) * stage_bytes);
-  const int64_t G = gridDim.x, b = blockIdx.x;
+  const int64_t G = gridDim.x * R, b = blockIdx.x * R + w;
   const int64_t i0 = p.nitems * b / G, i1 = p.nitems * (b + 1) / G;
   if (i1 <= i0) return;
   for (int s = 0; s < stages; ++s) mbar_init(&bars[s], 1);
@@ -571,8 +577,15 @@ cudaError_t launch_swap_tma(const SwapParams& p, Dir dir, int num_sms, int grid_
   }
   stages = std::max(2, std::min(stages, 32));
   const int bar_extra = variant == 1 ? 8 : 0;   // the "empty" barriers of the warp-specialised variant
-  while (stages > 2 && tma_smem_bytes(stage_bytes, stages) + bar_extra * stages > 227 * 1024) --stages;
-  const int smem = tma_smem_bytes(stage_bytes, stages) + bar_extra * stages;
+  const int rings = variant == 2 ? 2 : 1;
+  if (rings > 1 && stages_opt <= 0) stages = std::max(3, (stages + rings - 1) / rings + 1);
+  auto smem_for = [&](int st) {
+    return rings == 1 ? tma_smem_bytes(stage_bytes, st) + bar_extra * st
+                      : rings * ((tma_smem_bytes(stage_bytes, st) + 127) & ~127);
+  };
+  while (stages > 2 && smem_for(stages) > 227 * 1024) --stages;
+  if (smem_for(stages) > 227 * 1024) return cudaErrorInvalidConfiguration;
+  const int smem = smem_for(stages);
   // the opt-in smem attribute is per device; remember the largest set so far
   static thread_local int set_smem[2][3][64] = {};
   int dev = 0;
@@ -600,11 +613,11 @@ cudaError_t launch_swap_tma(const SwapParams& p, Dir dir, int num_sms, int grid_
     else
       swap_tma_ws_kernel<kMig><<<grid, 64, smem, s>>>(p, stages);
   } else if (dir == kOut) {
-    swap_tma_kernel<kOut><<<grid, 32, smem, s>>>(p, stages);
+    swap_tma_kernel<kOut><<<grid, 32 * rings, smem, s>>>(p, stages);
   } else if (dir == kIn) {
-    swap_tma_kernel<kIn><<<grid, 32, smem, s>>>(p, stages);
+    swap_tma_kernel<kIn><<<grid, 32 * rings, smem, s>>>(p, stages);
   } else {
-    swap_tma_kernel<kMig><<<grid, 32, smem, s>>>(p, stages);
+    swap_tma_kernel<kMig><<<grid, 32 * rings, smem, s>>>(p, stages);
   }
   if (ctas_used) *ctas_used = grid;
   return cudaGetLastError();

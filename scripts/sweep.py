@@ -534,9 +534,11 @@ def tma_variants():
     L, bs, H, D, NB, nblk = 32, 16, 8, 128, 4096, 2048
     ctx, layers, arena, U = setup(L, bs, H, D, NB, nblk)
     s = torch.cuda.Stream()
-    for v in (0, 1):
-        for st in (0, 2, 3, 4, 6):
-            for ctas in (0, 74, 32):
+    vs = [int(x) for x in os.environ.get("AQUA_SWEEP_TMA_VARIANTS", "0,1").split(",")]
+    sts = [int(x) for x in os.environ.get("AQUA_SWEEP_STAGES", "0,2,3,4,6").split(",")]
+    for v in vs:
+        for st in sts:
+            for ctas in (0, 74, 32, 16):
                 ctx.set_option(aqua.OPT_KERNEL, aqua.KERNEL_TMA)
                 ctx.set_option(aqua.OPT_TMA_VARIANT, v)
                 ctx.set_option(aqua.OPT_TMA_STAGES, st)
@@ -547,7 +549,7 @@ def tma_variants():
                                   "in_hbm_GBps": round(2 * nblk * U / i / 1e6, 1)}), flush=True)
     ctx.set_option(aqua.OPT_TMA_STAGES, 0)
     ctx.set_option(aqua.OPT_KERNEL, aqua.KERNEL_LDST)
-    for ctas in (0, 74, 32):
+    for ctas in (0, 74, 32, 16):
         ctx.set_option(aqua.OPT_MAX_CTAS, ctas)
         o, i = time_tickets(ctx, 5, s)
         print(json.dumps({"ldst_variant": 2, "ctas": ctas or 148, "out_hbm_GBps": round(2 * nblk * U / o / 1e6, 1),

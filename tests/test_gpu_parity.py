@@ -25,13 +25,13 @@ pytestmark = pytest.mark.gpu
 GOLD = os.path.join(os.path.dirname(__file__), "golden")
 ENGINES = {"tma": aqua.KERNEL_TMA, "ldst": aqua.KERNEL_LDST, "per_chunk": aqua.BASE_PER_CHUNK,
            "gather_temp": aqua.BASE_GATHER_TEMP, "batch": aqua.BASE_BATCH, "ce_host": aqua.KERNEL_CE_HOST,
-           "tma_ws": aqua.KERNEL_TMA}
+           "tma_ws": aqua.KERNEL_TMA, "tma_r2": aqua.KERNEL_TMA}
 
 
 def _engine(ctx, name):
-    """Select an engine; "tma_ws" is the TMA engine's warp-specialised variant."""
+    """Select an engine; "tma_ws" / "tma_r2" are the TMA engine's warp-specialised / two-ring variants."""
     ctx.set_option(aqua.OPT_KERNEL, ENGINES[name])
-    ctx.set_option(aqua.OPT_TMA_VARIANT, 1 if name == "tma_ws" else 0)
+    ctx.set_option(aqua.OPT_TMA_VARIANT, {"tma_ws": 1, "tma_r2": 2}.get(name, 0))
 
 
 def _ops(rig, ops, stream=0):
@@ -87,7 +87,7 @@ SHAPES = {
 
 
 @pytest.mark.parametrize("shape", list(SHAPES))
-@pytest.mark.parametrize("engine", ["tma", "tma_ws", "ldst"])
+@pytest.mark.parametrize("engine", ["tma", "tma_ws", "tma_r2", "ldst"])
 @pytest.mark.parametrize("seed", [0, 1])
 @pytest.mark.parametrize("ctas", [0, 3])
 def test_random_sequences_bytes(shape, engine, seed, ctas):
@@ -263,7 +263,7 @@ def test_errors_leave_state_unchanged_and_no_cpu_fallback():
     assert c.launch_count() == n0 + 1         # the copy ran as one of our kernels
 
 
-@pytest.mark.parametrize("engine", ["tma", "tma_ws", "ldst"])
+@pytest.mark.parametrize("engine", ["tma", "tma_ws", "tma_r2", "ldst"])
 def test_staged_descriptor_path_bytes(engine):
     """More than kInlineDesc (256) descriptors: the staging-ring upload path,
     whole-buffer compare (both directions, fragmented table)."""
@@ -291,7 +291,7 @@ def test_ticket_timing():
     assert e.value.code == aqua.E_STATE
 
 
-@pytest.mark.parametrize("engine", ["tma", "tma_ws", "ldst"])
+@pytest.mark.parametrize("engine", ["tma", "tma_ws", "tma_r2", "ldst"])
 def test_migrate_reclaim_relend_bytes(engine):
     """NEXT-1 on the GPU: images move lender -> host (reclaim) and back
     (re-offer) through the fused arena->arena kernel, byte for byte with the
@@ -324,7 +324,7 @@ def test_migrate_reclaim_relend_bytes(engine):
     _ops(rig, [("in", [1, 2, 3]), ("out", [2])])
 
 
-@pytest.mark.parametrize("engine", ["tma", "tma_ws", "ldst"])
+@pytest.mark.parametrize("engine", ["tma", "tma_ws", "tma_r2", "ldst"])
 def test_prefix_cache_bytes(engine):
     """NEXT-2 on the GPU: store a cached prefix (copy), load it into three
     new prompts, reclaim moves it to the host, load again -- whole buffers
@@ -536,7 +536,7 @@ def test_pattern_batch_kernel_matches_oracle_words():
     rig.assert_bytes_equal("pattern batch")
 
 
-@pytest.mark.parametrize("engine", ["tma", "tma_ws", "ldst"])
+@pytest.mark.parametrize("engine", ["tma", "tma_ws", "tma_r2", "ldst"])
 def test_many_small_blocks_whole_buffer(engine):
     """Scale edge: 131,072 blocks of S = 256 B (100,000-block prompt, 800 KB of
     staged descriptors, slot ids > 2^16), whole pool / arena compared with
