@@ -256,6 +256,8 @@ def run_ours(args):
         ctx.set_option(aqua.OPT_MAX_CTAS, args.max_ctas)
     if args.piece:
         ctx.set_option(aqua.OPT_TMA_PIECE, args.piece)
+    if args.inline_max >= 0:
+        ctx.set_option(aqua.OPT_INLINE_MAX, args.inline_max)
 
     arena_bytes = NBLK * U
     ipc_ptr = imported = None
@@ -575,6 +577,8 @@ def main():
     ap.add_argument("--engine", default="auto", choices=["auto", "tma", "ldst", "per_chunk", "gather_temp", "batch"])
     ap.add_argument("--max-ctas", type=int, default=0)
     ap.add_argument("--piece", type=int, default=0)
+    ap.add_argument("--inline-max", type=int, default=-1,
+                    help="AQUA_OPT_INLINE_MAX: largest call whose descriptors ride in the kernel parameters")
     ap.add_argument("--no-host-baselines", action="store_true")
     ap.add_argument("--host-reps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -79,6 +79,7 @@ struct aqua_ctx {
   int tma_stages = 0;
   int ldst_variant = 2;
   int tma_variant = 0;
+  int inline_max = aqua::kInlineDescBig;
   int num_sms = 148;
   uint64_t* d_layer_base = nullptr;
   // pinned -> device descriptor staging ring
@@ -383,7 +384,8 @@ aqua_status run_copy(aqua_ctx* c, const std::vector<Desc>& ds, aqua::Dir dir, cu
   *regions = 0;
   if (ds.empty()) return AQUA_OK;
   if (nc < 0) nc = 2 * c->L;
-  aqua::SwapParams p{};
+  aqua::SwapHeader p{};
+  const Desc* inl = nullptr;
   p.layer_base = c->d_layer_base;
   p.arena_base[0] = reinterpret_cast<uint64_t>(c->gpu.base);
   p.arena_base[1] = reinterpret_cast<uint64_t>(c->host.base);
@@ -423,9 +425,9 @@ aqua_status run_copy(aqua_ctx* c, const std::vector<Desc>& ds, aqua::Dir dir, cu
   if (engine == AQUA_KERNEL_TMA || engine == AQUA_KERNEL_LDST) {
     if (dev_desc) {
       p.desc = dev_desc;                      // already uploaded by the caller
-    } else if (ds.size() <= static_cast<size_t>(aqua::kInlineDesc)) {
+    } else if (ds.size() <= static_cast<size_t>(c->inline_max)) {
       p.desc = nullptr;                       // descriptors ride in the kernel parameters
-      std::copy(ds.begin(), ds.end(), p.inl);
+      inl = ds.data();
     } else {
       void* dd;
       aqua_status s = stage_upload(c, ds.data(), ds.size() * sizeof(Desc), st, &dd);
@@ -458,13 +460,13 @@ aqua_status run_copy(aqua_ctx* c, const std::vector<Desc>& ds, aqua::Dir dir, cu
       p.piece = piece;
       p.npieces = static_cast<int32_t>((c->S + piece - 1) / piece);
       p.nitems = p.ndesc * nc * p.npieces;
-      e = aqua::launch_swap_tma(p, dir, c->num_sms, cap, c->tma_stages, st, &ctas, c->tma_variant);
+      e = aqua::launch_swap_tma(p, inl, dir, c->num_sms, cap, c->tma_stages, st, &ctas, c->tma_variant);
     } else {
       p.piece = 4096;
       p.group = 1;
       p.npieces = static_cast<int32_t>((c->S + 4095) / 4096);
       p.nitems = p.ndesc * nc * p.npieces;
-      e = aqua::launch_swap_ldst(p, dir, c->num_sms, all_host && cap == kHostCtas ? 2 * kHostCtas : cap, st, &ctas,
+      e = aqua::launch_swap_ldst(p, inl, dir, c->num_sms, all_host && cap == kHostCtas ? 2 * kHostCtas : cap, st, &ctas,
                                  c->ldst_variant);
     }
     if (e != cudaSuccess) return cuda_fail(c, e, "swap kernel launch");
@@ -544,14 +546,14 @@ aqua_status run_copy(aqua_ctx* c, const std::vector<Desc>& ds, aqua::Dir dir, cu
     };
     int ctas = 0;
     if (dir == aqua::kOut) {
-      cudaError_t e = aqua::launch_swap_ldst(p, aqua::kOut, c->num_sms, c->max_ctas, st, &ctas, c->ldst_variant);
+      cudaError_t e = aqua::launch_swap_ldst(p, nullptr, aqua::kOut, c->num_sms, c->max_ctas, st, &ctas, c->ldst_variant);
       if (e != cudaSuccess) return cuda_fail(c, e, "gather kernel launch");
       c->launches++;
       return runs(true);
     }
     aqua_status rs = runs(false);
     if (rs) return rs;
-    cudaError_t e = aqua::launch_swap_ldst(p, aqua::kIn, c->num_sms, c->max_ctas, st, &ctas, c->ldst_variant);
+    cudaError_t e = aqua::launch_swap_ldst(p, nullptr, aqua::kIn, c->num_sms, c->max_ctas, st, &ctas, c->ldst_variant);
     if (e != cudaSuccess) return cuda_fail(c, e, "scatter kernel launch");
     c->launches++;
     return AQUA_OK;
@@ -579,7 +581,7 @@ aqua_status enqueue_copy(aqua_ctx* c, const std::vector<Desc>& ds, aqua::Dir dir
   const Desc* dd = nullptr;
   int up = 0;
   const bool fused = c->kernel == AQUA_KERNEL_AUTO || c->kernel == AQUA_KERNEL_TMA || c->kernel == AQUA_KERNEL_LDST;
-  if (fused && ds.size() > static_cast<size_t>(aqua::kInlineDesc)) {
+  if (fused && ds.size() > static_cast<size_t>(c->inline_max)) {
     void* d;
     if (aqua_status s = stage_upload(c, ds.data(), ds.size() * sizeof(Desc), st, &d)) return s;
     dd = static_cast<const Desc*>(d);
@@ -1579,6 +1581,10 @@ aqua_status aqua_set_option(aqua_ctx* c, int32_t opt, int64_t v) {
       if (v < 0 || v > 2) return fail(c, AQUA_E_INVAL, "tma variant");
       c->tma_variant = static_cast<int>(v);
       return AQUA_OK;
+    case AQUA_OPT_INLINE_MAX:
+      if (v < 0 || v > aqua::kInlineDescBig) return fail(c, AQUA_E_INVAL, "inline max");
+      c->inline_max = static_cast<int>(v);
+      return AQUA_OK;
   }
   return fail(c, AQUA_E_INVAL, "unknown option");
 }
@@ -1593,6 +1599,7 @@ aqua_status aqua_get_option(aqua_ctx* c, int32_t opt, int64_t* v) {
     case AQUA_OPT_TIMING: *v = c->timing; return AQUA_OK;
     case AQUA_OPT_LDST_VARIANT: *v = c->ldst_variant; return AQUA_OK;
     case AQUA_OPT_TMA_VARIANT: *v = c->tma_variant; return AQUA_OK;
+    case AQUA_OPT_INLINE_MAX: *v = c->inline_max; return AQUA_OK;
   }
   return fail(c, AQUA_E_INVAL, "unknown option");
 }

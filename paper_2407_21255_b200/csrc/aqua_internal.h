@@ -21,10 +21,16 @@ enum Dir : int { kOut = 0, kIn = 1, kMig = 2 };
 
 // Calls with at most kInlineDesc descriptors pass them inside the kernel
 // parameters (__grid_constant__): no staging copy on the critical path.
+// Two parameter sizes: 2 KiB of descriptors (small calls keep a small launch)
+// and, up to kInlineDescBig, the large-parameter launch of CUDA 12.1+ (32,764
+// bytes of parameters on sm_70+), which covers e.g. a 32K-token Llama-3-8B
+// prompt (2,048 blocks) in one launch without a descriptor upload.  Larger
+// calls go through the pinned staging ring + one H2D copy.
 constexpr int kInlineDesc = 256;
+constexpr int kInlineDescBig = 4064;
 
-struct SwapParams {
-  const Desc* desc;            // device array [ndesc], or nullptr -> use inl
+struct SwapHeader {
+  const Desc* desc;            // device array [ndesc], or nullptr -> use the inline array
   const uint64_t* layer_base;  // device array [L]
   uint64_t arena_base[2];      // device-visible bases: [0] GPU lender, [1] host
   int64_t ndesc;
@@ -35,8 +41,14 @@ struct SwapParams {
   int32_t c0, nc;              // chunk range [c0, c0+nc) of each block (layer-wise: c = 2l + kv)
   int64_t S, U, P_kv, P_b;
   int64_t nitems;              // ndesc * nc * npieces
-  Desc inl[kInlineDesc];       // inline descriptors when desc == nullptr
 };
+
+// The kernel parameter block: header + N inline descriptors.
+template <int N>
+struct SwapParamsT : SwapHeader {
+  Desc inl[N];                 // inline descriptors when desc == nullptr
+};
+static_assert(sizeof(SwapParamsT<kInlineDescBig>) + 16 <= 32764, "kernel parameter limit");
 
 struct PatternParams {
   const int32_t* bt;           // device block table of the prompt
@@ -68,9 +80,11 @@ cudaError_t launch_pattern_fill_batch(const FillBatchParams& p, int num_sms, cud
 
 // Launchers: return the CUDA error of the launch (cudaSuccess on success).
 // grid_cap = max CTAs (0 = derived from the SM count).
-cudaError_t launch_swap_tma(const SwapParams& p, Dir dir, int num_sms, int grid_cap, int stages,
+// h.desc == nullptr: the h.ndesc descriptors at `inl` (host memory, at most
+// kInlineDescBig) are copied into the kernel parameters.
+cudaError_t launch_swap_tma(const SwapHeader& h, const Desc* inl, Dir dir, int num_sms, int grid_cap, int stages,
                             cudaStream_t s, int* ctas_used, int variant = 0);
-cudaError_t launch_swap_ldst(const SwapParams& p, Dir dir, int num_sms, int grid_cap,
+cudaError_t launch_swap_ldst(const SwapHeader& h, const Desc* inl, Dir dir, int num_sms, int grid_cap,
                              cudaStream_t s, int* ctas_used, int variant = 0);
 cudaError_t launch_pattern_fill(const PatternParams& p, int num_sms, cudaStream_t s);
 cudaError_t launch_pattern_verify(const PatternParams& p, int num_sms, cudaStream_t s);

@@ -95,7 +95,7 @@ __device__ __forceinline__ void st_stream(void* p, const int4& v) {
 struct Cursor {
   int64_t j;
   int32_t c, q;
-  __device__ __forceinline__ void init(int64_t item, const SwapParams& p) {
+  __device__ __forceinline__ void init(int64_t item, const SwapHeader& p) {
     const int64_t per_desc = int64_t(p.nc) * p.npieces;
     j = item / per_desc;
     const int64_t r = item - j * per_desc;
@@ -105,14 +105,15 @@ struct Cursor {
   }
 };
 
-__device__ __forceinline__ Desc desc_at(const SwapParams& p, int64_t j) {
+template <class P>
+__device__ __forceinline__ Desc desc_at(const P& p, int64_t j) {
   return p.desc ? p.desc[j] : p.inl[j];
 }
 
 // chunk(l, kv, b) = layer_base[l] + kv*P_kv + b*P_b            (R1)
 // image chunk    = arena + slot*U + (2l+kv)*S                   (R3)
 template <Dir D>
-__device__ __forceinline__ void item_addrs(const SwapParams& p, const Desc d, int c, int q,
+__device__ __forceinline__ void item_addrs(const SwapHeader& p, const Desc d, int c, int q,
                                            const uint8_t*& src, uint8_t*& dst, uint32_t& bytes) {
   const int l = c >> 1, kv = c & 1;
   const int64_t off = int64_t(q) * p.piece;
@@ -157,7 +158,7 @@ struct Unit {
   int64_t left;     // items of this CTA not yet covered
 };
 
-__device__ __forceinline__ int unit_len(const SwapParams& p, const Unit& u) {
+__device__ __forceinline__ int unit_len(const SwapHeader& p, const Unit& u) {
   if (p.group == 1) return 1;
   int64_t k = p.c0 + p.nc - u.c;
   if (k > p.group) k = p.group;
@@ -165,7 +166,7 @@ __device__ __forceinline__ int unit_len(const SwapParams& p, const Unit& u) {
   return static_cast<int>(k);
 }
 
-__device__ __forceinline__ void unit_next(const SwapParams& p, Unit& u, int k) {
+__device__ __forceinline__ void unit_next(const SwapHeader& p, Unit& u, int k) {
   u.left -= k;
   if (p.group == 1) {
     if (++u.q == p.npieces) {
@@ -187,8 +188,8 @@ __device__ __forceinline__ void unit_next(const SwapParams& p, Unit& u, int k) {
 // blockDim.x / 32 = R independent rings per CTA (AQUA_OPT_TMA_VARIANT 2 is
 // R = 2; R = 1 is the product default): lane 0 of warp w drives ring w over the
 // w-th R-th of the CTA's item range, with its own stages and barriers.
-template <Dir D>
-__global__ void __launch_bounds__(128) swap_tma_kernel(const __grid_constant__ SwapParams p, const int stages) {
+template <Dir D, class P>
+__global__ void __launch_bounds__(128) swap_tma_kernel(const __grid_constant__ P p, const int stages) {
   extern __shared__ __align__(128) uint8_t smem_all[];
   if ((threadIdx.x & 31) != 0) return;
   const int64_t stage_bytes = int64_t(p.piece) * p.group;
@@ -277,8 +278,8 @@ __global__ void __launch_bounds__(128) swap_tma_kernel(const __grid_constant__ S
 // lane) only issues stores; "full" mbarriers carry the bulk-load bytes and
 // "empty" mbarriers hand a stage back once its store has read it, so loads
 // never wait behind a store's completion check.
-template <Dir D>
-__global__ void __launch_bounds__(64) swap_tma_ws_kernel(const __grid_constant__ SwapParams p, const int stages) {
+template <Dir D, class P>
+__global__ void __launch_bounds__(64) swap_tma_ws_kernel(const __grid_constant__ P p, const int stages) {
   extern __shared__ __align__(128) uint8_t smem[];
   const int64_t stage_bytes = int64_t(p.piece) * p.group;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + size_t(stages) * stage_bytes);
@@ -387,8 +388,8 @@ __device__ __forceinline__ void st_plain(void* p, const int4& v) {
 // 0 streaming hints (ld.nc.L1::no_allocate.L2::256B / st.L1::no_allocate);
 // 1 plain ld/st; 2 streaming hints + the next item's loads issued before the
 // current item's stores (software pipelined).
-template <Dir D, int UNROLL, int V>
-__global__ void __launch_bounds__(256) swap_ldst_kernel(const __grid_constant__ SwapParams p) {
+template <Dir D, int UNROLL, int V, class P>
+__global__ void __launch_bounds__(256) swap_ldst_kernel(const __grid_constant__ P p) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
@@ -556,9 +557,11 @@ int grid_for(int64_t work_units, int per_cta, int num_sms, int ctas_per_sm, int 
 
 int tma_smem_bytes(int piece, int stages) { return piece * stages + 8 * stages; }
 
-cudaError_t launch_swap_tma(const SwapParams& p, Dir dir, int num_sms, int grid_cap, int stages_opt,
-                            cudaStream_t s, int* ctas_used, int variant) {
-  if (p.nitems == 0) return cudaSuccess;
+namespace {
+
+template <class P>
+cudaError_t launch_tma_t(const P& p, Dir dir, int num_sms, int grid_cap, int stages_opt, cudaStream_t s,
+                         int* ctas_used, int variant) {
   // One CTA per SM and a shallow ring: 3 x 32 KiB or 64 KiB of loads in
   // flight per SM measured best for HBM on B200 (profiles/r01_stages.jsonl);
   // deeper rings lose 3-4 %.
@@ -586,56 +589,56 @@ cudaError_t launch_swap_tma(const SwapParams& p, Dir dir, int num_sms, int grid_
   while (stages > 2 && smem_for(stages) > 227 * 1024) --stages;
   if (smem_for(stages) > 227 * 1024) return cudaErrorInvalidConfiguration;
   const int smem = smem_for(stages);
-  // the opt-in smem attribute is per device; remember the largest set so far
-  static thread_local int set_smem[2][3][64] = {};
+  // the opt-in smem attribute is per device and per instantiation; set once
+  static thread_local bool set_smem[2][3][64] = {};
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
   const int vi = variant == 1 ? 1 : 0;
-  int& have = set_smem[vi][dir][dev & 63];
-  if (smem > have) {
+  bool& have = set_smem[vi][dir][dev & 63];
+  if (!have) {
     if (vi)
-      e = cudaFuncSetAttribute(dir == kOut ? swap_tma_ws_kernel<kOut>
-                               : dir == kIn ? swap_tma_ws_kernel<kIn> : swap_tma_ws_kernel<kMig>,
+      e = cudaFuncSetAttribute(dir == kOut ? swap_tma_ws_kernel<kOut, P>
+                               : dir == kIn ? swap_tma_ws_kernel<kIn, P> : swap_tma_ws_kernel<kMig, P>,
                                cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     else
-      e = cudaFuncSetAttribute(dir == kOut ? swap_tma_kernel<kOut>
-                               : dir == kIn ? swap_tma_kernel<kIn> : swap_tma_kernel<kMig>,
+      e = cudaFuncSetAttribute(dir == kOut ? swap_tma_kernel<kOut, P>
+                               : dir == kIn ? swap_tma_kernel<kIn, P> : swap_tma_kernel<kMig, P>,
                                cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e != cudaSuccess) return e;
-    have = 227 * 1024;
+    have = true;
   }
   if (vi) {
     if (dir == kOut)
-      swap_tma_ws_kernel<kOut><<<grid, 64, smem, s>>>(p, stages);
+      swap_tma_ws_kernel<kOut, P><<<grid, 64, smem, s>>>(p, stages);
     else if (dir == kIn)
-      swap_tma_ws_kernel<kIn><<<grid, 64, smem, s>>>(p, stages);
+      swap_tma_ws_kernel<kIn, P><<<grid, 64, smem, s>>>(p, stages);
     else
-      swap_tma_ws_kernel<kMig><<<grid, 64, smem, s>>>(p, stages);
+      swap_tma_ws_kernel<kMig, P><<<grid, 64, smem, s>>>(p, stages);
   } else if (dir == kOut) {
-    swap_tma_kernel<kOut><<<grid, 32 * rings, smem, s>>>(p, stages);
+    swap_tma_kernel<kOut, P><<<grid, 32 * rings, smem, s>>>(p, stages);
   } else if (dir == kIn) {
-    swap_tma_kernel<kIn><<<grid, 32 * rings, smem, s>>>(p, stages);
+    swap_tma_kernel<kIn, P><<<grid, 32 * rings, smem, s>>>(p, stages);
   } else {
-    swap_tma_kernel<kMig><<<grid, 32 * rings, smem, s>>>(p, stages);
+    swap_tma_kernel<kMig, P><<<grid, 32 * rings, smem, s>>>(p, stages);
   }
   if (ctas_used) *ctas_used = grid;
   return cudaGetLastError();
 }
 
-template <int V>
-void launch_ldst_v(const SwapParams& p, Dir dir, int grid, cudaStream_t s) {
+template <int V, class P>
+void launch_ldst_v(const P& p, Dir dir, int grid, cudaStream_t s) {
   if (dir == kOut)
-    swap_ldst_kernel<kOut, 8, V><<<grid, 256, 0, s>>>(p);
+    swap_ldst_kernel<kOut, 8, V, P><<<grid, 256, 0, s>>>(p);
   else if (dir == kIn)
-    swap_ldst_kernel<kIn, 8, V><<<grid, 256, 0, s>>>(p);
+    swap_ldst_kernel<kIn, 8, V, P><<<grid, 256, 0, s>>>(p);
   else
-    swap_ldst_kernel<kMig, 8, V><<<grid, 256, 0, s>>>(p);
+    swap_ldst_kernel<kMig, 8, V, P><<<grid, 256, 0, s>>>(p);
 }
 
-cudaError_t launch_swap_ldst(const SwapParams& p, Dir dir, int num_sms, int grid_cap, cudaStream_t s,
-                             int* ctas_used, int variant) {
-  if (p.nitems == 0) return cudaSuccess;
+template <class P>
+cudaError_t launch_ldst_t(const P& p, Dir dir, int num_sms, int grid_cap, cudaStream_t s, int* ctas_used,
+                          int variant) {
   // variant 2 (software pipelined, the default) is best with one 256-thread
   // CTA per SM: 6,624 / 6,572 GB/s on C2 (profiles/r01_ldst_variants.jsonl)
   const int grid = grid_for<void>(p.nitems, 8, num_sms, variant == 2 ? 1 : 4, grid_cap);
@@ -647,6 +650,41 @@ cudaError_t launch_swap_ldst(const SwapParams& p, Dir dir, int num_sms, int grid
     launch_ldst_v<0>(p, dir, grid, s);
   if (ctas_used) *ctas_used = grid;
   return cudaGetLastError();
+}
+
+// Builds the parameter block of the smallest size class that holds the
+// call's inline descriptors and hands it to `f`.
+template <class F>
+cudaError_t with_params(const SwapHeader& h, const Desc* inl, F&& f) {
+  if (h.desc || h.ndesc <= kInlineDesc) {
+    SwapParamsT<kInlineDesc> p;
+    static_cast<SwapHeader&>(p) = h;
+    if (!h.desc) std::copy(inl, inl + h.ndesc, p.inl);
+    return f(p);
+  }
+  if (h.ndesc > kInlineDescBig || !inl) return cudaErrorInvalidValue;
+  static thread_local SwapParamsT<kInlineDescBig> p;   // 32 KiB: off the stack
+  static_cast<SwapHeader&>(p) = h;
+  std::copy(inl, inl + h.ndesc, p.inl);
+  return f(p);
+}
+
+}  // namespace
+
+cudaError_t launch_swap_tma(const SwapHeader& h, const Desc* inl, Dir dir, int num_sms, int grid_cap,
+                            int stages_opt, cudaStream_t s, int* ctas_used, int variant) {
+  if (h.nitems == 0) return cudaSuccess;
+  return with_params(h, inl, [&](const auto& p) {
+    return launch_tma_t(p, dir, num_sms, grid_cap, stages_opt, s, ctas_used, variant);
+  });
+}
+
+cudaError_t launch_swap_ldst(const SwapHeader& h, const Desc* inl, Dir dir, int num_sms, int grid_cap,
+                             cudaStream_t s, int* ctas_used, int variant) {
+  if (h.nitems == 0) return cudaSuccess;
+  return with_params(h, inl, [&](const auto& p) {
+    return launch_ldst_t(p, dir, num_sms, grid_cap, s, ctas_used, variant);
+  });
 }
 
 cudaError_t launch_pattern_fill(const PatternParams& p, int num_sms, cudaStream_t s) {

@@ -634,11 +634,17 @@ if __name__ == "__main__":
 
 
 def latency():
-    """Host cost of one call (enqueue only) and device time of small calls."""
+    """Host cost of one call (enqueue only), device time of one call on an
+    idle GPU (ticket events), and back-to-back device time per call with the
+    calls queued behind a sleep kernel (no host gaps).  AQUA_SWEEP_INLINE sets
+    AQUA_OPT_INLINE_MAX (descriptors in the kernel parameters vs staged)."""
     import time
+    inline = int(os.environ.get("AQUA_SWEEP_INLINE", "-1"))
     L, bs, H, D = 32, 16, 8, 128
-    for nblk in (1, 8, 64, 256, 257, 2048):
-        ctx, layers, arena, U = setup(L, bs, H, D, 4096, nblk)
+    for nblk in (1, 8, 64, 256, 257, 1024, 2048, 4064, 4096):
+        ctx, layers, arena, U = setup(L, bs, H, D, max(4096, 2 * nblk), nblk)
+        if inline >= 0:
+            ctx.set_option(aqua.OPT_INLINE_MAX, inline)
         s = torch.cuda.Stream()
         o, i = time_swaps(ctx, 20, s)
         ctx.set_option(aqua.OPT_TIMING, 1)
@@ -659,12 +665,30 @@ def latency():
             t2 = time.perf_counter()
             enq.append((t1 - t0, t2 - t1))
         torch.cuda.synchronize()
-        print(json.dumps({"latency": nblk, "bytes": nblk * U, "out_ms": round(o, 4), "in_ms": round(i, 4),
+        q = []
+        for _ in range(5):
+            K = 20
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            with torch.cuda.stream(s):
+                torch.cuda._sleep(40_000_000)
+            a.record(s)
+            for _ in range(K):
+                ctx.swap_out([7], s.cuda_stream)
+                ctx.swap_in([7], s.cuda_stream)
+            b.record(s)
+            torch.cuda.synchronize()
+            q.append(a.elapsed_time(b) / (2 * K))
+        print(json.dumps({"latency": nblk, "bytes": nblk * U, "inline_max": ctx.get_option(aqua.OPT_INLINE_MAX),
+                          "out_ms": round(o, 4), "in_ms": round(i, 4),
                           "ticket_out_ms": round(statistics.median(d[0] for d in dev), 4),
                           "ticket_in_ms": round(statistics.median(d[1] for d in dev), 4),
+                          "queued_call_ms": round(statistics.median(q), 4),
+                          "queued_GBps": round(nblk * U / statistics.median(q) / 1e6, 1),
                           "enqueue_out_us": round(1e6 * statistics.median(e[0] for e in enq), 1),
                           "enqueue_in_us": round(1e6 * statistics.median(e[1] for e in enq), 1)}), flush=True)
         ctx.close()
+        del layers, arena
+        torch.cuda.empty_cache()
 
 
 if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "latency":

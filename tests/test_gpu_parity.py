@@ -264,13 +264,24 @@ def test_errors_leave_state_unchanged_and_no_cpu_fallback():
 
 
 @pytest.mark.parametrize("engine", ["tma", "tma_ws", "tma_r2", "ldst"])
-def test_staged_descriptor_path_bytes(engine):
-    """More than kInlineDesc (256) descriptors: the staging-ring upload path,
-    whole-buffer compare (both directions, fragmented table)."""
-    rig = Rig(L=2, bs=16, H=1, D=8, NB=700, lender_slots=300, host_slots=400)
+@pytest.mark.parametrize("tier", ["small_inline", "big_inline", "staged_256", "staged_4064"])
+def test_descriptor_tiers_bytes(engine, tier):
+    """Descriptor passing, whole-buffer compare (both directions, fragmented
+    table): calls of <= 256 blocks ride in the small parameter block, calls of
+    <= AQUA_OPT_INLINE_MAX (default 4064) in the large-parameter launch, and
+    larger calls go through the pinned staging ring (forced at 256 by the
+    option, and at the default limit by a 4,200-block call)."""
+    if tier == "staged_4064":
+        NB, a, b, lend, host = 9000, 4100, 4300, 4400, 4400
+    else:
+        NB, a, b, lend, host = 700, 257 if tier != "small_inline" else 200, 600, 300, 400
+    rig = Rig(L=2, bs=16, H=1, D=8, NB=NB, lender_slots=lend, host_slots=host)
     _engine(rig.ctx, engine)
-    perm = block_permutation(700, 700, seed=5).tolist()
-    _ops(rig, [("adopt", (1, perm[:257])), ("adopt", (2, perm[257:600])), ("out", [1, 2]),
+    if tier == "staged_256":
+        rig.ctx.set_option(aqua.OPT_INLINE_MAX, 256)
+    assert rig.ctx.get_option(aqua.OPT_INLINE_MAX) == (256 if tier == "staged_256" else 4064)
+    perm = block_permutation(NB, NB, seed=5).tolist()
+    _ops(rig, [("adopt", (1, perm[:a])), ("adopt", (2, perm[a:b])), ("out", [1, 2]),
                ("alloc", (3, 50)), ("in", [2, 1]), ("out", [3, 1]), ("in", [1])])
 
 
