@@ -106,6 +106,18 @@ def host_ctas():
                               "in_GBps": round(nblk * U / i / 1e6, 2)}), flush=True)
 
 
+def host_pcie():
+    """Host (PCIe) zero-copy path for an ncu capture: the TMA kernel writes
+    and reads a 1 GiB image in pinned host memory (C2 shape, 512 blocks)."""
+    L, bs, H, D, NB, nblk = 32, 16, 8, 128, 1024, 512
+    ctx, layers, arena, U = setup(L, bs, H, D, NB, nblk, host=True)
+    ctx.set_option(aqua.OPT_KERNEL, ENG["tma"])
+    s = torch.cuda.Stream()
+    o, i = time_tickets(ctx, 2, s)
+    print(json.dumps({"host_pcie": nblk * U, "out_GBps": round(nblk * U / o / 1e6, 2),
+                      "in_GBps": round(nblk * U / i / 1e6, 2)}), flush=True)
+
+
 def self_ctas():
     """CTAs (SMs) needed to saturate HBM on the self-lender path."""
     L, bs, H, D, NB, nblk = 32, 16, 8, 128, 4096, 2048
@@ -631,6 +643,8 @@ if __name__ == "__main__":
         host_ctas()
     elif what == "self_ctas":
         self_ctas()
+    elif what == "host_pcie":
+        host_pcie()
 
 
 def latency():
