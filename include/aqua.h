@@ -124,10 +124,19 @@ enum {
   AQUA_OPT_TMA_VARIANT = 7,   /* TMA engine: 0 (default) one ring per CTA; 1 warp-specialised (load warp + store
                                  warp); 2 two independent rings per CTA (one issuing warp each).  All three reach the
                                  same HBM rate (profiles/r01_tma_variants.jsonl, r01_tma_rings.jsonl) */
-  AQUA_OPT_INLINE_MAX = 8     /* largest call (in blocks, per launch) whose descriptors ride in the kernel
+  AQUA_OPT_INLINE_MAX = 8,    /* largest call (in blocks, per launch) whose descriptors ride in the kernel
                                  parameters instead of a pinned-ring upload + H2D copy: 0..4064 (default 4064,
                                  the 32,764-byte parameter limit of CUDA 12.1+; 256 = the small parameter block) */
+  AQUA_OPT_TMA_SCHED = 9,     /* TMA engine (variant 0) work distribution: 0 = each CTA one contiguous item range;
+                                 n > 0 = batches of n ring units claimed dynamically (atomic counter per launch);
+                                 -n = batches of n units dealt round robin (CTA b: b, b + grid, ...);
+                                 AQUA_TMA_SCHED_AUTO (default) = 4-unit claimed batches when the launch has one CTA
+                                 per SM and >= 8 batches per CTA, else 0 (profiles/r01_tma_sched*.jsonl) */
+  AQUA_OPT_TMA_STATIC_PCT = 10 /* dynamic schedule: percent of the items split statically (one contiguous range per
+                                 CTA) before the claimed batches; 0 = all claimed */
 };
+
+enum { AQUA_TMA_SCHED_AUTO = 1 << 30 };
 
 typedef struct aqua_ctx aqua_ctx;   /* one per borrower device (per TP rank) */
 

@@ -80,6 +80,12 @@ struct aqua_ctx {
   int ldst_variant = 2;
   int tma_variant = 0;
   int inline_max = aqua::kInlineDescBig;
+  int tma_sched = AQUA_TMA_SCHED_AUTO;   // AQUA_OPT_TMA_SCHED: 0 static, n > 0 dynamic n-unit batches, -n rr
+  int tma_static_pct = 0;       // AQUA_OPT_TMA_STATIC_PCT: statically split head of a dynamic launch
+  uint32_t* d_ctr = nullptr;    // kCtrSlots {next, done} pairs (inside the d_layer_base allocation)
+  uint32_t ctr_next = 0;
+  std::vector<uint64_t> ctr_tick;   // ticket of the last launch that used each pair
+  std::vector<int> ctr_pending;     // pairs used since the last record()
   int num_sms = 148;
   uint64_t* d_layer_base = nullptr;
   // pinned -> device descriptor staging ring
@@ -214,6 +220,8 @@ aqua_status get_event(aqua_ctx* c, bool timing, cudaEvent_t* ev) {
 // recorded before the copy; the ticket then measures the copy's device time.
 aqua_status record(aqua_ctx* c, cudaStream_t st, uint64_t* t, cudaEvent_t start = nullptr) {
   const uint64_t id = c->next_ticket++;
+  for (int s : c->ctr_pending) c->ctr_tick[s] = id;
+  c->ctr_pending.clear();
   if (c->dry) {
     *t = id;
     return AQUA_OK;
@@ -460,6 +468,28 @@ aqua_status run_copy(aqua_ctx* c, const std::vector<Desc>& ds, aqua::Dir dir, cu
       p.piece = piece;
       p.npieces = static_cast<int32_t>((c->S + piece - 1) / piece);
       p.nitems = p.ndesc * nc * p.npieces;
+      // work distribution: AUTO = claimed 4-unit batches when every SM runs
+      // one CTA and each gets >= 8 batches (they reach 6.68-6.81 TB/s vs 6.51
+      // for static ranges on C2, 6.58-6.61 vs 6.36 on C4); under an SM cap
+      // static ranges are as fast or faster (profiles/r01_tma_sched*.jsonl)
+      int sched = c->tma_sched;
+      if (sched == AQUA_TMA_SCHED_AUTO) {
+        const bool all_sms = cap == 0 || cap >= c->num_sms;
+        const int64_t units = p.nitems / p.group;
+        sched = all_sms && units >= int64_t(c->num_sms) * 4 * 8 ? 4 : 0;
+      }
+      if (sched > 0 && c->tma_variant == 0 && c->d_ctr) {
+        // dynamic batches of `sched` units; the counter pair's previous
+        // launch must be done with it (stream order or its ticket)
+        const int slot = static_cast<int>(c->ctr_next++ % aqua::kCtrSlots);
+        if (aqua_status s = wait_all(c, {c->ctr_tick[slot]}, st)) return s;
+        c->ctr_pending.push_back(slot);
+        p.work_ctr = c->d_ctr + 2 * slot;
+        p.batch = sched * p.group;
+        p.static_items = p.nitems * c->tma_static_pct / 100;
+      } else if (sched < 0 && c->tma_variant == 0) {
+        p.batch = -sched * p.group;            // static round-robin batches
+      }
       e = aqua::launch_swap_tma(p, inl, dir, c->num_sms, cap, c->tma_stages, st, &ctas, c->tma_variant);
     } else {
       p.piece = 4096;
@@ -723,9 +753,17 @@ aqua_status aqua_create(int device, const aqua_kv_layout* lay, aqua_ctx** out) {
   if (!c->dry) {
     DevGuard g(device);
     cudaError_t e = cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
-    if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void**>(&c->d_layer_base), c->L * sizeof(uint64_t));
+    // layer bases, then the counter pairs of dynamically scheduled launches
+    if (e == cudaSuccess)
+      e = cudaMalloc(reinterpret_cast<void**>(&c->d_layer_base),
+                     c->L * sizeof(uint64_t) + aqua::kCtrSlots * 2 * sizeof(uint32_t));
     if (e == cudaSuccess)
       e = cudaMemcpy(c->d_layer_base, c->layer_base.data(), c->L * sizeof(uint64_t), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) {
+      c->d_ctr = reinterpret_cast<uint32_t*>(c->d_layer_base + c->L);
+      e = cudaMemset(c->d_ctr, 0, aqua::kCtrSlots * 2 * sizeof(uint32_t));
+    }
+    c->ctr_tick.assign(aqua::kCtrSlots, 0);
     if (e != cudaSuccess) {
       std::string m = std::string("aqua_create: ") + cudaGetErrorString(e);
       cudaGetLastError();
@@ -1585,6 +1623,14 @@ aqua_status aqua_set_option(aqua_ctx* c, int32_t opt, int64_t v) {
       if (v < 0 || v > aqua::kInlineDescBig) return fail(c, AQUA_E_INVAL, "inline max");
       c->inline_max = static_cast<int>(v);
       return AQUA_OK;
+    case AQUA_OPT_TMA_SCHED:
+      if ((v < -(1 << 20) || v > (1 << 20)) && v != AQUA_TMA_SCHED_AUTO) return fail(c, AQUA_E_INVAL, "tma sched");
+      c->tma_sched = static_cast<int>(v);
+      return AQUA_OK;
+    case AQUA_OPT_TMA_STATIC_PCT:
+      if (v < 0 || v > 100) return fail(c, AQUA_E_INVAL, "tma static pct");
+      c->tma_static_pct = static_cast<int>(v);
+      return AQUA_OK;
   }
   return fail(c, AQUA_E_INVAL, "unknown option");
 }
@@ -1600,6 +1646,8 @@ aqua_status aqua_get_option(aqua_ctx* c, int32_t opt, int64_t* v) {
     case AQUA_OPT_LDST_VARIANT: *v = c->ldst_variant; return AQUA_OK;
     case AQUA_OPT_TMA_VARIANT: *v = c->tma_variant; return AQUA_OK;
     case AQUA_OPT_INLINE_MAX: *v = c->inline_max; return AQUA_OK;
+    case AQUA_OPT_TMA_SCHED: *v = c->tma_sched; return AQUA_OK;
+    case AQUA_OPT_TMA_STATIC_PCT: *v = c->tma_static_pct; return AQUA_OK;
   }
   return fail(c, AQUA_E_INVAL, "unknown option");
 }

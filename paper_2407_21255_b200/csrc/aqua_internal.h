@@ -41,7 +41,18 @@ struct SwapHeader {
   int32_t c0, nc;              // chunk range [c0, c0+nc) of each block (layer-wise: c = 2l + kv)
   int64_t S, U, P_kv, P_b;
   int64_t nitems;              // ndesc * nc * npieces
+  // TMA engine work distribution.  batch == 0: each CTA one contiguous item
+  // range.  batch > 0: batches of `batch` items, CTA b starting on batch b;
+  // then work_ctr == nullptr -> static round robin (b + G, b + 2G, ...), else
+  // dynamic claims through this {next, done} counter pair, which the last CTA
+  // resets to {0, 0}.
+  uint32_t* work_ctr;
+  int32_t batch;
+  int64_t static_items;        // dynamic only: items [0, static_items) split statically first
 };
+// Counter pairs per context for dynamically scheduled launches; a pair is
+// reused only after the ticket of its last launch (stream-ordered, like R7).
+constexpr int kCtrSlots = 256;
 
 // The kernel parameter block: header + N inline descriptors.
 template <int N>

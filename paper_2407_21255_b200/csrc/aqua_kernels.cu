@@ -97,11 +97,19 @@ struct Cursor {
   int32_t c, q;
   __device__ __forceinline__ void init(int64_t item, const SwapHeader& p) {
     const int64_t per_desc = int64_t(p.nc) * p.npieces;
-    j = item / per_desc;
-    const int64_t r = item - j * per_desc;
-    const int32_t cl = static_cast<int32_t>(r / p.npieces);
-    q = static_cast<int32_t>(r - int64_t(cl) * p.npieces);
-    c = p.c0 + cl;
+    uint32_t r;
+    if (item < (int64_t(1) << 32) && per_desc < (int64_t(1) << 32)) {   // 32-bit divides (64-bit: a long subroutine)
+      const uint32_t it = static_cast<uint32_t>(item), pd = static_cast<uint32_t>(per_desc);
+      const uint32_t jj = it / pd;
+      j = jj;
+      r = it - jj * pd;
+    } else {
+      j = item / per_desc;
+      r = static_cast<uint32_t>(item - j * per_desc);
+    }
+    const uint32_t cl = r / static_cast<uint32_t>(p.npieces);
+    q = static_cast<int32_t>(r - cl * static_cast<uint32_t>(p.npieces));
+    c = p.c0 + static_cast<int32_t>(cl);
   }
 };
 
@@ -188,6 +196,38 @@ __device__ __forceinline__ void unit_next(const SwapHeader& p, Unit& u, int k) {
 // blockDim.x / 32 = R independent rings per CTA (AQUA_OPT_TMA_VARIANT 2 is
 // R = 2; R = 1 is the product default): lane 0 of warp w drives ring w over the
 // w-th R-th of the CTA's item range, with its own stages and barriers.
+//
+// Dynamic distribution (p.work_ctr != nullptr, R = 1 only): the first
+// p.static_items items are split into one contiguous range per CTA; the rest
+// is cut into batches of p.batch items that CTAs claim with an atomicAdd on the
+// launch's counter, fetched one batch ahead so its latency hides behind the
+// ring (with no static head, CTA b starts on batch b).  Per-SM copy rates
+// differ by a few percent (ncu sm__cycles_active min/avg/max), so a purely
+// static split ends on the slowest SM; the claimed tail lets the fast ones
+// take more.  The loader runs ahead of the storer, so the batches it has
+// entered wait in a small queue.  p.batch > 0 without a counter deals the
+// batches round robin instead (b, b + G, ...; a tuning experiment).
+// Claim one batch.  atom.inc with bound 2^31 - 1 (= +1 for every count a
+// launch reaches), not atomicAdd: for a uniform-address add (and for inc with
+// bound 2^32 - 1, which ptxas rewrites as one) the compiler emits a
+// warp-aggregated atomic whose SHFL of the result waits for the atomic at
+// once; this inc is not aggregated, so the result is only waited for where it
+// is used, one batch later (SASS: ATOMG.E.INC, no SHFL).
+__device__ __forceinline__ uint32_t claim_one(uint32_t* ctr) {
+  uint32_t v;
+  asm volatile("atom.global.inc.u32 %0, [%1], 0x7FFFFFFF;" : "=r"(v) : "l"(ctr) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void dyn_finish(uint32_t* ctr) {
+  __threadfence();
+  if (atomicAdd(ctr + 1, 1u) == gridDim.x - 1) {   // last CTA: every claim is done
+    ctr[0] = 0;
+    ctr[1] = 0;
+    __threadfence();
+  }
+}
+
 template <Dir D, class P>
 __global__ void __launch_bounds__(128) swap_tma_kernel(const __grid_constant__ P p, const int stages) {
   extern __shared__ __align__(128) uint8_t smem_all[];
@@ -198,8 +238,41 @@ __global__ void __launch_bounds__(128) swap_tma_kernel(const __grid_constant__ P
   uint8_t* smem = smem_all + w * ring_bytes;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + size_t(stages) * stage_bytes);
   const int64_t G = gridDim.x * R, b = blockIdx.x * R + w;
-  const int64_t i0 = p.nitems * b / G, i1 = p.nitems * (b + 1) / G;
-  if (i1 <= i0) return;
+  const bool dyn = p.work_ctr != nullptr;
+  const bool batched = p.batch > 0;      // dynamic, or static round-robin batches (b, b + G, ...)
+  // dynamic with a static head: items [0, S0) in one contiguous range per
+  // CTA, then batches over [S0, nitems) claimed by whoever is free
+  const int64_t S0 = dyn ? p.static_items : 0;
+  const int64_t nbatch = batched ? (p.nitems - S0 + p.batch - 1) / p.batch : 0;
+  // The next batch id = raw + off: `raw` is the claim result (round robin:
+  // a count), kept apart from `off` so that nothing touches it before the
+  // switch that needs it and the atomic's latency stays hidden.
+  int64_t i0, i1, off = 0;
+  uint32_t raw = 0;
+  if (!batched) {
+    i0 = p.nitems * b / G;
+    i1 = p.nitems * (b + 1) / G;
+  } else if (dyn && S0 > 0) {
+    i0 = S0 * b / G;
+    i1 = S0 * (b + 1) / G;
+    raw = claim_one(p.work_ctr);
+  } else {
+    i0 = b * p.batch;
+    i1 = i0 + p.batch < p.nitems ? i0 + p.batch : p.nitems;
+    off = G;
+    raw = dyn ? claim_one(p.work_ctr) : static_cast<uint32_t>(b);
+  }
+  auto next_raw = [&](uint32_t r) { return dyn ? claim_one(p.work_ctr) : r + static_cast<uint32_t>(G); };
+  if (i1 <= i0) {                        // empty first range: start on the first claimed batch
+    const int64_t id = int64_t(raw) + off;
+    if (!dyn || id >= nbatch) {
+      if (dyn) dyn_finish(p.work_ctr);
+      return;
+    }
+    i0 = S0 + id * p.batch;
+    i1 = i0 + p.batch < p.nitems ? i0 + p.batch : p.nitems;
+    raw = next_raw(raw);
+  }
   for (int s = 0; s < stages; ++s) mbar_init(&bars[s], 1);
   fence_mbar_init();
   const uint64_t pol = policy_evict_first();
@@ -211,6 +284,16 @@ __global__ void __launch_bounds__(128) swap_tma_kernel(const __grid_constant__ P
     lu = Unit{cu.j, cu.c, cu.q, i1 - i0};
     su = lu;
   }
+  // batched: the ids of the batches the loader has entered but the storer
+  // has not (the loader runs up to stages - 1 units ahead)
+  int64_t queue[32];
+  int qh = 0, qt = 0;
+  auto open_batch = [&](int64_t id, Unit& u) {
+    const int64_t a = S0 + id * p.batch;
+    Cursor cu;
+    cu.init(a, p);
+    u = Unit{cu.j, cu.c, cu.q, (a + p.batch < p.nitems ? a + p.batch : p.nitems) - a};
+  };
   int lstage = 0, issued = 0;
   auto issue_load = [&]() {
     const int k = unit_len(p, lu);
@@ -234,6 +317,14 @@ __global__ void __launch_bounds__(128) swap_tma_kernel(const __grid_constant__ P
       }
     }
     unit_next(p, lu, k);
+    if (batched && lu.left == 0) {         // enter the next claimed batch, if any
+      const int64_t id = int64_t(raw) + off;
+      if (id < nbatch) {
+        queue[qt++ & 31] = id;
+        open_batch(id, lu);
+        raw = next_raw(raw);
+      }
+    }
     ++issued;
     if (++lstage == stages) lstage = 0;
   };
@@ -262,6 +353,7 @@ __global__ void __launch_bounds__(128) swap_tma_kernel(const __grid_constant__ P
     }
     bulk_commit();
     unit_next(p, su, k);
+    if (batched && su.left == 0 && qh != qt) open_batch(queue[qh++ & 31], su);
     if (++sstage == stages) {
       sstage = 0;
       parity ^= 1u;
@@ -272,6 +364,7 @@ __global__ void __launch_bounds__(128) swap_tma_kernel(const __grid_constant__ P
     }
   }
   bulk_wait<0>();
+  if (dyn) dyn_finish(p.work_ctr);
 }
 
 // Warp-specialised variant: warp 0 (one lane) only issues loads, warp 1 (one

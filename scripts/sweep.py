@@ -568,6 +568,54 @@ def tma_variants():
                           "in_hbm_GBps": round(2 * nblk * U / i / 1e6, 1)}), flush=True)
 
 
+def time_queued(ctx, stream, K=10, reps=3):
+    """Back-to-back device time per swap_out + swap_in pair, the calls queued
+    behind a sleep kernel (no host gaps): min over reps of (end - start) / K."""
+    best = 1e30
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            torch.cuda._sleep(20_000_000)
+        a.record(stream)
+        for _ in range(K):
+            ctx.swap_out([7], stream.cuda_stream)
+            ctx.swap_in([7], stream.cuda_stream)
+        b.record(stream)
+        torch.cuda.synchronize()
+        best = min(best, a.elapsed_time(b) / K)
+    return best
+
+
+def tma_sched():
+    """TMA engine work distribution: static contiguous ranges (0), dynamic
+    batches of n ring units (n > 0, with a statically split head of pct % of
+    the items), round-robin batches (-n); C2 and the C4 (70B/TP4, S = 8 KiB)
+    shape, all SMs and SM caps; back-to-back (queued) and per-call (ticket)
+    device times.  AQUA_SWEEP_SCHED = "n:pct,...", AQUA_SWEEP_CTAS = "0,64,16"."""
+    combos = [tuple(int(v) for v in x.split(":")) for x in
+              os.environ.get("AQUA_SWEEP_SCHED", "0:0,2:0,4:0,8:0,2:80,4:80,8:80,2:90,4:90,8:90,16:90").split(",")]
+    ctas_list = [int(x) for x in os.environ.get("AQUA_SWEEP_CTAS", "0,64,16").split(",")]
+    for name, (L, H, nblk) in (("c2", (32, 8, 2048)), ("c4", (80, 2, 4096))):
+        ctx, layers, arena, U = setup(L, 16, H, 128, 2 * nblk, nblk)
+        s = torch.cuda.Stream()
+        ctx.set_option(aqua.OPT_KERNEL, aqua.KERNEL_TMA)
+        for ctas in ctas_list:
+            ctx.set_option(aqua.OPT_MAX_CTAS, ctas)
+            for sc, pct in combos:
+                ctx.set_option(aqua.OPT_TMA_SCHED, sc)
+                ctx.set_option(aqua.OPT_TMA_STATIC_PCT, pct)
+                pair = time_queued(ctx, s)
+                o, i = time_tickets(ctx, 5, s)
+                print(json.dumps({"tma_sched": sc, "static_pct": pct, "shape": name, "ctas": ctas or 148,
+                                  "pair_ms": round(pair, 4), "swap_GBps": round(2 * nblk * U / pair / 1e6, 1),
+                                  "hbm_GBps": round(4 * nblk * U / pair / 1e6, 1),
+                                  "out_hbm_GBps": round(2 * nblk * U / o / 1e6, 1),
+                                  "in_hbm_GBps": round(2 * nblk * U / i / 1e6, 1)}), flush=True)
+        ctx.close()
+        del layers, arena
+        torch.cuda.empty_cache()
+
+
 def stages():
     L, bs, H, D, NB, nblk = 32, 16, 8, 128, 4096, 2048
     ctx, layers, arena, U = setup(L, bs, H, D, NB, nblk)
@@ -645,6 +693,8 @@ if __name__ == "__main__":
         self_ctas()
     elif what == "host_pcie":
         host_pcie()
+    elif what == "tma_sched":
+        tma_sched()
 
 
 def latency():

@@ -25,13 +25,22 @@ pytestmark = pytest.mark.gpu
 GOLD = os.path.join(os.path.dirname(__file__), "golden")
 ENGINES = {"tma": aqua.KERNEL_TMA, "ldst": aqua.KERNEL_LDST, "per_chunk": aqua.BASE_PER_CHUNK,
            "gather_temp": aqua.BASE_GATHER_TEMP, "batch": aqua.BASE_BATCH, "ce_host": aqua.KERNEL_CE_HOST,
-           "tma_ws": aqua.KERNEL_TMA, "tma_r2": aqua.KERNEL_TMA}
+           "tma_ws": aqua.KERNEL_TMA, "tma_r2": aqua.KERNEL_TMA, "tma_dyn": aqua.KERNEL_TMA,
+           "tma_dyn1": aqua.KERNEL_TMA, "tma_static": aqua.KERNEL_TMA, "tma_rr": aqua.KERNEL_TMA,
+           "tma_hyb": aqua.KERNEL_TMA}
 
 
 def _engine(ctx, name):
-    """Select an engine; "tma_ws" / "tma_r2" are the TMA engine's warp-specialised / two-ring variants."""
+    """Select an engine; "tma_ws" / "tma_r2" are the TMA engine's warp-specialised / two-ring variants,
+    "tma_dyn" / "tma_dyn1" its dynamic work distribution with batches of 8 / 1 ring units, "tma_rr" static
+    round-robin batches of 3 units, "tma_static" one contiguous item range per CTA, "tma_hyb" a static
+    head of 60 % of the items and dynamic batches of 2 units for the rest."""
     ctx.set_option(aqua.OPT_KERNEL, ENGINES[name])
     ctx.set_option(aqua.OPT_TMA_VARIANT, {"tma_ws": 1, "tma_r2": 2}.get(name, 0))
+    if name in ("tma_dyn", "tma_dyn1", "tma_static", "tma_rr", "tma_hyb"):
+        ctx.set_option(aqua.OPT_TMA_SCHED, {"tma_dyn": 8, "tma_dyn1": 1, "tma_static": 0, "tma_rr": -3,
+                                            "tma_hyb": 2}[name])
+        ctx.set_option(aqua.OPT_TMA_STATIC_PCT, 60 if name == "tma_hyb" else 0)
 
 
 def _ops(rig, ops, stream=0):
@@ -87,7 +96,7 @@ SHAPES = {
 
 
 @pytest.mark.parametrize("shape", list(SHAPES))
-@pytest.mark.parametrize("engine", ["tma", "tma_ws", "tma_r2", "ldst"])
+@pytest.mark.parametrize("engine", ["tma", "tma_ws", "tma_r2", "tma_dyn", "tma_dyn1", "tma_static", "tma_rr", "tma_hyb", "ldst"])
 @pytest.mark.parametrize("seed", [0, 1])
 @pytest.mark.parametrize("ctas", [0, 3])
 def test_random_sequences_bytes(shape, engine, seed, ctas):
@@ -263,7 +272,7 @@ def test_errors_leave_state_unchanged_and_no_cpu_fallback():
     assert c.launch_count() == n0 + 1         # the copy ran as one of our kernels
 
 
-@pytest.mark.parametrize("engine", ["tma", "tma_ws", "tma_r2", "ldst"])
+@pytest.mark.parametrize("engine", ["tma", "tma_ws", "tma_r2", "tma_dyn", "tma_dyn1", "tma_static", "tma_rr", "tma_hyb", "ldst"])
 @pytest.mark.parametrize("tier", ["small_inline", "big_inline", "staged_256", "staged_4064"])
 def test_descriptor_tiers_bytes(engine, tier):
     """Descriptor passing, whole-buffer compare (both directions, fragmented
@@ -302,7 +311,7 @@ def test_ticket_timing():
     assert e.value.code == aqua.E_STATE
 
 
-@pytest.mark.parametrize("engine", ["tma", "tma_ws", "tma_r2", "ldst"])
+@pytest.mark.parametrize("engine", ["tma", "tma_ws", "tma_r2", "tma_dyn", "tma_dyn1", "tma_static", "tma_rr", "tma_hyb", "ldst"])
 def test_migrate_reclaim_relend_bytes(engine):
     """NEXT-1 on the GPU: images move lender -> host (reclaim) and back
     (re-offer) through the fused arena->arena kernel, byte for byte with the
@@ -335,7 +344,7 @@ def test_migrate_reclaim_relend_bytes(engine):
     _ops(rig, [("in", [1, 2, 3]), ("out", [2])])
 
 
-@pytest.mark.parametrize("engine", ["tma", "tma_ws", "tma_r2", "ldst"])
+@pytest.mark.parametrize("engine", ["tma", "tma_ws", "tma_r2", "tma_dyn", "tma_dyn1", "tma_static", "tma_rr", "tma_hyb", "ldst"])
 def test_prefix_cache_bytes(engine):
     """NEXT-2 on the GPU: store a cached prefix (copy), load it into three
     new prompts, reclaim moves it to the host, load again -- whole buffers
@@ -547,7 +556,7 @@ def test_pattern_batch_kernel_matches_oracle_words():
     rig.assert_bytes_equal("pattern batch")
 
 
-@pytest.mark.parametrize("engine", ["tma", "tma_ws", "tma_r2", "ldst"])
+@pytest.mark.parametrize("engine", ["tma", "tma_ws", "tma_r2", "tma_dyn", "tma_dyn1", "tma_static", "tma_rr", "tma_hyb", "ldst"])
 def test_many_small_blocks_whole_buffer(engine):
     """Scale edge: 131,072 blocks of S = 256 B (100,000-block prompt, 800 KB of
     staged descriptors, slot ids > 2^16), whole pool / arena compared with
@@ -559,3 +568,27 @@ def test_many_small_blocks_whole_buffer(engine):
     perm = block_permutation(NB, NB, seed=13).tolist()
     _ops(rig, [("adopt", (1, perm[:100000])), ("adopt", (2, perm[100000:100500])), ("out", [1]),
                ("alloc", (3, 20000)), ("in", [1])])
+
+
+def test_dynamic_schedule_counter_reuse_across_streams():
+    """Dynamically scheduled TMA launches claim batches through one of 256
+    per-context counter pairs; 600 launches on three streams cycle through
+    every pair more than twice (a pair is reused only after its last launch's
+    ticket), and the bytes still equal the oracle's sequential execution."""
+    rig = Rig(L=2, bs=16, H=2, D=64, NB=96, lender_slots=64, host_slots=0, seed=3)
+    c, o = rig.ctx, rig.opool
+    c.set_option(aqua.OPT_KERNEL, aqua.KERNEL_TMA)
+    c.set_option(aqua.OPT_TMA_SCHED, 1)
+    c.set_option(aqua.OPT_MAX_CTAS, 5)
+    streams = [torch.cuda.Stream() for _ in range(3)]
+    for p in range(6):
+        assert c.alloc_blocks(p, 5) == o.alloc_blocks(p, 5)
+    rnd = random.Random(7)
+    n0 = c.launch_count()
+    for step in range(300):
+        sel = rnd.sample(range(6), rnd.randint(1, 3))
+        c.swap_out(sel, rnd.choice(streams).cuda_stream)
+        o.swap_out(sel)
+        assert c.swap_in(sel, rnd.choice(streams).cuda_stream)[0] == o.swap_in(sel)
+    assert c.launch_count() - n0 == 600
+    rig.assert_bytes_equal("600 dynamically scheduled launches")
