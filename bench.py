@@ -67,6 +67,17 @@ def _peaks():
 
 
 NVLINK_MEASURED = 770.0   # GB/s per direction, peer copy (B200_PROFILING.md); 900 nominal
+# The paper's end-to-end results on 8x H100-80G, quoted as context only; the paper
+# gives no swap GB/s or per-prompt swap latency for its own path.
+PAPER_CONTEXT = {
+    "ttft_under_burst": "20x lower than vLLM FCFS; 8x H100-80G, Llama-3.1-70B TP2, ShareGPT, 25 prompts then 2x rate "
+                        "for 1 min (P:57, P:983-985)",
+    "long_prompt_throughput": "4x vs FlexGen paging to DRAM (BASELINE.json says vLLM; the paper's baseline is FlexGen); "
+                              "8x H100-80G, OPT-30B, 8192-token prompts (P:57, P:1009)",
+    "a100_nvlink_copy": "50 GB/s at 4 MB, 200 GB/s at 64 MB, 2x A100-80GB (P:846-848)",
+    "here": "C3 responsiveness model on one B200 (profiles/r01_c3_model_*.json): CFS TTFT p50 28x below FCFS; "
+            "paging to the lender vs host DRAM keeps TPOT p99 1.8x lower",
+}
 
 
 class ClockSampler:
@@ -457,6 +468,8 @@ def run_ours(args):
         "parity": f"pattern verify: {mism} mismatching words over all {len(PIDS)} prompt(s) "
                   f"({NBLK * SHAPE['bs']} tokens) after {args.warmup + K} preempt/resume cycles",
         "host_baseline": host,
+        "preempt_resume_vs_host": (round(host["best_preempt_resume_ms"] / (out_avg + in_avg), 1) if host else None),
+        "paper_context": PAPER_CONTEXT,
     }
     print(json.dumps(line), flush=True)
     _cleanup(aqua, local, ipc_ptr, imported, ws)

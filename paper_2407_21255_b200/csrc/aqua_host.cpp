@@ -956,16 +956,20 @@ static aqua_status plan_out(aqua_ctx* c, int32_t n, const uint64_t* pids, std::v
     }
   }
   slots->assign(n, {});
-  auto git = c->gpu.free.begin();
-  auto hit = c->host.free.begin();
+  size_t total = 0;
+  for (int32_t i = 0; i < n; ++i) total += (*ps)[i]->ids.size();
+  ds->resize(total);
+  Desc* dp = ds->data();
+  aqua::IdSet::Scan gs = c->gpu.free.scan(), hs = c->host.free.scan();
   for (int32_t i = 0; i < n; ++i) {
-    auto& itr = (*loc)[i] == AQUA_LOC_PEER ? git : hit;
+    const std::vector<int32_t>& ids = (*ps)[i]->ids;
+    const int32_t np = static_cast<int32_t>(ids.size());
+    std::vector<int32_t>& sv = (*slots)[i];
+    sv.resize(np);
+    aqua::IdSet::fill((*loc)[i] == AQUA_LOC_PEER ? gs : hs, np, sv.data());   // lowest free slots (R4)
     const uint32_t bit = (*loc)[i] == AQUA_LOC_HOST ? kArenaBit : 0u;
-    for (int32_t b : (*ps)[i]->ids) {
-      const int32_t sl = *itr++;
-      (*slots)[i].push_back(sl);
-      ds->push_back(Desc{b, static_cast<uint32_t>(sl) | bit});
-    }
+    for (int32_t k = 0; k < np; ++k) dp[k] = Desc{ids[k], static_cast<uint32_t>(sv[k]) | bit};
+    dp += np;
   }
   return AQUA_OK;
 }
@@ -979,21 +983,19 @@ static aqua_status swap_out_impl(aqua_ctx* c, int32_t n, const uint64_t* pids, a
   std::vector<std::vector<int32_t>> slots;
   std::vector<Desc> ds;
   if (aqua_status s = plan_out(c, n, pids, &ps, &loc, &slots, &ds)) return s;
-  set_last(c, ds);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   uint64_t ticket = 0;
   if (aqua_status s = launch(c, ds, aqua::kOut, st, &ticket, layer_group, group_tickets)) return s;
+  set_last(c, ds);
   // commit bookkeeping
   for (int32_t i = 0; i < n; ++i) {
     Arena* a = arena_of(c, loc[i]);
-    for (int32_t s : slots[i]) {
-      a->free.erase(s);
-      a->tick[s] = ticket;
-    }
-    for (int32_t b : ps[i]->ids) {
-      c->free_blocks.insert(b);
-      c->btick[b] = ticket;
-    }
+    a->free.erase_all(slots[i].data(), slots[i].size());
+    uint64_t* st_tick = a->tick.data();
+    for (int32_t s : slots[i]) st_tick[s] = ticket;
+    c->free_blocks.insert_all(ps[i]->ids.data(), ps[i]->ids.size());
+    uint64_t* bt_tick = c->btick.data();
+    for (int32_t b : ps[i]->ids) bt_tick[b] = ticket;
     ps[i]->state = AQUA_ST_SWAPPED;
     ps[i]->loc = loc[i];
     ps[i]->ids = std::move(slots[i]);
@@ -1024,30 +1026,33 @@ static aqua_status swap_in_impl(aqua_ctx* c, int32_t n, const uint64_t* pids, aq
   if (n > 0 && !out_counts) return fail(c, AQUA_E_INVAL, "null out_counts");
   if (need > static_cast<int64_t>(c->free_blocks.size())) return fail(c, AQUA_E_NOBLOCKS, "pool exhausted");
   std::vector<Desc> ds;
+  ds.resize(static_cast<size_t>(need));
+  Desc* dp = ds.data();
   std::vector<std::vector<int32_t>> fresh(n);
-  auto fb = c->free_blocks.begin();
+  aqua::IdSet::Scan fs = c->free_blocks.scan();
   for (int32_t i = 0; i < n; ++i) {
+    const std::vector<int32_t>& sl = ps[i]->ids;
+    const int32_t np = static_cast<int32_t>(sl.size());
+    fresh[i].resize(np);
+    aqua::IdSet::fill(fs, np, fresh[i].data());                               // lowest free blocks (R4)
     const uint32_t bit = ps[i]->loc == AQUA_LOC_HOST ? kArenaBit : 0u;
-    for (int32_t s : ps[i]->ids) {
-      const int32_t b = *fb++;
-      fresh[i].push_back(b);
-      ds.push_back(Desc{b, static_cast<uint32_t>(s) | bit});
-    }
+    for (int32_t k = 0; k < np; ++k) dp[k] = Desc{fresh[i][k], static_cast<uint32_t>(sl[k]) | bit};
+    dp += np;
   }
-  set_last(c, ds);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   uint64_t ticket = 0;
   if (aqua_status s = launch(c, ds, aqua::kIn, st, &ticket, layer_group, group_tickets)) return s;
+  set_last(c, ds);
   c->free_blocks.erase_lowest(static_cast<int32_t>(need));
   int64_t k = 0;
   for (int32_t i = 0; i < n; ++i) {
     Arena* a = arena_of(c, ps[i]->loc);
-    for (int32_t s : ps[i]->ids) {
-      a->free.insert(s);
-      a->tick[s] = ticket;
-    }
+    a->free.insert_all(ps[i]->ids.data(), ps[i]->ids.size());
+    uint64_t* st_tick = a->tick.data();
+    for (int32_t s : ps[i]->ids) st_tick[s] = ticket;
+    uint64_t* bt_tick = c->btick.data();
     for (int32_t b : fresh[i]) {
-      c->btick[b] = ticket;
+      bt_tick[b] = ticket;
       out_ids[k++] = b;
     }
     out_counts[i] = static_cast<int32_t>(fresh[i].size());

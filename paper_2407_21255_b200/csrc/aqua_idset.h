@@ -75,6 +75,73 @@ class IdSet {
     return iterator(this, lo_);
   }
 
+  // Bulk insert / erase of n ids (same semantics as n single calls), with
+  // the counters kept in locals.
+  void insert_all(const int32_t* ids, size_t n) {
+    uint64_t* w = w_.data();
+    int32_t cnt = count_, lo = lo_;
+    for (size_t i = 0; i < n; ++i) {
+      const int32_t id = ids[i];
+      uint64_t& x = w[id >> 6];
+      const uint64_t b = uint64_t(1) << (id & 63);
+      if (!(x & b)) {
+        x |= b;
+        ++cnt;
+        if ((id >> 6) < lo) lo = id >> 6;
+      }
+    }
+    count_ = cnt;
+    lo_ = lo;
+  }
+  void erase_all(const int32_t* ids, size_t n) {
+    uint64_t* w = w_.data();
+    int32_t cnt = count_;
+    for (size_t i = 0; i < n; ++i) {
+      const int32_t id = ids[i];
+      uint64_t& x = w[id >> 6];
+      const uint64_t b = uint64_t(1) << (id & 63);
+      if (x & b) {
+        x &= ~b;
+        --cnt;
+      }
+    }
+    count_ = cnt;
+  }
+
+  // Ascending scan over the free ids that leaves the set unchanged; fill()
+  // writes the next k ids (fewer if the set runs out) with the scan state in
+  // locals, a few cycles per id.
+  struct Scan {
+    const uint64_t* w;
+    int32_t nw, word;
+    uint64_t bits;
+  };
+  Scan scan() {
+    const int32_t nw = static_cast<int32_t>(w_.size());
+    while (lo_ < nw && !w_[lo_]) ++lo_;
+    return Scan{w_.data(), nw, lo_, lo_ < nw ? w_[lo_] : 0};
+  }
+  static int32_t fill(Scan& s, int32_t k, int32_t* out) {
+    const uint64_t* w = s.w;
+    int32_t word = s.word, got = 0;
+    uint64_t bits = s.bits;
+    while (got < k) {
+      while (!bits) {
+        if (++word >= s.nw) {
+          s.word = word;
+          s.bits = 0;
+          return got;
+        }
+        bits = w[word];
+      }
+      out[got++] = word * 64 + __builtin_ctzll(bits);
+      bits &= bits - 1;
+    }
+    s.word = word;
+    s.bits = bits;
+    return got;
+  }
+
   // Remove the k lowest free ids (k <= size()).
   void erase_lowest(int32_t k) {
     const int32_t nw = static_cast<int32_t>(w_.size());

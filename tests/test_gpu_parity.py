@@ -467,15 +467,20 @@ def test_multistream_fuzz_equals_sequential(seed):
 
 
 @pytest.mark.parametrize("pieces", [1, 3, 8])
-@pytest.mark.parametrize("arena", ["lender", "host", "host_ce"])
+@pytest.mark.parametrize("arena", ["lender", "lender_dyn", "host", "host_ce"])
 def test_swap_exchange_bytes(pieces, arena):
     """aqua_swap_exchange == swap_out then swap_in (oracle), byte for byte,
     with the resume on another stream pipelined behind the preemption pieces
-    whose blocks it reuses."""
-    rig = Rig(L=3, bs=16, H=4, D=64, NB=40, lender_slots=30 if arena == "lender" else 0, host_slots=40)
+    whose blocks it reuses ("lender_dyn": both directions' kernels claim
+    1-unit batches from their own counters while they run concurrently)."""
+    rig = Rig(L=3, bs=16, H=4, D=64, NB=40, lender_slots=30 if arena in ("lender", "lender_dyn") else 0,
+              host_slots=40)
     c, o = rig.ctx, rig.opool
     if arena == "host_ce":
         c.set_option(aqua.OPT_KERNEL, aqua.KERNEL_CE_HOST)
+    if arena == "lender_dyn":
+        c.set_option(aqua.OPT_TMA_SCHED, 1)
+        c.set_option(aqua.OPT_TMA_PIECE, 4096)        # S = 8 KiB -> 2 pieces per chunk, many units
     perm = block_permutation(40, 40, seed=11).tolist()
     for pid, k in ((1, 6), (2, 5), (3, 7), (4, 9)):
         ids, perm = perm[:k], perm[k:]
