@@ -130,7 +130,7 @@ enum {
   AQUA_OPT_TMA_SCHED = 9,     /* TMA engine (variant 0) work distribution: 0 = each CTA one contiguous item range;
                                  n > 0 = batches of n ring units claimed dynamically (atomic counter per launch);
                                  -n = batches of n units dealt round robin (CTA b: b, b + grid, ...);
-                                 AQUA_TMA_SCHED_AUTO (default) = 4-unit claimed batches when the launch has one CTA
+                                 AQUA_TMA_SCHED_AUTO (default) = 2-unit claimed batches when the launch has one CTA
                                  per SM and >= 8 batches per CTA, else 0 (profiles/r01_tma_sched*.jsonl) */
   AQUA_OPT_TMA_STATIC_PCT = 10 /* dynamic schedule: percent of the items split statically (one contiguous range per
                                  CTA) before the claimed batches; 0 = all claimed */

@@ -468,15 +468,15 @@ aqua_status run_copy(aqua_ctx* c, const std::vector<Desc>& ds, aqua::Dir dir, cu
       p.piece = piece;
       p.npieces = static_cast<int32_t>((c->S + piece - 1) / piece);
       p.nitems = p.ndesc * nc * p.npieces;
-      // work distribution: AUTO = claimed 4-unit batches when every SM runs
-      // one CTA and each gets >= 8 batches (they reach 6.68-6.81 TB/s vs 6.51
-      // for static ranges on C2, 6.58-6.61 vs 6.36 on C4); under an SM cap
+      // work distribution: AUTO = claimed 2-unit batches (with a 4-stage
+      // ring) when every SM runs one CTA and each gets >= 8 batches: 6.79 /
+      // 6.72 TB/s on C2 / C4 vs 6.52 / 6.37 for static ranges; under an SM cap
       // static ranges are as fast or faster (profiles/r01_tma_sched*.jsonl)
       int sched = c->tma_sched;
       if (sched == AQUA_TMA_SCHED_AUTO) {
         const bool all_sms = cap == 0 || cap >= c->num_sms;
         const int64_t units = p.nitems / p.group;
-        sched = all_sms && units >= int64_t(c->num_sms) * 4 * 8 ? 4 : 0;
+        sched = all_sms && units >= int64_t(c->num_sms) * 2 * 8 ? 2 : 0;
       }
       if (sched > 0 && c->tma_variant == 0 && c->d_ctr) {
         // dynamic batches of `sched` units; the counter pair's previous

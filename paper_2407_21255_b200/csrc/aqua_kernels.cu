@@ -670,6 +670,9 @@ cudaError_t launch_tma_t(const P& p, Dir dir, int num_sms, int grid_cap, int sta
     const int64_t per_cta = (want_inflight + int64_t(grid) * stage_bytes - 1) / (int64_t(grid) * stage_bytes);
     stages = static_cast<int>(std::min<int64_t>(per_cta + 1, std::max(3, (200 * 1024) / stage_bytes)));
     stages = std::max(stages, 3);
+    // claimed batches run best one stage deeper: 4 x 32 KiB at 148 CTAs
+    // (profiles/r01_tma_sched6.jsonl: C2 6.79 vs 6.74 TB/s, C4 6.72 vs 6.54)
+    if (p.work_ctr) stages = std::max(stages, 4);
   }
   stages = std::max(2, std::min(stages, 32));
   const int bar_extra = variant == 1 ? 8 : 0;   // the "empty" barriers of the warp-specialised variant
