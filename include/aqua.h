@@ -122,8 +122,9 @@ enum {
   AQUA_OPT_TIMING = 5,        /* 1: each swap also records a start event; aqua_ticket_elapsed gives its device time */
   AQUA_OPT_LDST_VARIANT = 6,  /* LDST engine flavour: 0 streaming hints, 1 plain, 2 (default) software-pipelined */
   AQUA_OPT_TMA_VARIANT = 7,   /* TMA engine: 0 (default) one ring per CTA; 1 warp-specialised (load warp + store
-                                 warp); 2 two independent rings per CTA (one issuing warp each).  All three reach the
-                                 same HBM rate (profiles/r01_tma_variants.jsonl, r01_tma_rings.jsonl) */
+                                 warp); 2 two independent rings per CTA (one issuing warp each); 3 hybrid: the ring
+                                 plus 8 warps copying claimed batches through registers.  0-2 reach the same HBM
+                                 rate (profiles/r01_tma_variants.jsonl, r01_tma_rings.jsonl) */
   AQUA_OPT_INLINE_MAX = 8,    /* largest call (in blocks, per launch) whose descriptors ride in the kernel
                                  parameters instead of a pinned-ring upload + H2D copy: 0..4064 (default 4064,
                                  the 32,764-byte parameter limit of CUDA 12.1+; 256 = the small parameter block) */

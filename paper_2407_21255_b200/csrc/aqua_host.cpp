@@ -468,17 +468,29 @@ aqua_status run_copy(aqua_ctx* c, const std::vector<Desc>& ds, aqua::Dir dir, cu
       p.piece = piece;
       p.npieces = static_cast<int32_t>((c->S + piece - 1) / piece);
       p.nitems = p.ndesc * nc * p.npieces;
-      // work distribution: AUTO = claimed 2-unit batches (with a 4-stage
-      // ring) when every SM runs one CTA and each gets >= 8 batches: 6.79 /
-      // 6.72 TB/s on C2 / C4 vs 6.52 / 6.37 for static ranges; under an SM cap
-      // static ranges are as fast or faster (profiles/r01_tma_sched*.jsonl)
-      int sched = c->tma_sched;
+      // work distribution, AUTO:
+      // * every SM runs one CTA and each gets >= 8 batches: claimed 2-unit
+      //   batches with a 4-stage ring, 6.80 / 6.71 TB/s on C2 / C4 vs 6.52 /
+      //   6.37 for static ranges (profiles/r01_tma_sched*.jsonl);
+      // * under an SM cap, chunks smaller than a stage (several bulk ops per
+      //   unit, C4): the hybrid ring + LDST warps with 8-unit batches, 92-94
+      //   vs 73 GB/s per SM (r01_hybrid.jsonl); larger chunks: static ranges,
+      //   which already reach the ~100 GB/s per-SM limit.
+      int sched = c->tma_sched, variant = c->tma_variant;
       if (sched == AQUA_TMA_SCHED_AUTO) {
         const bool all_sms = cap == 0 || cap >= c->num_sms;
         const int64_t units = p.nitems / p.group;
-        sched = all_sms && units >= int64_t(c->num_sms) * 2 * 8 ? 2 : 0;
+        const int grid = static_cast<int>(std::min<int64_t>(all_sms ? c->num_sms : cap, p.nitems));
+        if (all_sms)
+          sched = units >= int64_t(c->num_sms) * 2 * 8 ? 2 : 0;
+        else if (p.group > 1 && !all_host && variant == 0 && units >= int64_t(grid) * 8 * 8)
+          sched = 8, variant = 3;
+        else
+          sched = 0;
       }
-      if (sched > 0 && c->tma_variant == 0 && c->d_ctr) {
+      const bool hybrid = variant == 3;          // TMA ring + LDST warps: always claimed batches
+      if (hybrid && sched <= 0) sched = 2;
+      if (sched > 0 && (variant == 0 || hybrid) && c->d_ctr) {
         // dynamic batches of `sched` units; the counter pair's previous
         // launch must be done with it (stream order or its ticket)
         const int slot = static_cast<int>(c->ctr_next++ % aqua::kCtrSlots);
@@ -487,10 +499,11 @@ aqua_status run_copy(aqua_ctx* c, const std::vector<Desc>& ds, aqua::Dir dir, cu
         p.work_ctr = c->d_ctr + 2 * slot;
         p.batch = sched * p.group;
         p.static_items = p.nitems * c->tma_static_pct / 100;
-      } else if (sched < 0 && c->tma_variant == 0) {
+      } else if (sched < 0 && variant == 0) {
         p.batch = -sched * p.group;            // static round-robin batches
       }
-      e = aqua::launch_swap_tma(p, inl, dir, c->num_sms, cap, c->tma_stages, st, &ctas, c->tma_variant);
+      e = aqua::launch_swap_tma(p, inl, dir, c->num_sms, cap, c->tma_stages, st, &ctas,
+                                hybrid && !p.work_ctr ? 0 : variant);
     } else {
       p.piece = 4096;
       p.group = 1;
@@ -1621,7 +1634,7 @@ aqua_status aqua_set_option(aqua_ctx* c, int32_t opt, int64_t v) {
       c->ldst_variant = static_cast<int>(v);
       return AQUA_OK;
     case AQUA_OPT_TMA_VARIANT:
-      if (v < 0 || v > 2) return fail(c, AQUA_E_INVAL, "tma variant");
+      if (v < 0 || v > 3) return fail(c, AQUA_E_INVAL, "tma variant");
       c->tma_variant = static_cast<int>(v);
       return AQUA_OK;
     case AQUA_OPT_INLINE_MAX:

@@ -222,21 +222,94 @@ __device__ __forceinline__ uint32_t claim_one(uint32_t* ctr) {
   return v;
 }
 
-__device__ __forceinline__ void dyn_finish(uint32_t* ctr) {
+// Called once by every claiming worker (`total` of them) after its last
+// claim; the last one resets the counter pair for the next launch.
+__device__ __forceinline__ void dyn_finish(uint32_t* ctr, uint32_t total) {
   __threadfence();
-  if (atomicAdd(ctr + 1, 1u) == gridDim.x - 1) {   // last CTA: every claim is done
+  if (atomicAdd(ctr + 1, 1u) == total - 1) {       // last worker: every claim is done
     ctr[0] = 0;
     ctr[1] = 0;
     __threadfence();
   }
 }
 
+// Hybrid variant (LW > 0 LDST warps, AQUA_OPT_TMA_VARIANT 3): besides the
+// TMA ring of warp 0, warps 1..LW claim batches of the same launch and copy
+// them item by item with 16-byte loads and stores through registers, two
+// rounds in flight per warp.  A CTA's TMA engine moves at most ~100 GB/s of
+// read + write (profiles/r01_tma_rings.jsonl: the same at 4 and 6 stages), so
+// under an SM cap the register path adds a second mover on the same SM.
 template <Dir D, class P>
-__global__ void __launch_bounds__(128) swap_tma_kernel(const __grid_constant__ P p, const int stages) {
+__device__ __forceinline__ void ldst_worker(const P& p, int64_t off, uint32_t total) {
+  const int lane = threadIdx.x & 31;
+  const int64_t S0 = p.static_items;
+  const int64_t nbatch = (p.nitems - S0 + p.batch - 1) / p.batch;
+  uint32_t raw = lane == 0 ? claim_one(p.work_ctr) : 0u;
+  int64_t id = int64_t(__shfl_sync(0xffffffffu, raw, 0)) + off;
+  while (id < nbatch) {
+    raw = lane == 0 ? claim_one(p.work_ctr) : 0u;       // the next batch, used after this one
+    const int64_t a = S0 + id * p.batch;
+    const int64_t e = a + p.batch < p.nitems ? a + p.batch : p.nitems;
+    Cursor cu;
+    cu.init(a, p);
+    int64_t j = cu.j;
+    int32_t c = cu.c, q = cu.q;
+    int4 va[8], vb[8];
+    for (int64_t it = a; it < e; ++it) {
+      const uint8_t* src;
+      uint8_t* dst;
+      uint32_t bytes;
+      item_addrs<D>(p, desc_at(p, j), c, q, src, dst, bytes);
+      const int nvec = static_cast<int>(bytes >> 4);
+      // rounds of 32 lanes x 8 vectors (4 KiB), ping-ponging between two
+      // register sets: round r + 1's loads are issued before round r's stores
+      auto load = [&](int4* v, int base) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int idx = base + u * 32 + lane;
+          if (idx < nvec) v[u] = ld_stream(src + size_t(idx) * 16);
+        }
+      };
+      auto store = [&](const int4* v, int base) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int idx = base + u * 32 + lane;
+          if (idx < nvec) st_stream(dst + size_t(idx) * 16, v[u]);
+        }
+      };
+      load(va, 0);
+      for (int base = 0; base < nvec; base += 512) {
+        if (base + 256 < nvec) load(vb, base + 256);
+        store(va, base);
+        if (base + 256 >= nvec) break;
+        if (base + 512 < nvec) load(va, base + 512);
+        store(vb, base + 256);
+      }
+      if (++q == p.npieces) {
+        q = 0;
+        if (++c == p.c0 + p.nc) {
+          c = p.c0;
+          ++j;
+        }
+      }
+    }
+    id = int64_t(__shfl_sync(0xffffffffu, raw, 0)) + off;
+  }
+  if (lane == 0) dyn_finish(p.work_ctr, total);
+}
+
+template <Dir D, class P, int LW>
+__global__ void __launch_bounds__(LW > 0 ? 32 * (1 + LW) : 128) swap_tma_kernel(const __grid_constant__ P p,
+                                                                                const int stages) {
   extern __shared__ __align__(128) uint8_t smem_all[];
+  const uint32_t workers = gridDim.x * (1 + LW);   // claiming workers (LW > 0: every warp claims)
+  if (LW > 0 && threadIdx.x >= 32) {
+    ldst_worker<D>(p, p.static_items > 0 ? 0 : int64_t(gridDim.x), workers);
+    return;
+  }
   if ((threadIdx.x & 31) != 0) return;
   const int64_t stage_bytes = int64_t(p.piece) * p.group;
-  const int64_t R = blockDim.x >> 5, w = threadIdx.x >> 5;
+  const int64_t R = LW > 0 ? 1 : blockDim.x >> 5, w = threadIdx.x >> 5;
   const int64_t ring_bytes = (stage_bytes * stages + 8 * stages + 127) & ~int64_t(127);
   uint8_t* smem = smem_all + w * ring_bytes;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + size_t(stages) * stage_bytes);
@@ -269,7 +342,7 @@ __global__ void __launch_bounds__(128) swap_tma_kernel(const __grid_constant__ P
   if (i1 <= i0) {                        // empty first range: start on the first claimed batch
     const int64_t id = int64_t(raw) + off;
     if (!dyn || id >= nbatch) {
-      if (dyn) dyn_finish(p.work_ctr);
+      if (dyn) dyn_finish(p.work_ctr, workers);
       return;
     }
     i0 = S0 + id * p.batch;
@@ -367,7 +440,7 @@ __global__ void __launch_bounds__(128) swap_tma_kernel(const __grid_constant__ P
     }
   }
   bulk_wait<0>();
-  if (dyn) dyn_finish(p.work_ctr);
+  if (dyn) dyn_finish(p.work_ctr, workers);
 }
 
 // Warp-specialised variant: warp 0 (one lane) only issues loads, warp 1 (one
@@ -680,6 +753,7 @@ cudaError_t launch_tma_t(const P& p, Dir dir, int num_sms, int grid_cap, int sta
   stages = std::max(2, std::min(stages, 32));
   const int bar_extra = variant == 1 ? 8 : 0;   // the "empty" barriers of the warp-specialised variant
   const int rings = variant == 2 ? 2 : 1;
+  constexpr int kLdstWarps = 8;                  // variant 3: TMA ring + 8 LDST warps per CTA
   if (rings > 1 && stages_opt <= 0) stages = std::max(3, (stages + rings - 1) / rings + 1);
   auto smem_for = [&](int st) {
     return rings == 1 ? tma_smem_bytes(stage_bytes, st) + bar_extra * st
@@ -689,37 +763,51 @@ cudaError_t launch_tma_t(const P& p, Dir dir, int num_sms, int grid_cap, int sta
   if (smem_for(stages) > 227 * 1024) return cudaErrorInvalidConfiguration;
   const int smem = smem_for(stages);
   // the opt-in smem attribute is per device and per instantiation; set once
-  static thread_local bool set_smem[2][3][64] = {};
+  static thread_local bool set_smem[3][3][64] = {};
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
-  const int vi = variant == 1 ? 1 : 0;
+  const int vi = variant == 1 ? 1 : variant == 3 ? 2 : 0;
   bool& have = set_smem[vi][dir][dev & 63];
   if (!have) {
-    if (vi)
+    if (vi == 1)
       e = cudaFuncSetAttribute(dir == kOut ? swap_tma_ws_kernel<kOut, P>
                                : dir == kIn ? swap_tma_ws_kernel<kIn, P> : swap_tma_ws_kernel<kMig, P>,
                                cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    else if (vi == 2)
+      e = cudaFuncSetAttribute(dir == kOut ? swap_tma_kernel<kOut, P, kLdstWarps>
+                               : dir == kIn ? swap_tma_kernel<kIn, P, kLdstWarps>
+                                            : swap_tma_kernel<kMig, P, kLdstWarps>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     else
-      e = cudaFuncSetAttribute(dir == kOut ? swap_tma_kernel<kOut, P>
-                               : dir == kIn ? swap_tma_kernel<kIn, P> : swap_tma_kernel<kMig, P>,
+      e = cudaFuncSetAttribute(dir == kOut ? swap_tma_kernel<kOut, P, 0>
+                               : dir == kIn ? swap_tma_kernel<kIn, P, 0> : swap_tma_kernel<kMig, P, 0>,
                                cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e != cudaSuccess) return e;
     have = true;
   }
-  if (vi) {
+  if (vi == 1) {
     if (dir == kOut)
       swap_tma_ws_kernel<kOut, P><<<grid, 64, smem, s>>>(p, stages);
     else if (dir == kIn)
       swap_tma_ws_kernel<kIn, P><<<grid, 64, smem, s>>>(p, stages);
     else
       swap_tma_ws_kernel<kMig, P><<<grid, 64, smem, s>>>(p, stages);
+  } else if (vi == 2) {
+    if (!p.work_ctr) return cudaErrorInvalidValue;    // the LDST warps only claim batches
+    constexpr int nt = 32 * (1 + kLdstWarps);
+    if (dir == kOut)
+      swap_tma_kernel<kOut, P, kLdstWarps><<<grid, nt, smem, s>>>(p, stages);
+    else if (dir == kIn)
+      swap_tma_kernel<kIn, P, kLdstWarps><<<grid, nt, smem, s>>>(p, stages);
+    else
+      swap_tma_kernel<kMig, P, kLdstWarps><<<grid, nt, smem, s>>>(p, stages);
   } else if (dir == kOut) {
-    swap_tma_kernel<kOut, P><<<grid, 32 * rings, smem, s>>>(p, stages);
+    swap_tma_kernel<kOut, P, 0><<<grid, 32 * rings, smem, s>>>(p, stages);
   } else if (dir == kIn) {
-    swap_tma_kernel<kIn, P><<<grid, 32 * rings, smem, s>>>(p, stages);
+    swap_tma_kernel<kIn, P, 0><<<grid, 32 * rings, smem, s>>>(p, stages);
   } else {
-    swap_tma_kernel<kMig, P><<<grid, 32 * rings, smem, s>>>(p, stages);
+    swap_tma_kernel<kMig, P, 0><<<grid, 32 * rings, smem, s>>>(p, stages);
   }
   if (ctas_used) *ctas_used = grid;
   return cudaGetLastError();

@@ -620,6 +620,28 @@ def tma_sched():
         torch.cuda.empty_cache()
 
 
+def hybrid():
+    """TMA ring alone (variant 0) vs ring + 8 LDST warps (variant 3) under SM
+    caps, C2 and C4 shapes, back-to-back device time."""
+    for name, (L, H, nblk) in (("c2", (32, 8, 2048)), ("c4", (80, 2, 4096))):
+        ctx, layers, arena, U = setup(L, 16, H, 128, 2 * nblk, nblk)
+        s = torch.cuda.Stream()
+        ctx.set_option(aqua.OPT_KERNEL, aqua.KERNEL_TMA)
+        for ctas in (148, 96, 64, 32, 16, 8):
+            ctx.set_option(aqua.OPT_MAX_CTAS, ctas)
+            for v, sc in ((0, aqua.TMA_SCHED_AUTO), (0, 2), (3, 2), (3, 8)):
+                ctx.set_option(aqua.OPT_TMA_VARIANT, v)
+                ctx.set_option(aqua.OPT_TMA_SCHED, sc)
+                pair = time_queued(ctx, s, K=10, reps=3)
+                print(json.dumps({"hybrid": v, "sched": "auto" if sc == aqua.TMA_SCHED_AUTO else sc, "shape": name,
+                                  "ctas": ctas, "pair_ms": round(pair, 4),
+                                  "hbm_GBps": round(4 * nblk * U / pair / 1e6, 1),
+                                  "per_sm_GBps": round(4 * nblk * U / pair / 1e6 / ctas, 1)}), flush=True)
+        ctx.close()
+        del layers, arena
+        torch.cuda.empty_cache()
+
+
 def stages():
     L, bs, H, D, NB, nblk = 32, 16, 8, 128, 4096, 2048
     ctx, layers, arena, U = setup(L, bs, H, D, NB, nblk)
@@ -699,6 +721,8 @@ if __name__ == "__main__":
         host_pcie()
     elif what == "tma_sched":
         tma_sched()
+    elif what == "hybrid":
+        hybrid()
 
 
 def latency():
