@@ -596,6 +596,7 @@ def tma_sched():
               os.environ.get("AQUA_SWEEP_SCHED", "0:0,2:0,4:0,8:0,2:80,4:80,8:80,2:90,4:90,8:90,16:90").split(",")]
     ctas_list = [int(x) for x in os.environ.get("AQUA_SWEEP_CTAS", "0,64,16").split(",")]
     stages_list = [int(x) for x in os.environ.get("AQUA_SWEEP_STAGES", "0").split(",")]
+    pieces = [int(x) for x in os.environ.get("AQUA_SWEEP_PIECES", "0").split(",")]
     for name, (L, H, nblk) in (("c2", (32, 8, 2048)), ("c4", (80, 2, 4096))):
         ctx, layers, arena, U = setup(L, 16, H, 128, 2 * nblk, nblk)
         s = torch.cuda.Stream()
@@ -604,12 +605,15 @@ def tma_sched():
             ctx.set_option(aqua.OPT_MAX_CTAS, ctas)
             for sc, pct in combos:
               for st in stages_list:
+               for pc in pieces:
+                ctx.set_option(aqua.OPT_TMA_PIECE, pc)
                 ctx.set_option(aqua.OPT_TMA_SCHED, sc)
                 ctx.set_option(aqua.OPT_TMA_STATIC_PCT, pct)
                 ctx.set_option(aqua.OPT_TMA_STAGES, st)
                 pair = time_queued(ctx, s, K=20, reps=5)
                 o, i = time_tickets(ctx, 5, s)
-                print(json.dumps({"tma_sched": sc, "static_pct": pct, "stages": st or "auto", "shape": name,
+                print(json.dumps({"tma_sched": sc, "static_pct": pct, "stages": st or "auto", "piece": pc or 32768,
+                                  "shape": name,
                                   "ctas": ctas or 148,
                                   "pair_ms": round(pair, 4), "swap_GBps": round(2 * nblk * U / pair / 1e6, 1),
                                   "hbm_GBps": round(4 * nblk * U / pair / 1e6, 1),
