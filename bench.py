@@ -411,11 +411,12 @@ def run_ours(args):
     if ws == 1:
         ach = 2 * NBLK * U / (out_avg / 1e3) / 1e9           # read + write bytes, same HBM
         roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": hbm_peak, "unit": "GB/s",
-                "frac": round(ach / hbm_peak, 4), "traffic": _ncu_traffic(),
+                "frac": round(ach / hbm_peak, 4), "traffic": _ncu_traffic(CFG["name"]),
                 "kernel": "swap_tma_kernel<kOut> (swap_out launch)" if args.engine in ("auto", "tma")
                 else f"{args.engine} swap_out", "peak_source": hbm_src,
                 "algorithmic_bytes_per_launch": 2 * NBLK * U,
-                "swap_in_achieved": round(2 * NBLK * U / (in_avg / 1e3) / 1e9, 1)}
+                "swap_in_achieved": round(2 * NBLK * U / (in_avg / 1e3) / 1e9, 1),
+                "ncu": _ncu_record() if CFG["name"] == "c2" else None}
     else:
         ach = NBLK * U / (out_avg / 1e3) / 1e9                # bytes across the link per direction
         roof = {"bound": "nvlink", "achieved": round(ach, 1), "peak": NVLINK_MEASURED, "unit": "GB/s",
@@ -509,14 +510,37 @@ def _cleanup(aqua, local, ipc_ptr, imported, ws):
         dist.destroy_process_group()
 
 
-def _ncu_traffic():
+def _ncu_summary():
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
     if os.path.exists(p):
         try:
-            return json.load(open(p)).get("swap_out_traffic_bytes")
+            return json.load(open(p))
         except Exception:
             return None
     return None
+
+
+def _ncu_traffic(config="c2"):
+    """dram__bytes_read.sum + dram__bytes_write.sum of one swap_out launch of
+    this configuration in the committed capture (None if not captured)."""
+    d = _ncu_summary()
+    if not d:
+        return None
+    if config == "c2":
+        return d.get("swap_out_traffic_bytes")
+    return (d.get(f"{config}_swap_out") or {}).get("traffic_B")
+
+
+def _ncu_record():
+    """The committed ncu capture of this kernel (SURVEY 8(d) report record:
+    achieved DRAM rate from the profiler, beside the event-timed one)."""
+    d = _ncu_summary()
+    if not d or "swap_out" not in d:
+        return None
+    o = d["swap_out"]
+    return {"dram_TBps": round(o.get("dram_TBps", 0.0), 3),
+            "pct_of_theoretical_dram": round(o.get("gpu_dram_throughput_pct_of_theoretical", 0.0), 1),
+            "gpu_time_ms": round(o.get("gpu_time_ms", 0.0), 4), "source": "profiles/ncu_summary.json"}
 
 
 def host_baselines(ctx_dev, layers, dev, aqua, args):
