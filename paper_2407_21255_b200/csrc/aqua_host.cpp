@@ -488,8 +488,13 @@ aqua_status run_copy(aqua_ctx* c, const std::vector<Desc>& ds, aqua::Dir dir, cu
         else
           sched = 0;
       }
-      const bool hybrid = variant == 3;          // TMA ring + LDST warps: always claimed batches
+      bool hybrid = variant == 3;                // TMA ring + LDST warps: always claimed batches
       if (hybrid && sched <= 0) sched = 2;
+      // claims count in 31 bits (atom.inc bound 2^31 - 1): far beyond any real call
+      if (sched > 0 && p.nitems / (int64_t(sched) * p.group) + 2 * c->num_sms >= (int64_t(1) << 31)) {
+        sched = 0;
+        if (hybrid) hybrid = false, variant = 0;
+      }
       if (sched > 0 && (variant == 0 || hybrid) && c->d_ctr) {
         // dynamic batches of `sched` units; the counter pair's previous
         // launch must be done with it (stream order or its ticket)
