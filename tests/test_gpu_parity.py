@@ -248,6 +248,55 @@ def test_c2_full_size_sampled_and_restore():
     assert int(cnt.item()) > 0
 
 
+@pytest.mark.parametrize("cap", [0, 32])
+def test_c4_full_size_sampled_and_restore(cap):
+    """BASELINE configs[3] per TP rank (Llama-3-70B KV over TP4: L=80, 2 KV
+    heads, S = 8 KiB) as bench.py --config c4 runs it: 32 prompts x 2048
+    tokens swapped out and back in one call each (4,096 descriptors: staged
+    upload, claimed batches of grouped chunks).  cap=32 caps the preemption
+    at 32 SMs, where AUTO runs the hybrid ring + LDST warps.  Sampled chunks vs
+    the oracle's closed-form words; every prompt restored (verify kernel)."""
+    L, bs, H, D, NB = 80, 16, 2, 128, 8192
+    lay = kp.Layout(L=L, bs=bs, H=H, D=D, e=2, NB=NB)
+    dev = torch.device("cuda", 0)
+    layers = [torch.zeros(lay.layer_bytes, dtype=torch.uint8, device=dev) for _ in range(L)]
+    nblk = 4096
+    arena = torch.zeros(nblk * lay.U, dtype=torch.uint8, device=dev)
+    c = aqua.Ctx(0, L, bs, H, D, 2, NB, [t.data_ptr() for t in layers])
+    c.lend(0, arena.data_ptr(), nblk * lay.U)
+    perm = block_permutation(NB, NB, seed=2).tolist()
+    c.adopt_blocks(1, perm[nblk:])                        # filler keeps the tables scattered
+    pids = list(range(100, 132))
+    seed = 77
+    for i, pid in enumerate(pids):
+        c.adopt_blocks(pid, perm[i * 128:(i + 1) * 128])
+        c.kv_fill_pattern(pid, 0, 128 * bs, seed)
+    c.set_option(aqua.OPT_MAX_CTAS, cap)
+    c.swap_out(pids)
+    c.set_option(aqua.OPT_MAX_CTAS, 0)
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(1)
+    img = arena.view(nblk, L, 2, bs, H, D * 2)
+    for _ in range(24):
+        pid = pids[int(rng.integers(0, 32))]
+        slots = c.query(pid, with_ids=True)[3]
+        jb = int(rng.integers(0, 128))
+        l, kv, i = int(rng.integers(0, L)), int(rng.integers(0, 2)), int(rng.integers(0, bs))
+        want = opat.token_words(seed, pid, jb * bs + i, l, kv, H, D).reshape(-1).view(np.uint8).reshape(H, D * 2)
+        assert np.array_equal(img[slots[jb], l, kv, i].cpu().numpy(), want)
+    for t_ in layers:
+        t_.fill_(0x5A)
+    c.free(1)
+    new, _ = c.swap_in(pids[::-1])
+    assert sorted(b for ids in new for b in ids) == list(range(nblk))
+    cnt = torch.zeros(1, dtype=torch.int64, device=dev)
+    for pid in pids:
+        c.kv_verify_pattern(pid, 128 * bs, seed, cnt.data_ptr())
+    torch.cuda.synchronize()
+    assert int(cnt.item()) == 0
+    c.close()
+
+
 def test_pattern_kernel_matches_oracle_words():
     rig = Rig(L=2, bs=16, H=2, D=64, NB=8, lender_slots=0)
     rig.ctx.adopt_blocks(3, [6, 2])
