@@ -51,3 +51,27 @@ def test_sm100a_cubin_and_bulk_copy_in_sass():
     assert "sm_100a" in out
     assert "UBLKCP" in out
     assert "swap_tma_kernel" in out and "swap_ldst_kernel" in out
+
+
+def test_product_kernel_sass_moves_payload_with_tma_only():
+    """The product swap kernel (TMA ring, no LDST warps): payload through
+    UBLKCP bulk copies only (no 128-bit LDG/STG), batches claimed with the
+    non-aggregated ATOMG.E.INC -- per-kernel cuobjdump SASS."""
+    import re
+    import shutil
+    import subprocess
+    import pytest
+    from paper_2407_21255_b200 import aqua
+    cob = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not os.path.exists(cob):
+        pytest.skip("cuobjdump not available")
+    txt = subprocess.run([cob, "-sass", aqua.LIB_PATH], capture_output=True, text=True).stdout
+    funcs = {f.split("\n", 1)[0].strip(): f for f in re.split(r"\n\s*Function : ", txt)[1:]}
+    prod = [f for n, f in funcs.items() if re.search(r"swap_tma_kernelILNS_3DirE\dENS_11SwapParamsTILi\d+EEELi0E", n)]
+    hyb = [f for n, f in funcs.items() if re.search(r"swap_tma_kernelILNS_3DirE\dENS_11SwapParamsTILi\d+EEELi8E", n)]
+    assert len(prod) == 6 and len(hyb) == 6        # 3 directions x 2 parameter sizes
+    for f in prod:
+        assert "UBLKCP.S.G" in f and "UBLKCP.G.S" in f and "ATOMG.E.INC" in f
+        assert not re.search(r"\b(LDG|STG)\.E[.\w]*\.128\b", f)
+    for f in hyb:                                   # the hybrid's LDST warps do move payload in registers
+        assert "UBLKCP.S.G" in f and re.search(r"\bSTG\.E[.\w]*\.128\b", f)
