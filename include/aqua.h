@@ -120,7 +120,8 @@ enum {
   AQUA_OPT_TMA_PIECE = 3,     /* bytes per TMA stage (multiple of 16, <= 65536; 0 = auto: 32 KiB) */
   AQUA_OPT_TMA_STAGES = 4,    /* TMA ring depth (2..32; 0 = auto: ~9 MiB of loads in flight chip-wide, 3..~200 KiB) */
   AQUA_OPT_TIMING = 5,        /* 1: each swap also records a start event; aqua_ticket_elapsed gives its device time */
-  AQUA_OPT_LDST_VARIANT = 6,  /* LDST engine flavour: 0 streaming hints, 1 plain, 2 (default) software-pipelined */
+  AQUA_OPT_LDST_VARIANT = 6,  /* LDST engine flavour: 0 streaming hints, 1 plain, 2 (default) software-pipelined,
+                                 3 claimed batches (every warp claims 2-piece batches, pieces of up to 32 KiB) */
   AQUA_OPT_TMA_VARIANT = 7,   /* TMA engine: 0 (default) one ring per CTA; 1 warp-specialised (load warp + store
                                  warp); 2 two independent rings per CTA (one issuing warp each); 3 hybrid: the ring
                                  plus 8 warps copying claimed batches through registers.  0-2 reach the same HBM

@@ -510,12 +510,22 @@ aqua_status run_copy(aqua_ctx* c, const std::vector<Desc>& ds, aqua::Dir dir, cu
       e = aqua::launch_swap_tma(p, inl, dir, c->num_sms, cap, c->tma_stages, st, &ctas,
                                 hybrid && !p.work_ctr ? 0 : variant);
     } else {
-      p.piece = 4096;
+      // variants 0-2: grid-stride 4 KiB items; variant 3: claimed batches of
+      // 2 pieces of up to 32 KiB per warp (the hybrid's register mover alone)
+      const bool claim = c->ldst_variant == 3 && c->d_ctr;
+      p.piece = claim ? static_cast<int>(std::min<int64_t>(c->S, 32768)) : 4096;
       p.group = 1;
-      p.npieces = static_cast<int32_t>((c->S + 4095) / 4096);
+      p.npieces = static_cast<int32_t>((c->S + p.piece - 1) / p.piece);
       p.nitems = p.ndesc * nc * p.npieces;
+      if (claim) {
+        const int slot = static_cast<int>(c->ctr_next++ % aqua::kCtrSlots);
+        if (aqua_status s = wait_all(c, {c->ctr_tick[slot]}, st)) return s;
+        c->ctr_pending.push_back(slot);
+        p.work_ctr = c->d_ctr + 2 * slot;
+        p.batch = 2;
+      }
       e = aqua::launch_swap_ldst(p, inl, dir, c->num_sms, all_host && cap == kHostCtas ? 2 * kHostCtas : cap, st, &ctas,
-                                 c->ldst_variant);
+                                 claim ? 3 : (c->ldst_variant == 3 ? 2 : c->ldst_variant));
     }
     if (e != cudaSuccess) return cuda_fail(c, e, "swap kernel launch");
     c->launches++;
@@ -594,14 +604,16 @@ aqua_status run_copy(aqua_ctx* c, const std::vector<Desc>& ds, aqua::Dir dir, cu
     };
     int ctas = 0;
     if (dir == aqua::kOut) {
-      cudaError_t e = aqua::launch_swap_ldst(p, nullptr, aqua::kOut, c->num_sms, c->max_ctas, st, &ctas, c->ldst_variant);
+      cudaError_t e = aqua::launch_swap_ldst(p, nullptr, aqua::kOut, c->num_sms, c->max_ctas, st, &ctas,
+                                                 c->ldst_variant == 3 ? 2 : c->ldst_variant);
       if (e != cudaSuccess) return cuda_fail(c, e, "gather kernel launch");
       c->launches++;
       return runs(true);
     }
     aqua_status rs = runs(false);
     if (rs) return rs;
-    cudaError_t e = aqua::launch_swap_ldst(p, nullptr, aqua::kIn, c->num_sms, c->max_ctas, st, &ctas, c->ldst_variant);
+    cudaError_t e = aqua::launch_swap_ldst(p, nullptr, aqua::kIn, c->num_sms, c->max_ctas, st, &ctas,
+                                               c->ldst_variant == 3 ? 2 : c->ldst_variant);
     if (e != cudaSuccess) return cuda_fail(c, e, "scatter kernel launch");
     c->launches++;
     return AQUA_OK;
@@ -1635,7 +1647,7 @@ aqua_status aqua_set_option(aqua_ctx* c, int32_t opt, int64_t v) {
       c->timing = v != 0;
       return AQUA_OK;
     case AQUA_OPT_LDST_VARIANT:
-      if (v < 0 || v > 2) return fail(c, AQUA_E_INVAL, "ldst variant");
+      if (v < 0 || v > 3) return fail(c, AQUA_E_INVAL, "ldst variant");
       c->ldst_variant = static_cast<int>(v);
       return AQUA_OK;
     case AQUA_OPT_TMA_VARIANT:

@@ -813,6 +813,13 @@ cudaError_t launch_tma_t(const P& p, Dir dir, int num_sms, int grid_cap, int sta
   return cudaGetLastError();
 }
 
+// LDST engine with claimed batches (AQUA_OPT_LDST_VARIANT 3): every warp of
+// a 256-thread CTA per SM is an ldst_worker (the hybrid's register mover).
+template <Dir D, class P>
+__global__ void __launch_bounds__(256) swap_ldst_claim_kernel(const __grid_constant__ P p) {
+  ldst_worker<D>(p, 0, gridDim.x * (blockDim.x >> 5));
+}
+
 template <int V, class P>
 void launch_ldst_v(const P& p, Dir dir, int grid, cudaStream_t s) {
   if (dir == kOut)
@@ -828,8 +835,16 @@ cudaError_t launch_ldst_t(const P& p, Dir dir, int num_sms, int grid_cap, cudaSt
                           int variant) {
   // variant 2 (software pipelined, the default) is best with one 256-thread
   // CTA per SM: 6,624 / 6,572 GB/s on C2 (profiles/r01_ldst_variants.jsonl)
-  const int grid = grid_for<void>(p.nitems, 8, num_sms, variant == 2 ? 1 : 4, grid_cap);
-  if (variant == 1)
+  const int grid = grid_for<void>(p.nitems, 8, num_sms, variant >= 2 ? 1 : 4, grid_cap);
+  if (variant == 3) {
+    if (!p.work_ctr) return cudaErrorInvalidValue;
+    if (dir == kOut)
+      swap_ldst_claim_kernel<kOut, P><<<grid, 256, 0, s>>>(p);
+    else if (dir == kIn)
+      swap_ldst_claim_kernel<kIn, P><<<grid, 256, 0, s>>>(p);
+    else
+      swap_ldst_claim_kernel<kMig, P><<<grid, 256, 0, s>>>(p);
+  } else if (variant == 1)
     launch_ldst_v<1>(p, dir, grid, s);
   else if (variant == 2)
     launch_ldst_v<2>(p, dir, grid, s);

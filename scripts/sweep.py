@@ -646,6 +646,26 @@ def hybrid():
         torch.cuda.empty_cache()
 
 
+def ldst_claim():
+    """LDST engine: grid-stride 4 KiB items (variant 2) vs claimed batches of
+    32 KiB pieces (variant 3), beside the TMA default, C2 and C4 shapes."""
+    for name, (L, H, nblk) in (("c2", (32, 8, 2048)), ("c4", (80, 2, 4096))):
+        ctx, layers, arena, U = setup(L, 16, H, 128, 2 * nblk, nblk)
+        s = torch.cuda.Stream()
+        for ctas in (148, 64, 16):
+            ctx.set_option(aqua.OPT_MAX_CTAS, ctas)
+            for eng, v in (("tma", 0), ("ldst", 2), ("ldst", 3)):
+                ctx.set_option(aqua.OPT_KERNEL, ENG[eng])
+                ctx.set_option(aqua.OPT_LDST_VARIANT, v if eng == "ldst" else 2)
+                pair = time_queued(ctx, s, K=10, reps=3)
+                print(json.dumps({"engine": eng, "ldst_variant": v if eng == "ldst" else None, "shape": name,
+                                  "ctas": ctas, "pair_ms": round(pair, 4),
+                                  "hbm_GBps": round(4 * nblk * U / pair / 1e6, 1)}), flush=True)
+        ctx.close()
+        del layers, arena
+        torch.cuda.empty_cache()
+
+
 def stages():
     L, bs, H, D, NB, nblk = 32, 16, 8, 128, 4096, 2048
     ctx, layers, arena, U = setup(L, bs, H, D, NB, nblk)
@@ -727,6 +747,8 @@ if __name__ == "__main__":
         tma_sched()
     elif what == "hybrid":
         hybrid()
+    elif what == "ldst_claim":
+        ldst_claim()
 
 
 def latency():

@@ -27,7 +27,7 @@ ENGINES = {"tma": aqua.KERNEL_TMA, "ldst": aqua.KERNEL_LDST, "per_chunk": aqua.B
            "gather_temp": aqua.BASE_GATHER_TEMP, "batch": aqua.BASE_BATCH, "ce_host": aqua.KERNEL_CE_HOST,
            "tma_ws": aqua.KERNEL_TMA, "tma_r2": aqua.KERNEL_TMA, "tma_dyn": aqua.KERNEL_TMA,
            "tma_dyn1": aqua.KERNEL_TMA, "tma_static": aqua.KERNEL_TMA, "tma_rr": aqua.KERNEL_TMA,
-           "tma_hyb": aqua.KERNEL_TMA, "tma_hybrid": aqua.KERNEL_TMA}
+           "tma_hyb": aqua.KERNEL_TMA, "tma_hybrid": aqua.KERNEL_TMA, "ldst_claim": aqua.KERNEL_LDST}
 
 
 def _engine(ctx, name):
@@ -38,6 +38,8 @@ def _engine(ctx, name):
     LDST warps claiming batches of the same launch."""
     ctx.set_option(aqua.OPT_KERNEL, ENGINES[name])
     ctx.set_option(aqua.OPT_TMA_VARIANT, {"tma_ws": 1, "tma_r2": 2, "tma_hybrid": 3}.get(name, 0))
+    if name.startswith("ldst"):
+        ctx.set_option(aqua.OPT_LDST_VARIANT, 3 if name == "ldst_claim" else 2)
     if name in ("tma_dyn", "tma_dyn1", "tma_static", "tma_rr", "tma_hyb"):
         ctx.set_option(aqua.OPT_TMA_SCHED, {"tma_dyn": 8, "tma_dyn1": 1, "tma_static": 0, "tma_rr": -3,
                                             "tma_hyb": 2}[name])
@@ -97,7 +99,8 @@ SHAPES = {
 
 
 @pytest.mark.parametrize("shape", list(SHAPES))
-@pytest.mark.parametrize("engine", ["tma", "tma_ws", "tma_r2", "tma_dyn", "tma_dyn1", "tma_static", "tma_rr", "tma_hyb", "tma_hybrid", "ldst"])
+@pytest.mark.parametrize("engine", ["tma", "tma_ws", "tma_r2", "tma_dyn", "tma_dyn1", "tma_static", "tma_rr", "tma_hyb", "tma_hybrid", "ldst",
+                                    "ldst_claim"])
 @pytest.mark.parametrize("seed", [0, 1])
 @pytest.mark.parametrize("ctas", [0, 3])
 def test_random_sequences_bytes(shape, engine, seed, ctas):
@@ -322,7 +325,8 @@ def test_errors_leave_state_unchanged_and_no_cpu_fallback():
     assert c.launch_count() == n0 + 1         # the copy ran as one of our kernels
 
 
-@pytest.mark.parametrize("engine", ["tma", "tma_ws", "tma_r2", "tma_dyn", "tma_dyn1", "tma_static", "tma_rr", "tma_hyb", "tma_hybrid", "ldst"])
+@pytest.mark.parametrize("engine", ["tma", "tma_ws", "tma_r2", "tma_dyn", "tma_dyn1", "tma_static", "tma_rr", "tma_hyb", "tma_hybrid", "ldst",
+                                    "ldst_claim"])
 @pytest.mark.parametrize("tier", ["small_inline", "big_inline", "staged_256", "staged_4064"])
 def test_descriptor_tiers_bytes(engine, tier):
     """Descriptor passing, whole-buffer compare (both directions, fragmented
@@ -361,7 +365,8 @@ def test_ticket_timing():
     assert e.value.code == aqua.E_STATE
 
 
-@pytest.mark.parametrize("engine", ["tma", "tma_ws", "tma_r2", "tma_dyn", "tma_dyn1", "tma_static", "tma_rr", "tma_hyb", "tma_hybrid", "ldst"])
+@pytest.mark.parametrize("engine", ["tma", "tma_ws", "tma_r2", "tma_dyn", "tma_dyn1", "tma_static", "tma_rr", "tma_hyb", "tma_hybrid", "ldst",
+                                    "ldst_claim"])
 def test_migrate_reclaim_relend_bytes(engine):
     """NEXT-1 on the GPU: images move lender -> host (reclaim) and back
     (re-offer) through the fused arena->arena kernel, byte for byte with the
@@ -394,7 +399,8 @@ def test_migrate_reclaim_relend_bytes(engine):
     _ops(rig, [("in", [1, 2, 3]), ("out", [2])])
 
 
-@pytest.mark.parametrize("engine", ["tma", "tma_ws", "tma_r2", "tma_dyn", "tma_dyn1", "tma_static", "tma_rr", "tma_hyb", "tma_hybrid", "ldst"])
+@pytest.mark.parametrize("engine", ["tma", "tma_ws", "tma_r2", "tma_dyn", "tma_dyn1", "tma_static", "tma_rr", "tma_hyb", "tma_hybrid", "ldst",
+                                    "ldst_claim"])
 def test_prefix_cache_bytes(engine):
     """NEXT-2 on the GPU: store a cached prefix (copy), load it into three
     new prompts, reclaim moves it to the host, load again -- whole buffers
@@ -611,7 +617,8 @@ def test_pattern_batch_kernel_matches_oracle_words():
     rig.assert_bytes_equal("pattern batch")
 
 
-@pytest.mark.parametrize("engine", ["tma", "tma_ws", "tma_r2", "tma_dyn", "tma_dyn1", "tma_static", "tma_rr", "tma_hyb", "tma_hybrid", "ldst"])
+@pytest.mark.parametrize("engine", ["tma", "tma_ws", "tma_r2", "tma_dyn", "tma_dyn1", "tma_static", "tma_rr", "tma_hyb", "tma_hybrid", "ldst",
+                                    "ldst_claim"])
 def test_many_small_blocks_whole_buffer(engine):
     """Scale edge: 131,072 blocks of S = 256 B (100,000-block prompt, 800 KB of
     staged descriptors, slot ids > 2^16), whole pool / arena compared with
