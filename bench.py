@@ -368,7 +368,7 @@ def run_ours(args):
 
     probe_ref = torch.stack([first_chunk(pid).cpu() for pid in PIDS])
     e2e_t, lat_out, lat_in = [], [], []
-    reps = max(10, min(K, 20))
+    reps = max(20, min(K, 50))
     for _ in range(reps):           # per-call host latency: sync on each ticket
         torch.cuda.synchronize()
         t0 = time.perf_counter()
