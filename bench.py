@@ -336,6 +336,10 @@ def run_ours(args):
     if ws > 1:
         dist.barrier()
     launches = ctx.launch_count() - n0
+    try:
+        shape = ctx.last_launch()          # what the library's AUTO policy launched (the swap_in of the last step)
+    except aqua.AquaError:                 # a baseline engine that launches no kernel of ours
+        shape = {"engine": args.engine}
     total_ms = start.elapsed_time(end)
     out_ms = [a.elapsed_time(b) for a, b, _ in ev]
     in_ms = [b.elapsed_time(c) for _, b, c in ev]
@@ -451,9 +455,8 @@ def run_ours(args):
                                       "the C-ABI call to its ticket completing (aqua_sync)"},
         "launch_ms": {"swap_out": {q: round(_pct(out_ms, v), 4) for q, v in (("p10", .1), ("p50", .5), ("p90", .9))},
                       "swap_in": {q: round(_pct(in_ms, v), 4) for q, v in (("p10", .1), ("p50", .5), ("p90", .9))}},
-        "launch_shape": {"ctas": args.max_ctas or _sm_count(), "threads_per_cta": 32,
-                         "engine": args.engine, "blocks_per_launch": NBLK, "block_tokens": SHAPE["bs"],
-                         "chunk_bytes": SHAPE["bs"] * SHAPE["H"] * SHAPE["D"] * SHAPE["e"], "block_bytes_U": U},
+        "launch_shape": dict(shape, blocks_per_launch=NBLK, block_tokens=SHAPE["bs"],
+                             chunk_bytes=SHAPE["bs"] * SHAPE["H"] * SHAPE["D"] * SHAPE["e"], block_bytes_U=U),
         "host": _host_info(),
         "roofline": roof,
         "cpu_baseline": cpu,

@@ -314,6 +314,12 @@ AQUA_API aqua_status aqua_last_descriptors(aqua_ctx* ctx, int32_t* blocks, int32
                                   int64_t cap, int64_t* n_out);
 /* Kernel launches issued by this ctx so far (swap + harness kernels). */
 AQUA_API aqua_status aqua_launch_count(aqua_ctx* ctx, uint64_t* launches);
+/* Shape of the most recent swap / migrate kernel launch (what AUTO chose), for reporting: CTAs, threads per CTA,
+ * TMA ring stages (0 for the LDST engine), engine (AQUA_KERNEL_TMA / AQUA_KERNEL_LDST), variant, items per claimed
+ * batch (0 = static ranges; < 0 never), descriptors passed in the kernel parameters (0 = staged upload).  Any out
+ * pointer may be NULL.  AQUA_E_STATE before the first launch (and for copy-engine-only calls, which launch none). */
+AQUA_API aqua_status aqua_last_launch(aqua_ctx* ctx, int32_t* grid, int32_t* threads, int32_t* stages,
+                                      int32_t* engine, int32_t* variant, int64_t* batch_items, int64_t* inline_desc);
 
 /* Cross-process lending (setup only).  The lender process
  * exports a 64-byte handle for a device allocation; the borrower process

@@ -35,7 +35,7 @@ SYMBOLS = [
     "aqua_swap_out", "aqua_swap_in", "aqua_swap_exchange", "aqua_swap_out_layers", "aqua_swap_in_layers", "aqua_free", "aqua_migrate", "aqua_reclaim", "aqua_prefix_store", "aqua_prefix_load",
     "aqua_prefix_drop", "aqua_prefix_query", "aqua_wait", "aqua_sync", "aqua_ticket_done", "aqua_ticket_elapsed",
     "aqua_query", "aqua_counts", "aqua_arena_base", "aqua_set_option", "aqua_get_option",
-    "aqua_last_descriptors", "aqua_launch_count", "aqua_ipc_export", "aqua_ipc_import",
+    "aqua_last_descriptors", "aqua_launch_count", "aqua_last_launch", "aqua_ipc_export", "aqua_ipc_import",
     "aqua_ipc_close", "aqua_ipc_alloc", "aqua_ipc_free", "aqua_can_access_peer", "aqua_kv_fill_pattern", "aqua_kv_fill_pattern_batch",
     "aqua_kv_verify_pattern",
     "aqua_strerror", "aqua_last_error", "aqua_version",
@@ -91,6 +91,7 @@ def _load() -> C.CDLL:
         "aqua_get_option": (C.c_int, [VP, I32, P(I64)]),
         "aqua_last_descriptors": (C.c_int, [VP, P(I32), P(I32), P(I32), I64, P(I64)]),
         "aqua_launch_count": (C.c_int, [VP, P(U64)]),
+        "aqua_last_launch": (C.c_int, [VP, P(I32), P(I32), P(I32), P(I32), P(I32), P(I64), P(I64)]),
         "aqua_ipc_export": (C.c_int, [VP, P(C.c_uint8)]),
         "aqua_ipc_import": (C.c_int, [C.c_int, P(C.c_uint8), P(VP)]),
         "aqua_ipc_close": (C.c_int, [C.c_int, VP]),
@@ -337,6 +338,17 @@ class Ctx:
         v = C.c_uint64()
         self._c(lib.aqua_launch_count(self.h, C.byref(v)))
         return v.value
+
+    def last_launch(self) -> dict:
+        """Shape of the most recent swap / migrate kernel launch (aqua_last_launch)."""
+        g, t, st, en, va = (C.c_int32() for _ in range(5))
+        b, il = C.c_int64(), C.c_int64()
+        self._c(lib.aqua_last_launch(self.h, C.byref(g), C.byref(t), C.byref(st), C.byref(en), C.byref(va),
+                                     C.byref(b), C.byref(il)))
+        return {"ctas": g.value, "threads_per_cta": t.value, "stages": st.value,
+                "engine": {KERNEL_TMA: "tma", KERNEL_LDST: "ldst"}.get(en.value, en.value), "variant": va.value,
+                "schedule": f"claimed batches of {b.value} items" if b.value > 0 else "static ranges",
+                "inline_descriptors": il.value}
 
     def kv_fill_pattern(self, pid: int, t0: int, t1: int, seed: int, stream: int = 0) -> None:
         self._c(lib.aqua_kv_fill_pattern(self.h, pid, t0, t1, seed, C.c_void_p(stream or None)))

@@ -119,6 +119,9 @@ struct aqua_ctx {
   std::string err;
   std::vector<int32_t> last_b, last_s, last_l;
   uint64_t launches = 0;
+  // shape of the last copy-kernel launch (aqua_last_launch)
+  int32_t last_grid = 0, last_threads = 0, last_stages = 0, last_engine = 0, last_variant = 0;
+  int64_t last_batch = 0, last_inline = 0;
 };
 
 namespace {
@@ -507,8 +510,12 @@ aqua_status run_copy(aqua_ctx* c, const std::vector<Desc>& ds, aqua::Dir dir, cu
       } else if (sched < 0 && variant == 0) {
         p.batch = -sched * p.group;            // static round-robin batches
       }
-      e = aqua::launch_swap_tma(p, inl, dir, c->num_sms, cap, c->tma_stages, st, &ctas,
-                                hybrid && !p.work_ctr ? 0 : variant);
+      aqua::LaunchInfo li;
+      const int v_used = hybrid && !p.work_ctr ? 0 : variant;
+      e = aqua::launch_swap_tma(p, inl, dir, c->num_sms, cap, c->tma_stages, st, &ctas, v_used, &li);
+      c->last_grid = li.grid, c->last_threads = li.threads, c->last_stages = li.stages;
+      c->last_engine = AQUA_KERNEL_TMA, c->last_variant = v_used, c->last_batch = p.batch;
+      c->last_inline = p.desc ? 0 : p.ndesc;
     } else {
       // variants 0-2: grid-stride 4 KiB items; variant 3: claimed batches of
       // 2 pieces of up to 32 KiB per warp (the hybrid's register mover alone)
@@ -524,8 +531,13 @@ aqua_status run_copy(aqua_ctx* c, const std::vector<Desc>& ds, aqua::Dir dir, cu
         p.work_ctr = c->d_ctr + 2 * slot;
         p.batch = 2;
       }
+      aqua::LaunchInfo li;
+      const int v_used = claim ? 3 : (c->ldst_variant == 3 ? 2 : c->ldst_variant);
       e = aqua::launch_swap_ldst(p, inl, dir, c->num_sms, all_host && cap == kHostCtas ? 2 * kHostCtas : cap, st, &ctas,
-                                 claim ? 3 : (c->ldst_variant == 3 ? 2 : c->ldst_variant));
+                                 v_used, &li);
+      c->last_grid = li.grid, c->last_threads = li.threads, c->last_stages = 0;
+      c->last_engine = AQUA_KERNEL_LDST, c->last_variant = v_used, c->last_batch = p.batch;
+      c->last_inline = p.desc ? 0 : p.ndesc;
     }
     if (e != cudaSuccess) return cuda_fail(c, e, "swap kernel launch");
     c->launches++;
@@ -1698,6 +1710,20 @@ aqua_status aqua_last_descriptors(aqua_ctx* c, int32_t* blocks, int32_t* slots, 
     if (slots) slots[i] = c->last_s[i];
     if (locs) locs[i] = c->last_l[i];
   }
+  return AQUA_OK;
+}
+
+aqua_status aqua_last_launch(aqua_ctx* c, int32_t* grid, int32_t* threads, int32_t* stages, int32_t* engine,
+                             int32_t* variant, int64_t* batch_items, int64_t* inline_desc) {
+  if (!c) return fail(nullptr, AQUA_E_INVAL, "null ctx");
+  if (!c->last_grid) return fail(c, AQUA_E_STATE, "no copy kernel launched yet");
+  if (grid) *grid = c->last_grid;
+  if (threads) *threads = c->last_threads;
+  if (stages) *stages = c->last_stages;
+  if (engine) *engine = c->last_engine;
+  if (variant) *variant = c->last_variant;
+  if (batch_items) *batch_items = c->last_batch;
+  if (inline_desc) *inline_desc = c->last_inline;
   return AQUA_OK;
 }
 

@@ -91,12 +91,17 @@ cudaError_t launch_pattern_fill_batch(const FillBatchParams& p, int num_sms, cud
 
 // Launchers: return the CUDA error of the launch (cudaSuccess on success).
 // grid_cap = max CTAs (0 = derived from the SM count).
+// What a launcher launched (reported by aqua_last_launch).
+struct LaunchInfo {
+  int grid = 0, threads = 0, stages = 0;
+};
+
 // h.desc == nullptr: the h.ndesc descriptors at `inl` (host memory, at most
 // kInlineDescBig) are copied into the kernel parameters.
 cudaError_t launch_swap_tma(const SwapHeader& h, const Desc* inl, Dir dir, int num_sms, int grid_cap, int stages,
-                            cudaStream_t s, int* ctas_used, int variant = 0);
+                            cudaStream_t s, int* ctas_used, int variant = 0, LaunchInfo* info = nullptr);
 cudaError_t launch_swap_ldst(const SwapHeader& h, const Desc* inl, Dir dir, int num_sms, int grid_cap,
-                             cudaStream_t s, int* ctas_used, int variant = 0);
+                             cudaStream_t s, int* ctas_used, int variant = 0, LaunchInfo* info = nullptr);
 cudaError_t launch_pattern_fill(const PatternParams& p, int num_sms, cudaStream_t s);
 cudaError_t launch_pattern_verify(const PatternParams& p, int num_sms, cudaStream_t s);
 

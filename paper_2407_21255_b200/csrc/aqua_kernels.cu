@@ -730,7 +730,7 @@ namespace {
 
 template <class P>
 cudaError_t launch_tma_t(const P& p, Dir dir, int num_sms, int grid_cap, int stages_opt, cudaStream_t s,
-                         int* ctas_used, int variant) {
+                         int* ctas_used, int variant, LaunchInfo* info) {
   // One CTA per SM and a shallow ring: 3 x 32 KiB or 64 KiB of loads in
   // flight per SM measured best for HBM on B200 (profiles/r01_stages.jsonl);
   // deeper rings lose 3-4 %.
@@ -810,6 +810,7 @@ cudaError_t launch_tma_t(const P& p, Dir dir, int num_sms, int grid_cap, int sta
     swap_tma_kernel<kMig, P, 0><<<grid, 32 * rings, smem, s>>>(p, stages);
   }
   if (ctas_used) *ctas_used = grid;
+  if (info) *info = LaunchInfo{grid, vi == 1 ? 64 : vi == 2 ? 32 * (1 + kLdstWarps) : 32 * rings, stages};
   return cudaGetLastError();
 }
 
@@ -832,7 +833,7 @@ void launch_ldst_v(const P& p, Dir dir, int grid, cudaStream_t s) {
 
 template <class P>
 cudaError_t launch_ldst_t(const P& p, Dir dir, int num_sms, int grid_cap, cudaStream_t s, int* ctas_used,
-                          int variant) {
+                          int variant, LaunchInfo* info) {
   // variant 2 (software pipelined, the default) is best with one 256-thread
   // CTA per SM: 6,624 / 6,572 GB/s on C2 (profiles/r01_ldst_variants.jsonl)
   const int grid = grid_for<void>(p.nitems, 8, num_sms, variant >= 2 ? 1 : 4, grid_cap);
@@ -851,6 +852,7 @@ cudaError_t launch_ldst_t(const P& p, Dir dir, int num_sms, int grid_cap, cudaSt
   else
     launch_ldst_v<0>(p, dir, grid, s);
   if (ctas_used) *ctas_used = grid;
+  if (info) *info = LaunchInfo{grid, 256, 0};
   return cudaGetLastError();
 }
 
@@ -874,18 +876,18 @@ cudaError_t with_params(const SwapHeader& h, const Desc* inl, F&& f) {
 }  // namespace
 
 cudaError_t launch_swap_tma(const SwapHeader& h, const Desc* inl, Dir dir, int num_sms, int grid_cap,
-                            int stages_opt, cudaStream_t s, int* ctas_used, int variant) {
+                            int stages_opt, cudaStream_t s, int* ctas_used, int variant, LaunchInfo* info) {
   if (h.nitems == 0) return cudaSuccess;
   return with_params(h, inl, [&](const auto& p) {
-    return launch_tma_t(p, dir, num_sms, grid_cap, stages_opt, s, ctas_used, variant);
+    return launch_tma_t(p, dir, num_sms, grid_cap, stages_opt, s, ctas_used, variant, info);
   });
 }
 
 cudaError_t launch_swap_ldst(const SwapHeader& h, const Desc* inl, Dir dir, int num_sms, int grid_cap,
-                             cudaStream_t s, int* ctas_used, int variant) {
+                             cudaStream_t s, int* ctas_used, int variant, LaunchInfo* info) {
   if (h.nitems == 0) return cudaSuccess;
   return with_params(h, inl, [&](const auto& p) {
-    return launch_ldst_t(p, dir, num_sms, grid_cap, s, ctas_used, variant);
+    return launch_ldst_t(p, dir, num_sms, grid_cap, s, ctas_used, variant, info);
   });
 }
 

@@ -654,3 +654,48 @@ def test_dynamic_schedule_counter_reuse_across_streams():
         assert c.swap_in(sel, rnd.choice(streams).cuda_stream)[0] == o.swap_in(sel)
     assert c.launch_count() - n0 == 600
     rig.assert_bytes_equal("600 dynamically scheduled launches")
+
+
+def test_auto_policy_launch_shapes():
+    """aqua_last_launch reports what AUTO chose: claimed
+    2-unit batches with a 4-stage ring at one CTA per SM; static ranges for a
+    small call; under an SM cap, static ranges for stage-sized chunks and the
+    hybrid ring + LDST warps for sub-stage chunks; copy engines for host-only
+    calls launch no swap kernel of ours."""
+    def ctx_for(L, H, NB, nslots):
+        S = 16 * H * 128 * 2
+        layers = [torch.zeros(2 * NB * S, dtype=torch.uint8, device="cuda") for _ in range(L)]
+        arena = torch.zeros(nslots * 2 * L * S, dtype=torch.uint8, device="cuda")
+        c = aqua.Ctx(0, L, 16, H, 128, 2, NB, [t.data_ptr() for t in layers])
+        c.lend(0, arena.data_ptr(), arena.numel())
+        return c, layers, arena
+
+    c, keep, arena = ctx_for(4, 8, 2600, 2600)            # S = 32 KiB: one chunk per stage
+    with pytest.raises(aqua.AquaError):
+        c.last_launch()
+    c.alloc_blocks(1, 2500)
+    c.swap_out([1])
+    sm = torch.cuda.get_device_properties(0).multi_processor_count
+    s = c.last_launch()
+    assert s["engine"] == "tma" and s["variant"] == 0 and s["ctas"] == sm and s["stages"] == 4
+    assert s["schedule"] == "claimed batches of 2 items" and s["inline_descriptors"] == 2500
+    c.swap_in([1])
+    c.alloc_blocks(2, 3)                                   # small call: static ranges
+    c.swap_out([2])
+    assert c.last_launch()["schedule"] == "static ranges"
+    c.set_option(aqua.OPT_MAX_CTAS, 16)
+    c.swap_out([1])
+    s = c.last_launch()
+    assert s["ctas"] == 16 and s["variant"] == 0 and s["schedule"] == "static ranges"
+    c.close()
+    del keep, arena
+
+    c, keep, arena = ctx_for(8, 2, 2600, 2600)            # S = 8 KiB: 4 chunks per stage
+    c.alloc_blocks(1, 2500)
+    c.set_option(aqua.OPT_MAX_CTAS, 16)
+    c.swap_out([1])
+    s = c.last_launch()
+    assert s["ctas"] == 16 and s["variant"] == 3 and s["threads_per_cta"] == 288
+    assert s["schedule"] == "claimed batches of 32 items"  # 8 units x 4 chunks
+    c.swap_in([1])
+    c.close()
