@@ -67,6 +67,7 @@ def _peaks():
 
 
 NVLINK_MEASURED = 770.0   # GB/s per direction, peer copy (B200_PROFILING.md); 900 nominal
+RW_BOUND = 6820.0         # GB/s read + write: a copy on DRAM that time-shares 7.36 TB/s reads and 6.35 TB/s writes
 # The paper's end-to-end results on 8x H100-80G, quoted as context only; the paper
 # gives no swap GB/s or per-prompt swap latency for its own path.
 PAPER_CONTEXT = {
@@ -420,7 +421,10 @@ def run_ours(args):
                 else f"{args.engine} swap_out", "peak_source": hbm_src,
                 "algorithmic_bytes_per_launch": 2 * NBLK * U,
                 "swap_in_achieved": round(2 * NBLK * U / (in_avg / 1e3) / 1e9, 1),
-                "ncu": _ncu_record() if CFG["name"] == "c2" else None}
+                "ncu": _ncu_record() if CFG["name"] == "c2" else None,
+                "rw_bound": {"value": RW_BOUND, "frac": round(ach / RW_BOUND, 4),
+                             "basis": "DRAM time-shared between reads and writes: 2 / (1/7.36 + 1/6.35) TB/s, pure "
+                                      "read / pure write probe on this B200 (profiles/r01_hbm_probe.jsonl)"}}
     else:
         ach = NBLK * U / (out_avg / 1e3) / 1e9                # bytes across the link per direction
         roof = {"bound": "nvlink", "achieved": round(ach, 1), "peak": NVLINK_MEASURED, "unit": "GB/s",
