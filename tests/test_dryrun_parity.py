@@ -413,6 +413,9 @@ def test_create_validates_layout():
             c.set_option(opt, val)
     assert c.get_option(aqua.OPT_INLINE_MAX) == 4064              # the 32,764-byte parameter limit
     assert c.get_option(aqua.OPT_TMA_SCHED) == aqua.TMA_SCHED_AUTO
+    with pytest.raises(aqua.AquaError) as e:
+        c.last_launch()                                          # a dry-run context never launches
+    assert e.value.code == aqua.E_STATE
     c.set_option(aqua.OPT_TMA_SCHED, -3)
     c.set_option(aqua.OPT_TMA_SCHED, aqua.TMA_SCHED_AUTO)
     c.set_option(aqua.OPT_INLINE_MAX, 0)
