@@ -1,0 +1,4 @@
+cd $GRAFT_REPO_ROOT
+timeout 1500 python -m pytest tests -m gpu -q -rf --timeout 300 -x 2>&1 | tail -4
+timeout 400 python bench.py --no-host-baselines --no-cpu-baseline > gpurun_out/b62.json 2> gpurun_out/bench.err; echo "bench exit $?"
+python -c "import json;d=json.load(open('gpurun_out/b62.json'));print(d['value'], d['launch_shape'], d['e2e']['value'])"
