@@ -471,25 +471,35 @@ aqua_status run_copy(aqua_ctx* c, const std::vector<Desc>& ds, aqua::Dir dir, cu
       p.piece = piece;
       p.npieces = static_cast<int32_t>((c->S + piece - 1) / piece);
       p.nitems = p.ndesc * nc * p.npieces;
-      // work distribution, AUTO:
-      // * every SM runs one CTA and each gets >= 8 batches: claimed 2-unit
-      //   batches with a 4-stage ring, 6.80 / 6.71 TB/s on C2 / C4 vs 6.52 /
-      //   6.37 for static ranges (profiles/r01_tma_sched*.jsonl);
-      // * under an SM cap, chunks smaller than a stage (several bulk ops per
-      //   unit, C4): the hybrid ring + LDST warps with 8-unit batches, 92-94
-      //   vs 73 GB/s per SM (r01_hybrid.jsonl); larger chunks: static ranges,
-      //   which already reach the ~100 GB/s per-SM limit.
+      // work distribution, AUTO (profiles/r01_tma_sched*.jsonl, r01_hybrid*.jsonl,
+      // r01_small_chunks.jsonl; a unit = one stage = `group` chunks):
+      // * one CTA per SM and >= 8 batches per CTA: claimed batches with a
+      //   4-stage ring -- 2-unit batches for chunks of >= 8 KiB (6.80 / 6.71
+      //   TB/s on C2 / C4 vs 6.52 / 6.37 static); 8-unit batches for 4 KiB
+      //   chunks (6.24 vs 5.83); for chunks <= 2 KiB the pool side is 16+
+      //   bulk ops per unit, and the hybrid ring + LDST warps with 2-unit
+      //   batches moves 5.82 vs 4.59 TB/s;
+      // * under an SM cap, sub-stage chunks: the hybrid (C4 at 32 CTAs 2.93
+      //   vs 2.33 TB/s; 2 KiB chunks 2.05 vs 1.99 at best for the ring);
+      //   stage-sized chunks: static ranges, already at the ~100 GB/s per-SM
+      //   limit.
       int sched = c->tma_sched, variant = c->tma_variant;
       if (sched == AQUA_TMA_SCHED_AUTO) {
         const bool all_sms = cap == 0 || cap >= c->num_sms;
         const int64_t units = p.nitems / p.group;
         const int grid = static_cast<int>(std::min<int64_t>(all_sms ? c->num_sms : cap, p.nitems));
-        if (all_sms)
-          sched = units >= int64_t(c->num_sms) * 2 * 8 ? 2 : 0;
-        else if (p.group > 1 && !all_host && variant == 0 && units >= int64_t(grid) * 8 * 8)
-          sched = 8, variant = 3;
-        else
+        const bool hybrid_ok = !all_host && variant == 0;
+        if (all_sms) {
+          if (p.group >= 16 && hybrid_ok)
+            sched = 2, variant = 3;
+          else
+            sched = p.group >= 8 ? 8 : 2;
+          if (units < int64_t(grid) * sched * 8) sched = 0, variant = c->tma_variant;
+        } else if (p.group > 1 && hybrid_ok && units >= int64_t(grid) * 8 * 8) {
+          sched = p.group >= 8 ? 2 : 8, variant = 3;
+        } else {
           sched = 0;
+        }
       }
       bool hybrid = variant == 3;                // TMA ring + LDST warps: always claimed batches
       if (hybrid && sched <= 0) sched = 2;

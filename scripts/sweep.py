@@ -666,6 +666,32 @@ def ldst_claim():
         torch.cuda.empty_cache()
 
 
+def small_chunks():
+    """Sub-stage chunks at full grid and under a cap: S = 2 / 4 / 8 KiB (e.g. one
+    KV head per TP8 rank: S = 4 KiB), TMA ring vs hybrid, 1 GiB per call."""
+    for H, D in ((1, 64), (1, 128), (2, 128)):
+        L = 32
+        S = 16 * H * D * 2
+        U = 2 * L * S
+        nblk = (1 << 30) // U
+        ctx, layers, arena, _ = setup(L, 16, H, D, 2 * nblk, nblk)
+        s = torch.cuda.Stream()
+        ctx.set_option(aqua.OPT_KERNEL, aqua.KERNEL_TMA)
+        for ctas in (148, 32):
+            ctx.set_option(aqua.OPT_MAX_CTAS, ctas)
+            for v, sc in ((0, aqua.TMA_SCHED_AUTO), (0, 2), (0, 8), (3, 2), (3, 8), (3, 16)):
+                ctx.set_option(aqua.OPT_TMA_VARIANT, v)
+                ctx.set_option(aqua.OPT_TMA_SCHED, sc)
+                pair = time_queued(ctx, s, K=10, reps=3)
+                print(json.dumps({"S": S, "variant": v, "sched": "auto" if sc == aqua.TMA_SCHED_AUTO else sc,
+                                  "ctas": ctas, "launch": ctx.last_launch()["schedule"],
+                                  "hbm_GBps": round(4 * nblk * U / pair / 1e6, 1)}), flush=True)
+        ctx.set_option(aqua.OPT_TMA_VARIANT, 0)
+        ctx.close()
+        del layers, arena
+        torch.cuda.empty_cache()
+
+
 def stages():
     L, bs, H, D, NB, nblk = 32, 16, 8, 128, 4096, 2048
     ctx, layers, arena, U = setup(L, bs, H, D, NB, nblk)
@@ -749,6 +775,8 @@ if __name__ == "__main__":
         hybrid()
     elif what == "ldst_claim":
         ldst_claim()
+    elif what == "small_chunks":
+        small_chunks()
 
 
 def latency():
