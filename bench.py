@@ -298,9 +298,14 @@ def run_ours(args):
             ctx.lend(local, ipc_ptr, arena_bytes)
             mode = "self-lender"
         else:
-            imported = aqua.ipc_import(local, handles[partner][2])
-            ctx.lend(aqua.MAPPED, imported, arena_bytes)
-            mode = f"peer-lender rank{partner}"
+            try:
+                imported = aqua.ipc_import(local, handles[partner][2])
+                ctx.lend(aqua.MAPPED, imported, arena_bytes)
+                mode = f"peer-lender rank{partner}"
+            except aqua.AquaError as err:        # no P2P path to the partner: page into our own HBM
+                imported = None
+                ctx.lend(local, ipc_ptr, arena_bytes)
+                mode = f"self-lender (peer rank{partner} unreachable: {err})"
     perm = block_permutation(NB, NB, seed=2).tolist()
     ctx.adopt_blocks(1, perm[NBLK:])      # filler: keeps the prompts' blocks scattered over the pool
     bpp = CFG["bpp"]
