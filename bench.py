@@ -303,8 +303,9 @@ def run_ours(args):
                 ctx.lend(aqua.MAPPED, imported, arena_bytes)
                 mode = f"peer-lender rank{partner}"
             except aqua.AquaError as err:        # no P2P path to the partner: page into our own HBM
-                imported = None
-                ctx.lend(local, ipc_ptr, arena_bytes)
+                imported = None                  # (a fresh arena: the partner may still write into ipc_ptr)
+                arena = torch.empty(arena_bytes, dtype=torch.uint8, device=dev)
+                ctx.lend(local, arena.data_ptr(), arena_bytes)
                 mode = f"self-lender (peer rank{partner} unreachable: {err})"
     perm = block_permutation(NB, NB, seed=2).tolist()
     ctx.adopt_blocks(1, perm[NBLK:])      # filler: keeps the prompts' blocks scattered over the pool
