@@ -117,5 +117,36 @@ int main() {
   }
   run("tma_write_32k", 1, [&] { tma_wr_kernel<<<sms, 32, 32768>>>(b, bytes, 32768, 0); });
   run("tma_write_32k_2cta", 1, [&] { tma_wr_kernel<<<sms * 2, 32, 32768>>>(b, bytes, 32768, 0); });
+  // per-SM rates: a few CTAs (one per SM), 256 MiB, deep rings
+  const size_t small = size_t(256) << 20;
+  auto runs = [&](const char* name, double mult, auto f) {
+    float best = 1e9;
+    for (int r = 0; r < 5; ++r) {
+      cudaEventRecord(e0);
+      f();
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+      float ms;
+      cudaEventElapsedTime(&ms, e0, e1);
+      if (r >= 1 && ms < best) best = ms;
+    }
+    printf("{\"probe\": \"%s\", \"ms\": %.4f, \"GBps\": %.1f}\n", name, best, mult * small / best / 1e6);
+  };
+  for (int g : {1, 8, 16}) {
+    for (int st : {4, 6}) {
+      char nm[64];
+      snprintf(nm, 64, "tma_read_%dsm_x%d", g, st);
+      runs(nm, 1, [&] { tma_rd_kernel<<<g, 32, st * 32768 + 8 * st>>>(a, small, 32768, st); });
+    }
+    char nm[64];
+    snprintf(nm, 64, "tma_write_%dsm", g);
+    runs(nm, 1, [&] { tma_wr_kernel<<<g, 32, 32768>>>(b, small, 32768, 0); });
+    snprintf(nm, 64, "ldg_read_%dsm_1024thr", g);
+    runs(nm, 1, [&] { rd_kernel<<<g, 1024>>>((const int4*)a, small / 16, sink); });
+    snprintf(nm, 64, "stg_write_%dsm_1024thr", g);
+    runs(nm, 1, [&] { wr_kernel<<<g, 1024>>>((int4*)b, small / 16); });
+    snprintf(nm, 64, "ldst_copy_%dsm_1024thr", g);
+    runs(nm, 2, [&] { cp_kernel<<<g, 1024>>>((const int4*)a, (int4*)b, small / 16); });
+  }
   return 0;
 }
