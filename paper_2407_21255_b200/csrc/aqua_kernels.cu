@@ -14,6 +14,19 @@
 // Work item = one piece (<= `piece` bytes) of one chunk (l, kv) of one
 // descriptor j.  Items are numbered j-major, then c = 2l + kv, then piece,
 // so consecutive items are consecutive bytes of the slot-major image.
+//
+// Engines (the host picks one per launch):
+//   swap_tma_kernel<D, P, 0>   product: one elected thread per SM drives a
+//                              ring of TMA bulk copies; work in static
+//                              ranges or claimed batches (AUTO)
+//   swap_tma_kernel<D, P, 8>   hybrid: the same ring + 8 warps moving
+//                              claimed batches through registers (capped
+//                              launches of sub-stage chunks, <= 2 KiB chunks)
+//   swap_tma_ws_kernel         warp-specialised ring (tuning experiment)
+//   swap_ldst_kernel           16-byte LDG/STG, grid-stride
+//   swap_ldst_claim_kernel     16-byte LDG/STG, claimed batches
+// P = SwapParamsT<256 or 4064>: the descriptors ride in the launch
+// parameters when they fit (else SwapHeader::desc points at a staged copy).
 #include "aqua_internal.h"
 
 #include <algorithm>
