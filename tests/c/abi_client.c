@@ -65,6 +65,16 @@ int main(void) {
   int32_t fb, pf, hf;
   CHECK(aqua_counts(ctx, &fb, &pf, &hf));
   EXPECT(fb == 8 && pf == 8 && hf == 8);
+  /* options and the launch report through the C ABI */
+  int64_t v = 0;
+  CHECK(aqua_get_option(ctx, AQUA_OPT_TMA_SCHED, &v));
+  EXPECT(v == AQUA_TMA_SCHED_AUTO);
+  CHECK(aqua_get_option(ctx, AQUA_OPT_INLINE_MAX, &v));
+  EXPECT(v == 4064);
+  EXPECT(aqua_set_option(ctx, AQUA_OPT_INLINE_MAX, 4065) == AQUA_E_INVAL);
+  CHECK(aqua_set_option(ctx, AQUA_OPT_TMA_VARIANT, 3));
+  int32_t grid = -1;
+  EXPECT(aqua_last_launch(ctx, &grid, NULL, NULL, NULL, NULL, NULL, NULL) == AQUA_E_STATE); /* dry: no launch */
   CHECK(aqua_destroy(ctx));
   printf("ok %s\n", aqua_version());
   return 0;
