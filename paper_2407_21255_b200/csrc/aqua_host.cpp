@@ -82,6 +82,7 @@ struct aqua_ctx {
   int inline_max = aqua::kInlineDescBig;
   int tma_sched = AQUA_TMA_SCHED_AUTO;   // AQUA_OPT_TMA_SCHED: 0 static, n > 0 dynamic n-unit batches, -n rr
   int tma_static_pct = 0;       // AQUA_OPT_TMA_STATIC_PCT: statically split head of a dynamic launch
+  int pack_vec = 64;            // register movers pack chunks of <= pack_vec x 16 B (AQUA_LDST_PACK env)
   uint32_t* d_ctr = nullptr;    // kCtrSlots {next, done} pairs (inside the d_layer_base allocation)
   uint32_t ctr_next = 0;
   std::vector<uint64_t> ctr_tick;   // ticket of the last launch that used each pair
@@ -397,6 +398,7 @@ aqua_status run_copy(aqua_ctx* c, const std::vector<Desc>& ds, aqua::Dir dir, cu
   if (nc < 0) nc = 2 * c->L;
   aqua::SwapHeader p{};
   const Desc* inl = nullptr;
+  p.pack_vec = c->pack_vec;
   p.layer_base = c->d_layer_base;
   p.arena_base[0] = reinterpret_cast<uint64_t>(c->gpu.base);
   p.arena_base[1] = reinterpret_cast<uint64_t>(c->host.base);
@@ -778,6 +780,7 @@ aqua_status aqua_create(int device, const aqua_kv_layout* lay, aqua_ctx** out) {
       return fail(nullptr, AQUA_E_INVAL, "layer_base must be 16-byte aligned");
 
   aqua_ctx* c = new aqua_ctx();
+  if (const char* pk = std::getenv("AQUA_LDST_PACK")) c->pack_vec = std::atoi(pk);   // tuning experiments
   // AQUA_KERNEL=auto|tma|ldst|ce_host overrides the default copy engine
   // (operational escape hatch; aqua_set_option still wins afterwards)
   if (const char* k = std::getenv("AQUA_KERNEL")) {

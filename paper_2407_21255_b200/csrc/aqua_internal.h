@@ -49,6 +49,7 @@ struct SwapHeader {
   uint32_t* work_ctr;
   int32_t batch;
   int64_t static_items;        // dynamic only: items [0, static_items) split statically first
+  int32_t pack_vec;            // register movers pack whole chunks of <= pack_vec 16-byte vectors per round
 };
 // Counter pairs per context for dynamically scheduled launches; a pair is
 // reused only after the ticket of its last launch (stream-ordered, like R7).

@@ -268,6 +268,52 @@ __device__ __forceinline__ void ldst_worker(const P& p, int64_t off, uint32_t to
     int64_t j = cu.j;
     int32_t c = cu.c, q = cu.q;
     int4 va[8], vb[8];
+    // Whole chunks of 512 B .. 2 KiB (npieces == 1): pack 256 / nvec chunks
+    // into each 4 KiB round.  Unroll slot u of every lane belongs to chunk
+    // (u * 32) / nvec of the round (uniform across the warp), so the
+    // descriptor reads stay warp-uniform.
+    const int nvec_s = static_cast<int>(p.S >> 4);
+    if (p.npieces == 1 && nvec_s >= 32 && nvec_s <= p.pack_vec && nvec_s < 256 && (256 % nvec_s) == 0) {
+      const int k = 256 / nvec_s;            // chunks per round
+      const int32_t rel0 = c - p.c0;         // position of item a within its descriptor
+      // loads of a round also compute the stores' addresses (kept per unroll
+      // slot in registers); 32-bit index math (rel < nc + batch)
+      auto load_round = [&](int4* v, uint8_t** dp, int64_t o0) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int32_t o = static_cast<int32_t>(o0) + (u * 32) / nvec_s;
+          dp[u] = nullptr;
+          if (a + o < e) {
+            const uint32_t rel = static_cast<uint32_t>(rel0 + o);
+            const uint32_t dj = rel / static_cast<uint32_t>(p.nc);
+            const int32_t cc = p.c0 + static_cast<int32_t>(rel - dj * static_cast<uint32_t>(p.nc));
+            const uint8_t* src;
+            uint32_t bytes;
+            item_addrs<D>(p, desc_at(p, j + dj), cc, 0, src, dp[u], bytes);
+            const size_t vo = size_t((u * 32) % nvec_s + lane) * 16;
+            v[u] = ld_stream(src + vo);
+            dp[u] += vo;
+          }
+        }
+      };
+      auto store_round = [&](const int4* v, uint8_t* const* dp) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (dp[u]) st_stream(dp[u], v[u]);
+      };
+      uint8_t *da[8], *db[8];
+      const int64_t n = e - a;
+      load_round(va, da, 0);
+      for (int64_t o = 0; o < n; o += 2 * k) {
+        if (o + k < n) load_round(vb, db, o + k);
+        store_round(va, da);
+        if (o + k >= n) break;
+        if (o + 2 * k < n) load_round(va, da, o + 2 * k);
+        store_round(vb, db);
+      }
+      id = int64_t(__shfl_sync(0xffffffffu, raw, 0)) + off;
+      continue;
+    }
     for (int64_t it = a; it < e; ++it) {
       const uint8_t* src;
       uint8_t* dst;

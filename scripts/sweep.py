@@ -669,7 +669,7 @@ def ldst_claim():
 def small_chunks():
     """Sub-stage chunks at full grid and under a cap: S = 2 / 4 / 8 KiB (e.g. one
     KV head per TP8 rank: S = 4 KiB), TMA ring vs hybrid, 1 GiB per call."""
-    for H, D in ((1, 64), (1, 128), (2, 128)):
+    for H, D in ((1, 16), (1, 32), (1, 64), (1, 128), (2, 128)):
         L = 32
         S = 16 * H * D * 2
         U = 2 * L * S

@@ -95,6 +95,9 @@ SHAPES = {
     "fp8_kv": (2, 16, 8, 128, 1),        # e = 1 (FP8 KV cache): S = 16 KiB
     "fp32_kv": (2, 16, 4, 128, 4),       # e = 4: S = 32 KiB (one full stage)
     "bs128": (1, 128, 8, 128),           # S = 256 KiB: 8 pieces per chunk
+    "s1k": (3, 16, 1, 32),               # S = 1 KiB: 4 chunks per register round (hybrid / ldst_claim packing)
+    "s2k": (2, 16, 1, 64),               # S = 2 KiB: 2 chunks per register round
+    "s512": (5, 16, 1, 16),              # S = 512 B: 8 chunks per register round, ragged descriptor crossings
 }
 
 
