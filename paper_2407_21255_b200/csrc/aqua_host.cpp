@@ -436,6 +436,17 @@ aqua_status run_copy(aqua_ctx* c, const std::vector<Desc>& ds, aqua::Dir dir, cu
     engine = AQUA_KERNEL_TMA;   // only host images go through the copy engines
   }
   if (engine == AQUA_KERNEL_TMA || engine == AQUA_KERNEL_LDST) {
+    // Block-major layout: kv_plane_stride == S puts a block's K and V chunks of a layer side by
+    // side in the pool, and they are side by side in the image (chunk
+    // 2l + kv): move them as one chunk of 2S (whole layers only).
+    int64_t S_eff = c->S;
+    if (c->P_kv == c->S && (c0 % 2) == 0 && (nc % 2) == 0) {
+      S_eff = 2 * c->S;
+      p.S = S_eff;
+      p.c0 = c0 / 2;
+      p.nc = nc / 2;
+      p.kv_merged = 1;
+    }
     if (dev_desc) {
       p.desc = dev_desc;                      // already uploaded by the caller
     } else if (ds.size() <= static_cast<size_t>(c->inline_max)) {
@@ -464,15 +475,15 @@ aqua_status run_copy(aqua_ctx* c, const std::vector<Desc>& ds, aqua::Dir dir, cu
       // group of whole small chunks that are contiguous in the image
       const int stage = c->tma_piece > 0 ? c->tma_piece : 32768;
       int piece = stage;
-      if (piece >= c->S) {
-        piece = static_cast<int>(c->S);
-        p.group = std::max(1, std::min(stage / piece, nc));
+      if (piece >= S_eff) {
+        piece = static_cast<int>(S_eff);
+        p.group = std::max(1, std::min(stage / piece, p.nc));
       } else {
         p.group = 1;
       }
       p.piece = piece;
-      p.npieces = static_cast<int32_t>((c->S + piece - 1) / piece);
-      p.nitems = p.ndesc * nc * p.npieces;
+      p.npieces = static_cast<int32_t>((S_eff + piece - 1) / piece);
+      p.nitems = p.ndesc * p.nc * p.npieces;
       // work distribution, AUTO (profiles/r01_tma_sched*.jsonl, r01_hybrid*.jsonl,
       // r01_small_chunks.jsonl; a unit = one stage = `group` chunks):
       // * one CTA per SM and >= 8 batches per CTA: claimed batches with a
@@ -532,10 +543,10 @@ aqua_status run_copy(aqua_ctx* c, const std::vector<Desc>& ds, aqua::Dir dir, cu
       // variants 0-2: grid-stride 4 KiB items; variant 3: claimed batches of
       // 2 pieces of up to 32 KiB per warp (the hybrid's register mover alone)
       const bool claim = c->ldst_variant == 3 && c->d_ctr;
-      p.piece = claim ? static_cast<int>(std::min<int64_t>(c->S, 32768)) : 4096;
+      p.piece = claim ? static_cast<int>(std::min<int64_t>(S_eff, 32768)) : 4096;
       p.group = 1;
-      p.npieces = static_cast<int32_t>((c->S + p.piece - 1) / p.piece);
-      p.nitems = p.ndesc * nc * p.npieces;
+      p.npieces = static_cast<int32_t>((S_eff + p.piece - 1) / p.piece);
+      p.nitems = p.ndesc * p.nc * p.npieces;
       if (claim) {
         const int slot = static_cast<int>(c->ctr_next++ % aqua::kCtrSlots);
         if (aqua_status s = wait_all(c, {c->ctr_tick[slot]}, st)) return s;

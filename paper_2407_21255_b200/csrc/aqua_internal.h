@@ -50,6 +50,7 @@ struct SwapHeader {
   int32_t batch;
   int64_t static_items;        // dynamic only: items [0, static_items) split statically first
   int32_t pack_vec;            // register movers pack whole chunks of <= pack_vec 16-byte vectors per round
+  int32_t kv_merged;           // 1: a "chunk" is a layer's adjacent K+V pair (c = l, S = 2 x chunk bytes)
 };
 // Counter pairs per context for dynamically scheduled launches; a pair is
 // reused only after the ticket of its last launch (stream-ordered, like R7).

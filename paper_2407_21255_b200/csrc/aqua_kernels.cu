@@ -136,7 +136,7 @@ __device__ __forceinline__ Desc desc_at(const P& p, int64_t j) {
 template <Dir D>
 __device__ __forceinline__ void item_addrs(const SwapHeader& p, const Desc d, int c, int q,
                                            const uint8_t*& src, uint8_t*& dst, uint32_t& bytes) {
-  const int l = c >> 1, kv = c & 1;
+  const int l = p.kv_merged ? c : c >> 1, kv = p.kv_merged ? 0 : c & 1;
   const int64_t off = int64_t(q) * p.piece;
   const uint32_t a = d.slot_arena >> 31;
   const int64_t slot = d.slot_arena & ~kArenaBit;

@@ -23,11 +23,12 @@ ENG = {"tma": aqua.KERNEL_TMA, "ldst": aqua.KERNEL_LDST, "gather_temp": aqua.BAS
        "batch": aqua.BASE_BATCH, "per_chunk": aqua.BASE_PER_CHUNK, "ce_host": aqua.KERNEL_CE_HOST}
 
 
-def setup(L, bs, H, D, NB, nblk, host=False):
+def setup(L, bs, H, D, NB, nblk, host=False, block_major=False):
     S = bs * H * D * 2
     U = 2 * L * S
     layers = [torch.zeros(2 * NB * S, dtype=torch.uint8, device="cuda") for _ in range(L)]
-    ctx = aqua.Ctx(0, L, bs, H, D, 2, NB, [t.data_ptr() for t in layers])
+    ctx = aqua.Ctx(0, L, bs, H, D, 2, NB, [t.data_ptr() for t in layers],
+                   S if block_major else 0, 2 * S if block_major else 0)
     arena = None
     if host:
         ctx.lend(aqua.HOST, 0, nblk * U)
@@ -667,14 +668,17 @@ def ldst_claim():
 
 
 def small_chunks():
-    """Sub-stage chunks at full grid and under a cap: S = 2 / 4 / 8 KiB (e.g. one
-    KV head per TP8 rank: S = 4 KiB), TMA ring vs hybrid, 1 GiB per call."""
+    """Sub-stage chunks at full grid and under a cap: S = 512 B .. 8 KiB (e.g. one
+    KV head per TP8 rank: S = 4 KiB), TMA ring vs hybrid, 1 GiB per call.
+    AQUA_SWEEP_BLOCK_MAJOR=1: the block-major layout (K and V of a layer
+    adjacent: moved as one 2S chunk)."""
+    bm = os.environ.get("AQUA_SWEEP_BLOCK_MAJOR") == "1"
     for H, D in ((1, 16), (1, 32), (1, 64), (1, 128), (2, 128)):
         L = 32
         S = 16 * H * D * 2
         U = 2 * L * S
         nblk = (1 << 30) // U
-        ctx, layers, arena, _ = setup(L, 16, H, D, 2 * nblk, nblk)
+        ctx, layers, arena, _ = setup(L, 16, H, D, 2 * nblk, nblk, block_major=bm)
         s = torch.cuda.Stream()
         ctx.set_option(aqua.OPT_KERNEL, aqua.KERNEL_TMA)
         for ctas in (148, 32):
@@ -683,7 +687,8 @@ def small_chunks():
                 ctx.set_option(aqua.OPT_TMA_VARIANT, v)
                 ctx.set_option(aqua.OPT_TMA_SCHED, sc)
                 pair = time_queued(ctx, s, K=10, reps=3)
-                print(json.dumps({"S": S, "variant": v, "sched": "auto" if sc == aqua.TMA_SCHED_AUTO else sc,
+                print(json.dumps({"S": S, "block_major": bm, "variant": v,
+                                  "sched": "auto" if sc == aqua.TMA_SCHED_AUTO else sc,
                                   "ctas": ctas, "launch": ctx.last_launch()["schedule"],
                                   "hbm_GBps": round(4 * nblk * U / pair / 1e6, 1)}), flush=True)
         ctx.set_option(aqua.OPT_TMA_VARIANT, 0)

@@ -153,11 +153,35 @@ def test_random_sequences_bytes(shape, engine, seed, ctas):
             rig.assert_bytes_equal(f"after failed {op}")
 
 
-def test_block_major_layout_bytes():
-    L, bs, H, D, NB = 3, 16, 2, 64, 12
+@pytest.mark.parametrize("engine", ["tma", "tma_dyn1", "tma_hybrid", "ldst", "ldst_claim", "ce_host"])
+@pytest.mark.parametrize("D", [64, 8, 16])
+def test_block_major_layout_bytes(engine, D):
+    """Block-major layout ([NB][2][bs][H][D] per layer, kv_plane_stride = S):
+    a layer's K and V chunks are adjacent in pool and image and move as one
+    2S chunk (S = 4 KiB, and 256 / 512 B where the register movers pack
+    several merged chunks per round)."""
+    L, bs, H, NB = 3, 16, 2, 12
     S = bs * H * D * 2
     rig = Rig(L=L, bs=bs, H=H, D=D, NB=NB, lender_slots=6, host_slots=6, kv_plane_stride=S, block_stride=2 * S)
+    _engine(rig.ctx, engine)
     _ops(rig, [("adopt", (1, [5, 0, 3])), ("alloc", (2, 4)), ("out", [1, 2]), ("alloc", (3, 2)), ("in", [2, 1])])
+
+
+def test_block_major_layerwise_bytes():
+    """Layer-wise swaps (chunk ranges of whole layers) on the merged K+V layout."""
+    L, bs, H, D, NB = 5, 16, 1, 32, 20
+    S = bs * H * D * 2
+    rig = Rig(L=L, bs=bs, H=H, D=D, NB=NB, lender_slots=8, host_slots=0, kv_plane_stride=S, block_stride=2 * S)
+    c, o = rig.ctx, rig.opool
+    perm = block_permutation(NB, 7, seed=4).tolist()
+    c.adopt_blocks(3, perm)
+    o.adopt_blocks(3, perm)
+    c.swap_out_layers([3], 2)
+    o.swap_out([3])
+    rig.assert_bytes_equal("layered swap_out, block-major")
+    new, _ = c.swap_in_layers([3], 2)
+    assert new == o.swap_in([3])
+    rig.assert_bytes_equal("layered swap_in, block-major")
 
 
 def test_adversarial_reuse_on_other_streams():
