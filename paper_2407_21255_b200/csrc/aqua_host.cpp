@@ -436,9 +436,9 @@ aqua_status run_copy(aqua_ctx* c, const std::vector<Desc>& ds, aqua::Dir dir, cu
     engine = AQUA_KERNEL_TMA;   // only host images go through the copy engines
   }
   if (engine == AQUA_KERNEL_TMA || engine == AQUA_KERNEL_LDST) {
-    // Block-major layout: kv_plane_stride == S puts a block's K and V chunks of a layer side by
-    // side in the pool, and they are side by side in the image (chunk
-    // 2l + kv): move them as one chunk of 2S (whole layers only).
+    // Block-major layout: kv_plane_stride == S puts a block's K and V chunks
+    // of a layer side by side in the pool, and they are side by side in the
+    // image (chunk 2l + kv): move them as one chunk of 2S (whole layers only).
     int64_t S_eff = c->S;
     if (c->P_kv == c->S && (c0 % 2) == 0 && (nc % 2) == 0) {
       S_eff = 2 * c->S;
@@ -461,6 +461,19 @@ aqua_status run_copy(aqua_ctx* c, const std::vector<Desc>& ds, aqua::Dir dir, cu
     }
     int ctas = 0;
     cudaError_t e;
+    // A counter pair for a launch with claimed batches of `batch` items; the
+    // pair's previous launch must be done with it (stream order or its
+    // ticket).  Claims count in 31 bits (atom.inc bound 2^31 - 1): a launch
+    // with more batches (far beyond any real call) falls back to static work.
+    auto take_counter = [&](int64_t batch) -> aqua_status {
+      if (!c->d_ctr || p.nitems / batch + 2 * c->num_sms >= (int64_t(1) << 31)) return AQUA_OK;
+      const int slot = static_cast<int>(c->ctr_next++ % aqua::kCtrSlots);
+      if (aqua_status s = wait_all(c, {c->ctr_tick[slot]}, st)) return s;
+      c->ctr_pending.push_back(slot);
+      p.work_ctr = c->d_ctr + 2 * slot;
+      p.batch = static_cast<int32_t>(batch);
+      return AQUA_OK;
+    };
     // A call whose images all live in host DRAM is PCIe-bound: 4 SMs already
     // saturate it (profiles/r01_host_ctas.jsonl), so cap it at 8 and leave
     // the other SMs to decode (unless the caller set a smaller cap).
@@ -514,27 +527,16 @@ aqua_status run_copy(aqua_ctx* c, const std::vector<Desc>& ds, aqua::Dir dir, cu
           sched = 0;
         }
       }
-      bool hybrid = variant == 3;                // TMA ring + LDST warps: always claimed batches
+      const bool hybrid = variant == 3;          // TMA ring + LDST warps: always claimed batches
       if (hybrid && sched <= 0) sched = 2;
-      // claims count in 31 bits (atom.inc bound 2^31 - 1): far beyond any real call
-      if (sched > 0 && p.nitems / (int64_t(sched) * p.group) + 2 * c->num_sms >= (int64_t(1) << 31)) {
-        sched = 0;
-        if (hybrid) hybrid = false, variant = 0;
-      }
-      if (sched > 0 && (variant == 0 || hybrid) && c->d_ctr) {
-        // dynamic batches of `sched` units; the counter pair's previous
-        // launch must be done with it (stream order or its ticket)
-        const int slot = static_cast<int>(c->ctr_next++ % aqua::kCtrSlots);
-        if (aqua_status s = wait_all(c, {c->ctr_tick[slot]}, st)) return s;
-        c->ctr_pending.push_back(slot);
-        p.work_ctr = c->d_ctr + 2 * slot;
-        p.batch = sched * p.group;
-        p.static_items = p.nitems * c->tma_static_pct / 100;
+      if (sched > 0 && (variant == 0 || hybrid)) {
+        if (aqua_status s = take_counter(int64_t(sched) * p.group)) return s;
+        if (p.work_ctr) p.static_items = p.nitems * c->tma_static_pct / 100;
       } else if (sched < 0 && variant == 0) {
         p.batch = -sched * p.group;            // static round-robin batches
       }
       aqua::LaunchInfo li;
-      const int v_used = hybrid && !p.work_ctr ? 0 : variant;
+      const int v_used = hybrid && !p.work_ctr ? 0 : variant;   // no counter: the plain ring
       e = aqua::launch_swap_tma(p, inl, dir, c->num_sms, cap, c->tma_stages, st, &ctas, v_used, &li);
       c->last_grid = li.grid, c->last_threads = li.threads, c->last_stages = li.stages;
       c->last_engine = AQUA_KERNEL_TMA, c->last_variant = v_used, c->last_batch = p.batch;
@@ -542,20 +544,21 @@ aqua_status run_copy(aqua_ctx* c, const std::vector<Desc>& ds, aqua::Dir dir, cu
     } else {
       // variants 0-2: grid-stride 4 KiB items; variant 3: claimed batches of
       // 2 pieces of up to 32 KiB per warp (the hybrid's register mover alone)
-      const bool claim = c->ldst_variant == 3 && c->d_ctr;
+      const bool claim = c->ldst_variant == 3;
       p.piece = claim ? static_cast<int>(std::min<int64_t>(S_eff, 32768)) : 4096;
       p.group = 1;
       p.npieces = static_cast<int32_t>((S_eff + p.piece - 1) / p.piece);
       p.nitems = p.ndesc * p.nc * p.npieces;
       if (claim) {
-        const int slot = static_cast<int>(c->ctr_next++ % aqua::kCtrSlots);
-        if (aqua_status s = wait_all(c, {c->ctr_tick[slot]}, st)) return s;
-        c->ctr_pending.push_back(slot);
-        p.work_ctr = c->d_ctr + 2 * slot;
-        p.batch = 2;
+        if (aqua_status s = take_counter(2)) return s;
+        if (!p.work_ctr) {                     // no counter: the grid-stride kernel moves <= 4 KiB items
+          p.piece = 4096;
+          p.npieces = static_cast<int32_t>((S_eff + p.piece - 1) / p.piece);
+          p.nitems = p.ndesc * p.nc * p.npieces;
+        }
       }
       aqua::LaunchInfo li;
-      const int v_used = claim ? 3 : (c->ldst_variant == 3 ? 2 : c->ldst_variant);
+      const int v_used = p.work_ctr ? 3 : (c->ldst_variant == 3 ? 2 : c->ldst_variant);
       e = aqua::launch_swap_ldst(p, inl, dir, c->num_sms, all_host && cap == kHostCtas ? 2 * kHostCtas : cap, st, &ctas,
                                  v_used, &li);
       c->last_grid = li.grid, c->last_threads = li.threads, c->last_stages = 0;
