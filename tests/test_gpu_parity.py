@@ -486,16 +486,20 @@ def test_layerwise_swaps_bytes(layer_group, nblk, where):
     rig.assert_bytes_equal("layered swap_in")
 
 
+@pytest.mark.parametrize("engine", ["auto", "tma_dyn1", "tma_hybrid"])
 @pytest.mark.parametrize("seed", [0, 1, 2])
-def test_multistream_fuzz_equals_sequential(seed):
+def test_multistream_fuzz_equals_sequential(seed, engine):
     """R7 end to end: random library ops (fills, swaps, migrations, prefix
     store/load, frees), each on a random one of three streams, must leave
     exactly the bytes of the oracle's sequential execution -- every reuse
-    of a block or slot is ordered by the library's tickets."""
+    of a block or slot is ordered by the library's tickets (and, with
+    claimed batches, every reuse of a launch counter pair)."""
     from oracle import pattern as opat
     rnd = random.Random(100 + seed)
     rig = Rig(L=3, bs=16, H=2, D=64, NB=64, lender_slots=24, host_slots=24, seed=seed)
     c, o = rig.ctx, rig.opool
+    if engine != "auto":
+        _engine(c, engine)
     streams = [torch.cuda.Stream() for _ in range(3)]
     ntok = {}
     pids = list(range(6))
