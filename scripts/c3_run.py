@@ -189,6 +189,8 @@ def main():
         prev = e0 + 0.020 + 40e-6 * tok
         e_end.append(prev)
     bytes_out, bytes_in = st["blocks_out"] * U, st["blocks_in"] * U
+    # NEXT-1 moves (reclaim lender -> host, re-offer host -> lender): device time per call
+    mig = [(k, n, ctx.ticket_elapsed(tk)) for k, n, tk, _ in st["swap_calls"] if k in ("reclaim", "migrate") and n]
 
     def pct(xs, q):
         xs = sorted(xs)
