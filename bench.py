@@ -454,6 +454,8 @@ def run_ours(args):
         "pairing": matching,
         "preempt_resume_ms": {"preempt_device_ms": round(out_avg, 4), "resume_device_ms": round(in_avg, 4),
                               "sum_device_ms": round(out_avg + in_avg, 4),
+                              "prompts_per_call": len(PIDS),
+                              "per_prompt_sum_device_ms": round((out_avg + in_avg) / len(PIDS), 4),
                               "preempt_host_p50_ms": round(1e3 * statistics.median(lat_out), 4),
                               "resume_host_p50_ms": round(1e3 * statistics.median(lat_in), 4),
                               "sum_host_p50_ms": round(1e3 * (statistics.median(lat_out) +
@@ -462,7 +464,9 @@ def run_ours(args):
                               "preempt_host_p99_ms": round(1e3 * _pct(lat_out, 0.99), 4),
                               "resume_host_p99_ms": round(1e3 * _pct(lat_in, 0.99), 4),
                               "what": "device = CUDA events on the swap stream around each call; host = wall time from "
-                                      "the C-ABI call to its ticket completing (aqua_sync)"},
+                                      "the C-ABI call to its ticket completing (aqua_sync); a call carries every "
+                                      "prompt of the config, per-prompt = whole call / prompts (equal prompt sizes, "
+                                      "so the byte-weighted attribution is the plain share)"},
         "launch_ms": {"swap_out": {q: round(_pct(out_ms, v), 4) for q, v in (("p10", .1), ("p50", .5), ("p90", .9))},
                       "swap_in": {q: round(_pct(in_ms, v), 4) for q, v in (("p10", .1), ("p50", .5), ("p90", .9))}},
         "launch_shape": dict(shape, blocks_per_launch=NBLK, block_tokens=SHAPE["bs"],
