@@ -134,8 +134,11 @@ enum {
                                  -n = batches of n units dealt round robin (CTA b: b, b + grid, ...);
                                  AQUA_TMA_SCHED_AUTO (default) = 2-unit claimed batches when the launch has one CTA
                                  per SM and >= 8 batches per CTA, else 0 (profiles/r01_tma_sched*.jsonl) */
-  AQUA_OPT_TMA_STATIC_PCT = 10 /* dynamic schedule: percent of the items split statically (one contiguous range per
+  AQUA_OPT_TMA_STATIC_PCT = 10, /* dynamic schedule: percent of the items split statically (one contiguous range per
                                  CTA) before the claimed batches; 0 = all claimed */
+  AQUA_OPT_RATE_GBPS = 11     /* paging budget in GB/s of swap per direction (0 = off): the copy kernels run on
+                                 ceil(rate / 50) SMs (one SM moves ~50 GB/s of swap on the HBM path), leaving the other
+                                 SMs and HBM bandwidth to decode; combines with AQUA_OPT_MAX_CTAS (the smaller cap wins) */
 };
 
 enum { AQUA_TMA_SCHED_AUTO = 1 << 30 };

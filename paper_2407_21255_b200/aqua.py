@@ -26,7 +26,7 @@ RESIDENT, SWAPPED = 1, 2
 LOC_LOCAL, LOC_PEER, LOC_HOST = 0, 1, 2
 KERNEL_AUTO, KERNEL_TMA, KERNEL_LDST, BASE_PER_CHUNK, BASE_GATHER_TEMP, BASE_BATCH, KERNEL_CE_HOST = 0, 1, 2, 3, 4, 5, 6
 (OPT_KERNEL, OPT_MAX_CTAS, OPT_TMA_PIECE, OPT_TMA_STAGES, OPT_TIMING, OPT_LDST_VARIANT, OPT_TMA_VARIANT,
- OPT_INLINE_MAX, OPT_TMA_SCHED, OPT_TMA_STATIC_PCT) = (1, 2, 3, 4, 5, 6, 7, 8, 9, 10)
+ OPT_INLINE_MAX, OPT_TMA_SCHED, OPT_TMA_STATIC_PCT, OPT_RATE_GBPS) = (1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11)
 TMA_SCHED_AUTO = 1 << 30
 
 # Every symbol include/aqua.h declares (checked by tests/test_abi.py).

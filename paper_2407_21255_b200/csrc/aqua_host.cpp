@@ -83,6 +83,7 @@ struct aqua_ctx {
   int tma_sched = AQUA_TMA_SCHED_AUTO;   // AQUA_OPT_TMA_SCHED: 0 static, n > 0 dynamic n-unit batches, -n rr
   int tma_static_pct = 0;       // AQUA_OPT_TMA_STATIC_PCT: statically split head of a dynamic launch
   int pack_vec = 64;            // register movers pack chunks of <= pack_vec x 16 B (AQUA_LDST_PACK env)
+  int rate_gbps = 0;            // AQUA_OPT_RATE_GBPS: paging budget -> CTA cap (0 = off)
   uint32_t* d_ctr = nullptr;    // kCtrSlots {next, done} pairs (inside the d_layer_base allocation)
   uint32_t ctr_next = 0;
   std::vector<uint64_t> ctr_tick;   // ticket of the last launch that used each pair
@@ -129,6 +130,7 @@ namespace {
 
 thread_local std::string g_err;
 constexpr int kHostCtas = 8;   // CTA cap for host-only swaps (PCIe-bound)
+constexpr int kSwapGBpsPerSm = 50;   // swap GB/s one SM sustains (per direction) on the HBM path
 
 // Makes `d` the current device for the scope of a call (no-op for dry runs).
 struct DevGuard {
@@ -478,6 +480,13 @@ aqua_status run_copy(aqua_ctx* c, const std::vector<Desc>& ds, aqua::Dir dir, cu
     // saturate it (profiles/r01_host_ctas.jsonl), so cap it at 8 and leave
     // the other SMs to decode (unless the caller set a smaller cap).
     int cap = c->max_ctas;
+    // A paging budget (GB/s of swap per direction) becomes an SM cap: one SM
+    // moves ~50 GB/s of swap through HBM (profiles/r01_hbm_probe2.jsonl,
+    // r01_hybrid*.jsonl: ~100 GB/s of read + write), so leave the rest to decode.
+    if (c->rate_gbps > 0) {
+      const int want = std::max(1, (c->rate_gbps + kSwapGBpsPerSm - 1) / kSwapGBpsPerSm);
+      if (cap == 0 || want < cap) cap = std::min(want, c->num_sms);
+    }
     bool all_host = true;
     for (const Desc& d : ds)
       all_host = all_host && ((d.slot_arena & kArenaBit) ||
@@ -1709,6 +1718,10 @@ aqua_status aqua_set_option(aqua_ctx* c, int32_t opt, int64_t v) {
       if (v < 0 || v > 100) return fail(c, AQUA_E_INVAL, "tma static pct");
       c->tma_static_pct = static_cast<int>(v);
       return AQUA_OK;
+    case AQUA_OPT_RATE_GBPS:
+      if (v < 0 || v > (1 << 20)) return fail(c, AQUA_E_INVAL, "rate");
+      c->rate_gbps = static_cast<int>(v);
+      return AQUA_OK;
   }
   return fail(c, AQUA_E_INVAL, "unknown option");
 }
@@ -1726,6 +1739,7 @@ aqua_status aqua_get_option(aqua_ctx* c, int32_t opt, int64_t* v) {
     case AQUA_OPT_INLINE_MAX: *v = c->inline_max; return AQUA_OK;
     case AQUA_OPT_TMA_SCHED: *v = c->tma_sched; return AQUA_OK;
     case AQUA_OPT_TMA_STATIC_PCT: *v = c->tma_static_pct; return AQUA_OK;
+    case AQUA_OPT_RATE_GBPS: *v = c->rate_gbps; return AQUA_OK;
   }
   return fail(c, AQUA_E_INVAL, "unknown option");
 }

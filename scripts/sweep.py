@@ -697,6 +697,26 @@ def small_chunks():
         torch.cuda.empty_cache()
 
 
+def rate():
+    """AQUA_OPT_RATE_GBPS: achieved swap GB/s per direction against the budget
+    (C2 and C4 shapes, back to back)."""
+    for name, (L, H, nblk) in (("c2", (32, 8, 2048)), ("c4", (80, 2, 4096))):
+        ctx, layers, arena, U = setup(L, 16, H, 128, 2 * nblk, nblk)
+        s = torch.cuda.Stream()
+        for r in (100, 200, 400, 800, 1600, 3200, 0):
+            ctx.set_option(aqua.OPT_RATE_GBPS, r)
+            pair = time_queued(ctx, s, K=6, reps=3)
+            ctx.swap_out([7], s.cuda_stream)
+            ctas = ctx.last_launch()["ctas"]
+            ctx.swap_in([7], s.cuda_stream)
+            torch.cuda.synchronize()
+            print(json.dumps({"rate_budget_GBps": r or None, "shape": name, "ctas": ctas,
+                              "swap_GBps_per_direction": round(2 * nblk * U / pair / 1e6, 1)}), flush=True)
+        ctx.close()
+        del layers, arena
+        torch.cuda.empty_cache()
+
+
 def stages():
     L, bs, H, D, NB, nblk = 32, 16, 8, 128, 4096, 2048
     ctx, layers, arena, U = setup(L, bs, H, D, NB, nblk)
@@ -782,6 +802,8 @@ if __name__ == "__main__":
         ldst_claim()
     elif what == "small_chunks":
         small_chunks()
+    elif what == "rate":
+        rate()
 
 
 def latency():

@@ -407,7 +407,7 @@ def test_create_validates_layout():
     c = aqua.Ctx(aqua.DRYRUN, 1, 16, 1, 8, 2, 4, [FAKE])
     for opt, val in ((aqua.OPT_KERNEL, 99), (aqua.OPT_TMA_PIECE, 17), (aqua.OPT_TMA_STAGES, 1),
                      (aqua.OPT_MAX_CTAS, -1), (aqua.OPT_TIMING, 2), (aqua.OPT_LDST_VARIANT, 4),
-                     (aqua.OPT_TMA_VARIANT, 4), (aqua.OPT_INLINE_MAX, 4065), (aqua.OPT_INLINE_MAX, -1), (aqua.OPT_TMA_STATIC_PCT, 101),
+                     (aqua.OPT_TMA_VARIANT, 4), (aqua.OPT_INLINE_MAX, 4065), (aqua.OPT_INLINE_MAX, -1), (aqua.OPT_TMA_STATIC_PCT, 101), (aqua.OPT_RATE_GBPS, -1),
                      (77, 0)):
         with pytest.raises(aqua.AquaError):
             c.set_option(opt, val)

@@ -718,6 +718,14 @@ def test_auto_policy_launch_shapes():
     c.swap_out([1])
     s = c.last_launch()
     assert s["ctas"] == 16 and s["variant"] == 0 and s["schedule"] == "static ranges"
+    c.swap_in([1])
+    c.set_option(aqua.OPT_MAX_CTAS, 0)
+    c.set_option(aqua.OPT_RATE_GBPS, 420)                 # budget -> ceil(420 / 50) = 9 SMs
+    c.swap_out([1])
+    assert c.last_launch()["ctas"] == 9
+    c.set_option(aqua.OPT_MAX_CTAS, 4)                    # the smaller cap wins
+    c.swap_in([1])
+    assert c.last_launch()["ctas"] == 4
     c.close()
     del keep, arena
 
