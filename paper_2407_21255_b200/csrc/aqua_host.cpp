@@ -391,6 +391,43 @@ aqua_status run_copy_ce_host(aqua_ctx* c, const std::vector<Desc>& ds, aqua::Dir
   return record(c, st, &c->ce_tick[di]);
 }
 
+// The TMA engine's AUTO work distribution for one launch (profiles/
+// r01_tma_sched*.jsonl, r01_hybrid*.jsonl, r01_small_chunks*.jsonl; a unit =
+// one stage = p.group chunks):
+// * one CTA per SM and >= 8 batches per CTA: claimed batches with a 4-stage
+//   ring -- 2-unit batches for chunks of >= 8 KiB (6.80 / 6.71 TB/s on C2 /
+//   C4 vs 6.52 / 6.37 static); 8-unit batches for 4 KiB chunks (6.24 vs
+//   5.83); for chunks <= 2 KiB the pool side is 16+ bulk ops per unit, and
+//   the hybrid ring + LDST warps with 2-unit batches moves 5.82 vs 4.59 TB/s;
+//   a caller-set small stage (AQUA_OPT_TMA_PIECE) keeps >= 64 KiB per batch
+//   (16 KiB pieces in 2-unit batches ran at 5.85 vs 6.62 TB/s);
+// * under an SM cap, sub-stage chunks: the hybrid (C4 at 32 CTAs 2.93 vs 2.33
+//   TB/s); stage-sized chunks: static ranges, already at the ~100 GB/s per-SM
+//   limit;
+// * host-only launches (PCIe-bound, capped): static ranges, no hybrid.
+// *sched: 0 static, n > 0 claimed batches of n units; *variant: 0 ring, 3 hybrid.
+void auto_schedule(const aqua_ctx* c, const aqua::SwapHeader& p, int cap, bool all_host, int* sched,
+                   int* variant) {
+  const bool all_sms = cap == 0 || cap >= c->num_sms;
+  const int64_t units = p.nitems / p.group;
+  const int grid = static_cast<int>(std::min<int64_t>(all_sms ? c->num_sms : cap, p.nitems));
+  const bool hybrid_ok = !all_host && *variant == 0;
+  const int variant_in = *variant;
+  if (all_sms) {
+    if (p.group >= 16 && hybrid_ok)
+      *sched = 2, *variant = 3;
+    else
+      *sched = p.group >= 8 ? 8 : 2;
+    const int64_t unit_bytes = int64_t(p.piece) * p.group;
+    *sched = static_cast<int>(std::max<int64_t>(*sched, (65536 + unit_bytes - 1) / unit_bytes));
+    if (units < int64_t(grid) * *sched * 8) *sched = 0, *variant = variant_in;
+  } else if (p.group > 1 && hybrid_ok && units >= int64_t(grid) * 8 * 8) {
+    *sched = p.group >= 8 ? 2 : 8, *variant = 3;
+  } else {
+    *sched = 0;
+  }
+}
+
 // Moves chunks [c0, c0 + nc) (c = 2l + kv; default: all 2L) of every
 // descriptor with the configured engine.
 aqua_status run_copy(aqua_ctx* c, const std::vector<Desc>& ds, aqua::Dir dir, cudaStream_t st,
@@ -506,40 +543,8 @@ aqua_status run_copy(aqua_ctx* c, const std::vector<Desc>& ds, aqua::Dir dir, cu
       p.piece = piece;
       p.npieces = static_cast<int32_t>((S_eff + piece - 1) / piece);
       p.nitems = p.ndesc * p.nc * p.npieces;
-      // work distribution, AUTO (profiles/r01_tma_sched*.jsonl, r01_hybrid*.jsonl,
-      // r01_small_chunks.jsonl; a unit = one stage = `group` chunks):
-      // * one CTA per SM and >= 8 batches per CTA: claimed batches with a
-      //   4-stage ring -- 2-unit batches for chunks of >= 8 KiB (6.80 / 6.71
-      //   TB/s on C2 / C4 vs 6.52 / 6.37 static); 8-unit batches for 4 KiB
-      //   chunks (6.24 vs 5.83); for chunks <= 2 KiB the pool side is 16+
-      //   bulk ops per unit, and the hybrid ring + LDST warps with 2-unit
-      //   batches moves 5.82 vs 4.59 TB/s;
-      // * under an SM cap, sub-stage chunks: the hybrid (C4 at 32 CTAs 2.93
-      //   vs 2.33 TB/s; 2 KiB chunks 2.05 vs 1.99 at best for the ring);
-      //   stage-sized chunks: static ranges, already at the ~100 GB/s per-SM
-      //   limit.
       int sched = c->tma_sched, variant = c->tma_variant;
-      if (sched == AQUA_TMA_SCHED_AUTO) {
-        const bool all_sms = cap == 0 || cap >= c->num_sms;
-        const int64_t units = p.nitems / p.group;
-        const int grid = static_cast<int>(std::min<int64_t>(all_sms ? c->num_sms : cap, p.nitems));
-        const bool hybrid_ok = !all_host && variant == 0;
-        if (all_sms) {
-          if (p.group >= 16 && hybrid_ok)
-            sched = 2, variant = 3;
-          else
-            sched = p.group >= 8 ? 8 : 2;
-          // a caller-set small stage (AQUA_OPT_TMA_PIECE) keeps >= 64 KiB per
-          // batch: 16 KiB pieces in 2-unit batches ran at 5.85 vs 6.62 TB/s
-          const int64_t unit_bytes = int64_t(p.piece) * p.group;
-          sched = static_cast<int>(std::max<int64_t>(sched, (65536 + unit_bytes - 1) / unit_bytes));
-          if (units < int64_t(grid) * sched * 8) sched = 0, variant = c->tma_variant;
-        } else if (p.group > 1 && hybrid_ok && units >= int64_t(grid) * 8 * 8) {
-          sched = p.group >= 8 ? 2 : 8, variant = 3;
-        } else {
-          sched = 0;
-        }
-      }
+      if (sched == AQUA_TMA_SCHED_AUTO) auto_schedule(c, p, cap, all_host, &sched, &variant);
       const bool hybrid = variant == 3;          // TMA ring + LDST warps: always claimed batches
       if (hybrid && sched <= 0) sched = 2;
       if (sched > 0 && (variant == 0 || hybrid)) {
