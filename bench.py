@@ -410,6 +410,12 @@ def run_ours(args):
     bytes_per_step = 2 * NBLK * U
     value = ws * K * bytes_per_step / (total_ms_max / 1e3) / 1e9
     out_avg, in_avg = statistics.mean(out_ms), statistics.mean(in_ms)
+    per_rank = None
+    if ws > 1:                        # every rank's own per-direction link rate (bytes across the link per launch)
+        from paper_2407_21255_b200.pairing import exchange
+        per_rank = [{"rank": r, "mode": m, "swap_out_GBps": round(NBLK * U / (o / 1e3) / 1e9, 1),
+                     "swap_in_GBps": round(NBLK * U / (i / 1e3) / 1e9, 1)}
+                    for r, m, o, i in exchange((rank, mode, out_avg, in_avg))]
 
     host = None
     if ws == 1 and not args.no_host_baselines and CFG["name"] == "c2":
@@ -452,6 +458,7 @@ def run_ours(args):
         "config": _config(args, n=ws),
         "mode": mode,
         "pairing": matching,
+        "per_rank": per_rank,
         "preempt_resume_ms": {"preempt_device_ms": round(out_avg, 4), "resume_device_ms": round(in_avg, 4),
                               "sum_device_ms": round(out_avg + in_avg, 4),
                               "prompts_per_call": len(PIDS),
