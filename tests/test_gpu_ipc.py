@@ -107,3 +107,26 @@ def test_ipc_lend_across_processes():
     assert "error" not in out, out
     assert out["lender"] == 0, "lender arena does not hold the borrower's image"
     assert out["borrower"] == 0, "resume from lent memory corrupted the KV"
+
+
+def test_bench_two_ranks_sharing_one_gpu():
+    """bench.py's N > 1 path end to end (the one the driver's scaling run
+    takes on 2-8 GPUs): torchrun with 2 ranks, each pairing with the other,
+    IPC-lending its arena and paging its 32K-token prompt into the partner's
+    memory; on one GPU (AQUA_BENCH_SHARED_GPU=1) the ranks share it.  The
+    line must carry both ranks' rates and a clean pattern verify."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, AQUA_BENCH_SHARED_GPU="1", MASTER_ADDR="127.0.0.1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_port()), os.path.join(root, "bench.py"),
+           "--gpus", "2", "--steps", "3", "--warmup", "3", "--no-host-baselines", "--no-cpu-baseline"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env, cwd=root)
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = json.loads([x for x in r.stdout.splitlines() if x.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and line["value"] > 0 and line["pairing"] == [1, 0]
+    assert [p["rank"] for p in line["per_rank"]] == [0, 1]
+    assert line["parity"].startswith("pattern verify: 0 mismatching words")
+    assert line["roofline"]["bound"] == "nvlink"
