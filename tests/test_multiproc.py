@@ -111,3 +111,25 @@ def test_tp_ranks_replicated_schedule():
         assert p.exitcode == 0
     for rank, hs, nout in res:
         assert len(set(hs)) == 1 and nout > 0
+
+
+def test_reference_arm_under_torchrun_world2():
+    """bench.py --impl reference under torchrun (N=2, CPU only): rank 0 alone
+    times the oracle and prints ONE line; the other rank exits 0 without work."""
+    import json
+    import socket
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(root, "bench.py"),
+           "--impl", "reference", "--gpus", "2", "--steps", "1", "--warmup", "3"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=root)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [json.loads(x) for x in r.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == 1 and lines[0]["impl"] == "reference" and lines[0]["value"] > 0
+    assert lines[0]["n_gpus"] == 2 and lines[0]["cpu_baseline"]["kind"] == "oracle"
