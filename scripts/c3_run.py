@@ -42,6 +42,7 @@ def main():
     ap.add_argument("--exchange", action="store_true", help="reschedules with both lists use aqua_swap_exchange")
     ap.add_argument("--native", action="store_true", help="run the loop in C++ (aqua_trace_run)")
     ap.add_argument("--no-verify", action="store_true")
+    ap.add_argument("--trace-seed", type=int, default=1, help="seed of the bursty trace (BASELINE configs[2]: 1)")
     ap.add_argument("--elastic", default="", help="t_reclaim,t_relend (virtual s): NEXT-1 lender reclaim + FCFS "
                                                    "fallback, then re-offer")
     args = ap.parse_args()
@@ -86,7 +87,7 @@ def main():
     ctx.set_option(aqua.OPT_TIMING, 1)               # per-swap device time via aqua_ticket_elapsed
     pol = POLICY_FCFS if args.policy == "fcfs" else POLICY_CFS
     sched = Scheduler(NB=NB, bs=bs, b=512, k=8, policy=pol)
-    trace = burst_trace(seed=1)
+    trace = burst_trace(seed=args.trace_seed)
     dec = torch.cuda.Stream(device=dev)
     swp = dec if args.serial else torch.cuda.Stream(device=dev)
     swp2 = torch.cuda.Stream(device=dev) if args.exchange else None
@@ -200,8 +201,8 @@ def main():
     tpot = [(e_end[last_it[p]] - e_end[first_it[p]]) / (plen[p][1] - 1) for p in last_it
             if p in first_it and plen[p][1] > 1]
     res = {
-        "config": "configs[2] bursty trace (seed 1, 373 requests, 25 @ 2.5/s then 5/s for 60 s then 2.5/s for 15 s), "
-                  "Llama-3-8B KV shape, NB=4152 (8.1 GiB), b=512, k=8",
+        "config": f"configs[2] bursty trace (seed {args.trace_seed}, {len(trace)} requests, 25 @ 2.5/s then 5/s for 60 s "
+                  "then 2.5/s for 15 s), Llama-3-8B KV shape, NB=4152 (8.1 GiB), b=512, k=8",
         "policy": args.policy,
         "mode": args.policy if args.policy != "cfs-peer" else
         ("self-lender (1 GPU)" if ws == 1 else ("IPC lender process, same GPU" if shared else "IPC peer lender GPU 1")),
