@@ -68,15 +68,21 @@ AQUA_API aqua_status aqua_cfs_destroy(aqua_cfs* s);
 /* Make a request runnable (arrival in virtual seconds). */
 AQUA_API aqua_status aqua_cfs_add(aqua_cfs* s, uint64_t pid, double arrival, int32_t prompt_tokens,
                                   int32_t output_tokens);
-/* Overwrite a runnable request's service counters (tests / restarts). */
+/* Overwrite a runnable request's service counters (tests / restarts).  A
+ * request added without KV that is given ctx > 0 here is a restart whose KV
+ * the caller holds as a swapped image (aqua_swap_out): the scheduler counts
+ * ceil(ctx / bs) blocks for it and pages it in when a plan includes it. */
 AQUA_API aqua_status aqua_cfs_set_state(aqua_cfs* s, uint64_t pid, int32_t phase, int32_t prefill_done,
                                         int32_t generated, int32_t ctx);
 /* Plan one iteration.  Arrays have capacity `cap`; *rescheduled = 1 when a
- * new plan was made (then page_out / page_in may be non-empty). */
+ * new plan was made (then page_out / page_in may be non-empty).  On any
+ * error (AQUA_E_INVAL: a list would exceed cap; AQUA_E_NOBLOCKS: nothing
+ * fits) the scheduler's state is unchanged. */
 AQUA_API aqua_status aqua_cfs_next(aqua_cfs* s, int32_t* rescheduled, uint64_t* page_out, int32_t* n_out,
                                    uint64_t* page_in, int32_t* n_in, aqua_cfs_work* work, int32_t* n_work,
                                    int32_t cap);
-/* Apply the planned iteration; finished pids (capacity cap) in work order. */
+/* Apply the planned iteration; finished pids (capacity cap) in work order.
+ * AQUA_E_INVAL (more finishes than cap) changes nothing. */
 AQUA_API aqua_status aqua_cfs_commit(aqua_cfs* s, uint64_t* finished, int32_t* n_fin, int32_t cap,
                                      double* vclock);
 /* The partition of the current runnable set (no side effects): decode ids in

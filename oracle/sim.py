@@ -79,9 +79,17 @@ class SimResult:
     timeline: List[Tuple[float, int]]      # (virtual time at iteration start, blocks owned)
 
 
-def run(trace: Sequence[Tuple[int, float, int, int]], cfg: SimConfig) -> SimResult:
+def run(trace: Sequence[Tuple[int, float, int, int]], cfg: SimConfig,
+        warm: Sequence[int] = ()) -> SimResult:
     """trace = [(id, arrival_s, prompt_tokens, output_tokens)] sorted by
-    (arrival, id)."""
+    (arrival, id).
+
+    warm (test entry state, not a workload feature): trace ids that arrive
+    with their prefill already done (f = ctx = P, g = 1, phase DECODE) and
+    their KV image already paged out, as after an earlier preemption (the
+    decode-only round-robin instances of SURVEY C-9).  Their images are
+    placed before iteration 0 by alloc_blocks + swap_out, one prompt at a
+    time in trace order; nothing is logged for this setup."""
     lay = Layout(L=1, bs=cfg.bs, H=1, D=8, e=2, NB=cfg.NB)   # metadata only
     pool = Pool(lay)
     if cfg.lender_slots > 0:
@@ -91,6 +99,11 @@ def run(trace: Sequence[Tuple[int, float, int, int]], cfg: SimConfig) -> SimResu
 
     pending = sorted(trace, key=lambda x: (x[1], x[0]))
     pi = 0
+    warm = set(warm)
+    for rid, _, P, _ in pending:
+        if rid in warm:
+            pool.alloc_blocks(rid, -(-P // lay.bs))
+            pool.swap_out([rid])
     run_set: Dict[int, Req] = {}
     log: List[tuple] = []
     ttft: Dict[int, float] = {}
@@ -138,6 +151,8 @@ def run(trace: Sequence[Tuple[int, float, int, int]], cfg: SimConfig) -> SimResu
         while pi < len(pending) and pending[pi][1] <= t:
             rid, a, P, O = pending[pi]
             run_set[rid] = Req(id=rid, arrival=a, P=P, O=O)
+            if rid in warm:
+                run_set[rid] = Req(id=rid, arrival=a, P=P, O=O, f=P, g=1, ctx=P, phase=DECODE)
             pi += 1
         if not run_set:
             t = pending[pi][1]          # idle: jump to the next arrival

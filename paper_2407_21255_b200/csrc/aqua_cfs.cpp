@@ -217,6 +217,12 @@ aqua_status aqua_cfs_set_state(aqua_cfs* s, uint64_t pid, int32_t phase, int32_t
   it->second.f = f;
   it->second.g = g;
   it->second.ctx = ctx;
+  if (ctx > 0 && it->second.where == kNone) {
+    // a restarted request with KV: the caller holds it as a swapped image
+    // (placed with aqua_swap_out), so the next plan pages it in
+    it->second.where = kSwapped;
+    it->second.blocks = static_cast<int32_t>((int64_t(ctx) + s->cfg.block_tokens - 1) / s->cfg.block_tokens);
+  }
   return AQUA_OK;
 }
 
@@ -246,6 +252,24 @@ aqua_status aqua_cfs_next(aqua_cfs* s, int32_t* rescheduled, uint64_t* page_out,
   }
   std::vector<uint64_t> outs, ins;
   std::vector<aqua_cfs_work> w;
+  // every failure below leaves the scheduler as it was on entry: the
+  // residency flips are undone (outs were resident, ins swapped; a prompt
+  // paged in and out again in one FCFS call ends swapped), and the
+  // admitted set, plan and cadence are restored
+  const std::vector<uint64_t> saved_admitted = s->admitted;
+  const Plan saved_plan = s->plan;
+  const bool saved_have = s->have_plan;
+  const int64_t saved_last = s->last;
+  auto fail = [&](aqua_status st) {
+    for (uint64_t id : outs) s->reqs.at(id).where = kResident;
+    for (uint64_t id : ins) s->reqs.at(id).where = kSwapped;
+    s->admitted = saved_admitted;
+    s->plan = saved_plan;
+    s->have_plan = saved_have;
+    s->last = saved_last;
+    *rescheduled = *n_out = *n_in = *n_work = 0;
+    return st;
+  };
   if (s->mode == AQUA_POLICY_FCFS) {
     // admission in arrival order while the full projections fit
     int64_t proj = 0;
@@ -301,7 +325,7 @@ aqua_status aqua_cfs_next(aqua_cfs* s, int32_t* rescheduled, uint64_t* page_out,
       s->plan = fcfs_plan();
       w = work_of(s, s->plan);
     }
-    if (w.empty()) return AQUA_E_NOBLOCKS;   // head-of-line prompt can never fit
+    if (w.empty()) return fail(AQUA_E_NOBLOCKS);   // head-of-line prompt can never fit
   } else {
     if (s->have_plan) w = work_of(s, s->plan);
     if (!s->have_plan || s->iter - s->last >= s->cfg.k || s->finished_prev || w.empty() || !fits(s, w)) {
@@ -322,11 +346,11 @@ aqua_status aqua_cfs_next(aqua_cfs* s, int32_t* rescheduled, uint64_t* page_out,
       for (uint64_t id : outs) s->reqs.at(id).where = kSwapped;
       for (uint64_t id : ins) s->reqs.at(id).where = kResident;
       w = work_of(s, s->plan);
-      if (w.empty()) return AQUA_E_NOBLOCKS;   // nothing fits: pool smaller than one prompt
+      if (w.empty()) return fail(AQUA_E_NOBLOCKS);   // nothing fits: pool smaller than one prompt
     }
   }
   const int32_t nmax = static_cast<int32_t>(std::max({outs.size(), ins.size(), w.size()}));
-  if (nmax > cap) return AQUA_E_INVAL;
+  if (nmax > cap) return fail(AQUA_E_INVAL);
   for (auto& x : w) {
     Req& r = s->reqs.at(x.pid);
     const int32_t need = blocks_for(s, r, x.tokens);
@@ -348,6 +372,15 @@ aqua_status aqua_cfs_next(aqua_cfs* s, int32_t* rescheduled, uint64_t* page_out,
 aqua_status aqua_cfs_commit(aqua_cfs* s, uint64_t* finished, int32_t* n_fin, int32_t cap, double* vclock) {
   if (!s || !n_fin) return AQUA_E_INVAL;
   if (!s->work_pending) return AQUA_E_STATE;
+  // count the finishes first, so a too-small `finished` array changes nothing
+  int32_t n_done = 0;
+  for (const auto& x : s->work) {
+    const Req& r = s->reqs.at(x.pid);
+    const bool decode_after = r.phase == AQUA_PHASE_DECODE || r.f + x.tokens == r.P;
+    const int32_t g_after = r.phase == AQUA_PHASE_DECODE ? r.g + 1 : 1;
+    n_done += decode_after && g_after >= r.O;
+  }
+  if (n_done > cap) return AQUA_E_INVAL;
   int64_t tokens = 0;
   for (const auto& x : s->work) tokens += x.tokens;
   s->vclock += s->cfg.t_base + s->cfg.t_token * static_cast<double>(tokens);
@@ -367,7 +400,6 @@ aqua_status aqua_cfs_commit(aqua_cfs* s, uint64_t* finished, int32_t* n_fin, int
     }
     if (r.phase == AQUA_PHASE_DECODE && r.g >= r.O) fin.push_back(r.id);
   }
-  if (static_cast<int32_t>(fin.size()) > cap) return AQUA_E_INVAL;
   for (size_t i = 0; i < fin.size(); ++i) {
     finished[i] = fin[i];
     s->reqs.erase(fin[i]);

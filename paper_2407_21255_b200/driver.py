@@ -25,7 +25,8 @@ def run_trace(trace: Sequence[Tuple[int, float, int, int]], ctx: "aqua.Ctx", sch
               on_iteration: Optional[Callable] = None, record_log: bool = True,
               stream_sync: Optional[Callable] = None, on_swap: Optional[Callable] = None,
               elastic: Optional[dict] = None, policy_after_relend: int = 0,
-              exchange_stream: Optional[int] = None, exchange_pieces: int = 16):
+              exchange_stream: Optional[int] = None, exchange_pieces: int = 16,
+              warm: Sequence[int] = (), max_iters: Optional[int] = None):
     """Run the whole trace.  Returns (log, stats).
 
     ``stream_sync(kind, ticket)`` lets a GPU caller order streams:
@@ -44,6 +45,10 @@ def run_trace(trace: Sequence[Tuple[int, float, int, int]], ctx: "aqua.Ctx", sch
     scheduler falls back to FCFS; at t_relend the memory is
     offered again, the host images move back (ascending pid, as many as fit)
     and CFS resumes.
+    ``warm`` (test entry state, as in the oracle's sim.run): trace ids that
+    arrive with prefill done (decode phase, g = 1, ctx = P) and their image
+    already paged out (alloc + swap_out before iteration 0, not logged).
+    ``max_iters`` stops after that many iterations.
     """
     pending = sorted(trace, key=lambda x: (x[1], x[0]))
     pi = 0
@@ -53,11 +58,19 @@ def run_trace(trace: Sequence[Tuple[int, float, int, int]], ctx: "aqua.Ctx", sch
     swap_calls = []
     reclaimed = relent = False
     swapped_at = {}          # pid -> arena of its image
-    while True:
+    warm = set(warm)
+    for rid, _, P, _ in pending:
+        if rid in warm:
+            ctx.alloc_blocks(rid, -(-P // ctx.bs), decode_stream)
+            ctx.swap_out([rid], swap_stream)
+            swapped_at[rid] = ctx.query(rid)[1]
+    while max_iters is None or i < max_iters:
         t = sched.vclock()
         while pi < len(pending) and pending[pi][1] <= t:
             rid, a, P, O = pending[pi]
             sched.add(rid, a, P, O)
+            if rid in warm:
+                sched.set_state(rid, 1, P, 1, P)
             pi += 1
         if elastic is not None and sched.stats()[0] > 0:
             if not reclaimed and t >= elastic["t_reclaim"]:

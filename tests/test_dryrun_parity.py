@@ -297,6 +297,55 @@ def test_full_c3_trace_call_log_matches_oracle():
     assert log == o.log
 
 
+@pytest.mark.parametrize("n,m,k", [(n, m, k) for n in (1, 3, 5, 6) for m in range(1, n + 1) for k in (1, 2, 3)])
+def test_round_robin_call_log_matches_oracle(n, m, k):
+    """C-9 instances (decode-only, bs=64, NB=m, ids in reverse arrival order;
+    the oracle side is pinned to the deque-rotation model in
+    test_oracle_cfs.py): the native scheduler + libaqua give the same log."""
+    order = [100 + n - 1 - j for j in range(n)]
+    tr = [(pid, -100.0 + j, 8, 10 ** 6) for j, pid in enumerate(order)]
+    o = osim.run(tr, osim.SimConfig(NB=m, bs=64, b=512, k=k, host_slots=64, max_iters=30), warm=order)
+    c = aqua.Ctx(aqua.DRYRUN, 1, 64, 1, 8, 2, m, [FAKE])
+    c.lend(aqua.HOST, FAKE * 3, 64 * c.U)
+    s = Scheduler(NB=m, bs=64, b=512, k=k)
+    log, st = run_trace(tr, c, s, warm=order, max_iters=30)
+    assert log == o.log
+    assert st["blocks_out"] == o.blocks_out and st["blocks_in"] == o.blocks_in
+
+
+def test_scheduler_failed_calls_change_nothing():
+    """aqua_cfs_next / aqua_cfs_commit with a too-small output capacity fail
+    with AQUA_E_INVAL and leave the scheduler as it was: a retry with room
+    gives exactly what an untouched twin gives (all-or-nothing, like the
+    paging calls)."""
+    def mk():
+        s = Scheduler(NB=2, bs=64, b=512, k=1, cap=64)
+        for j in range(4):
+            s.add(10 + j, float(j), 8, 3)
+            s.set_state(10 + j, PHASE_DECODE, 8, 1, 8)      # restart: image swapped out
+        return s
+    a, b = mk(), mk()
+    for it in range(12):
+        if a.stats()[0] == 0:
+            break
+        a.cap = 1
+        with pytest.raises(aqua.AquaError) as ei:
+            a.next()
+        assert ei.value.code == aqua.E_INVAL
+        a.cap = 64
+        ra, rb = a.next(), b.next()
+        assert ra == rb, it
+        fb = b.commit()
+        if fb[0]:
+            a.cap = len(fb[0]) - 1
+            with pytest.raises(aqua.AquaError):
+                a.commit()
+            a.cap = 64
+        assert a.commit() == fb
+        assert a.stats() == b.stats() and a.vclock() == b.vclock()
+    assert a.stats()[0] == 0
+
+
 @pytest.mark.parametrize("window", [(4.0, 9.0), (2.0, 30.0), (6.0, 6.5)])
 def test_elastic_trace_call_log_matches_oracle(window):
     """NEXT-1 end to end in metadata mode: lender reclaim -> images to DRAM,

@@ -112,6 +112,66 @@ def test_bruteforce_round_robin(n, m, k):
         assert all(r.ctx <= 64 for r in rs)
 
 
+def _sim_round_robin_expected(order, m, k, horizon):
+    """Deque-rotation model of the whole reschedule loop (SURVEY
+    C-9), independent of oracle.sim: `order` = pids in arrival order.  At
+    every i = s*k the plan is the window of m at the head of the queue (in
+    queue order), the queue is rotated by m, page_out = previous window
+    minus this one and page_in = this window minus the previous one, both
+    in arrival order; every iteration decodes the window, one token each."""
+    pos = {pid: j for j, pid in enumerate(order)}
+    q = collections.deque(order)
+    served = {pid: 0 for pid in order}
+    log = []
+    prev = []
+    win = []
+    for i in range(horizon):
+        if i % k == 0:
+            win = list(q)[:m]
+            q.rotate(-m)
+            log.append(("plan", i, tuple(win), ()))
+            out = sorted(set(prev) - set(win), key=pos.get)
+            inn = sorted(set(win) - set(prev), key=pos.get)
+            if out:
+                log.append(("swap_out", tuple(out)))
+            if inn:
+                log.append(("swap_in", tuple(inn)))
+            prev = win
+        log.append(("iter", i, tuple((pid, 8 + served[pid], 1) for pid in win)))
+        for pid in win:
+            served[pid] += 1
+    return log
+
+
+@pytest.mark.parametrize("ids", ["arrival", "reversed"])
+@pytest.mark.parametrize("n,m,k", [(n, m, k) for n in range(1, 7) for m in range(1, n + 1) for k in (1, 2, 3)])
+def test_sim_reschedule_round_robin(n, m, k, ids):
+    """C-9 pin of oracle.sim.run itself (not cfs.plan): n decode-only prompts
+    (8 tokens of KV, bs=64 -> one block for the whole 30-iteration horizon,
+    O huge), NB=m.  The full call log must equal the deque-rotation model:
+    plans exactly at i = 0 (mod k), page lists = set differences of
+    consecutive windows sorted by arrival, one block per paged prompt.  With
+    ids in reverse arrival order, sorting by id instead of (arrival, id)
+    fails; so does any off-by-one in the k cadence."""
+    order = list(range(n)) if ids == "arrival" else [100 + n - 1 - j for j in range(n)]
+    trace = [(pid, -100.0 + j, 8, 10 ** 6) for j, pid in enumerate(order)]
+    H = 30
+    res = sim.run(trace, sim.SimConfig(NB=m, bs=64, b=512, k=k, host_slots=64, max_iters=H), warm=order)
+    want = _sim_round_robin_expected(order, m, k, H)
+    got = []
+    for e in res.log:
+        if e[0] in ("swap_out", "swap_in"):
+            # one block / one slot per paged prompt (per-reschedule block counts)
+            per = [len(x[1]) for x in e[2]] if e[0] == "swap_out" else [len(x) for x in e[2]]
+            assert per == [1] * len(e[1]), e
+            got.append((e[0], e[1]))
+        else:
+            got.append(e)
+    assert got == want
+    assert res.blocks_out == sum(len(e[1]) for e in want if e[0] == "swap_out")
+    assert res.blocks_in == sum(len(e[1]) for e in want if e[0] == "swap_in")
+
+
 def _grid():
     states = []
     for phase, f, g, ctx in [(PREFILL, 0, 0, 0), (PREFILL, 20, 0, 20), (PREFILL, 40, 0, 40),
