@@ -66,7 +66,8 @@ def _peaks():
     return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s)"
 
 
-NVLINK_MEASURED = 770.0   # GB/s per direction, peer copy (B200_PROFILING.md); 900 nominal
+NVLINK_MEASURED = 770.0   # GB/s per direction, peer copy (B200_PROFILING.md)
+NVLINK_NOMINAL = 900.0    # GB/s per direction per GPU (NVLink 5), the north_star's denominator
 RW_BOUND = 6820.0         # GB/s read + write: a copy on DRAM that time-shares 7.36 TB/s reads and 6.35 TB/s writes
 # The paper's end-to-end results on 8x H100-80G, quoted as context only; the paper
 # gives no swap GB/s or per-prompt swap latency for its own path.
@@ -76,8 +77,10 @@ PAPER_CONTEXT = {
     "long_prompt_throughput": "4x vs FlexGen paging to DRAM (BASELINE.json says vLLM; the paper's baseline is FlexGen); "
                               "8x H100-80G, OPT-30B, 8192-token prompts (P:57, P:1009)",
     "a100_nvlink_copy": "50 GB/s at 4 MB, 200 GB/s at 64 MB, 2x A100-80GB (P:846-848)",
-    "here": "C3 responsiveness model on one B200 (profiles/r01_c3_model_*.json): CFS TTFT p50 28x below FCFS; "
-            "paging to the lender vs host DRAM keeps TPOT p99 1.8x lower",
+    "here_modelled": "MODELLED, not measured end to end: a responsiveness model of the C3 trace that puts each "
+                     "measured swap time on the critical path of the virtual-clock schedule "
+                     "(profiles/r01_c3_model_*.json) gives CFS a TTFT p50 28x below FCFS and, paging to the lender "
+                     "instead of host DRAM, a TPOT p99 1.8x lower",
 }
 
 
@@ -218,19 +221,27 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": round(val, 3), "unit": "GB/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * tot / args.steps, 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-        "config": _config(args, reference=True),
+        "config": _config(args, reference=True, n=args.gpus, roles=args.roles),
+        "sample": f"each timed step moves a {nblk}-block sample ({nblk}/{NBLK} of the config's {NBLK} blocks per "
+                  f"direction); value is GB/s over the sample's bytes, so it compares with our arm's GB/s",
         "cpu_baseline": {"value": round(val, 3), "unit": "GB/s", "cores": 1, "kind": "oracle", "sample": sample},
         "e2e": {"value": round(val, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
-def _config(args, reference=False, n=1):
+def _config(args, reference=False, n=1, roles="both"):
     U = 2 * SHAPE["L"] * SHAPE["bs"] * SHAPE["H"] * SHAPE["D"] * SHAPE["e"]
-    return {"workload": CFG["desc"] + "; step = preempt + resume "
-                        + ("(self-lender: arena in the same HBM)" if n == 1 else "(peer lender rank^1 over NVLink)"),
+    if n == 1:
+        how, lending = "(self-lender: arena in the same HBM)", "self (same HBM)"
+    elif roles == "split":
+        how = f"(ranks 0..{n // 2 - 1} page into HBM lent by ranks {n // 2}..{n - 1} over NVLink)"
+        lending = f"split roles: {n // 2} borrowers -> {n // 2} lenders over NVLink"
+    else:
+        how, lending = "(peer lender = partner rank over NVLink)", f"pairs over NVLink ({n} ranks, each both roles)"
+    return {"workload": CFG["desc"] + "; step = preempt + resume " + how,
             "name": CFG["name"], "prompts": CFG["nprompts"], "tokens_per_prompt": CFG["bpp"] * SHAPE["bs"],
-            "layout": dict(SHAPE, NB=NB), "lending": "self (same HBM)" if n == 1 else f"pairs over NVLink ({n} ranks)",
+            "layout": dict(SHAPE, NB=NB), "lending": lending,
             "engine": args.engine, "bytes_per_step": 2 * NBLK * U,
             "l2": f"inputs ({NBLK * U / 2**30:.1f} GiB per direction) >> 126 MB L2; no flush needed"}
 
@@ -274,27 +285,45 @@ def run_ours(args):
     arena_bytes = NBLK * U
     ipc_ptr = imported = None
     matching = None
+    borrower = True                  # this rank pages its own prompts (every rank unless --roles split)
+    roles = args.roles if ws > 1 else "both"
+    topology = None
     if ws == 1:
         arena = torch.empty(arena_bytes, dtype=torch.uint8, device=dev)
         ctx.lend(local, arena.data_ptr(), arena_bytes)
         mode = "self-lender"
     else:
-        from paper_2407_21255_b200.pairing import best_matching, exchange, measure_p2p
-        # pairing from the measured topology: P2P reachability
-        # rows from every rank, or (--measure-topology) rank 0's bandwidth
-        # matrix; then the max-min perfect matching
+        from paper_2407_21255_b200.pairing import best_bipartite, best_matching, exchange, measure_p2p
+        # pairing from the measured topology: rank 0's P2P
+        # bandwidth matrix (default), or P2P reachability rows from every
+        # rank (--no-measure-topology, and the shared-GPU test mode); then
+        # the max-min perfect matching (roles "both") or the max-min
+        # borrower -> lender assignment (roles "split", configs[3])
         if args.measure_topology and not shared:
             bw = measure_p2p(ws) if rank == 0 else None
             bw = exchange(bw)[0]
+            topology = "measured P2P copy GB/s (pairing.measure_p2p)"
         else:
             row = [0.0 if j == local else (1.0 if shared or aqua.can_access_peer(local, j) else 0.0)
                    for j in range(ws)]
             bw = exchange(row)
-        matching = best_matching(bw)
+            topology = "P2P reachability"
+        if roles == "split":
+            if ws % 2:
+                raise SystemExit("--roles split needs an even number of GPUs")
+            half = ws // 2
+            matching = best_bipartite(bw, list(range(half)), list(range(half, ws)))
+            borrower = rank < half
+        else:
+            matching = best_matching(bw)
         partner = matching[rank]
-        ipc_ptr = aqua.ipc_alloc(local, arena_bytes)          # what this rank lends to its partner
-        handles = exchange((rank, local, aqua.ipc_export(ipc_ptr)))
-        if partner == rank:
+        lends = roles == "both" or not borrower
+        if lends:
+            ipc_ptr = aqua.ipc_alloc(local, arena_bytes)      # what this rank lends to its partner
+        handles = exchange((rank, local, aqua.ipc_export(ipc_ptr) if lends else None))
+        if not borrower:
+            mode = f"lender for rank{partner}"
+        elif partner == rank:
             ctx.lend(local, ipc_ptr, arena_bytes)
             mode = "self-lender"
         else:
@@ -307,19 +336,21 @@ def run_ours(args):
                 arena = torch.empty(arena_bytes, dtype=torch.uint8, device=dev)
                 ctx.lend(local, arena.data_ptr(), arena_bytes)
                 mode = f"self-lender (peer rank{partner} unreachable: {err})"
-    perm = block_permutation(NB, NB, seed=2).tolist()
-    ctx.adopt_blocks(1, perm[NBLK:])      # filler: keeps the prompts' blocks scattered over the pool
     bpp = CFG["bpp"]
-    for i, pid in enumerate(PIDS):
-        ctx.adopt_blocks(pid, perm[i * bpp:(i + 1) * bpp])
-        ctx.kv_fill_pattern(pid, 0, bpp * bs, SEED_PATTERN)
+    if borrower:
+        perm = block_permutation(NB, NB, seed=2).tolist()
+        ctx.adopt_blocks(1, perm[NBLK:])      # filler: keeps the prompts' blocks scattered over the pool
+        for i, pid in enumerate(PIDS):
+            ctx.adopt_blocks(pid, perm[i * bpp:(i + 1) * bpp])
+            ctx.kv_fill_pattern(pid, 0, bpp * bs, SEED_PATTERN)
     torch.cuda.synchronize()
     swap = torch.cuda.Stream(device=dev)
     sw = swap.cuda_stream
 
-    for _ in range(args.warmup):
-        ctx.swap_out(PIDS, sw)
-        ctx.swap_in(PIDS, sw)
+    if borrower:
+        for _ in range(args.warmup):
+            ctx.swap_out(PIDS, sw)
+            ctx.swap_in(PIDS, sw)
     torch.cuda.synchronize()
 
     K = args.steps
@@ -332,7 +363,7 @@ def run_ours(args):
     with ClockSampler(local) as clk:
         start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         start.record(swap)
-        for k in range(K):
+        for k in range(K if borrower else 0):
             ev[k][0].record(swap)
             ctx.swap_out(PIDS, sw)
             ev[k][1].record(swap)
@@ -345,22 +376,24 @@ def run_ours(args):
     launches = ctx.launch_count() - n0
     try:
         shape = ctx.last_launch()          # what the library's AUTO policy launched (the swap_in of the last step)
-    except aqua.AquaError:                 # a baseline engine that launches no kernel of ours
+    except aqua.AquaError:                 # a baseline engine (or a lender rank) that launched no kernel of ours
         shape = {"engine": args.engine}
-    total_ms = start.elapsed_time(end)
-    out_ms = [a.elapsed_time(b) for a, b, _ in ev]
-    in_ms = [b.elapsed_time(c) for _, b, c in ev]
+    total_ms = start.elapsed_time(end) if borrower else 0.0
+    out_ms = [a.elapsed_time(b) for a, b, _ in ev] if borrower else [0.0]
+    in_ms = [b.elapsed_time(c) for _, b, c in ev] if borrower else [0.0]
     t = torch.tensor([total_ms], device="cpu" if shared else dev, dtype=torch.float64)
     if ws > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms_max = float(t.item())
 
     # parity at full size: the resumed prompt still holds its pattern
-    cnt = torch.zeros(1, dtype=torch.int64, device=dev)
-    for pid in PIDS:
-        ctx.kv_verify_pattern(pid, bpp * bs, SEED_PATTERN, cnt.data_ptr())
-    torch.cuda.synchronize()
-    mism = int(cnt.item())
+    mism = 0
+    if borrower:
+        cnt = torch.zeros(1, dtype=torch.int64, device=dev)
+        for pid in PIDS:
+            ctx.kv_verify_pattern(pid, bpp * bs, SEED_PATTERN, cnt.data_ptr())
+        torch.cuda.synchronize()
+        mism = int(cnt.item())
     if mism:
         raise SystemExit(f"rank {rank}: {mism} KV words differ after preempt/resume -- parity failure")
 
@@ -369,53 +402,66 @@ def run_ours(args):
     # kernels; a 16-byte probe of each resumed prompt's first K chunk comes
     # back device -> host; host-synchronised every step
     S0 = SHAPE["bs"] * SHAPE["H"] * SHAPE["D"] * SHAPE["e"]
-    bt_h = torch.empty(NBLK, dtype=torch.int32, pin_memory=True)
-    bt_d = torch.empty(NBLK, dtype=torch.int32, device=dev)
-    probe_h = torch.empty(len(PIDS), 16, dtype=torch.uint8, pin_memory=True)
+    e2e_t, lat_out, lat_in = [0.0], [0.0], [0.0]
+    if borrower:
+        bt_h = torch.empty(NBLK, dtype=torch.int32, pin_memory=True)
+        bt_d = torch.empty(NBLK, dtype=torch.int32, device=dev)
+        probe_h = torch.empty(len(PIDS), 16, dtype=torch.uint8, pin_memory=True)
 
-    def first_chunk(pid):
-        b = ctx.query(pid, with_ids=True)[3][0]
-        return layers[0][b * S0:b * S0 + 16]
+        def first_chunk(pid):
+            b = ctx.query(pid, with_ids=True)[3][0]
+            return layers[0][b * S0:b * S0 + 16]
 
-    probe_ref = torch.stack([first_chunk(pid).cpu() for pid in PIDS])
-    e2e_t, lat_out, lat_in = [], [], []
-    reps = max(20, min(K, 50))
-    for _ in range(reps):           # per-call host latency: sync on each ticket
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        ctx.sync(ctx.swap_out(PIDS, sw))
-        t1 = time.perf_counter()
-        ctx.sync(ctx.swap_in(PIDS, sw)[1])
-        t2 = time.perf_counter()
-        lat_out.append(t1 - t0)
-        lat_in.append(t2 - t1)
-    for _ in range(reps):           # the step as a user runs it: no sync between the calls
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        ctx.swap_out(PIDS, sw)
-        new, _ = ctx.swap_in(PIDS, sw)
-        with torch.cuda.stream(swap):
-            off = 0
-            for i, ids in enumerate(new):
-                bt_h.numpy()[off:off + len(ids)] = ids
-                off += len(ids)
-                b = ids[0]
-                probe_h[i].copy_(layers[0][b * S0:b * S0 + 16], non_blocking=True)
-            bt_d.copy_(bt_h, non_blocking=True)
-        swap.synchronize()
-        e2e_t.append(time.perf_counter() - t0)
-    if not torch.equal(probe_h, probe_ref):
-        raise SystemExit(f"rank {rank}: e2e probe of the resumed KV differs -- parity failure")
+        probe_ref = torch.stack([first_chunk(pid).cpu() for pid in PIDS])
+        e2e_t, lat_out, lat_in = [], [], []
+        reps = max(20, min(K, 50))
+        for _ in range(reps):           # per-call host latency: sync on each ticket
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            ctx.sync(ctx.swap_out(PIDS, sw))
+            t1 = time.perf_counter()
+            ctx.sync(ctx.swap_in(PIDS, sw)[1])
+            t2 = time.perf_counter()
+            lat_out.append(t1 - t0)
+            lat_in.append(t2 - t1)
+        for _ in range(reps):           # the step as a user runs it: no sync between the calls
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            ctx.swap_out(PIDS, sw)
+            new, _ = ctx.swap_in(PIDS, sw)
+            with torch.cuda.stream(swap):
+                off = 0
+                for i, ids in enumerate(new):
+                    bt_h.numpy()[off:off + len(ids)] = ids
+                    off += len(ids)
+                    b = ids[0]
+                    probe_h[i].copy_(layers[0][b * S0:b * S0 + 16], non_blocking=True)
+                bt_d.copy_(bt_h, non_blocking=True)
+            swap.synchronize()
+            e2e_t.append(time.perf_counter() - t0)
+        if not torch.equal(probe_h, probe_ref):
+            raise SystemExit(f"rank {rank}: e2e probe of the resumed KV differs -- parity failure")
 
     bytes_per_step = 2 * NBLK * U
-    value = ws * K * bytes_per_step / (total_ms_max / 1e3) / 1e9
+    n_borrowers = ws if roles == "both" else ws // 2
+    value = n_borrowers * K * bytes_per_step / (total_ms_max / 1e3) / 1e9
     out_avg, in_avg = statistics.mean(out_ms), statistics.mean(in_ms)
     per_rank = None
-    if ws > 1:                        # every rank's own per-direction link rate (bytes across the link per launch)
+    if ws > 1:                        # every rank's own per-direction link rate and preempt+resume latency
         from paper_2407_21255_b200.pairing import exchange
-        per_rank = [{"rank": r, "mode": m, "swap_out_GBps": round(NBLK * U / (o / 1e3) / 1e9, 1),
-                     "swap_in_GBps": round(NBLK * U / (i / 1e3) / 1e9, 1)}
-                    for r, m, o, i in exchange((rank, mode, out_avg, in_avg))]
+        per_rank = []
+        for r, m, b, o, i, lo, li, e2 in exchange((rank, mode, borrower, out_avg, in_avg,
+                                                   statistics.median(lat_out), statistics.median(lat_in),
+                                                   statistics.median(e2e_t))):
+            rec = {"rank": r, "mode": m}
+            if b:
+                rec.update({"swap_out_GBps": round(NBLK * U / (o / 1e3) / 1e9, 1),
+                            "swap_in_GBps": round(NBLK * U / (i / 1e3) / 1e9, 1),
+                            "preempt_device_ms": round(o, 4), "resume_device_ms": round(i, 4),
+                            "preempt_resume_device_ms": round(o + i, 4),
+                            "preempt_resume_host_p50_ms": round(1e3 * (lo + li), 4),
+                            "e2e_step_p50_ms": round(1e3 * e2, 4)})
+            per_rank.append(rec)
 
     host = None
     if ws == 1 and not args.no_host_baselines and CFG["name"] == "c2":
@@ -425,6 +471,7 @@ def run_ours(args):
         _cleanup(aqua, local, ipc_ptr, imported, ws)
         return
     hbm_peak, hbm_src = _peaks()
+    north = None
     if ws == 1:
         ach = 2 * NBLK * U / (out_avg / 1e3) / 1e9           # read + write bytes, same HBM
         roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": hbm_peak, "unit": "GB/s",
@@ -437,28 +484,47 @@ def run_ours(args):
                 "rw_bound": {"value": RW_BOUND, "frac": round(ach / RW_BOUND, 4),
                              "basis": "DRAM time-shared between reads and writes: 2 / (1/7.36 + 1/6.35) TB/s, pure "
                                       "read / pure write probe on this B200 (profiles/r01_hbm_probe.jsonl)"}}
+        north = {"per_pair_per_direction_GBps": {"swap_out": round(NBLK * U / (out_avg / 1e3) / 1e9, 1),
+                                                 "swap_in": round(NBLK * U / (in_avg / 1e3) / 1e9, 1)},
+                 "link": "none: at N=1 the lender is the same GPU's HBM (the north_star's '1 GPU (local/host)'); "
+                         "the 900 GB/s NVLink target applies from N=2"}
     else:
-        ach = NBLK * U / (out_avg / 1e3) / 1e9                # bytes across the link per direction
+        peers = [p for p in per_rank if "swap_out_GBps" in p]
+        lo_out = min(p["swap_out_GBps"] for p in peers)
+        lo_in = min(p["swap_in_GBps"] for p in peers)
+        ach = NBLK * U / (out_avg / 1e3) / 1e9                # rank 0's bytes across the link per direction
         roof = {"bound": "nvlink", "achieved": round(ach, 1), "peak": NVLINK_MEASURED, "unit": "GB/s",
-                "frac": round(ach / NVLINK_MEASURED, 4), "traffic": None, "nominal_peak": 900.0,
-                "kernel": "swap_out launch", "peak_source": "measured peer copy (B200_PROFILING.md)",
-                "algorithmic_bytes_per_launch": NBLK * U,
-                "swap_in_achieved": round(NBLK * U / (in_avg / 1e3) / 1e9, 1)}
+                "frac": round(ach / NVLINK_MEASURED, 4), "traffic": None,
+                "peak_source": "fallback: measured peer copy per direction (B200_PROFILING.md), "
+                               "MEASURED_PEAKS.json has no NVLink figure",
+                "nominal_peak": NVLINK_NOMINAL, "frac_of_nominal": round(ach / NVLINK_NOMINAL, 4),
+                "kernel": "swap_out launch (rank 0)", "algorithmic_bytes_per_launch": NBLK * U,
+                "swap_in_achieved": round(NBLK * U / (in_avg / 1e3) / 1e9, 1),
+                "traffic_note": "NVLink bytes need ncu --replay-mode application on a 2-GPU box "
+                                "(scripts/gpu_runs/r02_nvlink_ncu.sh); not captured yet"}
+        north = {"per_pair_per_direction_GBps": {"swap_out_min_over_pairs": lo_out, "swap_in_min_over_pairs": lo_in},
+                 "frac_of_900": {"swap_out": round(lo_out / NVLINK_NOMINAL, 4),
+                                 "swap_in": round(lo_in / NVLINK_NOMINAL, 4)},
+                 "frac_of_770_measured": {"swap_out": round(lo_out / NVLINK_MEASURED, 4),
+                                          "swap_in": round(lo_in / NVLINK_MEASURED, 4)},
+                 "target": ">= 0.8 of 900 GB/s per direction per GPU pair (BASELINE.json north_star)",
+                 "pairs": n_borrowers, "roles": roles, "topology": topology}
     cpu = None
     if ws == 1 and not args.no_cpu_baseline:
         cpu = cpu_oracle_sample(args.cpu_seconds)
         cpu.pop("seconds_per_step")
         cpu.pop("bytes_per_step")
         cpu["value"] = round(cpu["value"], 3)
-    e2e_val = ws * bytes_per_step / statistics.median(e2e_t) / 1e9
+    e2e_val = n_borrowers * bytes_per_step / statistics.median(e2e_t) / 1e9
     line = {
         "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": ws, "steps": K,
         "warmup": args.warmup, "ms_per_step": round(total_ms_max / K, 4), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-        "config": _config(args, n=ws),
+        "config": _config(args, n=ws, roles=roles),
         "mode": mode,
         "pairing": matching,
         "per_rank": per_rank,
+        "north_star": north,
         "preempt_resume_ms": {"preempt_device_ms": round(out_avg, 4), "resume_device_ms": round(in_avg, 4),
                               "sum_device_ms": round(out_avg + in_avg, 4),
                               "prompts_per_call": len(PIDS),
@@ -643,7 +709,12 @@ def main():
     ap.add_argument("--no-host-baselines", action="store_true")
     ap.add_argument("--host-reps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--measure-topology", action="store_true", help="N>1: pair GPUs by measured P2P bandwidth")
+    ap.add_argument("--measure-topology", action=argparse.BooleanOptionalAction, default=True,
+                    help="N>1: pair GPUs by rank 0's measured P2P bandwidth matrix (default); "
+                         "--no-measure-topology pairs by P2P reachability")
+    ap.add_argument("--roles", choices=["both", "split"], default="both",
+                    help="N>1: 'both' = every rank a borrower and a lender (bidirectional pairs); 'split' = ranks "
+                         "0..N/2-1 borrow from ranks N/2..N-1 (configs[3]: 4 borrowers -> 4 lenders)")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     args = ap.parse_args()
     if args.warmup < 3:

@@ -136,9 +136,18 @@ enum {
                                  per SM and >= 8 batches per CTA, else 0 (profiles/r01_tma_sched*.jsonl) */
   AQUA_OPT_TMA_STATIC_PCT = 10, /* dynamic schedule: percent of the items split statically (one contiguous range per
                                  CTA) before the claimed batches; 0 = all claimed */
-  AQUA_OPT_RATE_GBPS = 11     /* paging budget in GB/s of swap per direction (0 = off): the copy kernels run on
+  AQUA_OPT_RATE_GBPS = 11,    /* paging budget in GB/s of swap per direction (0 = off): the copy kernels run on
                                  ceil(rate / 50) SMs (one SM moves ~50 GB/s of swap on the HBM path), leaving the other
                                  SMs and HBM bandwidth to decode; combines with AQUA_OPT_MAX_CTAS (the smaller cap wins) */
+  AQUA_OPT_PEER_CTAS = 12,    /* CTA cap for launches that touch a PEER lender's arena (another GPU's HBM over
+                                 NVLink; 0 = all SMs).  Default 32: one SM issues ~63 GB/s of HBM writes and keeps
+                                 ~200 KiB of copies in flight under a cap, so ~15 SMs could carry
+                                 900 GB/s per direction; 32 leaves 2x margin for NVLink latency and the other 116
+                                 SMs to decode.  A placeholder until the per-SM NVLink rate is measured
+                                 (scripts/nvlink_peer.py); the smallest of this, MAX_CTAS and RATE_GBPS wins */
+  AQUA_OPT_PEER_TEST = 13     /* test hook, set before aqua_lend: 1 treats the next GPU arena as a peer (probe +
+                                 peer cap) even on the borrower's own device; 2 also makes its bulk-copy probe fail
+                                 (the LDST fallback); 0 (default) detects peers from the arena's device */
 };
 
 enum { AQUA_TMA_SCHED_AUTO = 1 << 30 };
@@ -323,6 +332,15 @@ AQUA_API aqua_status aqua_launch_count(aqua_ctx* ctx, uint64_t* launches);
  * pointer may be NULL.  AQUA_E_STATE before the first launch (and for copy-engine-only calls, which launch none). */
 AQUA_API aqua_status aqua_last_launch(aqua_ctx* ctx, int32_t* grid, int32_t* threads, int32_t* stages,
                                       int32_t* engine, int32_t* variant, int64_t* batch_items, int64_t* inline_desc);
+
+/* What aqua_lend found about an arena (which = AQUA_LOC_PEER for the GPU lender, AQUA_LOC_HOST for host DRAM):
+ * the device holding its memory (AQUA_HOST for host DRAM), whether it is a peer GPU (NVLink / P2P), and the
+ * result of the lend-time probe (bit 1 plain 16-byte loads/stores, 2 TMA bulk stores, 4 TMA bulk loads round-trip
+ * correctly; 7 = all; -1 = not probed: host arenas and the borrower's own HBM).  A peer arena whose bulk copies
+ * fail the probe is served by the LDST engine (plain loads and stores over NVLink) instead of TMA; one whose plain
+ * accesses fail is refused by aqua_lend with AQUA_E_PEER.  AQUA_E_STATE if that arena is not lent. */
+AQUA_API aqua_status aqua_arena_info(aqua_ctx* ctx, int32_t which, int32_t* device, int32_t* peer, int32_t* probe,
+                                     int32_t* nslots);
 
 /* Cross-process lending (setup only).  The lender process
  * exports a 64-byte handle for a device allocation; the borrower process

@@ -74,6 +74,32 @@ def write_tokens(pool, pid: int, t0: int, t1: int, seed: int) -> None:
                 ch[row:row + lay.H * lay.D * 2] = w.reshape(-1).view(np.uint8)
 
 
+def write_token_range(pool, pid: int, t0: int, t1: int, seed: int) -> None:
+    """write_tokens for a whole range at once (same bytes): the words of
+    tokens [t0, t1) are computed together per (layer, kv), then stored one
+    run of consecutive rows per block."""
+    lay = pool.lay
+    assert lay.e == 2
+    if t1 <= t0:
+        return
+    bt = pool.prompts[pid].blocks
+    row = lay.H * lay.D * 2
+    t = np.arange(t0, t1, dtype=np.uint64)[:, None, None]
+    h = np.arange(lay.H, dtype=np.uint64)[None, :, None]
+    d = np.arange(lay.D, dtype=np.uint64)[None, None, :]
+    for l in range(lay.L):
+        for kv in (0, 1):
+            z = splitmix64(np.uint64(seed) ^ pack(pid, t, l, kv, h, d))
+            w = (z & np.uint64(0xFFFF)).astype(np.uint16).reshape(t1 - t0, row // 2).view(np.uint8)
+            tt = t0
+            while tt < t1:
+                b, i = bt[tt // lay.bs], tt % lay.bs
+                n = min(lay.bs - i, t1 - tt)
+                ch = pool.chunk(l, kv, b)
+                ch[i * row:(i + n) * row] = w[tt - t0:tt - t0 + n].reshape(-1)
+                tt += n
+
+
 def check_tokens(pool, pid: int, ntok: int, seed: int) -> bool:
     """True iff tokens [0, ntok) of pid hold their closed-form words."""
     lay = pool.lay

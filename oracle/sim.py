@@ -279,3 +279,37 @@ def run(trace: Sequence[Tuple[int, float, int, int]], cfg: SimConfig,
         i += 1
     pool.check_invariants()
     return SimResult(log, ttft, finish, i, blocks_out, blocks_in, t, timeline)
+
+
+def replay_bytes(log: Sequence[tuple], pool: Pool, seed: int, on_iter=None) -> None:
+    """Bytes mode of the trace driver (SURVEY 8(d) parity protocol, scaled-down
+    C3): apply a call log that run() emitted to a bytes-mode Pool -- every
+    paging call through the Pool's own operations (C-4 / C-5), and
+    for each iteration the synthetic decode: tokens [ctx0, ctx0 + t) of each
+    work item get their closed-form words (C-11).  Each call's result must
+    equal the log's (ids, slots, locations).  on_iter(i) runs after iteration
+    i's tokens are written.  Elastic entries (reclaim / relend / migrate) are
+    not replayed."""
+    from . import pattern
+    for e in log:
+        kind = e[0]
+        if kind == "swap_out":
+            res = pool.swap_out(e[1])
+            assert tuple((loc, tuple(s)) for _, loc, s in res) == tuple(e[2]), e
+        elif kind == "swap_in":
+            res = pool.swap_in(e[1])
+            assert tuple(tuple(x) for x in res) == tuple(e[2]), e
+        elif kind == "alloc":
+            ids = pool.alloc_blocks(e[1], len(e[2]))
+            assert tuple(ids) == tuple(e[2]), e
+        elif kind == "free":
+            pool.free_prompt(e[1])
+        elif kind == "iter":
+            for pid, ctx0, t in e[2]:
+                pattern.write_token_range(pool, pid, ctx0, ctx0 + t, seed)
+            if on_iter is not None:
+                on_iter(e[1])
+        elif kind in ("plan", "policy"):
+            pass
+        else:
+            raise NotImplementedError(f"bytes replay of {kind!r}")

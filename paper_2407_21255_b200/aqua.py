@@ -26,7 +26,8 @@ RESIDENT, SWAPPED = 1, 2
 LOC_LOCAL, LOC_PEER, LOC_HOST = 0, 1, 2
 KERNEL_AUTO, KERNEL_TMA, KERNEL_LDST, BASE_PER_CHUNK, BASE_GATHER_TEMP, BASE_BATCH, KERNEL_CE_HOST = 0, 1, 2, 3, 4, 5, 6
 (OPT_KERNEL, OPT_MAX_CTAS, OPT_TMA_PIECE, OPT_TMA_STAGES, OPT_TIMING, OPT_LDST_VARIANT, OPT_TMA_VARIANT,
- OPT_INLINE_MAX, OPT_TMA_SCHED, OPT_TMA_STATIC_PCT, OPT_RATE_GBPS) = (1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11)
+ OPT_INLINE_MAX, OPT_TMA_SCHED, OPT_TMA_STATIC_PCT, OPT_RATE_GBPS, OPT_PEER_CTAS,
+ OPT_PEER_TEST) = (1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13)
 TMA_SCHED_AUTO = 1 << 30
 
 # Every symbol include/aqua.h declares (checked by tests/test_abi.py).
@@ -34,7 +35,7 @@ SYMBOLS = [
     "aqua_create", "aqua_destroy", "aqua_lend", "aqua_alloc_blocks", "aqua_adopt_blocks",
     "aqua_swap_out", "aqua_swap_in", "aqua_swap_exchange", "aqua_swap_out_layers", "aqua_swap_in_layers", "aqua_free", "aqua_migrate", "aqua_reclaim", "aqua_prefix_store", "aqua_prefix_load",
     "aqua_prefix_drop", "aqua_prefix_query", "aqua_wait", "aqua_sync", "aqua_ticket_done", "aqua_ticket_elapsed",
-    "aqua_query", "aqua_counts", "aqua_arena_base", "aqua_set_option", "aqua_get_option",
+    "aqua_query", "aqua_counts", "aqua_arena_base", "aqua_arena_info", "aqua_set_option", "aqua_get_option",
     "aqua_last_descriptors", "aqua_launch_count", "aqua_last_launch", "aqua_ipc_export", "aqua_ipc_import",
     "aqua_ipc_close", "aqua_ipc_alloc", "aqua_ipc_free", "aqua_can_access_peer", "aqua_kv_fill_pattern", "aqua_kv_fill_pattern_batch",
     "aqua_kv_verify_pattern",
@@ -87,6 +88,7 @@ def _load() -> C.CDLL:
         "aqua_query": (C.c_int, [VP, U64, P(I32), P(I32), P(I32), P(I32), I32]),
         "aqua_counts": (C.c_int, [VP, P(I32), P(I32), P(I32)]),
         "aqua_arena_base": (C.c_int, [VP, I32, P(VP), P(I32)]),
+        "aqua_arena_info": (C.c_int, [VP, I32, P(I32), P(I32), P(I32), P(I32)]),
         "aqua_set_option": (C.c_int, [VP, I32, I64]),
         "aqua_get_option": (C.c_int, [VP, I32, P(I64)]),
         "aqua_last_descriptors": (C.c_int, [VP, P(I32), P(I32), P(I32), I64, P(I64)]),
@@ -315,6 +317,12 @@ class Ctx:
         p, n = C.c_void_p(), C.c_int32()
         self._c(lib.aqua_arena_base(self.h, loc, C.byref(p), C.byref(n)))
         return p.value or 0, n.value
+
+    def arena_info(self, which: int) -> dict:
+        """aqua_arena_info: which = LOC_PEER (the GPU lender) or LOC_HOST."""
+        d, pe, pr, n = (C.c_int32() for _ in range(4))
+        self._c(lib.aqua_arena_info(self.h, which, C.byref(d), C.byref(pe), C.byref(pr), C.byref(n)))
+        return {"device": d.value, "peer": bool(pe.value), "probe": pr.value, "nslots": n.value}
 
     def set_option(self, opt: int, value: int) -> None:
         self._c(lib.aqua_set_option(self.h, opt, value))

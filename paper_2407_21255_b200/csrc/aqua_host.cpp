@@ -11,6 +11,8 @@
 // GPU every data call fails (only AQUA_DRYRUN contexts run without one).
 #include "aqua.h"
 
+#include <nvtx3/nvToolsExt.h>
+
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
@@ -39,6 +41,9 @@ struct Arena {
   uint64_t bytes = 0;
   int32_t nslots = 0;
   bool owned = false;
+  bool peer = false;           // memory of another GPU (P2P / NVLink)
+  int mem_device = -1;         // the GPU holding a GPU arena's memory (MAPPED: from the pointer)
+  int probe = -1;              // lend-time probe bits (aqua_arena_info), -1 = not probed
   aqua::IdSet free;            // lowest-first (R4)
   std::vector<uint64_t> tick;  // last library ticket that touched each slot
 };
@@ -84,6 +89,8 @@ struct aqua_ctx {
   int tma_static_pct = 0;       // AQUA_OPT_TMA_STATIC_PCT: statically split head of a dynamic launch
   int pack_vec = 64;            // register movers pack chunks of <= pack_vec x 16 B (AQUA_LDST_PACK env)
   int rate_gbps = 0;            // AQUA_OPT_RATE_GBPS: paging budget -> CTA cap (0 = off)
+  int peer_ctas = 32;           // AQUA_OPT_PEER_CTAS: CTA cap for launches touching a peer arena
+  int peer_test = 0;            // AQUA_OPT_PEER_TEST
   uint32_t* d_ctr = nullptr;    // kCtrSlots {next, done} pairs (inside the d_layer_base allocation)
   uint32_t ctr_next = 0;
   std::vector<uint64_t> ctr_tick;   // ticket of the last launch that used each pair
@@ -116,6 +123,7 @@ struct aqua_ctx {
   // AQUA_KERNEL_CE_HOST staging buffers, one per direction (out, in), and
   // the ticket of their last use
   uint8_t* ce_temp[2] = {nullptr, nullptr};
+  size_t ce_cap[2] = {0, 0};
   uint64_t ce_tick[2] = {0, 0};
   bool poisoned = false;
   std::string err;
@@ -127,6 +135,17 @@ struct aqua_ctx {
 };
 
 namespace {
+
+// NVTX ranges around the public calls (host-side tracing: nsys / ncu NVTX
+// filters).  Header-only NVTX v3; without an attached tool a push/pop costs
+// a few nanoseconds.
+struct NvtxScope {
+  explicit NvtxScope(const char* name) { nvtxRangePushA(name); }
+  ~NvtxScope() { nvtxRangePop(); }
+  NvtxScope(const NvtxScope&) = delete;
+  NvtxScope& operator=(const NvtxScope&) = delete;
+};
+#define AQUA_NVTX(name) NvtxScope aqua_nvtx_scope_(name)
 
 thread_local std::string g_err;
 constexpr int kHostCtas = 8;   // CTA cap for host-only swaps (PCIe-bound)
@@ -333,8 +352,21 @@ aqua_status run_copy_ce_host(aqua_ctx* c, const std::vector<Desc>& ds, aqua::Dir
                              int32_t c0, int32_t nc) {
   const int di = dir == aqua::kOut ? 0 : 1;
   const size_t per = static_cast<size_t>(nc) * c->S;           // bytes of one descriptor's range
-  const size_t chunk = std::max<size_t>(1, kCeChunk / per);     // descriptors per chunk
-  if (!c->ce_temp[di]) CK(c, cudaMalloc(reinterpret_cast<void**>(&c->ce_temp[di]), chunk * per));
+  if (c->ce_cap[di] < per) {
+    // first use, or a range larger than the buffer: (re)allocate once the
+    // buffer's last user has finished
+    if (c->ce_temp[di]) {
+      auto it = c->live.find(c->ce_tick[di]);
+      if (it != c->live.end()) CK(c, cudaEventSynchronize(it->second.ev));
+      CK(c, cudaFree(c->ce_temp[di]));
+      c->ce_temp[di] = nullptr;
+      c->ce_cap[di] = 0;
+    }
+    const size_t cap = std::max(kCeChunk, per);
+    CK(c, cudaMalloc(reinterpret_cast<void**>(&c->ce_temp[di]), cap));
+    c->ce_cap[di] = cap;
+  }
+  const size_t chunk = c->ce_cap[di] / per;                      // descriptors per chunk (>= 1)
   if (aqua_status s = wait_all(c, {c->ce_tick[di]}, st)) return s;   // the buffer's last user
   uint8_t* tmp = c->ce_temp[di];
   const int kernel_engine = AQUA_KERNEL_TMA;
@@ -529,6 +561,23 @@ aqua_status run_copy(aqua_ctx* c, const std::vector<Desc>& ds, aqua::Dir dir, cu
       all_host = all_host && ((d.slot_arena & kArenaBit) ||
                               (dir == aqua::kMig && (static_cast<uint32_t>(d.block) & kArenaBit)));
     if (all_host && (cap == 0 || cap > kHostCtas)) cap = kHostCtas;
+    // A launch that touches a peer lender's arena is NVLink-bound: cap it at
+    // peer_ctas (the rest of the SMs stay with decode), and serve it with
+    // plain loads/stores if the lend-time probe saw bulk copies misbehave.
+    bool touches_peer = false;
+    if (c->gpu.present && c->gpu.peer)
+      for (const Desc& d : ds) {
+        const bool img_gpu = !(d.slot_arena & kArenaBit);
+        const bool src_gpu = dir == aqua::kMig && !(static_cast<uint32_t>(d.block) & kArenaBit);
+        if (img_gpu || src_gpu) {
+          touches_peer = true;
+          break;
+        }
+      }
+    if (touches_peer) {
+      if (c->peer_ctas > 0 && (cap == 0 || cap > c->peer_ctas)) cap = c->peer_ctas;
+      if ((c->gpu.probe & 6) != 6 && engine == AQUA_KERNEL_TMA) engine = AQUA_KERNEL_LDST;
+    }
     if (engine == AQUA_KERNEL_TMA) {
       // stage = 32 KiB (or the option): one piece of a large chunk, or a
       // group of whole small chunks that are contiguous in the image
@@ -624,8 +673,6 @@ aqua_status run_copy(aqua_ctx* c, const std::vector<Desc>& ds, aqua::Dir dir, cu
     if (need > c->temp_cap) {
       CK(c, cudaDeviceSynchronize());
       if (c->d_temp) cudaFree(c->d_temp);
-    for (uint8_t* t : c->ce_temp)
-      if (t) cudaFree(t);
       c->d_temp = nullptr;
       CK(c, cudaMalloc(reinterpret_cast<void**>(&c->d_temp), need));
       c->temp_cap = need;
@@ -789,6 +836,7 @@ const char* aqua_strerror(aqua_status s) {
 const char* aqua_last_error(aqua_ctx* c) { return c ? c->err.c_str() : g_err.c_str(); }
 
 aqua_status aqua_create(int device, const aqua_kv_layout* lay, aqua_ctx** out) {
+  AQUA_NVTX("aqua_create");
   if (!out || !lay) return fail(nullptr, AQUA_E_INVAL, "null argument");
   *out = nullptr;
   if (device < 0 && device != AQUA_DRYRUN) return fail(nullptr, AQUA_E_INVAL, "bad device");
@@ -863,6 +911,7 @@ aqua_status aqua_create(int device, const aqua_kv_layout* lay, aqua_ctx** out) {
 }
 
 aqua_status aqua_destroy(aqua_ctx* c) {
+  AQUA_NVTX("aqua_destroy");
   if (!c) return AQUA_E_INVAL;
   if (!c->dry) {
     DevGuard g(c->device);
@@ -886,6 +935,8 @@ aqua_status aqua_destroy(aqua_ctx* c) {
     if (c->h_stage) cudaFreeHost(c->h_stage);
     if (c->d_stage) cudaFree(c->d_stage);
     if (c->d_temp) cudaFree(c->d_temp);
+    for (uint8_t* t : c->ce_temp)
+      if (t) cudaFree(t);
     cudaGetLastError();
   }
   delete c;
@@ -893,6 +944,7 @@ aqua_status aqua_destroy(aqua_ctx* c) {
 }
 
 aqua_status aqua_lend(aqua_ctx* c, int lender, void* base, uint64_t bytes, int32_t* out_nslots) {
+  AQUA_NVTX("aqua_lend");
   if (aqua_status s = precheck(c)) return s;
   const bool is_host = lender == AQUA_HOST;
   Arena& a = is_host ? c->host : c->gpu;
@@ -956,6 +1008,47 @@ aqua_status aqua_lend(aqua_ctx* c, int lender, void* base, uint64_t bytes, int32
       }
     }
   }
+  if (!c->dry && !is_host && na.base) {
+    DevGuard g(c->device);
+    int mem_dev = lender;
+    if (lender == AQUA_MAPPED) {
+      cudaPointerAttributes at{};
+      if (cudaPointerGetAttributes(&at, base) == cudaSuccess && at.type == cudaMemoryTypeDevice)
+        mem_dev = at.device;
+      else
+        cudaGetLastError();
+    }
+    na.mem_device = mem_dev;
+    na.peer = (mem_dev >= 0 && mem_dev != c->device) || c->peer_test > 0;
+    if (na.peer) {
+      // once per lent arena: do plain, bulk-store and bulk-load accesses
+      // reach it correctly? (restores the bytes it touches)
+      int* d_res = nullptr;
+      int res = 0;
+      cudaError_t e = cudaMalloc(reinterpret_cast<void**>(&d_res), sizeof(int));
+      if (e == cudaSuccess) e = cudaMemset(d_res, 0, sizeof(int));
+      if (e == cudaSuccess) e = aqua::launch_peer_probe(na.base, static_cast<int64_t>(bytes), d_res, nullptr);
+      if (e == cudaSuccess) e = cudaMemcpy(&res, d_res, sizeof(int), cudaMemcpyDeviceToHost);
+      if (d_res) cudaFree(d_res);
+      if (e != cudaSuccess) {
+        if (na.owned) {
+          DevGuard g2(lender);
+          cudaFree(na.base);
+        }
+        return cuda_fail(c, e, "lender probe");
+      }
+      if (c->peer_test == 2) res &= 1;
+      na.probe = res;
+      if (!(res & 1)) {
+        if (na.owned) {
+          DevGuard g2(lender);
+          cudaFree(na.base);
+        }
+        return fail(c, AQUA_E_PEER, "lender arena: plain loads/stores do not round-trip");
+      }
+    }
+    c->peer_test = 0;   // the hook applies to one lend
+  }
   na.free.init(na.nslots, true);
   na.tick.assign(na.nslots, 0);
   a = std::move(na);
@@ -964,6 +1057,7 @@ aqua_status aqua_lend(aqua_ctx* c, int lender, void* base, uint64_t bytes, int32
 }
 
 aqua_status aqua_alloc_blocks(aqua_ctx* c, uint64_t pid, int32_t n, aqua_stream_t stream, int32_t* out_ids) {
+  AQUA_NVTX("aqua_alloc_blocks");
   if (aqua_status s = precheck(c)) return s;
   if (n < 0 || (n > 0 && !out_ids)) return fail(c, AQUA_E_INVAL, "n < 0 or null out_ids");
   auto it = c->prompts.find(pid);
@@ -987,6 +1081,7 @@ aqua_status aqua_alloc_blocks(aqua_ctx* c, uint64_t pid, int32_t n, aqua_stream_
 }
 
 aqua_status aqua_adopt_blocks(aqua_ctx* c, uint64_t pid, int32_t n, const int32_t* ids, aqua_stream_t stream) {
+  AQUA_NVTX("aqua_adopt_blocks");
   if (aqua_status s = precheck(c)) return s;
   if (n < 0 || (n > 0 && !ids)) return fail(c, AQUA_E_INVAL, "n < 0 or null ids");
   std::unordered_set<int32_t> seen;
@@ -1152,16 +1247,19 @@ static aqua_status swap_in_impl(aqua_ctx* c, int32_t n, const uint64_t* pids, aq
 }
 
 aqua_status aqua_swap_out(aqua_ctx* c, int32_t n, const uint64_t* pids, aqua_stream_t stream, uint64_t* out_ticket) {
+  AQUA_NVTX("aqua_swap_out");
   return swap_out_impl(c, n, pids, stream, out_ticket, 0, nullptr);
 }
 
 aqua_status aqua_swap_in(aqua_ctx* c, int32_t n, const uint64_t* pids, aqua_stream_t stream, int32_t* out_ids,
                          int64_t out_ids_cap, int32_t* out_counts, uint64_t* out_ticket) {
+  AQUA_NVTX("aqua_swap_in");
   return swap_in_impl(c, n, pids, stream, out_ids, out_ids_cap, out_counts, out_ticket, 0, nullptr);
 }
 
 aqua_status aqua_swap_out_layers(aqua_ctx* c, int32_t n, const uint64_t* pids, aqua_stream_t stream,
                                  int32_t layer_group, uint64_t* out_tickets) {
+  AQUA_NVTX("aqua_swap_out_layers");
   if (!c) return fail(nullptr, AQUA_E_INVAL, "null ctx");
   if (layer_group < 1 || !out_tickets) return fail(c, AQUA_E_INVAL, "layer_group >= 1 and out_tickets needed");
   const int32_t ng = (c->L + layer_group - 1) / layer_group;
@@ -1176,6 +1274,7 @@ aqua_status aqua_swap_out_layers(aqua_ctx* c, int32_t n, const uint64_t* pids, a
 aqua_status aqua_swap_in_layers(aqua_ctx* c, int32_t n, const uint64_t* pids, aqua_stream_t stream,
                                 int32_t layer_group, int32_t* out_ids, int64_t out_ids_cap, int32_t* out_counts,
                                 uint64_t* out_tickets) {
+  AQUA_NVTX("aqua_swap_in_layers");
   if (!c) return fail(nullptr, AQUA_E_INVAL, "null ctx");
   if (layer_group < 1 || !out_tickets) return fail(c, AQUA_E_INVAL, "layer_group >= 1 and out_tickets needed");
   const int32_t ng = (c->L + layer_group - 1) / layer_group;
@@ -1197,6 +1296,7 @@ aqua_status aqua_swap_exchange(aqua_ctx* c, int32_t n_out, const uint64_t* out_p
                                const uint64_t* in_pids, aqua_stream_t out_stream, aqua_stream_t in_stream,
                                int32_t pieces, int32_t* out_ids, int64_t out_ids_cap, int32_t* out_counts,
                                uint64_t* out_ticket, uint64_t* in_ticket) {
+  AQUA_NVTX("aqua_swap_exchange");
   if (aqua_status s = precheck(c)) return s;
   if (out_ticket) *out_ticket = 0;
   if (in_ticket) *in_ticket = 0;
@@ -1413,6 +1513,7 @@ static aqua_status migrate_impl(aqua_ctx* c, const std::vector<uint64_t>& pids, 
 
 aqua_status aqua_migrate(aqua_ctx* c, int32_t n, const uint64_t* pids, int32_t dst_loc, aqua_stream_t stream,
                          uint64_t* out_ticket) {
+  AQUA_NVTX("aqua_migrate");
   if (aqua_status s = precheck(c)) return s;
   if (out_ticket) *out_ticket = 0;
   if (n < 0 || (n > 0 && !pids)) return fail(c, AQUA_E_INVAL, "n < 0 or null pids");
@@ -1421,6 +1522,7 @@ aqua_status aqua_migrate(aqua_ctx* c, int32_t n, const uint64_t* pids, int32_t d
 }
 
 aqua_status aqua_reclaim(aqua_ctx* c, aqua_stream_t stream, uint64_t* out_ticket) {
+  AQUA_NVTX("aqua_reclaim");
   if (aqua_status s = precheck(c)) return s;
   if (out_ticket) *out_ticket = 0;
   if (!c->gpu.present) return AQUA_OK;                 // idempotent
@@ -1463,6 +1565,7 @@ aqua_status aqua_reclaim(aqua_ctx* c, aqua_stream_t stream, uint64_t* out_ticket
 // ---------------------------------------------------------------- NEXT-2
 aqua_status aqua_prefix_store(aqua_ctx* c, uint64_t fid, uint64_t src_pid, int32_t n, aqua_stream_t stream,
                               uint64_t* out_ticket) {
+  AQUA_NVTX("aqua_prefix_store");
   if (aqua_status s = precheck(c)) return s;
   if (out_ticket) *out_ticket = 0;
   if (c->prefixes.count(fid)) return fail(c, AQUA_E_INVAL, "prefix id in use");
@@ -1507,6 +1610,7 @@ aqua_status aqua_prefix_store(aqua_ctx* c, uint64_t fid, uint64_t src_pid, int32
 
 aqua_status aqua_prefix_load(aqua_ctx* c, uint64_t fid, uint64_t dst_pid, aqua_stream_t stream, int32_t* out_ids,
                              int32_t cap, uint64_t* out_ticket) {
+  AQUA_NVTX("aqua_prefix_load");
   if (aqua_status s = precheck(c)) return s;
   if (out_ticket) *out_ticket = 0;
   auto fi = c->prefixes.find(fid);
@@ -1567,6 +1671,7 @@ aqua_status aqua_prefix_query(aqua_ctx* c, uint64_t fid, int32_t* location, int3
 }
 
 aqua_status aqua_free(aqua_ctx* c, uint64_t pid, aqua_stream_t stream) {
+  AQUA_NVTX("aqua_free");
   if (aqua_status s = precheck(c)) return s;
   auto it = c->prompts.find(pid);
   if (it == c->prompts.end()) return fail(c, AQUA_E_STATE, "unknown pid");
@@ -1594,6 +1699,7 @@ aqua_status aqua_free(aqua_ctx* c, uint64_t pid, aqua_stream_t stream) {
 }
 
 aqua_status aqua_wait(aqua_ctx* c, uint64_t ticket, aqua_stream_t stream) {
+  AQUA_NVTX("aqua_wait");
   if (aqua_status s = precheck(c)) return s;
   if (c->dry) return AQUA_OK;
   DevGuard g(c->device);
@@ -1604,6 +1710,7 @@ aqua_status aqua_wait(aqua_ctx* c, uint64_t ticket, aqua_stream_t stream) {
 }
 
 aqua_status aqua_sync(aqua_ctx* c, uint64_t ticket) {
+  AQUA_NVTX("aqua_sync");
   if (aqua_status s = precheck(c)) return s;
   if (c->dry) return AQUA_OK;
   auto it = c->live.find(ticket);
@@ -1680,6 +1787,19 @@ aqua_status aqua_arena_base(aqua_ctx* c, int32_t loc, void** base, int32_t* nslo
   return AQUA_OK;
 }
 
+aqua_status aqua_arena_info(aqua_ctx* c, int32_t which, int32_t* device, int32_t* peer, int32_t* probe,
+                            int32_t* nslots) {
+  if (!c) return fail(nullptr, AQUA_E_INVAL, "null ctx");
+  if (which != AQUA_LOC_PEER && which != AQUA_LOC_HOST) return fail(c, AQUA_E_INVAL, "which");
+  const Arena& a = which == AQUA_LOC_HOST ? c->host : c->gpu;
+  if (!a.present) return fail(c, AQUA_E_STATE, "arena not lent");
+  if (device) *device = which == AQUA_LOC_HOST ? AQUA_HOST : (a.mem_device >= 0 ? a.mem_device : a.device);
+  if (peer) *peer = a.peer ? 1 : 0;
+  if (probe) *probe = a.probe;
+  if (nslots) *nslots = a.nslots;
+  return AQUA_OK;
+}
+
 aqua_status aqua_set_option(aqua_ctx* c, int32_t opt, int64_t v) {
   if (!c) return fail(nullptr, AQUA_E_INVAL, "null ctx");
   switch (opt) {
@@ -1727,6 +1847,14 @@ aqua_status aqua_set_option(aqua_ctx* c, int32_t opt, int64_t v) {
       if (v < 0 || v > (1 << 20)) return fail(c, AQUA_E_INVAL, "rate");
       c->rate_gbps = static_cast<int>(v);
       return AQUA_OK;
+    case AQUA_OPT_PEER_CTAS:
+      if (v < 0 || v > (1 << 20)) return fail(c, AQUA_E_INVAL, "peer ctas");
+      c->peer_ctas = static_cast<int>(v);
+      return AQUA_OK;
+    case AQUA_OPT_PEER_TEST:
+      if (v < 0 || v > 2) return fail(c, AQUA_E_INVAL, "peer test");
+      c->peer_test = static_cast<int>(v);
+      return AQUA_OK;
   }
   return fail(c, AQUA_E_INVAL, "unknown option");
 }
@@ -1745,6 +1873,8 @@ aqua_status aqua_get_option(aqua_ctx* c, int32_t opt, int64_t* v) {
     case AQUA_OPT_TMA_SCHED: *v = c->tma_sched; return AQUA_OK;
     case AQUA_OPT_TMA_STATIC_PCT: *v = c->tma_static_pct; return AQUA_OK;
     case AQUA_OPT_RATE_GBPS: *v = c->rate_gbps; return AQUA_OK;
+    case AQUA_OPT_PEER_CTAS: *v = c->peer_ctas; return AQUA_OK;
+    case AQUA_OPT_PEER_TEST: *v = c->peer_test; return AQUA_OK;
   }
   return fail(c, AQUA_E_INVAL, "unknown option");
 }

@@ -107,6 +107,11 @@ cudaError_t launch_swap_ldst(const SwapHeader& h, const Desc* inl, Dir dir, int 
 cudaError_t launch_pattern_fill(const PatternParams& p, int num_sms, cudaStream_t s);
 cudaError_t launch_pattern_verify(const PatternParams& p, int num_sms, cudaStream_t s);
 
+// One-warp probe of a lent GPU arena (aqua_lend): plain, TMA bulk-store and
+// TMA bulk-load round trips over its first <= 4 KiB, which it restores.
+// *d_result bits: 1 plain ok, 2 bulk store ok, 4 bulk load ok.
+cudaError_t launch_peer_probe(uint8_t* arena, int64_t bytes, int* d_result, cudaStream_t s);
+
 // Max dynamic shared memory the TMA kernel will request (for attribute setup).
 int tma_smem_bytes(int piece, int stages);
 

@@ -781,6 +781,96 @@ int grid_for(int64_t work_units, int per_cta, int num_sms, int ctas_per_sm, int 
   return static_cast<int>(g);
 }
 
+
+// ------------------------------------------------------------ lender probe
+// Checks, once per lent GPU arena, that the three kinds of access the copy
+// engines make reach it correctly: plain 16-byte loads/stores (LDST engine),
+// TMA bulk stores (swap_out) and TMA bulk loads (swap_in pull).  The first
+// n bytes of the arena are saved in shared memory and restored at the end,
+// so the probe leaves the arena's bytes as it found them (invariant I2).
+// result bits: 1 plain ok, 2 bulk store ok, 4 bulk load ok.
+constexpr int kProbeBytes = 4096;
+
+__device__ __forceinline__ uint4 probe_word(int i, uint32_t salt) {
+  const uint32_t x = 0x9E3779B9u * static_cast<uint32_t>(i + 1) ^ salt;
+  return make_uint4(x, ~x, x * 3u, x ^ 0xA5A5A5A5u);
+}
+__device__ __forceinline__ bool same(const uint4& a, const uint4& b) {
+  return a.x == b.x && a.y == b.y && a.z == b.z && a.w == b.w;
+}
+
+__global__ void __launch_bounds__(32) peer_probe_kernel(uint8_t* remote, int n, int* result) {
+  __shared__ alignas(128) uint4 saved[kProbeBytes / 16];
+  __shared__ alignas(128) uint4 buf[kProbeBytes / 16];
+  __shared__ alignas(8) uint64_t bar;
+  const int lane = threadIdx.x, nv = n / 16;
+  volatile uint4* r = reinterpret_cast<volatile uint4*>(remote);
+  bool plain = true, bstore = true, bload = true;
+  for (int i = lane; i < nv; i += 32) {
+    const uint4 v = const_cast<const uint4&>(r[i]);
+    saved[i] = v;
+  }
+  // plain stores, read back
+  for (int i = lane; i < nv; i += 32) const_cast<uint4&>(r[i]) = probe_word(i, 0x1234u);
+  __threadfence_system();
+  __syncwarp();
+  for (int i = lane; i < nv; i += 32) plain = plain && same(const_cast<const uint4&>(r[i]), probe_word(i, 0x1234u));
+  // a TMA bulk store of another pattern, read back with plain loads
+  for (int i = lane; i < nv; i += 32) buf[i] = probe_word(i, 0xBEEFu);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncwarp();
+  if (lane == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(remote),
+                 "r"(smem_u32(buf)), "r"(nv * 16)
+                 : "memory");
+    bulk_commit();
+    bulk_wait<0>();
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+  }
+  __syncwarp();
+  __threadfence_system();
+  for (int i = lane; i < nv; i += 32) bstore = bstore && same(const_cast<const uint4&>(r[i]), probe_word(i, 0xBEEFu));
+  // plain stores of a third pattern, fetched with a TMA bulk load
+  for (int i = lane; i < nv; i += 32) {
+    const_cast<uint4&>(r[i]) = probe_word(i, 0x5151u);
+    buf[i] = make_uint4(0, 0, 0, 0);
+  }
+  __threadfence_system();
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncwarp();
+  if (lane == 0) {
+    mbar_expect_tx(&bar, nv * 16);
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(buf)),
+        "l"(remote), "r"(nv * 16), "r"(smem_u32(&bar))
+        : "memory");
+  }
+  __syncwarp();
+  mbar_wait(&bar, 0);
+  for (int i = lane; i < nv; i += 32) bload = bload && same(buf[i], probe_word(i, 0x5151u));
+  // restore the arena's bytes
+  for (int i = lane; i < nv; i += 32) const_cast<uint4&>(r[i]) = saved[i];
+  __threadfence_system();
+  const unsigned ok_plain = __all_sync(0xffffffffu, plain), ok_bs = __all_sync(0xffffffffu, bstore),
+                 ok_bl = __all_sync(0xffffffffu, bload);
+  if (lane == 0) *result = (ok_plain ? 1 : 0) | (ok_bs ? 2 : 0) | (ok_bl ? 4 : 0);
+}
+
+}  // namespace
+
+cudaError_t launch_peer_probe(uint8_t* remote, int64_t bytes, int* d_result, cudaStream_t s) {
+  const int n = static_cast<int>(std::min<int64_t>(bytes, kProbeBytes)) & ~15;
+  if (n <= 0) return cudaSuccess;
+  peer_probe_kernel<<<1, 32, 0, s>>>(remote, n, d_result);
+  return cudaGetLastError();
+}
+
+namespace {
+
 }  // namespace
 
 int tma_smem_bytes(int piece, int stages) { return piece * stages + 8 * stages; }

@@ -53,6 +53,30 @@ def best_matching(bw: Sequence[Sequence[float]]) -> List[int]:
     return best
 
 
+def best_bipartite(bw: Sequence[Sequence[float]], borrowers: Sequence[int], lenders: Sequence[int]) -> List[int]:
+    """Split roles (BASELINE configs[3]: borrower GPUs each paging to one of
+    as many lender GPUs): the one-to-one assignment of lenders to
+    borrowers that maximises the minimum link bandwidth min(bw[b][l],
+    bw[l][b]) over its pairs; ties -> lexicographically smallest partner
+    list.  Returns partner[r] for every rank (a borrower's lender, a
+    lender's borrower; ranks in neither list map to themselves).  Brute
+    force over permutations (24 for 4 + 4 GPUs)."""
+    import itertools
+    if len(borrowers) != len(lenders):
+        raise ValueError("split roles need as many lenders as borrowers")
+    n = len(bw)
+    best, best_key = None, None
+    for perm in itertools.permutations(lenders):
+        part = list(range(n))
+        for b, l in zip(borrowers, perm):
+            part[b], part[l] = l, b
+        vals = [min(bw[b][l], bw[l][b]) for b, l in zip(borrowers, perm)]
+        key = (min(vals) if vals else float("inf"), [-x for x in part])
+        if best_key is None or key > best_key:
+            best, best_key = part, key
+    return best
+
+
 def measure_p2p(ndev: int, nbytes: int = 256 << 20, reps: int = 3) -> List[List[float]]:
     """Measured device-to-device copy bandwidth (GB/s) between every pair of
     the visible GPUs (one process, torch copies; setup only).  0 where P2P

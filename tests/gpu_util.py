@@ -14,7 +14,7 @@ class Rig:
     identical initial bytes."""
 
     def __init__(self, L=2, bs=16, H=2, D=64, e=2, NB=40, lender_slots=12, host_slots=0, seed=0,
-                 kv_plane_stride=0, block_stride=0, device=0, lender_device=None):
+                 kv_plane_stride=0, block_stride=0, device=0, lender_device=None, peer_test=0):
         self.lay = kp.Layout(L=L, bs=bs, H=H, D=D, e=e, NB=NB,
                              kv_plane_stride=kv_plane_stride or None, block_stride=block_stride or None)
         lb = self.lay.layer_bytes
@@ -26,6 +26,8 @@ class Rig:
         self.ctx = aqua.Ctx(device, L, bs, H, D, e, NB, [t.data_ptr() for t in self.layers],
                             kv_plane_stride, block_stride)
         self.peer = self.host = None
+        if peer_test:
+            self.ctx.set_option(aqua.OPT_PEER_TEST, peer_test)
         if lender_slots:
             g = kv_random_bytes(lender_slots * U, seed=100 + seed)
             ldev = torch.device("cuda", device if lender_device is None else lender_device)

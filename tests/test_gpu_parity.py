@@ -486,6 +486,72 @@ def test_layerwise_swaps_bytes(layer_group, nblk, where):
     rig.assert_bytes_equal("layered swap_in")
 
 
+def test_host_engines_switching_in_one_ctx():
+    """The copy-engine host path's staging buffers survive engine switches in
+    one ctx: CE_HOST, then the gather-temp baseline growing its own buffer,
+    then AUTO (which picks CE_HOST for host-only calls), mixing whole-prompt
+    and layer-wise calls whose per-descriptor range differs (S = 10 KiB, so
+    the ranges do not divide the 256 MiB staging chunk).  Whole-buffer
+    equality with the oracle after every call."""
+    rig = Rig(L=3, bs=16, H=5, D=64, NB=96, lender_slots=0, host_slots=80, seed=4)
+    c, o = rig.ctx, rig.opool
+    rnd = random.Random(11)
+    plan = ["ce", "ce_layers", "gather", "auto", "gather_big", "auto_layers", "ce", "auto", "auto_layers"]
+    pids = list(range(6))
+    for p in pids:
+        n = rnd.randint(2, 9)
+        assert c.alloc_blocks(p, n) == o.alloc_blocks(p, n)
+    rig.assert_bytes_equal("setup")
+    resident = set(pids)
+    for step, mode in enumerate(plan):
+        c.set_option(aqua.OPT_KERNEL, {"ce": aqua.KERNEL_CE_HOST, "ce_layers": aqua.KERNEL_CE_HOST,
+                                       "gather": aqua.BASE_GATHER_TEMP, "gather_big": aqua.BASE_GATHER_TEMP,
+                                       "auto": aqua.KERNEL_AUTO, "auto_layers": aqua.KERNEL_AUTO}[mode])
+        k = len(pids) if mode == "gather_big" else rnd.randint(1, 3)
+        outs = sorted(resident)[:k] if mode == "gather_big" else rnd.sample(sorted(resident), min(k, len(resident)))
+        if outs:
+            if mode.endswith("layers"):
+                c.swap_out_layers(outs, 2)
+            else:
+                c.swap_out(outs)
+            o.swap_out(outs)
+            resident -= set(outs)
+            rig.assert_bytes_equal(f"{mode} swap_out {outs}")
+        ins = rnd.sample(sorted(set(pids) - resident), rnd.randint(1, len(set(pids) - resident)))
+        if mode.endswith("layers"):
+            new, _ = c.swap_in_layers(ins, 2)
+        else:
+            new, _ = c.swap_in(ins)
+        assert new == o.swap_in(ins)
+        resident |= set(ins)
+        rig.assert_bytes_equal(f"{mode} swap_in {ins}")
+    c.close()                       # explicit: the leak check sees every staging buffer freed
+
+
+def test_host_staging_freed_by_destroy():
+    """aqua_destroy releases the copy-engine staging buffers: contexts that
+    page to host DRAM through the copy engines do not leak device memory."""
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    free0 = torch.cuda.mem_get_info()[0]
+    for it in range(4):
+        rig = Rig(L=2, bs=16, H=2, D=64, NB=16, lender_slots=0, host_slots=8, seed=it)
+        rig.ctx.set_option(aqua.OPT_KERNEL, aqua.KERNEL_CE_HOST)
+        rig.ctx.alloc_blocks(1, 4)
+        rig.opool.alloc_blocks(1, 4)
+        rig.ctx.swap_out([1])
+        rig.opool.swap_out([1])
+        rig.ctx.swap_in([1])
+        rig.opool.swap_in([1])
+        rig.assert_bytes_equal("ce round trip")
+        rig.ctx.close()
+        del rig
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    free1 = torch.cuda.mem_get_info()[0]
+    assert free0 - free1 < (256 << 20), (free0, free1)
+
+
 @pytest.mark.parametrize("engine", ["auto", "tma_dyn1", "tma_hybrid"])
 @pytest.mark.parametrize("seed", [0, 1, 2])
 def test_multistream_fuzz_equals_sequential(seed, engine):

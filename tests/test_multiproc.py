@@ -74,6 +74,30 @@ def test_best_matching_from_measured_matrix():
     assert best_matching(bw3) == [2, 1, 0]
 
 
+def test_best_bipartite_split_roles():
+    """configs[3]'s roles: borrowers 0-3 each page to one of lenders 4-7."""
+    import itertools
+    from paper_2407_21255_b200.pairing import best_bipartite
+    n = 8
+    uniform = [[0 if i == j else 770.0 for j in range(n)] for i in range(n)]
+    assert best_bipartite(uniform, [0, 1, 2, 3], [4, 5, 6, 7]) == [4, 5, 6, 7, 0, 1, 2, 3]
+    bw = [row[:] for row in uniform]
+    bw[0][4] = bw[4][0] = 90.0                       # a slow link is avoided
+    m = best_bipartite(bw, [0, 1, 2, 3], [4, 5, 6, 7])
+    assert m[0] != 4 and all(m[m[i]] == i for i in range(n)) and sorted(m[:4]) == [4, 5, 6, 7]
+    # brute-force check of the max-min objective on a random matrix
+    import random
+    rnd = random.Random(3)
+    bw = [[0 if i == j else rnd.choice([300.0, 500.0, 770.0]) for j in range(n)] for i in range(n)]
+    m = best_bipartite(bw, [0, 1, 2, 3], [4, 5, 6, 7])
+    got = min(min(bw[b][m[b]], bw[m[b]][b]) for b in range(4))
+    want = max(min(min(bw[b][l], bw[l][b]) for b, l in zip(range(4), p))
+               for p in itertools.permutations(range(4, 8)))
+    assert got == want
+    with pytest.raises(ValueError):
+        best_bipartite(uniform, [0, 1], [2])
+
+
 def _tp_worker(rank, world, port, q):
     """Two TP ranks in dry-run mode with their own KV-head shard: the
     replicated native scheduler gives both the same call log."""

@@ -381,3 +381,34 @@ def test_relend_moves_back_lowest_pids_that_fit():
         assert not mig
     assert ("policy", r.log[i_rel][1], "cfs") in r.log[i_rel:i_rel + 4]
     assert r.log[i_rel + (2 if mig else 1) + 1][0] == "plan"   # a fresh CFS plan right after
+
+
+def test_replay_bytes_keeps_every_prompt_closed_form():
+    """sim.replay_bytes (the bytes mode of the trace driver) pinned to the
+    closed-form content (C-11, invariant I8): after every 6th iteration, each
+    prompt it ran holds exactly its pattern words for all its KV tokens,
+    across any number of preemptions; the call results equal the log."""
+    from oracle import kvpool as kp
+    from oracle import pattern
+    from workloads import burst_trace, kv_random_bytes
+    tr = burst_trace(seed=3, burst_s=4.0, tail_s=2.0, prompt=(120, 0.8, 1, 400), output=(20, 0.7, 1, 80))
+    cfg = sim.SimConfig(NB=60, bs=16, lender_slots=120, host_slots=400, k=4)
+    res = sim.run(tr, cfg)
+    assert res.blocks_out > 0
+    lay = kp.Layout(L=2, bs=16, H=2, D=8, e=2, NB=60)
+    pool = kp.Pool(lay, [kv_random_bytes(lay.layer_bytes, seed=l) for l in range(2)])
+    pool.lend(kp.LOC_PEER, 120 * lay.U, kv_random_bytes(120 * lay.U, seed=5))
+    pool.lend(kp.LOC_HOST, 400 * lay.U, kv_random_bytes(400 * lay.U, seed=6))
+    iters = {e[1]: e[2] for e in res.log if e[0] == "iter"}
+    checked = []
+
+    def check(i):
+        if i % 6:
+            checked.append(i)
+            return
+        for pid, ctx0, t in iters[i]:
+            assert pattern.check_tokens(pool, pid, ctx0 + t, seed=3), (i, pid)
+        checked.append(i)
+
+    sim.replay_bytes(res.log, pool, 3, on_iter=check)
+    assert len(checked) == res.iters

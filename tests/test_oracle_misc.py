@@ -104,3 +104,32 @@ def test_trace_shape():
     rng = np.random.default_rng(0)
     x = lognormal_lengths(rng, 10000, 2000, 0.8, 1, 8192)
     assert abs(np.median(x) - 2000) / 2000 < 0.1 and x.max() <= 8192 and x.min() >= 1
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_write_token_range_equals_tokenwise_writes(seed):
+    """The range writer (used by the bytes-mode trace replay) stores exactly
+    the bytes of the token-by-token writer, for ranges that start and end
+    mid-block on a scattered block table; nothing else in the pool moves."""
+    rng = np.random.default_rng(seed)
+    lay = kp.Layout(L=2, bs=16, H=2, D=8, e=2, NB=20)
+    init = [kv_random_bytes(lay.layer_bytes, seed=s) for s in range(2)]
+    a = kp.Pool(lay, [x.copy() for x in init])
+    b = kp.Pool(lay, [x.copy() for x in init])
+    ids = rng.permutation(20)[:9].tolist()
+    a.adopt_blocks(4, ids)
+    b.adopt_blocks(4, ids)
+    t = 0
+    while t < 9 * 16:
+        n = int(rng.integers(1, 40))
+        n = min(n, 9 * 16 - t)
+        pattern.write_tokens(a, 4, t, t + n, seed=7)
+        pattern.write_token_range(b, 4, t, t + n, seed=7)
+        for l in range(2):
+            assert np.array_equal(a.layers[l], b.layers[l]), (t, n)
+        t += n
+    assert pattern.check_tokens(b, 4, 9 * 16, seed=7)
+    # one word against the scalar reference
+    w = int(b.chunk(1, 1, ids[3])[(5 * 2 + 1) * 8 * 2 + 3 * 2:][:2].view(np.uint16)[0])
+    want = pattern.splitmix64_int(7 ^ ((4 << 46) | ((3 * 16 + 5) << 26) | (1 << 18) | (1 << 17) | (1 << 10) | 3))
+    assert w == want & 0xFFFF
