@@ -120,22 +120,19 @@ enum {
   AQUA_OPT_TMA_PIECE = 3,     /* bytes per TMA stage (multiple of 16, <= 65536; 0 = auto: 32 KiB) */
   AQUA_OPT_TMA_STAGES = 4,    /* TMA ring depth (2..32; 0 = auto: ~9 MiB of loads in flight chip-wide, 3..~200 KiB) */
   AQUA_OPT_TIMING = 5,        /* 1: each swap also records a start event; aqua_ticket_elapsed gives its device time */
-  AQUA_OPT_LDST_VARIANT = 6,  /* LDST engine flavour: 0 streaming hints, 1 plain, 2 (default) software-pipelined,
-                                 3 claimed batches (every warp claims 2-piece batches, pieces of up to 32 KiB) */
-  AQUA_OPT_TMA_VARIANT = 7,   /* TMA engine: 0 (default) one ring per CTA; 1 warp-specialised (load warp + store
-                                 warp); 2 two independent rings per CTA (one issuing warp each); 3 hybrid: the ring
-                                 plus 8 warps copying claimed batches through registers.  0-2 reach the same HBM
-                                 rate (profiles/r01_tma_variants.jsonl, r01_tma_rings.jsonl) */
+  AQUA_OPT_LDST_VARIANT = 6,  /* LDST engine flavour: 2 (software-pipelined, the only one left; 0, 1 and 3 were
+                                 round-1/2 experiments, retired: AQUA_E_INVAL) */
+  AQUA_OPT_TMA_VARIANT = 7,   /* TMA engine: 0 (default) one ring per CTA driven by one warp; 3 hybrid: the ring
+                                 plus 8 warps copying claimed batches through registers.  1 and 2 (warp-specialised,
+                                 two rings) reached the same HBM rate in round 1 and were retired: AQUA_E_INVAL */
   AQUA_OPT_INLINE_MAX = 8,    /* largest call (in blocks, per launch) whose descriptors ride in the kernel
                                  parameters instead of a pinned-ring upload + H2D copy: 0..4064 (default 4064,
                                  the 32,764-byte parameter limit of CUDA 12.1+; 256 = the small parameter block) */
-  AQUA_OPT_TMA_SCHED = 9,     /* TMA engine (variant 0) work distribution: 0 = each CTA one contiguous item range;
+  AQUA_OPT_TMA_SCHED = 9,     /* TMA engine work distribution: 0 = each CTA one contiguous item range;
                                  n > 0 = batches of n ring units claimed dynamically (atomic counter per launch);
-                                 -n = batches of n units dealt round robin (CTA b: b, b + grid, ...);
-                                 AQUA_TMA_SCHED_AUTO (default) = 2-unit claimed batches when the launch has one CTA
-                                 per SM and >= 8 batches per CTA, else 0 (profiles/r01_tma_sched*.jsonl) */
-  AQUA_OPT_TMA_STATIC_PCT = 10, /* dynamic schedule: percent of the items split statically (one contiguous range per
-                                 CTA) before the claimed batches; 0 = all claimed */
+                                 AQUA_TMA_SCHED_AUTO (default) = the AUTO policy.  Round-robin
+                                 batches (-n) were retired in round 2: AQUA_E_INVAL */
+  AQUA_OPT_TMA_STATIC_PCT = 10, /* retired in round 2 (a static head before the claimed batches): only 0 */
   AQUA_OPT_RATE_GBPS = 11,    /* paging budget in GB/s of swap per direction (0 = off): the copy kernels run on
                                  ceil(rate / 50) SMs (one SM moves ~50 GB/s of swap on the HBM path), leaving the other
                                  SMs and HBM bandwidth to decode; combines with AQUA_OPT_MAX_CTAS (the smaller cap wins) */

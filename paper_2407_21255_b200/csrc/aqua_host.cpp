@@ -85,9 +85,9 @@ struct aqua_ctx {
   int ldst_variant = 2;
   int tma_variant = 0;
   int inline_max = aqua::kInlineDescBig;
-  int tma_sched = AQUA_TMA_SCHED_AUTO;   // AQUA_OPT_TMA_SCHED: 0 static, n > 0 dynamic n-unit batches, -n rr
-  int tma_static_pct = 0;       // AQUA_OPT_TMA_STATIC_PCT: statically split head of a dynamic launch
+  int tma_sched = AQUA_TMA_SCHED_AUTO;   // AQUA_OPT_TMA_SCHED: 0 static, n > 0 claimed n-unit batches
   int pack_vec = 64;            // register movers pack chunks of <= pack_vec x 16 B (AQUA_LDST_PACK env)
+  int hybrid_ldst_units = 0;    // hybrid register warps' batch in units (0: AUTO / the ring's; AQUA_HYBRID_LDST_UNITS env)
   int rate_gbps = 0;            // AQUA_OPT_RATE_GBPS: paging budget -> CTA cap (0 = off)
   int peer_ctas = 32;           // AQUA_OPT_PEER_CTAS: CTA cap for launches touching a peer arena
   int peer_test = 0;            // AQUA_OPT_PEER_TEST
@@ -424,39 +424,62 @@ aqua_status run_copy_ce_host(aqua_ctx* c, const std::vector<Desc>& ds, aqua::Dir
 }
 
 // The TMA engine's AUTO work distribution for one launch (profiles/
-// r01_tma_sched*.jsonl, r01_hybrid*.jsonl, r01_small_chunks*.jsonl; a unit =
-// one stage = p.group chunks):
-// * one CTA per SM and >= 8 batches per CTA: claimed batches with a 4-stage
-//   ring -- 2-unit batches for chunks of >= 8 KiB (6.80 / 6.71 TB/s on C2 /
-//   C4 vs 6.52 / 6.37 static); 8-unit batches for 4 KiB chunks (6.24 vs
-//   5.83); for chunks <= 2 KiB the pool side is 16+ bulk ops per unit, and
-//   the hybrid ring + LDST warps with 2-unit batches moves 5.82 vs 4.59 TB/s;
-//   a caller-set small stage (AQUA_OPT_TMA_PIECE) keeps >= 64 KiB per batch
-//   (16 KiB pieces in 2-unit batches ran at 5.85 vs 6.62 TB/s);
-// * under an SM cap, sub-stage chunks: the hybrid (C4 at 32 CTAs 2.93 vs 2.33
-//   TB/s); stage-sized chunks: static ranges, already at the ~100 GB/s per-SM
-//   limit;
+// r01_tma_sched*.jsonl, r01_hybrid*.jsonl, r02_small_chunks_*.jsonl,
+// r02_hybrid_split_batches.jsonl; a unit = one stage = p.group chunks;
+// p.piece = the chunk size when p.group > 1):
+// * one CTA per SM: claimed batches with a 4-stage ring -- 2-unit batches for
+//   chunks of >= 8 KiB (6.80 / 6.71 TB/s on C2 / C4 vs 6.52 / 6.37 static).
+//   Chunks below a stage are grouped per unit and the warp's lanes issue the
+//   unit's pool-side copies (round 2); by chunk size: 4 KiB and 2 KiB 4-unit
+//   batches (6.43 / 6.35 TB/s), 1 KiB 32-unit batches (6.04; 8: 5.78, 2: 4.96).
+//   Below 1 KiB the TMA unit's per-request cost (~60 cycles) caps the ring
+//   alone (512 B: 3.73 TB/s), so the hybrid ring + LDST warps runs, the ring
+//   claiming 32-unit batches and the register warps 2-unit ones (5.22 vs 4.82
+//   with one batch size for both).  Fewer than 8 batches per CTA halve the
+//   ring's batch, down to 2 units, then static ranges.  A caller-set small
+//   stage (AQUA_OPT_TMA_PIECE) keeps >= 64 KiB per batch (16 KiB pieces in
+//   2-unit batches ran at 5.85 vs 6.62 TB/s);
+// * under an SM cap, sub-stage chunks: the hybrid, ring 32-unit / register
+//   warps 2-unit batches (32 CTAs: 1.39 / 1.75 / 2.46 TB/s at 512 B / 1 KiB /
+//   2 KiB vs 1.32 / 1.63 / 2.19 with 4-unit batches for both); stage-sized
+//   chunks: static ranges, already at the ~100 GB/s per-SM limit;
 // * host-only launches (PCIe-bound, capped): static ranges, no hybrid.
-// *sched: 0 static, n > 0 claimed batches of n units; *variant: 0 ring, 3 hybrid.
+// *sched: 0 static, n > 0 claimed batches of n units; *variant: 0 ring, 3
+// hybrid; *ldst_units: the hybrid register warps' batch (units; 0 = *sched).
 void auto_schedule(const aqua_ctx* c, const aqua::SwapHeader& p, int cap, bool all_host, int* sched,
-                   int* variant) {
+                   int* variant, int* ldst_units) {
   const bool all_sms = cap == 0 || cap >= c->num_sms;
   const int64_t units = p.nitems / p.group;
   const int grid = static_cast<int>(std::min<int64_t>(all_sms ? c->num_sms : cap, p.nitems));
   const bool hybrid_ok = !all_host && *variant == 0;
-  const int variant_in = *variant;
+  const int64_t unit_bytes = int64_t(p.piece) * p.group;
+  const int min_sched = static_cast<int>(std::max<int64_t>(2, (65536 + unit_bytes - 1) / unit_bytes));
+  bool hybrid = false;
   if (all_sms) {
-    if (p.group >= 16 && hybrid_ok)
-      *sched = 2, *variant = 3;
-    else
-      *sched = p.group >= 8 ? 8 : 2;
-    const int64_t unit_bytes = int64_t(p.piece) * p.group;
-    *sched = static_cast<int>(std::max<int64_t>(*sched, (65536 + unit_bytes - 1) / unit_bytes));
-    if (units < int64_t(grid) * *sched * 8) *sched = 0, *variant = variant_in;
-  } else if (p.group > 1 && hybrid_ok && units >= int64_t(grid) * 8 * 8) {
-    *sched = p.group >= 8 ? 2 : 8, *variant = 3;
+    if (p.group == 1 || p.piece >= 8192) {
+      *sched = 2;
+    } else if (p.piece >= 2048) {
+      *sched = 4;
+    } else {
+      *sched = 32;
+      hybrid = p.piece < 1024 && hybrid_ok;
+    }
+  } else if (p.group > 1 && hybrid_ok) {
+    *sched = 32;
+    hybrid = true;
   } else {
     *sched = 0;
+    return;
+  }
+  *sched = std::max(*sched, min_sched);
+  while (*sched > min_sched && units < int64_t(grid) * *sched * 8) *sched /= 2;
+  if (units < int64_t(grid) * *sched * 8) {
+    *sched = 0;                          // too small a call for claims: static ranges, the plain ring
+    return;
+  }
+  if (hybrid) {
+    *variant = 3;
+    if (*ldst_units <= 0) *ldst_units = 2;
   }
 }
 
@@ -534,10 +557,11 @@ aqua_status run_copy(aqua_ctx* c, const std::vector<Desc>& ds, aqua::Dir dir, cu
     cudaError_t e;
     // A counter pair for a launch with claimed batches of `batch` items; the
     // pair's previous launch must be done with it (stream order or its
-    // ticket).  Claims count in 31 bits (atom.inc bound 2^31 - 1): a launch
-    // with more batches (far beyond any real call) falls back to static work.
+    // ticket).  Claims count items in 32 bits, each worker claiming at most
+    // one batch past the end: a launch with more items (far beyond any real
+    // call) falls back to static work.
     auto take_counter = [&](int64_t batch) -> aqua_status {
-      if (!c->d_ctr || p.nitems / batch + 2 * c->num_sms >= (int64_t(1) << 31)) return AQUA_OK;
+      if (!c->d_ctr || p.nitems + int64_t(c->num_sms) * 9 * 2 * batch >= (int64_t(1) << 31)) return AQUA_OK;
       const int slot = static_cast<int>(c->ctr_next++ % aqua::kCtrSlots);
       if (aqua_status s = wait_all(c, {c->ctr_tick[slot]}, st)) return s;
       c->ctr_pending.push_back(slot);
@@ -593,14 +617,14 @@ aqua_status run_copy(aqua_ctx* c, const std::vector<Desc>& ds, aqua::Dir dir, cu
       p.npieces = static_cast<int32_t>((S_eff + piece - 1) / piece);
       p.nitems = p.ndesc * p.nc * p.npieces;
       int sched = c->tma_sched, variant = c->tma_variant;
-      if (sched == AQUA_TMA_SCHED_AUTO) auto_schedule(c, p, cap, all_host, &sched, &variant);
+      int ldst_units = c->hybrid_ldst_units;   // the hybrid's register warps: batches of this many units
+      if (sched == AQUA_TMA_SCHED_AUTO) auto_schedule(c, p, cap, all_host, &sched, &variant, &ldst_units);
+      if (ldst_units <= 0) ldst_units = sched;
       const bool hybrid = variant == 3;          // TMA ring + LDST warps: always claimed batches
       if (hybrid && sched <= 0) sched = 2;
-      if (sched > 0 && (variant == 0 || hybrid)) {
+      if (sched > 0) {
         if (aqua_status s = take_counter(int64_t(sched) * p.group)) return s;
-        if (p.work_ctr) p.static_items = p.nitems * c->tma_static_pct / 100;
-      } else if (sched < 0 && variant == 0) {
-        p.batch = -sched * p.group;            // static round-robin batches
+        if (hybrid && p.work_ctr) p.batch_ldst = static_cast<int32_t>(int64_t(ldst_units) * p.group);
       }
       aqua::LaunchInfo li;
       const int v_used = hybrid && !p.work_ctr ? 0 : variant;   // no counter: the plain ring
@@ -609,27 +633,16 @@ aqua_status run_copy(aqua_ctx* c, const std::vector<Desc>& ds, aqua::Dir dir, cu
       c->last_engine = AQUA_KERNEL_TMA, c->last_variant = v_used, c->last_batch = p.batch;
       c->last_inline = p.desc ? 0 : p.ndesc;
     } else {
-      // variants 0-2: grid-stride 4 KiB items; variant 3: claimed batches of
-      // 2 pieces of up to 32 KiB per warp (the hybrid's register mover alone)
-      const bool claim = c->ldst_variant == 3;
-      p.piece = claim ? static_cast<int>(std::min<int64_t>(S_eff, 32768)) : 4096;
+      // grid-stride 4 KiB items, software pipelined
+      p.piece = 4096;
       p.group = 1;
       p.npieces = static_cast<int32_t>((S_eff + p.piece - 1) / p.piece);
       p.nitems = p.ndesc * p.nc * p.npieces;
-      if (claim) {
-        if (aqua_status s = take_counter(2)) return s;
-        if (!p.work_ctr) {                     // no counter: the grid-stride kernel moves <= 4 KiB items
-          p.piece = 4096;
-          p.npieces = static_cast<int32_t>((S_eff + p.piece - 1) / p.piece);
-          p.nitems = p.ndesc * p.nc * p.npieces;
-        }
-      }
       aqua::LaunchInfo li;
-      const int v_used = p.work_ctr ? 3 : (c->ldst_variant == 3 ? 2 : c->ldst_variant);
       e = aqua::launch_swap_ldst(p, inl, dir, c->num_sms, all_host && cap == kHostCtas ? 2 * kHostCtas : cap, st, &ctas,
-                                 v_used, &li);
+                                 &li);
       c->last_grid = li.grid, c->last_threads = li.threads, c->last_stages = 0;
-      c->last_engine = AQUA_KERNEL_LDST, c->last_variant = v_used, c->last_batch = p.batch;
+      c->last_engine = AQUA_KERNEL_LDST, c->last_variant = 2, c->last_batch = 0;
       c->last_inline = p.desc ? 0 : p.ndesc;
     }
     if (e != cudaSuccess) return cuda_fail(c, e, "swap kernel launch");
@@ -707,16 +720,14 @@ aqua_status run_copy(aqua_ctx* c, const std::vector<Desc>& ds, aqua::Dir dir, cu
     };
     int ctas = 0;
     if (dir == aqua::kOut) {
-      cudaError_t e = aqua::launch_swap_ldst(p, nullptr, aqua::kOut, c->num_sms, c->max_ctas, st, &ctas,
-                                                 c->ldst_variant == 3 ? 2 : c->ldst_variant);
+      cudaError_t e = aqua::launch_swap_ldst(p, nullptr, aqua::kOut, c->num_sms, c->max_ctas, st, &ctas);
       if (e != cudaSuccess) return cuda_fail(c, e, "gather kernel launch");
       c->launches++;
       return runs(true);
     }
     aqua_status rs = runs(false);
     if (rs) return rs;
-    cudaError_t e = aqua::launch_swap_ldst(p, nullptr, aqua::kIn, c->num_sms, c->max_ctas, st, &ctas,
-                                               c->ldst_variant == 3 ? 2 : c->ldst_variant);
+    cudaError_t e = aqua::launch_swap_ldst(p, nullptr, aqua::kIn, c->num_sms, c->max_ctas, st, &ctas);
     if (e != cudaSuccess) return cuda_fail(c, e, "scatter kernel launch");
     c->launches++;
     return AQUA_OK;
@@ -861,6 +872,7 @@ aqua_status aqua_create(int device, const aqua_kv_layout* lay, aqua_ctx** out) {
 
   aqua_ctx* c = new aqua_ctx();
   if (const char* pk = std::getenv("AQUA_LDST_PACK")) c->pack_vec = std::atoi(pk);   // tuning experiments
+  if (const char* hu = std::getenv("AQUA_HYBRID_LDST_UNITS")) c->hybrid_ldst_units = std::atoi(hu);
   // AQUA_KERNEL=auto|tma|ldst|ce_host overrides the default copy engine
   // (operational escape hatch; aqua_set_option still wins afterwards)
   if (const char* k = std::getenv("AQUA_KERNEL")) {
@@ -1824,11 +1836,11 @@ aqua_status aqua_set_option(aqua_ctx* c, int32_t opt, int64_t v) {
       c->timing = v != 0;
       return AQUA_OK;
     case AQUA_OPT_LDST_VARIANT:
-      if (v < 0 || v > 3) return fail(c, AQUA_E_INVAL, "ldst variant");
+      if (v != 2) return fail(c, AQUA_E_INVAL, "ldst variant (only 2 remains; 0, 1, 3 retired in round 2)");
       c->ldst_variant = static_cast<int>(v);
       return AQUA_OK;
     case AQUA_OPT_TMA_VARIANT:
-      if (v < 0 || v > 3) return fail(c, AQUA_E_INVAL, "tma variant");
+      if (v != 0 && v != 3) return fail(c, AQUA_E_INVAL, "tma variant (0 ring, 3 hybrid; 1, 2 retired in round 2)");
       c->tma_variant = static_cast<int>(v);
       return AQUA_OK;
     case AQUA_OPT_INLINE_MAX:
@@ -1836,12 +1848,12 @@ aqua_status aqua_set_option(aqua_ctx* c, int32_t opt, int64_t v) {
       c->inline_max = static_cast<int>(v);
       return AQUA_OK;
     case AQUA_OPT_TMA_SCHED:
-      if ((v < -(1 << 20) || v > (1 << 20)) && v != AQUA_TMA_SCHED_AUTO) return fail(c, AQUA_E_INVAL, "tma sched");
+      if ((v < 0 || v > (1 << 20)) && v != AQUA_TMA_SCHED_AUTO)
+        return fail(c, AQUA_E_INVAL, "tma sched (0 static, n > 0 claimed batches, AUTO; round robin retired)");
       c->tma_sched = static_cast<int>(v);
       return AQUA_OK;
     case AQUA_OPT_TMA_STATIC_PCT:
-      if (v < 0 || v > 100) return fail(c, AQUA_E_INVAL, "tma static pct");
-      c->tma_static_pct = static_cast<int>(v);
+      if (v != 0) return fail(c, AQUA_E_INVAL, "tma static pct (retired in round 2: only 0)");
       return AQUA_OK;
     case AQUA_OPT_RATE_GBPS:
       if (v < 0 || v > (1 << 20)) return fail(c, AQUA_E_INVAL, "rate");
@@ -1871,7 +1883,7 @@ aqua_status aqua_get_option(aqua_ctx* c, int32_t opt, int64_t* v) {
     case AQUA_OPT_TMA_VARIANT: *v = c->tma_variant; return AQUA_OK;
     case AQUA_OPT_INLINE_MAX: *v = c->inline_max; return AQUA_OK;
     case AQUA_OPT_TMA_SCHED: *v = c->tma_sched; return AQUA_OK;
-    case AQUA_OPT_TMA_STATIC_PCT: *v = c->tma_static_pct; return AQUA_OK;
+    case AQUA_OPT_TMA_STATIC_PCT: *v = 0; return AQUA_OK;
     case AQUA_OPT_RATE_GBPS: *v = c->rate_gbps; return AQUA_OK;
     case AQUA_OPT_PEER_CTAS: *v = c->peer_ctas; return AQUA_OK;
     case AQUA_OPT_PEER_TEST: *v = c->peer_test; return AQUA_OK;

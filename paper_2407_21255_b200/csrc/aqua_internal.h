@@ -42,13 +42,13 @@ struct SwapHeader {
   int64_t S, U, P_kv, P_b;
   int64_t nitems;              // ndesc * nc * npieces
   // TMA engine work distribution.  batch == 0: each CTA one contiguous item
-  // range.  batch > 0: batches of `batch` items, CTA b starting on batch b;
-  // then work_ctr == nullptr -> static round robin (b + G, b + 2G, ...), else
-  // dynamic claims through this {next, done} counter pair, which the last CTA
-  // resets to {0, 0}.
+  // range.  batch > 0: batches of `batch` items, CTA b starting on batch b,
+  // then claims through this {items claimed, workers done} counter pair,
+  // which the last claiming worker resets to {0, 0}.  The hybrid's register
+  // warps claim batches of batch_ldst items (0: batch).
   uint32_t* work_ctr;
   int32_t batch;
-  int64_t static_items;        // dynamic only: items [0, static_items) split statically first
+  int32_t batch_ldst;
   int32_t pack_vec;            // register movers pack whole chunks of <= pack_vec 16-byte vectors per round
   int32_t kv_merged;           // 1: a "chunk" is a layer's adjacent K+V pair (c = l, S = 2 x chunk bytes)
 };
@@ -103,7 +103,7 @@ struct LaunchInfo {
 cudaError_t launch_swap_tma(const SwapHeader& h, const Desc* inl, Dir dir, int num_sms, int grid_cap, int stages,
                             cudaStream_t s, int* ctas_used, int variant = 0, LaunchInfo* info = nullptr);
 cudaError_t launch_swap_ldst(const SwapHeader& h, const Desc* inl, Dir dir, int num_sms, int grid_cap,
-                             cudaStream_t s, int* ctas_used, int variant = 0, LaunchInfo* info = nullptr);
+                             cudaStream_t s, int* ctas_used, LaunchInfo* info = nullptr);
 cudaError_t launch_pattern_fill(const PatternParams& p, int num_sms, cudaStream_t s);
 cudaError_t launch_pattern_verify(const PatternParams& p, int num_sms, cudaStream_t s);
 

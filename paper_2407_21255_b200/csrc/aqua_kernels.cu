@@ -16,15 +16,19 @@
 // so consecutive items are consecutive bytes of the slot-major image.
 //
 // Engines (the host picks one per launch):
-//   swap_tma_kernel<D, P, 0>   product: one elected thread per SM drives a
-//                              ring of TMA bulk copies; work in static
-//                              ranges or claimed batches (AUTO)
+//   swap_tma_kernel<D, P, 0>   product: one warp per SM drives a ring of TMA
+//                              bulk copies (lane 0 the whole-stage copies,
+//                              the lanes together a unit's scattered pool-
+//                              side chunks); work in static ranges or
+//                              claimed batches (AUTO)
 //   swap_tma_kernel<D, P, 8>   hybrid: the same ring + 8 warps moving
 //                              claimed batches through registers (capped
-//                              launches of sub-stage chunks, <= 2 KiB chunks)
-//   swap_tma_ws_kernel         warp-specialised ring (tuning experiment)
-//   swap_ldst_kernel           16-byte LDG/STG, grid-stride
-//   swap_ldst_claim_kernel     16-byte LDG/STG, claimed batches
+//                              launches of sub-stage chunks)
+//   swap_ldst_kernel           16-byte LDG/STG, grid-stride, software
+//                              pipelined (second engine; peer fallback)
+// Round 1's tuning experiments (warp-specialised ring, two rings per CTA,
+// round-robin batches, a static head, unpipelined / claimed LDST flavours)
+// were retired in round 2: AUTO never chose them.
 // P = SwapParamsT<256 or 4064>: the descriptors ride in the launch
 // parameters when they fit (else SwapHeader::desc points at a staged copy).
 #include "aqua_internal.h"
@@ -48,9 +52,6 @@ __device__ __forceinline__ void fence_mbar_init() {
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
@@ -205,33 +206,27 @@ __device__ __forceinline__ void unit_next(const SwapHeader& p, Unit& u, int k) {
   }
 }
 
-// blockDim.x / 32 = R independent rings per CTA (AQUA_OPT_TMA_VARIANT 2 is
-// R = 2; R = 1 is the product default): lane 0 of warp w drives ring w over the
-// w-th R-th of the CTA's item range, with its own stages and barriers.
-//
 // Work distribution.  Static (p.batch == 0): each CTA owns one contiguous
-// item range.  Claimed batches (p.work_ctr != nullptr, R = 1 only; the
-// default with one CTA per SM): the first p.static_items items (0 by default)
-// are split into one contiguous range per CTA; the rest is cut into batches
-// of p.batch items that CTAs claim from the launch's counter, fetched one
-// batch ahead so its latency hides behind the ring (with no static head, CTA
-// b starts on batch b).  Per-SM copy rates differ by a few percent (ncu
-// sm__cycles_active min..max 4.4 % with static ranges, 0.6 % claimed), and
-// consecutive claims keep the pieces in flight chip-wide in a narrow window
-// of the image: 6.80 vs 6.52 TB/s on C2.  The loader runs
-// ahead of the storer, so the batches it has entered wait in a small queue.
-// p.batch > 0 without a counter deals the batches round robin instead
-// (b, b + G, ...; a tuning experiment).
+// item range.  Claimed batches (p.batch > 0, p.work_ctr set; the default
+// with one CTA per SM): CTA b starts on batch b, then claims batches of
+// p.batch items from the launch's counter, fetched one batch ahead so its
+// latency hides behind the ring.  Per-SM copy rates differ by a few percent
+// (ncu sm__cycles_active min..max 4.4 % with static ranges, 0.6 % claimed),
+// and consecutive claims keep the pieces in flight chip-wide in a narrow
+// window of the image: 6.80 vs 6.52 TB/s on C2.  The loader
+// runs ahead of the storer, so the batches it has entered wait in a small
+// queue.
 //
-// Claim one batch.  atom.inc with bound 2^31 - 1 (= +1 for every count a
-// launch reaches), not atomicAdd: for a uniform-address add (and for inc with
-// bound 2^32 - 1, which ptxas rewrites as one) the compiler emits a
-// warp-aggregated atomic whose SHFL of the result waits for the atomic at
-// once; this inc is not aggregated, so the result is only waited for where it
-// is used, one batch later (SASS: ATOMG.E.INC, no SHFL).
-__device__ __forceinline__ uint32_t claim_one(uint32_t* ctr) {
+// Claim n items (a batch): the counter counts items claimed beyond the
+// CTAs' first batches.  Inline atom.add, not atomicAdd: for a uniform-address
+// atomicAdd the compiler emits a warp-aggregated atomic whose SHFL of the
+// result waits for the atomic at once; this one is issued by one lane and its
+// result is only waited for where it is used, one batch later (round 1 used
+// atom.inc on batch ids for the same reason; item counts let the hybrid's
+// ring and register warps claim batches of different sizes).
+__device__ __forceinline__ uint32_t claim_items(uint32_t* ctr, uint32_t n) {
   uint32_t v;
-  asm volatile("atom.global.inc.u32 %0, [%1], 0x7FFFFFFF;" : "=r"(v) : "l"(ctr) : "memory");
+  asm volatile("atom.global.add.u32 %0, [%1], %2;" : "=r"(v) : "l"(ctr), "r"(n) : "memory");
   return v;
 }
 
@@ -252,17 +247,17 @@ __device__ __forceinline__ void dyn_finish(uint32_t* ctr, uint32_t total) {
 // rounds in flight per warp.  A CTA's TMA engine moves at most ~100 GB/s of
 // read + write (profiles/r01_tma_rings.jsonl: the same at 4 and 6 stages), so
 // under an SM cap the register path adds a second mover on the same SM.
+// `base` = the items the rings' first (static) batches cover; the register
+// warps claim batches of p.batch_ldst items.
 template <Dir D, class P>
-__device__ __forceinline__ void ldst_worker(const P& p, int64_t off, uint32_t total) {
+__device__ __forceinline__ void ldst_worker(const P& p, int64_t base, uint32_t total) {
   const int lane = threadIdx.x & 31;
-  const int64_t S0 = p.static_items;
-  const int64_t nbatch = (p.nitems - S0 + p.batch - 1) / p.batch;
-  uint32_t raw = lane == 0 ? claim_one(p.work_ctr) : 0u;
-  int64_t id = int64_t(__shfl_sync(0xffffffffu, raw, 0)) + off;
-  while (id < nbatch) {
-    raw = lane == 0 ? claim_one(p.work_ctr) : 0u;       // the next batch, used after this one
-    const int64_t a = S0 + id * p.batch;
-    const int64_t e = a + p.batch < p.nitems ? a + p.batch : p.nitems;
+  const uint32_t bw = static_cast<uint32_t>(p.batch_ldst > 0 ? p.batch_ldst : p.batch);
+  uint32_t raw = lane == 0 ? claim_items(p.work_ctr, bw) : 0u;
+  int64_t a = int64_t(__shfl_sync(0xffffffffu, raw, 0)) + base;
+  while (a < p.nitems) {
+    raw = lane == 0 ? claim_items(p.work_ctr, bw) : 0u;  // the next batch, used after this one
+    const int64_t e = a + bw < p.nitems ? a + bw : p.nitems;
     Cursor cu;
     cu.init(a, p);
     int64_t j = cu.j;
@@ -311,7 +306,7 @@ __device__ __forceinline__ void ldst_worker(const P& p, int64_t off, uint32_t to
         if (o + 2 * k < n) load_round(va, da, o + 2 * k);
         store_round(vb, db);
       }
-      id = int64_t(__shfl_sync(0xffffffffu, raw, 0)) + off;
+      a = int64_t(__shfl_sync(0xffffffffu, raw, 0)) + base;
       continue;
     }
     for (int64_t it = a; it < e; ++it) {
@@ -352,64 +347,62 @@ __device__ __forceinline__ void ldst_worker(const P& p, int64_t off, uint32_t to
         }
       }
     }
-    id = int64_t(__shfl_sync(0xffffffffu, raw, 0)) + off;
+    a = int64_t(__shfl_sync(0xffffffffu, raw, 0)) + base;
   }
   if (lane == 0) dyn_finish(p.work_ctr, total);
 }
 
+// The ring is driven by all 32 lanes of warp 0 in lockstep: they keep the
+// same cursors and wait on the same mbarriers.  Whole-stage bulk copies
+// (a piece of a large chunk, or the image side of a grouped unit: k chunks
+// contiguous in the image) are issued by lane 0; the pool side of a grouped
+// unit -- k separate chunks at scattered block addresses -- is spread over
+// the lanes, lane t issuing chunk t (t + 32, ... when k > 32).  With small
+// chunks (S <= 2 KiB: 16+ pool-side copies per 32 KiB stage) one issuing
+// thread was the limit; the lanes compute their chunk
+// addresses and issue their copies in parallel.  Each lane commits its own
+// bulk-store groups and waits for them before the warp refills a stage.
 template <Dir D, class P, int LW>
-__global__ void __launch_bounds__(LW > 0 ? 32 * (1 + LW) : 128) swap_tma_kernel(const __grid_constant__ P p,
-                                                                                const int stages) {
-  extern __shared__ __align__(128) uint8_t smem_all[];
+__global__ void __launch_bounds__(LW > 0 ? 32 * (1 + LW) : 32) swap_tma_kernel(const __grid_constant__ P p,
+                                                                               const int stages) {
+  extern __shared__ __align__(128) uint8_t smem[];
   const uint32_t workers = gridDim.x * (1 + LW);   // claiming workers (LW > 0: every warp claims)
   if (LW > 0 && threadIdx.x >= 32) {
-    ldst_worker<D>(p, p.static_items > 0 ? 0 : int64_t(gridDim.x), workers);
+    ldst_worker<D>(p, int64_t(gridDim.x) * p.batch, workers);
     return;
   }
-  if ((threadIdx.x & 31) != 0) return;
+  const int lane = threadIdx.x;
   const int64_t stage_bytes = int64_t(p.piece) * p.group;
-  const int64_t R = LW > 0 ? 1 : blockDim.x >> 5, w = threadIdx.x >> 5;
-  const int64_t ring_bytes = (stage_bytes * stages + 8 * stages + 127) & ~int64_t(127);
-  uint8_t* smem = smem_all + w * ring_bytes;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + size_t(stages) * stage_bytes);
-  const int64_t G = gridDim.x * R, b = blockIdx.x * R + w;
-  const bool dyn = p.work_ctr != nullptr;
-  const bool batched = p.batch > 0;      // dynamic, or static round-robin batches (b, b + G, ...)
-  // dynamic with a static head: items [0, S0) in one contiguous range per
-  // CTA, then batches over [S0, nitems) claimed by whoever is free
-  const int64_t S0 = dyn ? p.static_items : 0;
-  const int64_t nbatch = batched ? (p.nitems - S0 + p.batch - 1) / p.batch : 0;
-  // The next batch id = raw + off: `raw` is the claim result (round robin:
-  // a count), kept apart from `off` so that nothing touches it before the
-  // switch that needs it and the atomic's latency stays hidden.
-  int64_t i0, i1, off = 0;
+  const int64_t G = gridDim.x, b = blockIdx.x;
+  const bool dyn = p.batch > 0;          // claimed batches (a counter pair is always set then)
+  // The next batch starts at G * batch + shfl(raw): `raw` is lane 0's claim
+  // result, kept untouched until the switch that needs it so the atomic's
+  // latency hides.
+  int64_t i0, i1;
   uint32_t raw = 0;
-  if (!batched) {
+  if (!dyn) {
     i0 = p.nitems * b / G;
     i1 = p.nitems * (b + 1) / G;
-  } else if (dyn && S0 > 0) {
-    i0 = S0 * b / G;
-    i1 = S0 * (b + 1) / G;
-    raw = claim_one(p.work_ctr);
   } else {
     i0 = b * p.batch;
     i1 = i0 + p.batch < p.nitems ? i0 + p.batch : p.nitems;
-    off = G;
-    raw = dyn ? claim_one(p.work_ctr) : static_cast<uint32_t>(b);
+    if (lane == 0) raw = claim_items(p.work_ctr, p.batch);
   }
-  auto next_raw = [&](uint32_t r) { return dyn ? claim_one(p.work_ctr) : r + static_cast<uint32_t>(G); };
-  if (i1 <= i0) {                        // empty first range: start on the first claimed batch
-    const int64_t id = int64_t(raw) + off;
-    if (!dyn || id >= nbatch) {
-      if (dyn) dyn_finish(p.work_ctr, workers);
-      return;
-    }
-    i0 = S0 + id * p.batch;
-    i1 = i0 + p.batch < p.nitems ? i0 + p.batch : p.nitems;
-    raw = next_raw(raw);
+  auto next_start = [&]() {
+    const int64_t a = int64_t(__shfl_sync(0xffffffffu, raw, 0)) + G * p.batch;
+    if (lane == 0) raw = claim_items(p.work_ctr, p.batch);
+    return a;
+  };
+  if (i1 <= i0) {                        // fewer batches than CTAs: nothing of our own
+    if (dyn && lane == 0) dyn_finish(p.work_ctr, workers);
+    return;
   }
-  for (int s = 0; s < stages; ++s) mbar_init(&bars[s], 1);
-  fence_mbar_init();
+  if (lane == 0) {
+    for (int s = 0; s < stages; ++s) mbar_init(&bars[s], 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
   const uint64_t pol = policy_evict_first();
 
   Unit lu, su;
@@ -419,12 +412,11 @@ __global__ void __launch_bounds__(LW > 0 ? 32 * (1 + LW) : 128) swap_tma_kernel(
     lu = Unit{cu.j, cu.c, cu.q, i1 - i0};
     su = lu;
   }
-  // batched: the ids of the batches the loader has entered but the storer
+  // the first items of the batches the loader has entered but the storer
   // has not (the loader runs up to stages - 1 units ahead)
   int64_t queue[32];
   int qh = 0, qt = 0;
-  auto open_batch = [&](int64_t id, Unit& u) {
-    const int64_t a = S0 + id * p.batch;
+  auto open_batch = [&](int64_t a, Unit& u) {
     Cursor cu;
     cu.init(a, p);
     u = Unit{cu.j, cu.c, cu.q, (a + p.batch < p.nitems ? a + p.batch : p.nitems) - a};
@@ -437,27 +429,26 @@ __global__ void __launch_bounds__(LW > 0 ? 32 * (1 + LW) : 128) swap_tma_kernel(
     const uint8_t* src;
     uint8_t* dst;
     uint32_t bytes;
-    item_addrs<D>(p, d, lu.c, lu.q, src, dst, bytes);
-    if (k == 1) {
-      mbar_expect_tx(&bars[lstage], bytes);
-      bulk_g2s(buf, src, bytes, &bars[lstage], pol);
-    } else if (D != kOut) {                // image side: one contiguous load of k chunks
-      mbar_expect_tx(&bars[lstage], bytes * k);
-      bulk_g2s(buf, src, bytes * k, &bars[lstage], pol);
-    } else {                               // pool side: k scattered chunk loads
-      mbar_expect_tx(&bars[lstage], bytes * k);
-      for (int t = 0; t < k; ++t) {
+    if (k == 1 || D != kOut) {             // one copy: a piece, or the image side of k chunks
+      if (lane == 0) {
+        item_addrs<D>(p, d, lu.c, lu.q, src, dst, bytes);
+        mbar_expect_tx(&bars[lstage], bytes * k);
+        bulk_g2s(buf, src, bytes * k, &bars[lstage], pol);
+      }
+    } else {                               // pool side: k scattered chunk loads over the lanes
+      if (lane == 0) mbar_expect_tx(&bars[lstage], static_cast<uint32_t>(p.S) * k);
+      __syncwarp();
+      for (int t = lane; t < k; t += 32) {
         item_addrs<D>(p, d, lu.c + t, 0, src, dst, bytes);
         bulk_g2s(buf + size_t(t) * bytes, src, bytes, &bars[lstage], pol);
       }
     }
     unit_next(p, lu, k);
-    if (batched && lu.left == 0) {         // enter the next claimed batch, if any
-      const int64_t id = int64_t(raw) + off;
-      if (id < nbatch) {
-        queue[qt++ & 31] = id;
-        open_batch(id, lu);
-        raw = next_raw(raw);
+    if (dyn && lu.left == 0) {             // enter the next claimed batch, if any
+      const int64_t a = next_start();
+      if (a < p.nitems) {
+        queue[qt++ & 31] = a;
+        open_batch(a, lu);
       }
     }
     ++issued;
@@ -475,148 +466,42 @@ __global__ void __launch_bounds__(LW > 0 ? 32 * (1 + LW) : 128) swap_tma_kernel(
     const uint8_t* src;
     uint8_t* dst;
     uint32_t bytes;
-    item_addrs<D>(p, d, su.c, su.q, src, dst, bytes);
-    if (k == 1) {
-      bulk_s2g(dst, buf, bytes, pol);
-    } else if (D != kIn) {                 // image side: one contiguous store of k chunks
-      bulk_s2g(dst, buf, bytes * k, pol);
-    } else {                               // pool side: k scattered chunk stores
-      for (int t = 0; t < k; ++t) {
+    if (k == 1 || D != kIn) {              // one copy: a piece, or the image side of k chunks
+      if (lane == 0) {
+        item_addrs<D>(p, d, su.c, su.q, src, dst, bytes);
+        bulk_s2g(dst, buf, bytes * k, pol);
+      }
+    } else {                               // pool side: k scattered chunk stores over the lanes
+      for (int t = lane; t < k; t += 32) {
         item_addrs<D>(p, d, su.c + t, 0, src, dst, bytes);
         bulk_s2g(dst, buf + size_t(t) * bytes, bytes, pol);
       }
     }
     bulk_commit();
     unit_next(p, su, k);
-    if (batched && su.left == 0 && qh != qt) open_batch(queue[qh++ & 31], su);
+    if (dyn && su.left == 0 && qh != qt) open_batch(queue[qh++ & 31], su);
     if (++sstage == stages) {
       sstage = 0;
       parity ^= 1u;
     }
     if (lu.left > 0) {
-      bulk_wait_read<1>();  // the stores of the previous unit have finished reading its stage
+      bulk_wait_read<1>();  // this lane's stores of the previous unit have read its stage
+      __syncwarp();         // ... and every other lane's
       issue_load();         // -> the stage of the previous unit
     }
   }
   bulk_wait<0>();
-  if (dyn) dyn_finish(p.work_ctr, workers);
-}
-
-// Warp-specialised variant: warp 0 (one lane) only issues loads, warp 1 (one
-// lane) only issues stores; "full" mbarriers carry the bulk-load bytes and
-// "empty" mbarriers hand a stage back once its store has read it, so loads
-// never wait behind a store's completion check.
-template <Dir D, class P>
-__global__ void __launch_bounds__(64) swap_tma_ws_kernel(const __grid_constant__ P p, const int stages) {
-  extern __shared__ __align__(128) uint8_t smem[];
-  const int64_t stage_bytes = int64_t(p.piece) * p.group;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + size_t(stages) * stage_bytes);
-  uint64_t* empty = full + stages;
-  const int64_t G = gridDim.x, b = blockIdx.x;
-  const int64_t i0 = p.nitems * b / G, i1 = p.nitems * (b + 1) / G;
-  if (i1 <= i0) return;
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < stages; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
-    }
-    fence_mbar_init();
-  }
-  __syncthreads();
-  if ((threadIdx.x & 31) != 0) return;
-  const uint64_t pol = policy_evict_first();
-  Unit u;
-  {
-    Cursor cu;
-    cu.init(i0, p);
-    u = Unit{cu.j, cu.c, cu.q, i1 - i0};
-  }
-  int stage = 0;
-  uint32_t ph = 0;
-  if (threadIdx.x == 0) {                    // producer: bulk loads
-    while (u.left > 0) {
-      mbar_wait(&empty[stage], ph ^ 1u);     // fresh barriers pass at once
-      const int k = unit_len(p, u);
-      const Desc d = desc_at(p, u.j);
-      uint8_t* buf = smem + size_t(stage) * stage_bytes;
-      const uint8_t* src;
-      uint8_t* dst;
-      uint32_t bytes;
-      item_addrs<D>(p, d, u.c, u.q, src, dst, bytes);
-      if (k == 1) {
-        mbar_expect_tx(&full[stage], bytes);
-        bulk_g2s(buf, src, bytes, &full[stage], pol);
-      } else if (D != kOut) {
-        mbar_expect_tx(&full[stage], bytes * k);
-        bulk_g2s(buf, src, bytes * k, &full[stage], pol);
-      } else {
-        mbar_expect_tx(&full[stage], bytes * k);
-        for (int t = 0; t < k; ++t) {
-          item_addrs<D>(p, d, u.c + t, 0, src, dst, bytes);
-          bulk_g2s(buf + size_t(t) * bytes, src, bytes, &full[stage], pol);
-        }
-      }
-      unit_next(p, u, k);
-      if (++stage == stages) {
-        stage = 0;
-        ph ^= 1u;
-      }
-    }
-  } else {                                    // consumer: bulk stores
-    int prev = -1;
-    while (u.left > 0) {
-      mbar_wait(&full[stage], ph);
-      const int k = unit_len(p, u);
-      const Desc d = desc_at(p, u.j);
-      uint8_t* buf = smem + size_t(stage) * stage_bytes;
-      const uint8_t* src;
-      uint8_t* dst;
-      uint32_t bytes;
-      item_addrs<D>(p, d, u.c, u.q, src, dst, bytes);
-      if (k == 1) {
-        bulk_s2g(dst, buf, bytes, pol);
-      } else if (D != kIn) {
-        bulk_s2g(dst, buf, bytes * k, pol);
-      } else {
-        for (int t = 0; t < k; ++t) {
-          item_addrs<D>(p, d, u.c + t, 0, src, dst, bytes);
-          bulk_s2g(dst, buf + size_t(t) * bytes, bytes, pol);
-        }
-      }
-      bulk_commit();
-      if (prev >= 0) {
-        bulk_wait_read<1>();                  // the previous unit's store has read its stage
-        mbar_arrive(&empty[prev]);
-      }
-      prev = stage;
-      unit_next(p, u, k);
-      if (++stage == stages) {
-        stage = 0;
-        ph ^= 1u;
-      }
-    }
-    bulk_wait<0>();
-  }
+  if (dyn && lane == 0) dyn_finish(p.work_ctr, workers);
 }
 
 // ------------------------------------------------------------ LDG/STG kernel
 // Grid-stride over items of up to 512*UNROLL bytes; a warp moves one item
 // with UNROLL independent 16-byte loads per lane in flight.
-__device__ __forceinline__ int4 ld_plain(const void* p) {
-  int4 r;
-  asm volatile("ld.global.v4.s32 {%0, %1, %2, %3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
-  return r;
-}
-__device__ __forceinline__ void st_plain(void* p, const int4& v) {
-  asm volatile("st.global.v4.s32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
-               : "memory");
-}
-
-// V selects the access flavour (tuning experiments, AQUA_OPT_LDST_VARIANT):
-// 0 streaming hints (ld.nc.L1::no_allocate.L2::256B / st.L1::no_allocate);
-// 1 plain ld/st; 2 streaming hints + the next item's loads issued before the
-// current item's stores (software pipelined).
-template <Dir D, int UNROLL, int V, class P>
+// Streaming hints (ld.nc.L1::no_allocate.L2::256B / st.L1::no_allocate) and
+// the next item's loads issued before the current item's stores (software
+// pipelined; the plain and unpipelined flavours measured in round 1 were
+// slower, profiles/r01_ldst_variants.jsonl).
+template <Dir D, int UNROLL, class P>
 __global__ void __launch_bounds__(256) swap_ldst_kernel(const __grid_constant__ P p) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
@@ -631,46 +516,31 @@ __global__ void __launch_bounds__(256) swap_ldst_kernel(const __grid_constant__ 
 #pragma unroll
     for (int u = 0; u < UNROLL; ++u) {
       const int idx = u * 32 + lane;
-      if (idx < *nvec) v[u] = V == 1 ? ld_plain(src + size_t(idx) * 16) : ld_stream(src + size_t(idx) * 16);
+      if (idx < *nvec) v[u] = ld_stream(src + size_t(idx) * 16);
     }
   };
   auto store = [&](const int4* v, uint8_t* dst, int nvec) {
 #pragma unroll
     for (int u = 0; u < UNROLL; ++u) {
       const int idx = u * 32 + lane;
-      if (idx < nvec) {
-        if (V == 1)
-          st_plain(dst + size_t(idx) * 16, v[u]);
-        else
-          st_stream(dst + size_t(idx) * 16, v[u]);
-      }
+      if (idx < nvec) st_stream(dst + size_t(idx) * 16, v[u]);
     }
   };
-  if (V != 2) {
-    for (int64_t it = warp; it < p.nitems; it += nwarps) {
-      int4 v[UNROLL];
-      uint8_t* dst;
-      int nvec;
-      load(it, v, &dst, &nvec);
-      store(v, dst, nvec);
-    }
-  } else {
-    int4 a[UNROLL], b[UNROLL];
-    uint8_t *da = nullptr, *db = nullptr;
-    int na = 0, nb = 0;
-    int64_t it = warp;
-    if (it < p.nitems) load(it, a, &da, &na);
-    while (it < p.nitems) {
-      const int64_t nx = it + nwarps;
-      if (nx < p.nitems) load(nx, b, &db, &nb);
-      store(a, da, na);
-      it = nx;
-      if (it >= p.nitems) break;
-      const int64_t ny = it + nwarps;
-      if (ny < p.nitems) load(ny, a, &da, &na);
-      store(b, db, nb);
-      it = ny;
-    }
+  int4 a[UNROLL], b[UNROLL];
+  uint8_t *da = nullptr, *db = nullptr;
+  int na = 0, nb = 0;
+  int64_t it = warp;
+  if (it < p.nitems) load(it, a, &da, &na);
+  while (it < p.nitems) {
+    const int64_t nx = it + nwarps;
+    if (nx < p.nitems) load(nx, b, &db, &nb);
+    store(a, da, na);
+    it = nx;
+    if (it >= p.nitems) break;
+    const int64_t ny = it + nwarps;
+    if (ny < p.nitems) load(ny, a, &da, &na);
+    store(b, db, nb);
+    it = ny;
   }
 }
 
@@ -900,30 +770,19 @@ cudaError_t launch_tma_t(const P& p, Dir dir, int num_sms, int grid_cap, int sta
     if (p.work_ctr) stages = std::max(stages, 4);
   }
   stages = std::max(2, std::min(stages, 32));
-  const int bar_extra = variant == 1 ? 8 : 0;   // the "empty" barriers of the warp-specialised variant
-  const int rings = variant == 2 ? 2 : 1;
   constexpr int kLdstWarps = 8;                  // variant 3: TMA ring + 8 LDST warps per CTA
-  if (rings > 1 && stages_opt <= 0) stages = std::max(3, (stages + rings - 1) / rings + 1);
-  auto smem_for = [&](int st) {
-    return rings == 1 ? tma_smem_bytes(stage_bytes, st) + bar_extra * st
-                      : rings * ((tma_smem_bytes(stage_bytes, st) + 127) & ~127);
-  };
-  while (stages > 2 && smem_for(stages) > 227 * 1024) --stages;
-  if (smem_for(stages) > 227 * 1024) return cudaErrorInvalidConfiguration;
-  const int smem = smem_for(stages);
+  while (stages > 2 && tma_smem_bytes(stage_bytes, stages) > 227 * 1024) --stages;
+  if (tma_smem_bytes(stage_bytes, stages) > 227 * 1024) return cudaErrorInvalidConfiguration;
+  const int smem = tma_smem_bytes(stage_bytes, stages);
   // the opt-in smem attribute is per device and per instantiation; set once
-  static thread_local bool set_smem[3][3][64] = {};
+  static thread_local bool set_smem[2][3][64] = {};
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
-  const int vi = variant == 1 ? 1 : variant == 3 ? 2 : 0;
-  bool& have = set_smem[vi][dir][dev & 63];
+  const bool hybrid = variant == 3;
+  bool& have = set_smem[hybrid][dir][dev & 63];
   if (!have) {
-    if (vi == 1)
-      e = cudaFuncSetAttribute(dir == kOut ? swap_tma_ws_kernel<kOut, P>
-                               : dir == kIn ? swap_tma_ws_kernel<kIn, P> : swap_tma_ws_kernel<kMig, P>,
-                               cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    else if (vi == 2)
+    if (hybrid)
       e = cudaFuncSetAttribute(dir == kOut ? swap_tma_kernel<kOut, P, kLdstWarps>
                                : dir == kIn ? swap_tma_kernel<kIn, P, kLdstWarps>
                                             : swap_tma_kernel<kMig, P, kLdstWarps>,
@@ -935,14 +794,7 @@ cudaError_t launch_tma_t(const P& p, Dir dir, int num_sms, int grid_cap, int sta
     if (e != cudaSuccess) return e;
     have = true;
   }
-  if (vi == 1) {
-    if (dir == kOut)
-      swap_tma_ws_kernel<kOut, P><<<grid, 64, smem, s>>>(p, stages);
-    else if (dir == kIn)
-      swap_tma_ws_kernel<kIn, P><<<grid, 64, smem, s>>>(p, stages);
-    else
-      swap_tma_ws_kernel<kMig, P><<<grid, 64, smem, s>>>(p, stages);
-  } else if (vi == 2) {
+  if (hybrid) {
     if (!p.work_ctr) return cudaErrorInvalidValue;    // the LDST warps only claim batches
     constexpr int nt = 32 * (1 + kLdstWarps);
     if (dir == kOut)
@@ -952,54 +804,29 @@ cudaError_t launch_tma_t(const P& p, Dir dir, int num_sms, int grid_cap, int sta
     else
       swap_tma_kernel<kMig, P, kLdstWarps><<<grid, nt, smem, s>>>(p, stages);
   } else if (dir == kOut) {
-    swap_tma_kernel<kOut, P, 0><<<grid, 32 * rings, smem, s>>>(p, stages);
+    swap_tma_kernel<kOut, P, 0><<<grid, 32, smem, s>>>(p, stages);
   } else if (dir == kIn) {
-    swap_tma_kernel<kIn, P, 0><<<grid, 32 * rings, smem, s>>>(p, stages);
+    swap_tma_kernel<kIn, P, 0><<<grid, 32, smem, s>>>(p, stages);
   } else {
-    swap_tma_kernel<kMig, P, 0><<<grid, 32 * rings, smem, s>>>(p, stages);
+    swap_tma_kernel<kMig, P, 0><<<grid, 32, smem, s>>>(p, stages);
   }
   if (ctas_used) *ctas_used = grid;
-  if (info) *info = LaunchInfo{grid, vi == 1 ? 64 : vi == 2 ? 32 * (1 + kLdstWarps) : 32 * rings, stages};
+  if (info) *info = LaunchInfo{grid, hybrid ? 32 * (1 + kLdstWarps) : 32, stages};
   return cudaGetLastError();
-}
-
-// LDST engine with claimed batches (AQUA_OPT_LDST_VARIANT 3): every warp of
-// a 256-thread CTA per SM is an ldst_worker (the hybrid's register mover).
-template <Dir D, class P>
-__global__ void __launch_bounds__(256) swap_ldst_claim_kernel(const __grid_constant__ P p) {
-  ldst_worker<D>(p, 0, gridDim.x * (blockDim.x >> 5));
-}
-
-template <int V, class P>
-void launch_ldst_v(const P& p, Dir dir, int grid, cudaStream_t s) {
-  if (dir == kOut)
-    swap_ldst_kernel<kOut, 8, V, P><<<grid, 256, 0, s>>>(p);
-  else if (dir == kIn)
-    swap_ldst_kernel<kIn, 8, V, P><<<grid, 256, 0, s>>>(p);
-  else
-    swap_ldst_kernel<kMig, 8, V, P><<<grid, 256, 0, s>>>(p);
 }
 
 template <class P>
 cudaError_t launch_ldst_t(const P& p, Dir dir, int num_sms, int grid_cap, cudaStream_t s, int* ctas_used,
-                          int variant, LaunchInfo* info) {
-  // variant 2 (software pipelined, the default) is best with one 256-thread
-  // CTA per SM: 6,624 / 6,572 GB/s on C2 (profiles/r01_ldst_variants.jsonl)
-  const int grid = grid_for<void>(p.nitems, 8, num_sms, variant >= 2 ? 1 : 4, grid_cap);
-  if (variant == 3) {
-    if (!p.work_ctr) return cudaErrorInvalidValue;
-    if (dir == kOut)
-      swap_ldst_claim_kernel<kOut, P><<<grid, 256, 0, s>>>(p);
-    else if (dir == kIn)
-      swap_ldst_claim_kernel<kIn, P><<<grid, 256, 0, s>>>(p);
-    else
-      swap_ldst_claim_kernel<kMig, P><<<grid, 256, 0, s>>>(p);
-  } else if (variant == 1)
-    launch_ldst_v<1>(p, dir, grid, s);
-  else if (variant == 2)
-    launch_ldst_v<2>(p, dir, grid, s);
+                          LaunchInfo* info) {
+  // software pipelined, one 256-thread CTA per SM: 6,624 / 6,572 GB/s on C2
+  // (profiles/r01_ldst_variants.jsonl)
+  const int grid = grid_for<void>(p.nitems, 8, num_sms, 1, grid_cap);
+  if (dir == kOut)
+    swap_ldst_kernel<kOut, 8, P><<<grid, 256, 0, s>>>(p);
+  else if (dir == kIn)
+    swap_ldst_kernel<kIn, 8, P><<<grid, 256, 0, s>>>(p);
   else
-    launch_ldst_v<0>(p, dir, grid, s);
+    swap_ldst_kernel<kMig, 8, P><<<grid, 256, 0, s>>>(p);
   if (ctas_used) *ctas_used = grid;
   if (info) *info = LaunchInfo{grid, 256, 0};
   return cudaGetLastError();
@@ -1033,10 +860,10 @@ cudaError_t launch_swap_tma(const SwapHeader& h, const Desc* inl, Dir dir, int n
 }
 
 cudaError_t launch_swap_ldst(const SwapHeader& h, const Desc* inl, Dir dir, int num_sms, int grid_cap,
-                             cudaStream_t s, int* ctas_used, int variant, LaunchInfo* info) {
+                             cudaStream_t s, int* ctas_used, LaunchInfo* info) {
   if (h.nitems == 0) return cudaSuccess;
   return with_params(h, inl, [&](const auto& p) {
-    return launch_ldst_t(p, dir, num_sms, grid_cap, s, ctas_used, variant, info);
+    return launch_ldst_t(p, dir, num_sms, grid_cap, s, ctas_used, info);
   });
 }
 

@@ -526,28 +526,13 @@ def layer_overlap():
         torch.cuda.empty_cache()
 
 
-def ldst_variants():
-    """LDST engine flavours (AQUA_OPT_LDST_VARIANT) on C2, self-lender."""
-    L, bs, H, D, NB, nblk = 32, 16, 8, 128, 4096, 2048
-    ctx, layers, arena, U = setup(L, bs, H, D, NB, nblk)
-    s = torch.cuda.Stream()
-    ctx.set_option(aqua.OPT_KERNEL, aqua.KERNEL_LDST)
-    for v in (0, 1, 2):
-        for ctas in (0, 148, 296):
-            ctx.set_option(aqua.OPT_LDST_VARIANT, v)
-            ctx.set_option(aqua.OPT_MAX_CTAS, ctas)
-            o, i = time_tickets(ctx, 5, s)
-            print(json.dumps({"ldst_variant": v, "ctas": ctas or 592, "out_hbm_GBps": round(2 * nblk * U / o / 1e6, 1),
-                              "in_hbm_GBps": round(2 * nblk * U / i / 1e6, 1)}), flush=True)
-
-
 def tma_variants():
-    """TMA engine: one issuing thread (0) vs warp-specialised load/store warps (1),
-    C2 self-lender, across ring depths and SM caps; LDST v2 for reference."""
+    """TMA engine: the ring (0) vs the hybrid ring + LDST warps (3), C2
+    self-lender, across ring depths and SM caps; LDST for reference."""
     L, bs, H, D, NB, nblk = 32, 16, 8, 128, 4096, 2048
     ctx, layers, arena, U = setup(L, bs, H, D, NB, nblk)
     s = torch.cuda.Stream()
-    vs = [int(x) for x in os.environ.get("AQUA_SWEEP_TMA_VARIANTS", "0,1").split(",")]
+    vs = [int(x) for x in os.environ.get("AQUA_SWEEP_TMA_VARIANTS", "0,3").split(",")]
     sts = [int(x) for x in os.environ.get("AQUA_SWEEP_STAGES", "0,2,3,4,6").split(",")]
     for v in vs:
         for st in sts:
@@ -588,13 +573,11 @@ def time_queued(ctx, stream, K=10, reps=3):
 
 
 def tma_sched():
-    """TMA engine work distribution: static contiguous ranges (0), dynamic
-    batches of n ring units (n > 0, with a statically split head of pct % of
-    the items), round-robin batches (-n); C2 and the C4 (70B/TP4, S = 8 KiB)
+    """TMA engine work distribution: static contiguous ranges (0), claimed
+    batches of n ring units (n > 0); C2 and the C4 (70B/TP4, S = 8 KiB)
     shape, all SMs and SM caps; back-to-back (queued) and per-call (ticket)
-    device times.  AQUA_SWEEP_SCHED = "n:pct,...", AQUA_SWEEP_CTAS = "0,64,16"."""
-    combos = [tuple(int(v) for v in x.split(":")) for x in
-              os.environ.get("AQUA_SWEEP_SCHED", "0:0,2:0,4:0,8:0,2:80,4:80,8:80,2:90,4:90,8:90,16:90").split(",")]
+    device times.  AQUA_SWEEP_SCHED = "n,...", AQUA_SWEEP_CTAS = "0,64,16"."""
+    combos = [(int(x), 0) for x in os.environ.get("AQUA_SWEEP_SCHED", "0,1,2,4,8,16").split(",")]
     ctas_list = [int(x) for x in os.environ.get("AQUA_SWEEP_CTAS", "0,64,16").split(",")]
     stages_list = [int(x) for x in os.environ.get("AQUA_SWEEP_STAGES", "0").split(",")]
     pieces = [int(x) for x in os.environ.get("AQUA_SWEEP_PIECES", "0").split(",")]
@@ -609,7 +592,6 @@ def tma_sched():
                for pc in pieces:
                 ctx.set_option(aqua.OPT_TMA_PIECE, pc)
                 ctx.set_option(aqua.OPT_TMA_SCHED, sc)
-                ctx.set_option(aqua.OPT_TMA_STATIC_PCT, pct)
                 ctx.set_option(aqua.OPT_TMA_STAGES, st)
                 pair = time_queued(ctx, s, K=20, reps=5)
                 o, i = time_tickets(ctx, 5, s)
@@ -647,26 +629,6 @@ def hybrid():
         torch.cuda.empty_cache()
 
 
-def ldst_claim():
-    """LDST engine: grid-stride 4 KiB items (variant 2) vs claimed batches of
-    32 KiB pieces (variant 3), beside the TMA default, C2 and C4 shapes."""
-    for name, (L, H, nblk) in (("c2", (32, 8, 2048)), ("c4", (80, 2, 4096))):
-        ctx, layers, arena, U = setup(L, 16, H, 128, 2 * nblk, nblk)
-        s = torch.cuda.Stream()
-        for ctas in (148, 64, 16):
-            ctx.set_option(aqua.OPT_MAX_CTAS, ctas)
-            for eng, v in (("tma", 0), ("ldst", 2), ("ldst", 3)):
-                ctx.set_option(aqua.OPT_KERNEL, ENG[eng])
-                ctx.set_option(aqua.OPT_LDST_VARIANT, v if eng == "ldst" else 2)
-                pair = time_queued(ctx, s, K=10, reps=3)
-                print(json.dumps({"engine": eng, "ldst_variant": v if eng == "ldst" else None, "shape": name,
-                                  "ctas": ctas, "pair_ms": round(pair, 4),
-                                  "hbm_GBps": round(4 * nblk * U / pair / 1e6, 1)}), flush=True)
-        ctx.close()
-        del layers, arena
-        torch.cuda.empty_cache()
-
-
 def small_chunks():
     """Sub-stage chunks at full grid and under a cap: S = 512 B .. 8 KiB (e.g. one
     KV head per TP8 rank: S = 4 KiB), TMA ring vs hybrid, 1 GiB per call.
@@ -692,6 +654,52 @@ def small_chunks():
                                   "ctas": ctas, "launch": ctx.last_launch()["schedule"],
                                   "hbm_GBps": round(4 * nblk * U / pair / 1e6, 1)}), flush=True)
         ctx.set_option(aqua.OPT_TMA_VARIANT, 0)
+        ctx.close()
+        del layers, arena
+        torch.cuda.empty_cache()
+
+
+def small_chunks2():
+    """Round 2: sub-stage chunks (plane-major, S = 512 B .. 8 KiB, 1 GiB per
+    call): the TMA ring with claimed batches of n units (the warp's lanes
+    issue a unit's pool-side copies) and the hybrid ring + LDST warps; all
+    SMs and a 32-SM cap.  (The register movers alone and a staged kernel --
+    TMA for the image side only, registers for the pool side -- were
+    measured with this sweep and removed: profiles/r02_small_chunks_*.jsonl.)"""
+    Ss = [int(x) for x in os.environ.get("AQUA_SWEEP_S", "512,1024,2048,4096,8192").split(",")]
+    for S in Ss:
+        L, H = 32, 1
+        D = S // 32 if S <= 4096 else 128
+        if S > 4096:
+            H = S // 4096
+        U = 2 * L * S
+        nblk = (1 << 30) // U
+        ctx, layers, arena, _ = setup(L, 16, H, D, 2 * nblk, nblk)
+        s = torch.cuda.Stream()
+        for cap in (0, 32):
+            combos = [("ring", 0, 0, n) for n in (2, 4, 8, 16, 32)]
+            combos += [("hybrid", 0, 3, n) for n in (1, 2, 4)]
+            combos += [("auto", 0, 0, aqua.TMA_SCHED_AUTO)]
+            only = os.environ.get("AQUA_SWEEP_ENGINES")
+            if only:
+                combos = [x for x in combos if x[0] in only.split(",")]
+            hyb_n = os.environ.get("AQUA_SWEEP_HYBRID_UNITS")
+            if hyb_n:
+                combos = [x for x in combos if x[0] != "hybrid"] + [("hybrid", 0, 3, int(n)) for n in hyb_n.split(",")]
+            for eng, grid, v, n in combos:
+                ctx.set_option(aqua.OPT_KERNEL, aqua.KERNEL_TMA)
+                ctx.set_option(aqua.OPT_TMA_VARIANT, v)
+                ctx.set_option(aqua.OPT_TMA_SCHED, n)
+                ctx.set_option(aqua.OPT_MAX_CTAS, cap)
+                pair = time_queued(ctx, s, K=10, reps=3)
+                ll = ctx.last_launch()
+                print(json.dumps({"S": S, "cap": cap or 148, "engine": eng, "sched_units": n, "grid": ll["ctas"],
+                                  "ldst_units": int(os.environ.get("AQUA_HYBRID_LDST_UNITS", "0")),
+                                  "stages": ll["stages"],
+                                  "threads": ll["threads_per_cta"], "launch": ll["schedule"],
+                                  "hbm_GBps": round(4 * nblk * U / pair / 1e6, 1)}), flush=True)
+        ctx.set_option(aqua.OPT_TMA_VARIANT, 0)
+        ctx.set_option(aqua.OPT_TMA_SCHED, aqua.TMA_SCHED_AUTO)
         ctx.close()
         del layers, arena
         torch.cuda.empty_cache()
@@ -772,8 +780,6 @@ if __name__ == "__main__":
         prefix()
     elif what == "migrate":
         migrate()
-    elif what == "ldst_variants":
-        ldst_variants()
     elif what == "tma_variants":
         tma_variants()
     elif what == "layer_overlap":
@@ -798,10 +804,10 @@ if __name__ == "__main__":
         tma_sched()
     elif what == "hybrid":
         hybrid()
-    elif what == "ldst_claim":
-        ldst_claim()
     elif what == "small_chunks":
         small_chunks()
+    elif what == "small_chunks2":
+        small_chunks2()
     elif what == "rate":
         rate()
 

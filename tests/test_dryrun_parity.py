@@ -456,7 +456,12 @@ def test_create_validates_layout():
     c = aqua.Ctx(aqua.DRYRUN, 1, 16, 1, 8, 2, 4, [FAKE])
     for opt, val in ((aqua.OPT_KERNEL, 99), (aqua.OPT_TMA_PIECE, 17), (aqua.OPT_TMA_STAGES, 1),
                      (aqua.OPT_MAX_CTAS, -1), (aqua.OPT_TIMING, 2), (aqua.OPT_LDST_VARIANT, 4),
-                     (aqua.OPT_TMA_VARIANT, 4), (aqua.OPT_INLINE_MAX, 4065), (aqua.OPT_INLINE_MAX, -1), (aqua.OPT_TMA_STATIC_PCT, 101), (aqua.OPT_RATE_GBPS, -1),
+                     (aqua.OPT_TMA_VARIANT, 4), (aqua.OPT_INLINE_MAX, 4065), (aqua.OPT_INLINE_MAX, -1),
+                     (aqua.OPT_TMA_STATIC_PCT, 101), (aqua.OPT_RATE_GBPS, -1), (aqua.OPT_PEER_CTAS, -1),
+                     (aqua.OPT_PEER_TEST, 3),
+                     # round 1's experiments, retired in round 2
+                     (aqua.OPT_LDST_VARIANT, 0), (aqua.OPT_LDST_VARIANT, 3), (aqua.OPT_TMA_VARIANT, 1),
+                     (aqua.OPT_TMA_VARIANT, 2), (aqua.OPT_TMA_VARIANT, 4), (aqua.OPT_TMA_SCHED, -3), (aqua.OPT_TMA_STATIC_PCT, 60),
                      (77, 0)):
         with pytest.raises(aqua.AquaError):
             c.set_option(opt, val)
@@ -465,8 +470,9 @@ def test_create_validates_layout():
     with pytest.raises(aqua.AquaError) as e:
         c.last_launch()                                          # a dry-run context never launches
     assert e.value.code == aqua.E_STATE
-    c.set_option(aqua.OPT_TMA_SCHED, -3)
+    c.set_option(aqua.OPT_TMA_SCHED, 8)
     c.set_option(aqua.OPT_TMA_SCHED, aqua.TMA_SCHED_AUTO)
+    assert c.get_option(aqua.OPT_PEER_CTAS) == 32
     c.set_option(aqua.OPT_INLINE_MAX, 0)
     assert c.get_option(aqua.OPT_INLINE_MAX) == 0
     with pytest.raises(aqua.AquaError) as e:

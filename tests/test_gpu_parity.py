@@ -25,25 +25,20 @@ pytestmark = pytest.mark.gpu
 GOLD = os.path.join(os.path.dirname(__file__), "golden")
 ENGINES = {"tma": aqua.KERNEL_TMA, "ldst": aqua.KERNEL_LDST, "per_chunk": aqua.BASE_PER_CHUNK,
            "gather_temp": aqua.BASE_GATHER_TEMP, "batch": aqua.BASE_BATCH, "ce_host": aqua.KERNEL_CE_HOST,
-           "tma_ws": aqua.KERNEL_TMA, "tma_r2": aqua.KERNEL_TMA, "tma_dyn": aqua.KERNEL_TMA,
-           "tma_dyn1": aqua.KERNEL_TMA, "tma_static": aqua.KERNEL_TMA, "tma_rr": aqua.KERNEL_TMA,
-           "tma_hyb": aqua.KERNEL_TMA, "tma_hybrid": aqua.KERNEL_TMA, "ldst_claim": aqua.KERNEL_LDST}
+           "tma_dyn": aqua.KERNEL_TMA, "tma_dyn1": aqua.KERNEL_TMA, "tma_static": aqua.KERNEL_TMA,
+           "tma_hybrid": aqua.KERNEL_TMA}
+# the engines and schedules the library can run (round 1's AUTO-unused experiments were retired in round 2)
+KERNEL_ENGINES = ["tma", "tma_dyn", "tma_dyn1", "tma_static", "tma_hybrid", "ldst"]
 
 
 def _engine(ctx, name):
-    """Select an engine; "tma_ws" / "tma_r2" are the TMA engine's warp-specialised / two-ring variants,
-    "tma_dyn" / "tma_dyn1" its dynamic work distribution with batches of 8 / 1 ring units, "tma_rr" static
-    round-robin batches of 3 units, "tma_static" one contiguous item range per CTA, "tma_hyb" a static
-    head of 60 % of the items and dynamic batches of 2 units for the rest, "tma_hybrid" the ring plus 8
-    LDST warps claiming batches of the same launch."""
+    """Select an engine; "tma" is the AUTO schedule of the TMA ring, "tma_dyn" / "tma_dyn1" its claimed batches
+    of 8 / 1 ring units, "tma_static" one contiguous item range per CTA, "tma_hybrid" the ring plus 8 LDST
+    warps claiming batches of the same launch."""
     ctx.set_option(aqua.OPT_KERNEL, ENGINES[name])
-    ctx.set_option(aqua.OPT_TMA_VARIANT, {"tma_ws": 1, "tma_r2": 2, "tma_hybrid": 3}.get(name, 0))
-    if name.startswith("ldst"):
-        ctx.set_option(aqua.OPT_LDST_VARIANT, 3 if name == "ldst_claim" else 2)
-    if name in ("tma_dyn", "tma_dyn1", "tma_static", "tma_rr", "tma_hyb"):
-        ctx.set_option(aqua.OPT_TMA_SCHED, {"tma_dyn": 8, "tma_dyn1": 1, "tma_static": 0, "tma_rr": -3,
-                                            "tma_hyb": 2}[name])
-        ctx.set_option(aqua.OPT_TMA_STATIC_PCT, 60 if name == "tma_hyb" else 0)
+    ctx.set_option(aqua.OPT_TMA_VARIANT, 3 if name == "tma_hybrid" else 0)
+    if name in ("tma_dyn", "tma_dyn1", "tma_static"):
+        ctx.set_option(aqua.OPT_TMA_SCHED, {"tma_dyn": 8, "tma_dyn1": 1, "tma_static": 0}[name])
 
 
 def _ops(rig, ops, stream=0):
@@ -95,15 +90,14 @@ SHAPES = {
     "fp8_kv": (2, 16, 8, 128, 1),        # e = 1 (FP8 KV cache): S = 16 KiB
     "fp32_kv": (2, 16, 4, 128, 4),       # e = 4: S = 32 KiB (one full stage)
     "bs128": (1, 128, 8, 128),           # S = 256 KiB: 8 pieces per chunk
-    "s1k": (3, 16, 1, 32),               # S = 1 KiB: 4 chunks per register round (hybrid / ldst_claim packing)
+    "s1k": (3, 16, 1, 32),               # S = 1 KiB: 4 chunks per register round (hybrid packing)
     "s2k": (2, 16, 1, 64),               # S = 2 KiB: 2 chunks per register round
     "s512": (5, 16, 1, 16),              # S = 512 B: 8 chunks per register round, ragged descriptor crossings
 }
 
 
 @pytest.mark.parametrize("shape", list(SHAPES))
-@pytest.mark.parametrize("engine", ["tma", "tma_ws", "tma_r2", "tma_dyn", "tma_dyn1", "tma_static", "tma_rr", "tma_hyb", "tma_hybrid", "ldst",
-                                    "ldst_claim"])
+@pytest.mark.parametrize("engine", KERNEL_ENGINES)
 @pytest.mark.parametrize("seed", [0, 1])
 @pytest.mark.parametrize("ctas", [0, 3])
 def test_random_sequences_bytes(shape, engine, seed, ctas):
@@ -153,7 +147,7 @@ def test_random_sequences_bytes(shape, engine, seed, ctas):
             rig.assert_bytes_equal(f"after failed {op}")
 
 
-@pytest.mark.parametrize("engine", ["tma", "tma_dyn1", "tma_hybrid", "ldst", "ldst_claim", "ce_host"])
+@pytest.mark.parametrize("engine", ["tma", "tma_dyn1", "tma_hybrid", "ldst", "ce_host"])
 @pytest.mark.parametrize("D", [64, 8, 16])
 def test_block_major_layout_bytes(engine, D):
     """Block-major layout ([NB][2][bs][H][D] per layer, kv_plane_stride = S):
@@ -352,8 +346,7 @@ def test_errors_leave_state_unchanged_and_no_cpu_fallback():
     assert c.launch_count() == n0 + 1         # the copy ran as one of our kernels
 
 
-@pytest.mark.parametrize("engine", ["tma", "tma_ws", "tma_r2", "tma_dyn", "tma_dyn1", "tma_static", "tma_rr", "tma_hyb", "tma_hybrid", "ldst",
-                                    "ldst_claim"])
+@pytest.mark.parametrize("engine", KERNEL_ENGINES)
 @pytest.mark.parametrize("tier", ["small_inline", "big_inline", "staged_256", "staged_4064"])
 def test_descriptor_tiers_bytes(engine, tier):
     """Descriptor passing, whole-buffer compare (both directions, fragmented
@@ -392,8 +385,7 @@ def test_ticket_timing():
     assert e.value.code == aqua.E_STATE
 
 
-@pytest.mark.parametrize("engine", ["tma", "tma_ws", "tma_r2", "tma_dyn", "tma_dyn1", "tma_static", "tma_rr", "tma_hyb", "tma_hybrid", "ldst",
-                                    "ldst_claim"])
+@pytest.mark.parametrize("engine", KERNEL_ENGINES)
 def test_migrate_reclaim_relend_bytes(engine):
     """NEXT-1 on the GPU: images move lender -> host (reclaim) and back
     (re-offer) through the fused arena->arena kernel, byte for byte with the
@@ -426,8 +418,7 @@ def test_migrate_reclaim_relend_bytes(engine):
     _ops(rig, [("in", [1, 2, 3]), ("out", [2])])
 
 
-@pytest.mark.parametrize("engine", ["tma", "tma_ws", "tma_r2", "tma_dyn", "tma_dyn1", "tma_static", "tma_rr", "tma_hyb", "tma_hybrid", "ldst",
-                                    "ldst_claim"])
+@pytest.mark.parametrize("engine", KERNEL_ENGINES)
 def test_prefix_cache_bytes(engine):
     """NEXT-2 on the GPU: store a cached prefix (copy), load it into three
     new prompts, reclaim moves it to the host, load again -- whole buffers
@@ -714,8 +705,7 @@ def test_pattern_batch_kernel_matches_oracle_words():
     rig.assert_bytes_equal("pattern batch")
 
 
-@pytest.mark.parametrize("engine", ["tma", "tma_ws", "tma_r2", "tma_dyn", "tma_dyn1", "tma_static", "tma_rr", "tma_hyb", "tma_hybrid", "ldst",
-                                    "ldst_claim"])
+@pytest.mark.parametrize("engine", KERNEL_ENGINES)
 def test_many_small_blocks_whole_buffer(engine):
     """Scale edge: 131,072 blocks of S = 256 B (100,000-block prompt, 800 KB of
     staged descriptors, slot ids > 2^16), whole pool / arena compared with
@@ -757,13 +747,13 @@ def test_auto_policy_launch_shapes():
     """aqua_last_launch reports what AUTO chose: claimed
     2-unit batches with a 4-stage ring at one CTA per SM; static ranges for a
     small call; under an SM cap, static ranges for stage-sized chunks and the
-    hybrid ring + LDST warps for sub-stage chunks; copy engines for host-only
-    calls launch no swap kernel of ours."""
-    def ctx_for(L, H, NB, nslots):
-        S = 16 * H * 128 * 2
+    hybrid ring + LDST warps for sub-stage chunks; at full grid the batch size
+    by chunk size, and the hybrid for 512 B chunks."""
+    def ctx_for(L, H, NB, nslots, D=128):
+        S = 16 * H * D * 2
         layers = [torch.zeros(2 * NB * S, dtype=torch.uint8, device="cuda") for _ in range(L)]
         arena = torch.zeros(nslots * 2 * L * S, dtype=torch.uint8, device="cuda")
-        c = aqua.Ctx(0, L, 16, H, 128, 2, NB, [t.data_ptr() for t in layers])
+        c = aqua.Ctx(0, L, 16, H, D, 2, NB, [t.data_ptr() for t in layers])
         c.lend(0, arena.data_ptr(), arena.numel())
         return c, layers, arena
 
@@ -801,6 +791,21 @@ def test_auto_policy_launch_shapes():
     c.swap_out([1])
     s = c.last_launch()
     assert s["ctas"] == 16 and s["variant"] == 3 and s["threads_per_cta"] == 288
-    assert s["schedule"] == "claimed batches of 32 items"  # 8 units x 4 chunks
+    assert s["schedule"] == "claimed batches of 128 items"  # the ring's 32 units x 4 chunks
     c.swap_in([1])
     c.close()
+    del keep, arena
+
+    # sub-stage chunks at full grid (round 2, profiles/r02_small_chunks_*.jsonl): 2 KiB -> ring, 4-unit
+    # batches; 1 KiB -> ring, 32-unit batches halved while a CTA would get < 8; 512 B -> the hybrid (its
+    # ring's 32-unit batches halved the same way)
+    for D, variant, items in ((64, 0, 4 * 16), (32, 0, 8 * 32), (16, 3, 4 * 64)):
+        c, keep, arena = ctx_for(32, 1, 5000, 5000, D=D)
+        c.alloc_blocks(1, 5000)
+        c.swap_out([1])
+        s = c.last_launch()
+        assert s["ctas"] == sm and s["variant"] == variant, (D, s)
+        assert s["schedule"] == f"claimed batches of {items} items", (D, s)
+        c.swap_in([1])
+        c.close()
+        del keep, arena
