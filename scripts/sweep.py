@@ -686,7 +686,10 @@ def small_chunks2():
             hyb_n = os.environ.get("AQUA_SWEEP_HYBRID_UNITS")
             if hyb_n:
                 combos = [x for x in combos if x[0] != "hybrid"] + [("hybrid", 0, 3, int(n)) for n in hyb_n.split(",")]
-            for eng, grid, v, n in combos:
+            st_list = [int(x) for x in os.environ.get("AQUA_SWEEP_RING_STAGES", "0").split(",")]
+            combos = [(e, st, v, n) for (e, _, v, n) in combos for st in st_list]
+            for eng, stg, v, n in combos:
+                ctx.set_option(aqua.OPT_TMA_STAGES, stg)
                 ctx.set_option(aqua.OPT_KERNEL, aqua.KERNEL_TMA)
                 ctx.set_option(aqua.OPT_TMA_VARIANT, v)
                 ctx.set_option(aqua.OPT_TMA_SCHED, n)
@@ -700,6 +703,7 @@ def small_chunks2():
                                   "hbm_GBps": round(4 * nblk * U / pair / 1e6, 1)}), flush=True)
         ctx.set_option(aqua.OPT_TMA_VARIANT, 0)
         ctx.set_option(aqua.OPT_TMA_SCHED, aqua.TMA_SCHED_AUTO)
+        ctx.set_option(aqua.OPT_TMA_STAGES, 0)
         ctx.close()
         del layers, arena
         torch.cuda.empty_cache()
