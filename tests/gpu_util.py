@@ -1,5 +1,7 @@
 """Shared helpers for the -m gpu parity tests: device buffers filled from the
 seeded generators, and an oracle Pool holding the same initial bytes."""
+import weakref
+
 import numpy as np
 import torch
 
@@ -11,7 +13,9 @@ from workloads import kv_random_bytes
 class Rig:
     """A borrower pool (L device tensors), a GPU lender arena (caller-owned
     device tensor) and a pinned host arena, mirrored by an oracle Pool with
-    identical initial bytes."""
+    identical initial bytes.  Every Rig's ctx is destroyed after its test
+    (tests/conftest.py), so a leak check sees the library free everything."""
+    live = weakref.WeakSet()
 
     def __init__(self, L=2, bs=16, H=2, D=64, e=2, NB=40, lender_slots=12, host_slots=0, seed=0,
                  kv_plane_stride=0, block_stride=0, device=0, lender_device=None, peer_test=0):
@@ -25,6 +29,7 @@ class Rig:
         U = self.lay.U
         self.ctx = aqua.Ctx(device, L, bs, H, D, e, NB, [t.data_ptr() for t in self.layers],
                             kv_plane_stride, block_stride)
+        Rig.live.add(self)
         self.peer = self.host = None
         if peer_test:
             self.ctx.set_option(aqua.OPT_PEER_TEST, peer_test)
@@ -52,3 +57,9 @@ class Rig:
             assert np.array_equal(self.peer.cpu().numpy(), self.opool.peer.data), f"{what}: lender arena differs"
         if self.host is not None:
             assert np.array_equal(self.host.numpy(), self.opool.host.data), f"{what}: host arena differs"
+
+
+def close_all():
+    """Destroy every live Rig's context (the conftest fixture runs this after each test)."""
+    for r in list(Rig.live):
+        r.ctx.close()

@@ -55,8 +55,10 @@ def test_sm100a_cubin_and_bulk_copy_in_sass():
 
 def test_product_kernel_sass_moves_payload_with_tma_only():
     """The product swap kernel (TMA ring, no LDST warps): payload through
-    UBLKCP bulk copies only (no 128-bit LDG/STG), batches claimed with the
-    non-aggregated ATOMG.E.INC -- per-kernel cuobjdump SASS."""
+    UBLKCP bulk copies only (no 128-bit LDG/STG), batches claimed with a
+    non-aggregated ATOMG.E.ADD of the batch's item count (no REDUX: the
+    compiler did not turn it into a warp-aggregated atomic)
+    -- per-kernel cuobjdump SASS."""
     import re
     import shutil
     import subprocess
@@ -71,7 +73,7 @@ def test_product_kernel_sass_moves_payload_with_tma_only():
     hyb = [f for n, f in funcs.items() if re.search(r"swap_tma_kernelILNS_3DirE\dENS_11SwapParamsTILi\d+EEELi8E", n)]
     assert len(prod) == 6 and len(hyb) == 6        # 3 directions x 2 parameter sizes
     for f in prod:
-        assert "UBLKCP.S.G" in f and "UBLKCP.G.S" in f and "ATOMG.E.INC" in f
+        assert "UBLKCP.S.G" in f and "UBLKCP.G.S" in f and "ATOMG.E.ADD" in f and "REDUX" not in f
         assert not re.search(r"\b(LDG|STG)\.E[.\w]*\.128\b", f)
     for f in hyb:                                   # the hybrid's LDST warps do move payload in registers
         assert "UBLKCP.S.G" in f and re.search(r"\bSTG\.E[.\w]*\.128\b", f)
