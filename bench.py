@@ -183,8 +183,8 @@ def cpu_oracle_sample(seconds: float = 10.0, nblk: int = 128):
     memcpy = a.nbytes / sorted(mt)[2] / 1e9
     return {"value": moved / t_work / 1e9, "unit": "GB/s", "cores": 1, "kind": "oracle",
             "host_memcpy_1core_GBps": round(memcpy, 2),
-            "sample": f"{reps} x (swap_out + swap_in) of a {nblk}-block prompt (U=2 MiB, "
-                      f"{nblk * lay.U / 2**20:.0f} MiB per direction) of the configs[1] shape, "
+            "sample": f"{reps} x (swap_out + swap_in) of a {nblk}-block prompt (U={lay.U / 2**20:g} MiB, "
+                      f"{nblk * lay.U / 2**20:.0f} MiB per direction) of the {CFG['name']} shape, "
                       f"numpy bytes mode, {t_work:.1f} s", "seconds_per_step": t_work / reps,
             "bytes_per_step": 2 * nblk * lay.U}
 
@@ -216,7 +216,7 @@ def run_reference(args):
     moved = args.steps * 2 * nblk * lay.U
     val = moved / tot / 1e9
     sample = (f"each step = swap_out + swap_in of a {nblk}-block prompt ({nblk * lay.U / 2**20:.0f} MiB per "
-              f"direction) of the configs[1] shape (Llama-3-8B KV, block 16), oracle bytes mode, 1 core")
+              f"direction) of the {CFG['name']} shape (U = {lay.U / 2**20:g} MiB per block), oracle bytes mode, 1 core")
     line = {
         "impl": "reference", "metric": METRIC, "value": round(val, 3), "unit": "GB/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * tot / args.steps, 3),

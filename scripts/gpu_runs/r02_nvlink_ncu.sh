@@ -19,3 +19,6 @@ for n in 2 4 8; do
 done
 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 8 --master-addr 127.0.0.1 --master-port 29530 \
   bench.py --gpus 8 --config c4 --roles split --steps 20 --warmup 3 > gpurun_out/r02_bench_c4_split.json
+# C3 with the lender in another process on GPU 1 (IPC over NVLink), call log checked against the oracle
+timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29540 \
+  scripts/c3_run.py --policy cfs-peer --check-oracle > gpurun_out/r02_c3_peer_nvlink.json
