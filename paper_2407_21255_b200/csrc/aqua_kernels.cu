@@ -34,6 +34,7 @@
 #include "aqua_internal.h"
 
 #include <algorithm>
+#include <cstdlib>
 
 namespace aqua {
 namespace {
@@ -747,6 +748,30 @@ int tma_smem_bytes(int piece, int stages) { return piece * stages + 8 * stages; 
 
 namespace {
 
+// One ring kernel instantiation (LW register warps); the opt-in shared
+// memory attribute is per device and per instantiation: set once.
+template <int LW, class P>
+cudaError_t launch_ring(const P& p, Dir dir, int grid, int smem, int stages, cudaStream_t s, int dev) {
+  static thread_local bool set_smem[3][64] = {};
+  bool& have = set_smem[dir][dev & 63];
+  if (!have) {
+    const cudaError_t e = cudaFuncSetAttribute(dir == kOut  ? swap_tma_kernel<kOut, P, LW>
+                                               : dir == kIn ? swap_tma_kernel<kIn, P, LW>
+                                                            : swap_tma_kernel<kMig, P, LW>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (e != cudaSuccess) return e;
+    have = true;
+  }
+  constexpr int nt = 32 * (1 + LW);
+  if (dir == kOut)
+    swap_tma_kernel<kOut, P, LW><<<grid, nt, smem, s>>>(p, stages);
+  else if (dir == kIn)
+    swap_tma_kernel<kIn, P, LW><<<grid, nt, smem, s>>>(p, stages);
+  else
+    swap_tma_kernel<kMig, P, LW><<<grid, nt, smem, s>>>(p, stages);
+  return cudaGetLastError();
+}
+
 template <class P>
 cudaError_t launch_tma_t(const P& p, Dir dir, int num_sms, int grid_cap, int stages_opt, cudaStream_t s,
                          int* ctas_used, int variant, LaunchInfo* info) {
@@ -770,48 +795,27 @@ cudaError_t launch_tma_t(const P& p, Dir dir, int num_sms, int grid_cap, int sta
     if (p.work_ctr) stages = std::max(stages, 4);
   }
   stages = std::max(2, std::min(stages, 32));
-  constexpr int kLdstWarps = 8;                  // variant 3: TMA ring + 8 LDST warps per CTA
   while (stages > 2 && tma_smem_bytes(stage_bytes, stages) > 227 * 1024) --stages;
   if (tma_smem_bytes(stage_bytes, stages) > 227 * 1024) return cudaErrorInvalidConfiguration;
   const int smem = tma_smem_bytes(stage_bytes, stages);
-  // the opt-in smem attribute is per device and per instantiation; set once
-  static thread_local bool set_smem[2][3][64] = {};
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
   const bool hybrid = variant == 3;
-  bool& have = set_smem[hybrid][dir][dev & 63];
-  if (!have) {
-    if (hybrid)
-      e = cudaFuncSetAttribute(dir == kOut ? swap_tma_kernel<kOut, P, kLdstWarps>
-                               : dir == kIn ? swap_tma_kernel<kIn, P, kLdstWarps>
-                                            : swap_tma_kernel<kMig, P, kLdstWarps>,
-                               cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    else
-      e = cudaFuncSetAttribute(dir == kOut ? swap_tma_kernel<kOut, P, 0>
-                               : dir == kIn ? swap_tma_kernel<kIn, P, 0> : swap_tma_kernel<kMig, P, 0>,
-                               cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    if (e != cudaSuccess) return e;
-    have = true;
-  }
+  // variant 3: TMA ring + 8 register warps per CTA (4 and 16 measured worse,
+  // profiles/r02_hybrid_warps.jsonl)
+  constexpr int kLdstWarps = 8;
+  int nt = 32;
   if (hybrid) {
     if (!p.work_ctr) return cudaErrorInvalidValue;    // the LDST warps only claim batches
-    constexpr int nt = 32 * (1 + kLdstWarps);
-    if (dir == kOut)
-      swap_tma_kernel<kOut, P, kLdstWarps><<<grid, nt, smem, s>>>(p, stages);
-    else if (dir == kIn)
-      swap_tma_kernel<kIn, P, kLdstWarps><<<grid, nt, smem, s>>>(p, stages);
-    else
-      swap_tma_kernel<kMig, P, kLdstWarps><<<grid, nt, smem, s>>>(p, stages);
-  } else if (dir == kOut) {
-    swap_tma_kernel<kOut, P, 0><<<grid, 32, smem, s>>>(p, stages);
-  } else if (dir == kIn) {
-    swap_tma_kernel<kIn, P, 0><<<grid, 32, smem, s>>>(p, stages);
+    e = launch_ring<kLdstWarps>(p, dir, grid, smem, stages, s, dev);
+    nt = 32 * (1 + kLdstWarps);
   } else {
-    swap_tma_kernel<kMig, P, 0><<<grid, 32, smem, s>>>(p, stages);
+    e = launch_ring<0>(p, dir, grid, smem, stages, s, dev);
   }
+  if (e != cudaSuccess) return e;
   if (ctas_used) *ctas_used = grid;
-  if (info) *info = LaunchInfo{grid, hybrid ? 32 * (1 + kLdstWarps) : 32, stages};
+  if (info) *info = LaunchInfo{grid, nt, stages};
   return cudaGetLastError();
 }
 
