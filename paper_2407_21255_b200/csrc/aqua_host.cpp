@@ -392,25 +392,29 @@ aqua_status run_copy_ce_host(aqua_ctx* c, const std::vector<Desc>& ds, aqua::Dir
     };
     // the staging buffer acts as a GPU "arena" of slots of `per` bytes whose
     // chunk c sits at (c - c0)*S: base shifted by -c0*S, U = per
+    // (the staging buffer is the borrower's own memory, never a peer's)
     const int saved_kernel = c->kernel;
     uint8_t* saved_base = c->gpu.base;
     const int64_t saved_U = c->U;
+    const bool saved_peer = c->gpu.peer;
     c->kernel = kernel_engine;
     c->gpu.base = tmp - int64_t(c0) * c->S;
     c->U = static_cast<int64_t>(per);
+    c->gpu.peer = false;
     int regions = 0;
     aqua_status s = AQUA_OK;
     if (dir == aqua::kOut) {
       s = run_copy(c, td, aqua::kOut, st, &regions, c0, nc, nullptr);
-      c->kernel = saved_kernel, c->gpu.base = saved_base, c->U = saved_U;
+      c->kernel = saved_kernel, c->gpu.base = saved_base, c->U = saved_U, c->gpu.peer = saved_peer;
       if (!s) s = dma(true);
     } else {
-      c->kernel = saved_kernel, c->gpu.base = saved_base, c->U = saved_U;
+      c->kernel = saved_kernel, c->gpu.base = saved_base, c->U = saved_U, c->gpu.peer = saved_peer;
       s = dma(false);
       if (!s) {
         c->kernel = kernel_engine, c->gpu.base = tmp - int64_t(c0) * c->S, c->U = static_cast<int64_t>(per);
+        c->gpu.peer = false;
         s = run_copy(c, td, aqua::kIn, st, &regions, c0, nc, nullptr);
-        c->kernel = saved_kernel, c->gpu.base = saved_base, c->U = saved_U;
+        c->kernel = saved_kernel, c->gpu.base = saved_base, c->U = saved_U, c->gpu.peer = saved_peer;
       }
     }
     if (s) return s;

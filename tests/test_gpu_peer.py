@@ -167,3 +167,68 @@ def test_peer_exchange_and_migration_bytes():
     c.migrate([2], aqua.LOC_PEER)
     o.migrate([2], kp.LOC_PEER)
     rig.assert_bytes_equal("migrate back to the peer")
+
+
+@pytest.mark.parametrize("shape", ["c4_shape", "s2k", "ragged_10KiB", "s512"])
+@pytest.mark.parametrize("mode", [1, 2])
+@pytest.mark.parametrize("seed", [0, 1])
+def test_random_sequences_peer_policy_one_gpu(shape, mode, seed):
+    """The peer path's host logic on any box: random alloc / swap_out /
+    swap_in / free / migrate sequences against a same-GPU arena treated as a
+    peer (mode 1: TMA capped at 32 CTAs; mode 2: bulk probe failed -> LDST),
+    whole-buffer equality with the oracle after every call, and errors that
+    agree and change nothing."""
+    from test_gpu_parity import SHAPES, _ops
+    L, bs, H, D, *e = SHAPES[shape]
+    rnd = random.Random(seed * 7 + mode + len(shape))
+    rig = Rig(L=L, bs=bs, H=H, D=D, e=(e or [2])[0], NB=24, lender_slots=10, host_slots=8, seed=seed,
+              peer_test=mode)
+    assert rig.ctx.arena_info(aqua.LOC_PEER)["probe"] == (7 if mode == 1 else 1)
+    c, o = rig.ctx, rig.opool
+    pids = list(range(5))
+    for _ in range(30):
+        k = rnd.random()
+        p = rnd.choice(pids)
+        if k < 0.3:
+            op = ("alloc", (p, rnd.randint(0, 4)))
+        elif k < 0.55:
+            op = ("out", rnd.sample(pids, rnd.randint(1, 3)))
+        elif k < 0.8:
+            op = ("in", rnd.sample(pids, rnd.randint(1, 3)))
+        elif k < 0.9:
+            op = ("mig", (rnd.sample(pids, rnd.randint(1, 2)), rnd.choice([aqua.LOC_PEER, aqua.LOC_HOST])))
+        else:
+            op = ("free", p)
+        name, arg = op
+        # does the call move an image to or from the (pretend) peer arena?
+        on_peer = lambda ps: any(q in o.prompts and o.prompts[q].location == kp.LOC_PEER for q in ps)
+        try:
+            touches = name == "mig" or (name == "in" and on_peer(arg))
+            if name == "mig":
+                c.migrate(arg[0], arg[1])
+                o.migrate(arg[0], arg[1])
+                rig.assert_bytes_equal(f"after {op}")
+            else:
+                _ops(rig, [op])
+            touches = touches or (name == "out" and on_peer(arg))
+            if touches:
+                launch = c.last_launch()
+                assert launch["ctas"] <= 32 and launch["engine"] == ("tma" if mode == 1 else "ldst"), launch
+        except (kp.AquaError, aqua.AquaError) as err:
+            code_o = code_c = None
+            call_o = {"alloc": lambda: o.alloc_blocks(*arg), "out": lambda: o.swap_out(arg),
+                      "in": lambda: o.swap_in(arg), "free": lambda: o.free_prompt(arg),
+                      "mig": lambda: o.migrate(arg[0], arg[1])}[name]
+            call_c = {"alloc": lambda: c.alloc_blocks(*arg), "out": lambda: c.swap_out(arg),
+                      "in": lambda: c.swap_in(arg, cap=4096), "free": lambda: c.free(arg),
+                      "mig": lambda: c.migrate(arg[0], arg[1])}[name]
+            try:
+                call_o()
+            except kp.AquaError as eo:
+                code_o = eo.code
+            try:
+                call_c()
+            except aqua.AquaError as ec:
+                code_c = ec.code
+            assert code_o is not None and code_o == code_c, (op, code_o, code_c, err)
+            rig.assert_bytes_equal(f"after failed {op}")
