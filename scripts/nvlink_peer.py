@@ -14,6 +14,8 @@ GB/s per direction, fraction of 900 (nominal) and 770 (measured peer copy),
 and the pattern verify of the resumed prompts.  --bidir also runs the
 mirror pair (the lender GPU borrowing from the borrower GPU) concurrently,
 so both link directions carry swaps (configs[4] "bidirectional").
+`--lender 0` on a one-GPU box runs the same code against the borrower's own
+HBM (a smoke test of the script; the cap then does not apply: not a peer).
 
 This calibrates the peer CTA cap (the minimum SMs that
 carry the link) and is the command the NVLink ncu recipe wraps
@@ -97,7 +99,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     args = ap.parse_args()
-    if torch.cuda.device_count() < 2:
+    if max(args.borrower, args.lender) >= torch.cuda.device_count():
         print(json.dumps({"skipped": "needs 2 GPUs (peer lender over NVLink)",
                           "devices": torch.cuda.device_count()}))
         return
@@ -131,6 +133,7 @@ def main():
                          "ctas": launch["ctas"], "engine": launch["engine"], "stages": launch["stages"],
                          "schedule": launch["schedule"], "verify_mismatches": s.verify()})
         print(json.dumps({"config": args.config, "peer_ctas": cap, "bidir": args.bidir,
+                          "smoke_same_gpu": args.borrower == args.lender,
                           "bytes_per_direction": sides[0].nblk * sides[0].U, "pairs": recs}), flush=True)
     for s in sides:
         s.ctx.close()
