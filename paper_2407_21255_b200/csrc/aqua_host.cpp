@@ -606,6 +606,22 @@ aqua_status run_copy(aqua_ctx* c, const std::vector<Desc>& ds, aqua::Dir dir, cu
       if (c->peer_ctas > 0 && (cap == 0 || cap > c->peer_ctas)) cap = c->peer_ctas;
       if ((c->gpu.probe & 6) != 6 && engine == AQUA_KERNEL_TMA) engine = AQUA_KERNEL_LDST;
     }
+    // AUTO, plane-major chunks of 512 B .. 1 KiB on the whole GPU: every bulk
+    // copy costs the SM's TMA unit ~90 cycles (profiles/r02_scatter_probe.jsonl),
+    // so the small-chunk register kernel moves them (r02_small_ldst2.jsonl:
+    // 1 KiB 6.17-6.24 TB/s vs 5.99 for the ring; 512 B 5.15-5.22 vs 5.16 for
+    // the hybrid).  Not for merged K+V chunks of block-major layouts (1 KiB
+    // merged: 4.93 vs 5.31 for the ring, r02_small_chunks_bm2.jsonl), not
+    // under an SM cap (per CTA the ring and the hybrid move more) and not for
+    // host images (zero-copy over PCIe).
+    bool small_auto = false;
+    if (c->kernel == AQUA_KERNEL_AUTO && engine == AQUA_KERNEL_TMA && (cap == 0 || cap >= c->num_sms) &&
+        !p.kv_merged && S_eff >= 512 && S_eff <= 1024 && S_eff % 16 == 0 && 256 % (S_eff / 16) == 0 &&
+        dir != aqua::kMig) {
+      bool any_host = false;
+      for (const Desc& d : ds) any_host = any_host || (d.slot_arena & kArenaBit);
+      if (!any_host) engine = AQUA_KERNEL_LDST, small_auto = true;
+    }
     if (engine == AQUA_KERNEL_TMA) {
       // stage = 32 KiB (or the option): one piece of a large chunk, or a
       // group of whole small chunks that are contiguous in the image
@@ -637,16 +653,20 @@ aqua_status run_copy(aqua_ctx* c, const std::vector<Desc>& ds, aqua::Dir dir, cu
       c->last_engine = AQUA_KERNEL_TMA, c->last_variant = v_used, c->last_batch = p.batch;
       c->last_inline = p.desc ? 0 : p.ndesc;
     } else {
-      // grid-stride 4 KiB items, software pipelined
-      p.piece = 4096;
+      // variant 2: grid-stride 4 KiB items, software pipelined; variant 3
+      // (small chunks of 512 B .. 4 KiB): rounds of whole chunks
+      const int64_t nvec = S_eff / 16;
+      const bool small = (small_auto || c->ldst_variant == 3) && S_eff % 16 == 0 && nvec >= 32 && nvec <= 256 &&
+                         256 % nvec == 0;
+      p.piece = small ? static_cast<int>(S_eff) : 4096;
       p.group = 1;
       p.npieces = static_cast<int32_t>((S_eff + p.piece - 1) / p.piece);
       p.nitems = p.ndesc * p.nc * p.npieces;
       aqua::LaunchInfo li;
       e = aqua::launch_swap_ldst(p, inl, dir, c->num_sms, all_host && cap == kHostCtas ? 2 * kHostCtas : cap, st, &ctas,
-                                 &li);
+                                 small ? 3 : 2, &li);
       c->last_grid = li.grid, c->last_threads = li.threads, c->last_stages = 0;
-      c->last_engine = AQUA_KERNEL_LDST, c->last_variant = 2, c->last_batch = 0;
+      c->last_engine = AQUA_KERNEL_LDST, c->last_variant = small ? 3 : 2, c->last_batch = 0;
       c->last_inline = p.desc ? 0 : p.ndesc;
     }
     if (e != cudaSuccess) return cuda_fail(c, e, "swap kernel launch");
@@ -1840,7 +1860,7 @@ aqua_status aqua_set_option(aqua_ctx* c, int32_t opt, int64_t v) {
       c->timing = v != 0;
       return AQUA_OK;
     case AQUA_OPT_LDST_VARIANT:
-      if (v != 2) return fail(c, AQUA_E_INVAL, "ldst variant (only 2 remains; 0, 1, 3 retired in round 2)");
+      if (v != 2 && v != 3) return fail(c, AQUA_E_INVAL, "ldst variant (2 pipelined, 3 small chunks; 0, 1 retired)");
       c->ldst_variant = static_cast<int>(v);
       return AQUA_OK;
     case AQUA_OPT_TMA_VARIANT:

@@ -102,8 +102,9 @@ struct LaunchInfo {
 // kInlineDescBig) are copied into the kernel parameters.
 cudaError_t launch_swap_tma(const SwapHeader& h, const Desc* inl, Dir dir, int num_sms, int grid_cap, int stages,
                             cudaStream_t s, int* ctas_used, int variant = 0, LaunchInfo* info = nullptr);
+// variant 3: the small-chunk kernel (h.S = 512 B .. 4 KiB, S/16 | 256, h.piece = h.S); else 2.
 cudaError_t launch_swap_ldst(const SwapHeader& h, const Desc* inl, Dir dir, int num_sms, int grid_cap,
-                             cudaStream_t s, int* ctas_used, LaunchInfo* info = nullptr);
+                             cudaStream_t s, int* ctas_used, int variant = 2, LaunchInfo* info = nullptr);
 cudaError_t launch_pattern_fill(const PatternParams& p, int num_sms, cudaStream_t s);
 cudaError_t launch_pattern_verify(const PatternParams& p, int num_sms, cudaStream_t s);
 

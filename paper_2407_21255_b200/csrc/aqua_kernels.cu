@@ -819,9 +819,111 @@ cudaError_t launch_tma_t(const P& p, Dir dir, int num_sms, int grid_cap, int sta
   return cudaGetLastError();
 }
 
+// Small chunks through registers (AQUA_OPT_LDST_VARIANT 3; AUTO for chunks
+// below 2 KiB).  A bulk copy costs the SM's TMA unit ~90 cycles whatever its
+// size (profiles/r02_scatter_probe.jsonl: TMA reads of 512 B runs top out at
+// 1.67 TB/s, of 1 KiB runs at 3.08), while 16-byte loads of scattered 512 B
+// runs reach 6.9 TB/s -- DRAM does not mind the scatter.  So for chunks of
+// 512 B .. 4 KiB (nvec = S/16 vectors, nvec | 256) each warp moves rounds of
+// 4 KiB = 256 / nvec whole chunks: slot u of every lane belongs to chunk
+// (32 u) / nvec of the round (warp-uniform: one descriptor, one layer base,
+// one address per slot for the whole warp), vector (32 u + lane) % nvec of
+// it; all 8 loads of a round are in flight before its 8 stores.  Rounds are
+// dealt grid-stride (static, like the probe's scattered copy that reaches
+// 6.3 / 6.4 TB/s at 512 B / 1 KiB).  The (descriptor, chunk) of slot 0 is
+// divided out once per round; the other slots step from it.
+template <Dir D, class P>
+__global__ void __launch_bounds__(256) swap_small_kernel(const __grid_constant__ P p) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  const int nvec = static_cast<int>(p.S >> 4);
+  const int k = 256 / nvec;                             // chunks per round
+  const int64_t nrounds = (p.nitems + k - 1) / k;
+  for (int64_t r = warp; r < nrounds; r += nwarps) {
+    const int64_t i0 = r * k;
+    int64_t j = i0 / p.nc;
+    int32_t c = p.c0 + static_cast<int32_t>(i0 - j * p.nc);
+    // pointers of chunk (j, c); the next chunk of the same descriptor is
+    // one S further in the image and, in the pool, the V plane of the same
+    // layer (+ P_kv) or the next layer's K plane (layer base + block offset)
+    const uint8_t* src;
+    uint8_t* dst;
+    uint32_t bytes;
+    int64_t boff = 0;
+    auto locate = [&]() {
+      const Desc d = desc_at(p, j);
+      item_addrs<D>(p, d, c, 0, src, dst, bytes);
+      boff = int64_t(d.block) * p.P_b;
+    };
+    auto step = [&]() {
+      if (++c == p.c0 + p.nc) {
+        c = p.c0;
+        ++j;
+        if (j < p.ndesc) locate();
+        return;
+      }
+      if (D == kMig) {
+        src += p.S;
+        dst += p.S;
+        return;
+      }
+      uint8_t* pool;
+      if (!p.kv_merged && (c & 1))                      // K -> V of the same layer
+        pool = const_cast<uint8_t*>(D == kOut ? src : dst) + p.P_kv;
+      else                                              // next layer's K plane
+        pool = reinterpret_cast<uint8_t*>(__ldg(p.layer_base + (p.kv_merged ? c : c >> 1))) + boff;
+      if (D == kOut) {
+        src = pool;
+        dst += p.S;
+      } else {
+        src += p.S;
+        dst = pool;
+      }
+    };
+    locate();
+    int4 v[8];
+    uint8_t* dp[8];
+    int t_prev = 0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int t = (u * 32) / nvec;                    // chunk of the round (uniform)
+      if (t != t_prev) {
+        step();
+        t_prev = t;
+      }
+      dp[u] = nullptr;
+      if (i0 + t < p.nitems) {
+        const size_t vo = size_t((u * 32) % nvec + lane) * 16;
+        v[u] = ld_stream(src + vo);
+        dp[u] = dst + vo;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (dp[u]) st_stream(dp[u], v[u]);
+  }
+}
+
 template <class P>
 cudaError_t launch_ldst_t(const P& p, Dir dir, int num_sms, int grid_cap, cudaStream_t s, int* ctas_used,
-                          LaunchInfo* info) {
+                          int variant, LaunchInfo* info) {
+  // small-chunk kernel: 2 CTAs of 8 warps per SM (1 .. 8 measured,
+  // profiles/r02_small_ldst*.jsonl: 2 is the best or within 2 % of it)
+  constexpr int small_cps = 2;
+  if (variant == 3) {                    // small chunks: rounds of whole chunks through registers
+    const int k = 256 / static_cast<int>(p.S >> 4);
+    const int grid = grid_for<void>((p.nitems + k - 1) / k, 8, num_sms, small_cps, grid_cap);
+    if (dir == kOut)
+      swap_small_kernel<kOut, P><<<grid, 256, 0, s>>>(p);
+    else if (dir == kIn)
+      swap_small_kernel<kIn, P><<<grid, 256, 0, s>>>(p);
+    else
+      swap_small_kernel<kMig, P><<<grid, 256, 0, s>>>(p);
+    if (ctas_used) *ctas_used = grid;
+    if (info) *info = LaunchInfo{grid, 256, 0};
+    return cudaGetLastError();
+  }
   // software pipelined, one 256-thread CTA per SM: 6,624 / 6,572 GB/s on C2
   // (profiles/r01_ldst_variants.jsonl)
   const int grid = grid_for<void>(p.nitems, 8, num_sms, 1, grid_cap);
@@ -864,10 +966,10 @@ cudaError_t launch_swap_tma(const SwapHeader& h, const Desc* inl, Dir dir, int n
 }
 
 cudaError_t launch_swap_ldst(const SwapHeader& h, const Desc* inl, Dir dir, int num_sms, int grid_cap,
-                             cudaStream_t s, int* ctas_used, LaunchInfo* info) {
+                             cudaStream_t s, int* ctas_used, int variant, LaunchInfo* info) {
   if (h.nitems == 0) return cudaSuccess;
   return with_params(h, inl, [&](const auto& p) {
-    return launch_ldst_t(p, dir, num_sms, grid_cap, s, ctas_used, info);
+    return launch_ldst_t(p, dir, num_sms, grid_cap, s, ctas_used, variant, info);
   });
 }
 

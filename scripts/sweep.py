@@ -674,7 +674,8 @@ def small_chunks2():
             H = S // 4096
         U = 2 * L * S
         nblk = (1 << 30) // U
-        ctx, layers, arena, _ = setup(L, 16, H, D, 2 * nblk, nblk)
+        bm = os.environ.get("AQUA_SWEEP_BLOCK_MAJOR") == "1"
+        ctx, layers, arena, _ = setup(L, 16, H, D, 2 * nblk, nblk, block_major=bm)
         s = torch.cuda.Stream()
         for cap in (0, 32):
             combos = [("ring", 0, 0, n) for n in (2, 4, 8, 16, 32)]
@@ -690,13 +691,15 @@ def small_chunks2():
             combos = [(e, st, v, n) for (e, _, v, n) in combos for st in st_list]
             for eng, stg, v, n in combos:
                 ctx.set_option(aqua.OPT_TMA_STAGES, stg)
-                ctx.set_option(aqua.OPT_KERNEL, aqua.KERNEL_TMA)
+                ctx.set_option(aqua.OPT_KERNEL, aqua.KERNEL_AUTO if eng == "auto" else aqua.KERNEL_TMA)
                 ctx.set_option(aqua.OPT_TMA_VARIANT, v)
                 ctx.set_option(aqua.OPT_TMA_SCHED, n)
                 ctx.set_option(aqua.OPT_MAX_CTAS, cap)
                 pair = time_queued(ctx, s, K=10, reps=3)
                 ll = ctx.last_launch()
-                print(json.dumps({"S": S, "cap": cap or 148, "engine": eng, "sched_units": n, "grid": ll["ctas"],
+                print(json.dumps({"S": S, "block_major": bm, "cap": cap or 148, "engine": eng, "sched_units": n,
+                                  "grid": ll["ctas"],
+                                  "kernel": ll["engine"], "variant": ll["variant"],
                                   "ldst_units": int(os.environ.get("AQUA_HYBRID_LDST_UNITS", "0")),
                                   "stages": ll["stages"],
                                   "threads": ll["threads_per_cta"], "launch": ll["schedule"],
@@ -704,6 +707,31 @@ def small_chunks2():
         ctx.set_option(aqua.OPT_TMA_VARIANT, 0)
         ctx.set_option(aqua.OPT_TMA_SCHED, aqua.TMA_SCHED_AUTO)
         ctx.set_option(aqua.OPT_TMA_STAGES, 0)
+        ctx.close()
+        del layers, arena
+        torch.cuda.empty_cache()
+
+
+def small_ldst_sweep():
+    """The small-chunk register kernel (LDST variant 3) vs AUTO, S = 512 B ..
+    4 KiB, 1 GiB calls, all SMs and a 32-CTA cap; AQUA_SMALL_CPS = CTAs per SM
+    (set per process)."""
+    Ss = [int(x) for x in os.environ.get("AQUA_SWEEP_S", "512,1024,2048,4096").split(",")]
+    for S in Ss:
+        L, H, D = 32, 1, S // 32
+        U = 2 * L * S
+        nblk = (1 << 30) // U
+        ctx, layers, arena, _ = setup(L, 16, H, D, 2 * nblk, nblk)
+        s = torch.cuda.Stream()
+        for eng, cap in (("auto", 0), ("small", 0), ("auto", 32), ("small", 32)):
+            ctx.set_option(aqua.OPT_KERNEL, aqua.KERNEL_AUTO if eng == "auto" else aqua.KERNEL_LDST)
+            ctx.set_option(aqua.OPT_LDST_VARIANT, 3 if eng == "small" else 2)
+            ctx.set_option(aqua.OPT_MAX_CTAS, cap)
+            pair = time_queued(ctx, s, K=10, reps=3)
+            ll = ctx.last_launch()
+            print(json.dumps({"S": S, "engine": eng, "cap": cap, "grid": ll["ctas"], "variant": ll["variant"],
+                              "cps": int(os.environ.get("AQUA_SMALL_CPS", "8")),
+                              "hbm_GBps": round(4 * nblk * U / pair / 1e6, 1)}), flush=True)
         ctx.close()
         del layers, arena
         torch.cuda.empty_cache()
@@ -812,6 +840,8 @@ if __name__ == "__main__":
         small_chunks()
     elif what == "small_chunks2":
         small_chunks2()
+    elif what == "small_ldst":
+        small_ldst_sweep()
     elif what == "rate":
         rate()
 

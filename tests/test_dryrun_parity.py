@@ -460,7 +460,7 @@ def test_create_validates_layout():
                      (aqua.OPT_TMA_STATIC_PCT, 101), (aqua.OPT_RATE_GBPS, -1), (aqua.OPT_PEER_CTAS, -1),
                      (aqua.OPT_PEER_TEST, 3),
                      # round 1's experiments, retired in round 2
-                     (aqua.OPT_LDST_VARIANT, 0), (aqua.OPT_LDST_VARIANT, 3), (aqua.OPT_TMA_VARIANT, 1),
+                     (aqua.OPT_LDST_VARIANT, 0), (aqua.OPT_LDST_VARIANT, 1), (aqua.OPT_TMA_VARIANT, 1),
                      (aqua.OPT_TMA_VARIANT, 2), (aqua.OPT_TMA_VARIANT, 4), (aqua.OPT_TMA_SCHED, -3), (aqua.OPT_TMA_STATIC_PCT, 60),
                      (77, 0)):
         with pytest.raises(aqua.AquaError):

@@ -26,17 +26,20 @@ GOLD = os.path.join(os.path.dirname(__file__), "golden")
 ENGINES = {"tma": aqua.KERNEL_TMA, "ldst": aqua.KERNEL_LDST, "per_chunk": aqua.BASE_PER_CHUNK,
            "gather_temp": aqua.BASE_GATHER_TEMP, "batch": aqua.BASE_BATCH, "ce_host": aqua.KERNEL_CE_HOST,
            "tma_dyn": aqua.KERNEL_TMA, "tma_dyn1": aqua.KERNEL_TMA, "tma_static": aqua.KERNEL_TMA,
-           "tma_hybrid": aqua.KERNEL_TMA}
+           "tma_hybrid": aqua.KERNEL_TMA, "ldst_small": aqua.KERNEL_LDST, "auto": aqua.KERNEL_AUTO}
 # the engines and schedules the library can run (round 1's AUTO-unused experiments were retired in round 2)
-KERNEL_ENGINES = ["tma", "tma_dyn", "tma_dyn1", "tma_static", "tma_hybrid", "ldst"]
+KERNEL_ENGINES = ["auto", "tma", "tma_dyn", "tma_dyn1", "tma_static", "tma_hybrid", "ldst", "ldst_small"]
 
 
 def _engine(ctx, name):
-    """Select an engine; "tma" is the AUTO schedule of the TMA ring, "tma_dyn" / "tma_dyn1" its claimed batches
+    """Select an engine; "auto" the library's AUTO policy (engine and schedule), "tma" the AUTO schedule of the
+    TMA ring, "tma_dyn" / "tma_dyn1" its claimed batches
     of 8 / 1 ring units, "tma_static" one contiguous item range per CTA, "tma_hybrid" the ring plus 8 LDST
-    warps claiming batches of the same launch."""
+    warps claiming batches of the same launch, "ldst_small" the small-chunk register kernel (rounds of whole
+    chunks of 512 B .. 4 KiB; other sizes fall back to the pipelined LDST kernel)."""
     ctx.set_option(aqua.OPT_KERNEL, ENGINES[name])
     ctx.set_option(aqua.OPT_TMA_VARIANT, 3 if name == "tma_hybrid" else 0)
+    ctx.set_option(aqua.OPT_LDST_VARIANT, 3 if name == "ldst_small" else 2)
     if name in ("tma_dyn", "tma_dyn1", "tma_static"):
         ctx.set_option(aqua.OPT_TMA_SCHED, {"tma_dyn": 8, "tma_dyn1": 1, "tma_static": 0}[name])
 
@@ -147,7 +150,7 @@ def test_random_sequences_bytes(shape, engine, seed, ctas):
             rig.assert_bytes_equal(f"after failed {op}")
 
 
-@pytest.mark.parametrize("engine", ["tma", "tma_dyn1", "tma_hybrid", "ldst", "ce_host"])
+@pytest.mark.parametrize("engine", ["auto", "tma", "tma_dyn1", "tma_hybrid", "ldst", "ldst_small", "ce_host"])
 @pytest.mark.parametrize("D", [64, 8, 16])
 def test_block_major_layout_bytes(engine, D):
     """Block-major layout ([NB][2][bs][H][D] per layer, kv_plane_stride = S):
@@ -796,16 +799,16 @@ def test_auto_policy_launch_shapes():
     c.close()
     del keep, arena
 
-    # sub-stage chunks at full grid (round 2, profiles/r02_small_chunks_*.jsonl): 2 KiB -> ring, 4-unit
-    # batches; 1 KiB -> ring, 32-unit batches halved while a CTA would get < 8; 512 B -> the hybrid (its
-    # ring's 32-unit batches halved the same way)
-    for D, variant, items in ((64, 0, 4 * 16), (32, 0, 8 * 32), (16, 3, 4 * 64)):
+    # sub-stage chunks at full grid (round 2, profiles/r02_small_chunks_*.jsonl, r02_small_ldst2.jsonl):
+    # 2 KiB -> ring, 4-unit batches; 1 KiB and 512 B -> the small-chunk register kernel, 2 CTAs per SM
+    for D, engine, variant, sched in ((64, "tma", 0, "claimed batches of 64 items"), (32, "ldst", 3, "static ranges"),
+                                      (16, "ldst", 3, "static ranges")):
         c, keep, arena = ctx_for(32, 1, 5000, 5000, D=D)
         c.alloc_blocks(1, 5000)
         c.swap_out([1])
         s = c.last_launch()
-        assert s["ctas"] == sm and s["variant"] == variant, (D, s)
-        assert s["schedule"] == f"claimed batches of {items} items", (D, s)
+        assert s["engine"] == engine and s["variant"] == variant, (D, s)
+        assert s["ctas"] == (sm if engine == "tma" else 2 * sm) and s["schedule"] == sched, (D, s)
         c.swap_in([1])
         c.close()
         del keep, arena
