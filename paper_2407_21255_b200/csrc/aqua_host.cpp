@@ -606,18 +606,18 @@ aqua_status run_copy(aqua_ctx* c, const std::vector<Desc>& ds, aqua::Dir dir, cu
       if (c->peer_ctas > 0 && (cap == 0 || cap > c->peer_ctas)) cap = c->peer_ctas;
       if ((c->gpu.probe & 6) != 6 && engine == AQUA_KERNEL_TMA) engine = AQUA_KERNEL_LDST;
     }
-    // AUTO, plane-major chunks of 512 B .. 1 KiB on the whole GPU: every bulk
-    // copy costs the SM's TMA unit ~90 cycles (profiles/r02_scatter_probe.jsonl),
-    // so the small-chunk register kernel moves them (r02_small_ldst2.jsonl:
-    // 1 KiB 6.17-6.24 TB/s vs 5.99 for the ring; 512 B 5.15-5.22 vs 5.16 for
-    // the hybrid).  Not for merged K+V chunks of block-major layouts (1 KiB
-    // merged: 4.93 vs 5.31 for the ring, r02_small_chunks_bm2.jsonl), not
-    // under an SM cap (per CTA the ring and the hybrid move more) and not for
-    // host images (zero-copy over PCIe).
+    // AUTO, plane-major 1 KiB chunks on the whole GPU: every bulk copy costs
+    // the SM's TMA unit ~90 cycles (profiles/r02_scatter_probe.jsonl), so the
+    // small-chunk register kernel moves them (r02_small_ldst2.jsonl,
+    // r02_small_chunks_auto_final.jsonl: 6.13-6.24 TB/s vs 5.99 for the ring).
+    // At 512 B it ties the hybrid (4.96-5.22 vs 5.13-5.17, less steady), so
+    // the hybrid stays; merged K+V chunks of block-major layouts go to the
+    // ring (1 KiB merged: 4.93 vs 5.31, r02_small_chunks_bm2.jsonl); an SM
+    // cap keeps the ring / hybrid (more per CTA); host images (zero-copy over
+    // PCIe) never take it.
     bool small_auto = false;
     if (c->kernel == AQUA_KERNEL_AUTO && engine == AQUA_KERNEL_TMA && (cap == 0 || cap >= c->num_sms) &&
-        !p.kv_merged && S_eff >= 512 && S_eff <= 1024 && S_eff % 16 == 0 && 256 % (S_eff / 16) == 0 &&
-        dir != aqua::kMig) {
+        !p.kv_merged && S_eff == 1024 && dir != aqua::kMig) {
       bool any_host = false;
       for (const Desc& d : ds) any_host = any_host || (d.slot_arena & kArenaBit);
       if (!any_host) engine = AQUA_KERNEL_LDST, small_auto = true;
