@@ -1056,7 +1056,7 @@ aqua_status aqua_lend(aqua_ctx* c, int lender, void* base, uint64_t bytes, int32
     }
     na.mem_device = mem_dev;
     na.peer = (mem_dev >= 0 && mem_dev != c->device) || c->peer_test > 0;
-    if (na.peer) {
+    if (na.peer && bytes >= 16) {   // (an arena too small to hold a 16-byte vector has no slots to probe)
       // once per lent arena: do plain, bulk-store and bulk-load accesses
       // reach it correctly? (restores the bytes it touches)
       int* d_res = nullptr;
