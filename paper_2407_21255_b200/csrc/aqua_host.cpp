@@ -606,18 +606,17 @@ aqua_status run_copy(aqua_ctx* c, const std::vector<Desc>& ds, aqua::Dir dir, cu
       if (c->peer_ctas > 0 && (cap == 0 || cap > c->peer_ctas)) cap = c->peer_ctas;
       if ((c->gpu.probe & 6) != 6 && engine == AQUA_KERNEL_TMA) engine = AQUA_KERNEL_LDST;
     }
-    // AUTO, plane-major 1 KiB chunks on the whole GPU: every bulk copy costs
-    // the SM's TMA unit ~90 cycles (profiles/r02_scatter_probe.jsonl), so the
-    // small-chunk register kernel moves them (r02_small_ldst2.jsonl,
-    // r02_small_chunks_auto_final.jsonl: 6.13-6.24 TB/s vs 5.99 for the ring).
-    // At 512 B it ties the hybrid (4.96-5.22 vs 5.13-5.17, less steady), so
-    // the hybrid stays; merged K+V chunks of block-major layouts go to the
-    // ring (1 KiB merged: 4.93 vs 5.31, r02_small_chunks_bm2.jsonl); an SM
-    // cap keeps the ring / hybrid (more per CTA); host images (zero-copy over
-    // PCIe) never take it.
+    // AUTO, plane-major chunks of 512 B and 1 KiB on the whole GPU: every bulk
+    // copy costs the SM's TMA unit ~90 cycles (profiles/r02_scatter_probe.jsonl),
+    // so the small-chunk register kernel moves them (device time per call,
+    // r02_small_device.jsonl: 512 B 5.81 / 5.80 TB/s vs 4.61 / 5.11 for the
+    // hybrid, 1 KiB 5.99 / 5.98 vs 5.80 / 5.85 for the ring).  Merged K+V
+    // chunks of block-major layouts stay on the ring (1 KiB merged: 4.93 vs
+    // 5.31, r02_small_chunks_bm2.jsonl); an SM cap keeps the ring / hybrid
+    // (more per CTA); host images (zero-copy over PCIe) never take it.
     bool small_auto = false;
     if (c->kernel == AQUA_KERNEL_AUTO && engine == AQUA_KERNEL_TMA && (cap == 0 || cap >= c->num_sms) &&
-        !p.kv_merged && S_eff == 1024 && dir != aqua::kMig) {
+        !p.kv_merged && (S_eff == 512 || S_eff == 1024) && dir != aqua::kMig) {
       bool any_host = false;
       for (const Desc& d : ds) any_host = any_host || (d.slot_arena & kArenaBit);
       if (!any_host) engine = AQUA_KERNEL_LDST, small_auto = true;

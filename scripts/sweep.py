@@ -713,9 +713,13 @@ def small_chunks2():
 
 
 def small_ldst_sweep():
-    """The small-chunk register kernel (LDST variant 3) vs AUTO, S = 512 B ..
-    4 KiB, 1 GiB calls, all SMs and a 32-CTA cap; AQUA_SMALL_CPS = CTAs per SM
-    (set per process)."""
+    """The small-chunk register kernel (LDST variant 3) vs AUTO, the ring and
+    the hybrid, S = 512 B .. 4 KiB, 1 GiB calls, all SMs and a 32-CTA cap.
+    Two clocks: `queued` = back-to-back calls from Python (host bookkeeping and
+    the binding's id lists included: with 512 B chunks a 1 GiB call is 32,768
+    blocks and the host side takes longer than the kernel), `device` = each
+    call's device time from the library's timing events (descriptor upload +
+    kernel)."""
     Ss = [int(x) for x in os.environ.get("AQUA_SWEEP_S", "512,1024,2048,4096").split(",")]
     for S in Ss:
         L, H, D = 32, 1, S // 32
@@ -723,15 +727,20 @@ def small_ldst_sweep():
         nblk = (1 << 30) // U
         ctx, layers, arena, _ = setup(L, 16, H, D, 2 * nblk, nblk)
         s = torch.cuda.Stream()
-        for eng, cap in (("auto", 0), ("small", 0), ("auto", 32), ("small", 32)):
-            ctx.set_option(aqua.OPT_KERNEL, aqua.KERNEL_AUTO if eng == "auto" else aqua.KERNEL_LDST)
+        for eng, cap in (("auto", 0), ("small", 0), ("ring", 0), ("hybrid", 0), ("auto", 32), ("small", 32)):
+            ctx.set_option(aqua.OPT_KERNEL, {"auto": aqua.KERNEL_AUTO, "small": aqua.KERNEL_LDST}.get(eng, aqua.KERNEL_TMA))
             ctx.set_option(aqua.OPT_LDST_VARIANT, 3 if eng == "small" else 2)
+            ctx.set_option(aqua.OPT_TMA_VARIANT, 3 if eng == "hybrid" else 0)
             ctx.set_option(aqua.OPT_MAX_CTAS, cap)
             pair = time_queued(ctx, s, K=10, reps=3)
+            o, i = time_tickets(ctx, 5, s)
             ll = ctx.last_launch()
-            print(json.dumps({"S": S, "engine": eng, "cap": cap, "grid": ll["ctas"], "variant": ll["variant"],
-                              "cps": int(os.environ.get("AQUA_SMALL_CPS", "8")),
-                              "hbm_GBps": round(4 * nblk * U / pair / 1e6, 1)}), flush=True)
+            print(json.dumps({"S": S, "engine": eng, "cap": cap, "kernel": ll["engine"], "grid": ll["ctas"],
+                              "variant": ll["variant"], "launch": ll["schedule"],
+                              "hbm_GBps_queued": round(4 * nblk * U / pair / 1e6, 1),
+                              "hbm_GBps_device_out": round(2 * nblk * U / o / 1e6, 1),
+                              "hbm_GBps_device_in": round(2 * nblk * U / i / 1e6, 1)}), flush=True)
+        ctx.set_option(aqua.OPT_TMA_VARIANT, 0)
         ctx.close()
         del layers, arena
         torch.cuda.empty_cache()

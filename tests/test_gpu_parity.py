@@ -800,10 +800,9 @@ def test_auto_policy_launch_shapes():
     del keep, arena
 
     # sub-stage chunks at full grid (round 2, profiles/r02_small_chunks_*.jsonl, r02_small_ldst2.jsonl):
-    # 2 KiB -> ring, 4-unit batches; 1 KiB -> the small-chunk register kernel, 2 CTAs per SM; 512 B -> the
-    # hybrid (its ring's 32-unit batches halved to 4 for this call)
+    # 2 KiB -> ring, 4-unit batches; 1 KiB and 512 B -> the small-chunk register kernel, 2 CTAs per SM
     for D, engine, variant, sched in ((64, "tma", 0, "claimed batches of 64 items"), (32, "ldst", 3, "static ranges"),
-                                      (16, "tma", 3, "claimed batches of 256 items")):
+                                      (16, "ldst", 3, "static ranges")):
         c, keep, arena = ctx_for(32, 1, 5000, 5000, D=D)
         c.alloc_blocks(1, 5000)
         c.swap_out([1])
