@@ -66,12 +66,12 @@ def _load() -> C.CDLL:
         "aqua_create": (C.c_int, [C.c_int, P(KVLayout), P(VP)]),
         "aqua_destroy": (C.c_int, [VP]),
         "aqua_lend": (C.c_int, [VP, C.c_int, VP, U64, P(I32)]),
-        "aqua_alloc_blocks": (C.c_int, [VP, U64, I32, VP, P(I32)]),
+        # hot calls: pointer arguments as raw addresses (VP) of per-Ctx scratch buffers
+        "aqua_alloc_blocks": (C.c_int, [VP, U64, I32, VP, VP]),
         "aqua_adopt_blocks": (C.c_int, [VP, U64, I32, P(I32), VP]),
-        "aqua_swap_out": (C.c_int, [VP, I32, P(U64), VP, P(U64)]),
-        "aqua_swap_in": (C.c_int, [VP, I32, P(U64), VP, P(I32), I64, P(I32), P(U64)]),
-        "aqua_swap_exchange": (C.c_int, [VP, I32, P(U64), I32, P(U64), VP, VP, I32, P(I32), I64, P(I32), P(U64),
-                                         P(U64)]),
+        "aqua_swap_out": (C.c_int, [VP, I32, VP, VP, VP]),
+        "aqua_swap_in": (C.c_int, [VP, I32, VP, VP, VP, I64, VP, VP]),
+        "aqua_swap_exchange": (C.c_int, [VP, I32, VP, I32, VP, VP, VP, I32, VP, I64, VP, VP, VP]),
         "aqua_swap_out_layers": (C.c_int, [VP, I32, P(U64), VP, I32, P(U64)]),
         "aqua_swap_in_layers": (C.c_int, [VP, I32, P(U64), VP, I32, P(I32), I64, P(I32), P(U64)]),
         "aqua_free": (C.c_int, [VP, U64, VP]),
@@ -83,7 +83,7 @@ def _load() -> C.CDLL:
         "aqua_prefix_query": (C.c_int, [VP, U64, P(I32), P(I32), P(I32), I32]),
         "aqua_wait": (C.c_int, [VP, U64, VP]),
         "aqua_sync": (C.c_int, [VP, U64]),
-        "aqua_ticket_done": (C.c_int, [VP, U64, P(I32)]),
+        "aqua_ticket_done": (C.c_int, [VP, U64, VP]),
         "aqua_ticket_elapsed": (C.c_int, [VP, U64, P(C.c_float)]),
         "aqua_query": (C.c_int, [VP, U64, P(I32), P(I32), P(I32), P(I32), I32]),
         "aqua_counts": (C.c_int, [VP, P(I32), P(I32), P(I32)]),
@@ -145,6 +145,22 @@ class Ctx:
         self.L, self.bs, self.H, self.D, self.e, self.NB = L, bs, H, D, e, NB
         self.S = bs * H * D * e
         self.U = 2 * L * self.S
+        # Scratch buffers of the hot calls, allocated once with their
+        # addresses cached: numpy's .ctypes costs microseconds per call,
+        # several times the library's own cost of a small swap
+        # (profiles/r02_host_cost.jsonl).  A Ctx is not reentrant.
+        self._pid = np.empty(64, np.uint64)
+        self._pid_a = self._pid.ctypes.data
+        self._pid2 = np.empty(64, np.uint64)
+        self._pid2_a = self._pid2.ctypes.data
+        self._cnt = np.empty(64, np.int32)
+        self._cnt_a = self._cnt.ctypes.data
+        self._ids = np.empty(max(NB, 1), np.int32)     # no call returns more than NB block ids
+        self._ids_a = self._ids.ctypes.data
+        self._tk = (C.c_uint64 * 2)()
+        self._tk_a = C.addressof(self._tk)
+        self._d32 = C.c_int32()
+        self._d32_a = C.addressof(self._d32)
 
     def close(self):
         if self.h:
@@ -165,9 +181,47 @@ class Ctx:
         self._c(lib.aqua_lend(self.h, lender_device, C.c_void_p(base or None), nbytes, C.byref(n)))
         return n.value
 
+    def _pids_arg(self, pids, second: bool = False) -> int:
+        """Copies pids into a scratch buffer; returns its address."""
+        n = len(pids)
+        buf = self._pid2 if second else self._pid
+        if n > len(buf):
+            buf = np.empty(2 * n, np.uint64)
+            if second:
+                self._pid2, self._pid2_a = buf, buf.ctypes.data
+            else:
+                self._pid, self._pid_a = buf, buf.ctypes.data
+        if n == 1:
+            buf[0] = pids[0]
+        elif n:
+            buf[:n] = pids
+        return self._pid2_a if second else self._pid_a
+
+    def _counts_arg(self, n: int) -> int:
+        if n > len(self._cnt):
+            self._cnt = np.empty(2 * n, np.int32)
+            self._cnt_a = self._cnt.ctypes.data
+        return self._cnt_a
+
+    def _tables(self, n: int) -> List[List[int]]:
+        """The new block tables of an n-prompt swap-in from the scratch buffers."""
+        if n == 1:
+            return [self._ids[:int(self._cnt[0])].tolist()]
+        ids, cnt = self._ids, self._cnt[:n].tolist()
+        out, k = [], 0
+        for c in cnt:
+            out.append(ids[k:k + c].tolist())
+            k += c
+        return out
+
     def alloc_blocks(self, pid: int, n: int, stream: int = 0) -> List[int]:
+        if 0 <= n <= len(self._ids):
+            st = lib.aqua_alloc_blocks(self.h, pid, n, stream or None, self._ids_a)
+            if st:
+                _check(st, self.h)
+            return self._ids[:n].tolist()
         out = np.empty(max(n, 1), np.int32)
-        self._c(lib.aqua_alloc_blocks(self.h, pid, n, C.c_void_p(stream or None), _i32p(out)))
+        self._c(lib.aqua_alloc_blocks(self.h, pid, n, stream or None, out.ctypes.data))
         return out[:n].tolist()
 
     def adopt_blocks(self, pid: int, ids: Sequence[int], stream: int = 0) -> None:
@@ -175,10 +229,10 @@ class Ctx:
         self._c(lib.aqua_adopt_blocks(self.h, pid, len(a), _i32p(a), C.c_void_p(stream or None)))
 
     def swap_out(self, pids: Sequence[int], stream: int = 0) -> int:
-        a = np.ascontiguousarray(pids, dtype=np.uint64)
-        t = C.c_uint64()
-        self._c(lib.aqua_swap_out(self.h, len(a), _u64p(a), C.c_void_p(stream or None), C.byref(t)))
-        return t.value
+        st = lib.aqua_swap_out(self.h, len(pids), self._pids_arg(pids), stream or None, self._tk_a)
+        if st:
+            _check(st, self.h)
+        return self._tk[0]
 
     def _cap(self, pids) -> int:
         """Capacity for the new block ids of `pids` (0 for unknown pids: the
@@ -191,37 +245,44 @@ class Ctx:
         return n
 
     def swap_in(self, pids: Sequence[int], stream: int = 0, cap: int = -1) -> Tuple[List[List[int]], int]:
-        a = np.ascontiguousarray(pids, dtype=np.uint64)
+        n = len(pids)
         if cap < 0:
-            cap = self._cap(a)
+            # the scratch holds NB ids, the most a pool can hand out; a call
+            # needing more gets the exact capacity so that the library reports
+            # its own error (pool exhausted) rather than "out_ids too small"
+            st = lib.aqua_swap_in(self.h, n, self._pids_arg(pids), stream or None, self._ids_a, len(self._ids),
+                                  self._counts_arg(n), self._tk_a)
+            if st == OK:
+                return self._tables(n), self._tk[0]
+            if st != E_INVAL or b"out_ids too small" not in (lib.aqua_last_error(self.h) or b""):
+                _check(st, self.h)
+            cap = self._cap(pids)
         ids = np.empty(max(cap, 1), np.int32)
-        counts = np.empty(max(len(a), 1), np.int32)
-        t = C.c_uint64()
-        self._c(lib.aqua_swap_in(self.h, len(a), _u64p(a), C.c_void_p(stream or None), _i32p(ids), cap,
-                                 _i32p(counts), C.byref(t)))
+        counts = np.empty(max(n, 1), np.int32)
+        self._c(lib.aqua_swap_in(self.h, n, self._pids_arg(pids), stream or None, ids.ctypes.data, cap,
+                                 counts.ctypes.data, self._tk_a))
         out, k = [], 0
-        for i in range(len(a)):
+        for i in range(n):
             out.append(ids[k:k + counts[i]].tolist())
             k += counts[i]
-        return out, t.value
+        return out, self._tk[0]
 
     def swap_exchange(self, out_pids: Sequence[int], in_pids: Sequence[int], out_stream: int = 0,
                       in_stream: int = 0, pieces: int = 16):
         """-> (new block tables of in_pids, out_ticket, in_ticket)"""
-        a = np.ascontiguousarray(out_pids, dtype=np.uint64)
-        b = np.ascontiguousarray(in_pids, dtype=np.uint64)
-        cap = self._cap(b)
-        ids = np.empty(max(cap, 1), np.int32)
-        counts = np.empty(max(len(b), 1), np.int32)
-        to, ti = C.c_uint64(), C.c_uint64()
-        self._c(lib.aqua_swap_exchange(self.h, len(a), _u64p(a), len(b), _u64p(b), C.c_void_p(out_stream or None),
-                                       C.c_void_p(in_stream or None), pieces, _i32p(ids), cap, _i32p(counts),
-                                       C.byref(to), C.byref(ti)))
+        na, nb = len(out_pids), len(in_pids)
+        cap = self._cap(in_pids)
+        ids = self._ids if cap <= len(self._ids) else np.empty(cap, np.int32)
+        a_addr = self._pids_arg(out_pids)
+        b_addr = self._pids_arg(in_pids, second=True)
+        self._c(lib.aqua_swap_exchange(self.h, na, a_addr, nb, b_addr, out_stream or None, in_stream or None, pieces,
+                                       ids.ctypes.data if ids is not self._ids else self._ids_a, max(cap, 0),
+                                       self._counts_arg(nb), self._tk_a, self._tk_a + 8))
         out, k = [], 0
-        for i in range(len(b)):
-            out.append(ids[k:k + counts[i]].tolist())
-            k += counts[i]
-        return out, to.value, ti.value
+        for c in self._cnt[:nb].tolist():
+            out.append(ids[k:k + c].tolist())
+            k += c
+        return out, self._tk[0], self._tk[1]
 
     def swap_out_layers(self, pids: Sequence[int], layer_group: int, stream: int = 0) -> List[int]:
         a = np.ascontiguousarray(pids, dtype=np.uint64)
@@ -247,7 +308,9 @@ class Ctx:
         return out, [int(x) for x in t[:ng]]
 
     def free(self, pid: int, stream: int = 0) -> None:
-        self._c(lib.aqua_free(self.h, pid, C.c_void_p(stream or None)))
+        st = lib.aqua_free(self.h, pid, stream or None)
+        if st:
+            _check(st, self.h)
 
     def migrate(self, pids: Sequence[int], dst_loc: int, stream: int = 0) -> int:
         a = np.ascontiguousarray(pids, dtype=np.uint64)
@@ -284,15 +347,16 @@ class Ctx:
         self._c(lib.aqua_prefix_drop(self.h, fid))
 
     def wait(self, ticket: int, stream: int = 0) -> None:
-        self._c(lib.aqua_wait(self.h, ticket, C.c_void_p(stream or None)))
+        st = lib.aqua_wait(self.h, ticket, stream or None)
+        if st:
+            _check(st, self.h)
 
     def sync(self, ticket: int) -> None:
         self._c(lib.aqua_sync(self.h, ticket))
 
     def ticket_done(self, ticket: int) -> bool:
-        d = C.c_int32()
-        self._c(lib.aqua_ticket_done(self.h, ticket, C.byref(d)))
-        return bool(d.value)
+        self._c(lib.aqua_ticket_done(self.h, ticket, self._d32_a))
+        return bool(self._d32.value)
 
     def ticket_elapsed(self, ticket: int) -> float:
         v = C.c_float()
