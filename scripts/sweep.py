@@ -41,12 +41,19 @@ def setup(L, bs, H, D, NB, nblk, host=False, block_major=False):
     return ctx, layers, arena, U
 
 
-def time_tickets(ctx, reps, stream):
-    """Device time of each copy from the library's timing events (excludes
-    host enqueue gaps)."""
+def time_tickets(ctx, reps, stream, sleep_cycles=2_000_000):
+    """Device time of each copy from the library's timing events.  A ticket's
+    start event is recorded before the library prepares the launch, so on an
+    idle GPU it would also count the host's descriptor work and the launch
+    call (~10 us with the 32 KiB parameter block, more for 32K-block calls);
+    a ~1 ms sleep kernel queued first keeps the stream busy until the swap
+    kernel is enqueued (swap_in already queues behind swap_out)."""
     ctx.set_option(aqua.OPT_TIMING, 1)
     outs, ins = [], []
     for _ in range(reps + 2):
+        if sleep_cycles:
+            with torch.cuda.stream(stream):
+                torch.cuda._sleep(sleep_cycles)
         t1 = ctx.swap_out([7], stream.cuda_stream)
         _, t2 = ctx.swap_in([7], stream.cuda_stream)
         torch.cuda.synchronize()
@@ -915,3 +922,41 @@ def latency():
 
 if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "latency":
     latency()
+
+
+def small_calls():
+    """Device time of 1..64-block calls (C2 shape, 2 MiB blocks) by engine
+    and stage size, each measured behind a sleep kernel (no host gap), next
+    to a 1-element torch kernel timed the same way (the launch + event floor)."""
+    L, bs, H, D = 32, 16, 8, 128
+    s = torch.cuda.Stream()
+    x = torch.zeros(1, device="cuda")
+    floor = []
+    for _ in range(50):
+        with torch.cuda.stream(s):
+            torch.cuda._sleep(200_000)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(s)
+            x.add_(1)
+            b.record(s)
+        torch.cuda.synchronize()
+        floor.append(a.elapsed_time(b))
+    print(json.dumps({"small_calls": "floor", "one_tiny_kernel_us": round(1e3 * statistics.median(floor), 2)}),
+          flush=True)
+    for nblk in (1, 2, 4, 8, 16, 64):
+        ctx, layers, arena, U = setup(L, bs, H, D, 4096, nblk)
+        for eng, piece in (("auto", 0), ("tma", 16384), ("tma", 8192), ("ldst", 0)):
+            ctx.set_option(aqua.OPT_KERNEL, aqua.KERNEL_AUTO if eng == "auto" else ENG[eng])
+            ctx.set_option(aqua.OPT_TMA_PIECE, piece)
+            o, i = time_tickets(ctx, 30, s, sleep_cycles=200_000)
+            ll = ctx.last_launch()
+            print(json.dumps({"small_calls": nblk, "bytes": nblk * U, "engine": eng, "piece": piece,
+                              "grid": ll["ctas"], "schedule": ll["schedule"],
+                              "out_us": round(1e3 * o, 2), "in_us": round(1e3 * i, 2)}), flush=True)
+        ctx.close()
+        del layers, arena
+        torch.cuda.empty_cache()
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "small_calls":
+    small_calls()
