@@ -960,3 +960,24 @@ def small_calls():
 
 if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "small_calls":
     small_calls()
+
+
+def ncu_small():
+    """For an ncu capture of the small-chunk kernel under AUTO: 1 GiB calls
+    of S = AQUA_SWEEP_S (plane-major, L = 32, H = 1), 2 warm-up pairs then
+    one swap_out + swap_in pair (launches 5 and 6)."""
+    S = int(os.environ.get("AQUA_SWEEP_S", "512"))
+    L, H, D = 32, 1, S // 32
+    U = 2 * L * S
+    nblk = (1 << 30) // U
+    ctx, layers, arena, _ = setup(L, 16, H, D, 2 * nblk, nblk)
+    s = torch.cuda.Stream()
+    for _ in range(3):
+        ctx.swap_out([7], s.cuda_stream)
+        ctx.swap_in([7], s.cuda_stream)
+    torch.cuda.synchronize()
+    print(json.dumps({"ncu_small": S, "blocks": nblk, "launch": ctx.last_launch()}), flush=True)
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "ncu_small":
+    ncu_small()
