@@ -20,6 +20,12 @@ out is not in the next batch).  Three placements of the images:
 For each: decode alone, paging alone, both serialised on one stream, and both
 on separate streams; prints one JSON line per placement with the overlap
 gain = serial / concurrent and the fraction of the shorter side hidden.
+
+--decode gemm swaps the decode proxy for a tensor-core-bound one (bf16
+GEMMs, the weight-multiply part of a large-batch decode step): then the two
+sides compete for SMs, not HBM, and --caps (AQUA_OPT_MAX_CTAS values for the
+self-lender swap) trades paging speed against the SMs left to the GEMMs --
+the CTA-cap mitigation of NEXT-4.
 """
 import argparse
 import json
@@ -38,23 +44,46 @@ S = bs * H * D * 2
 U = 2 * L * S
 
 
+def _ctas(ctx):
+    try:
+        return ctx.last_launch()["ctas"]
+    except aqua.AquaError:
+        return None
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--weights-gb", type=float, default=16.0)
     ap.add_argument("--steps", type=int, default=40)
     ap.add_argument("--nblk", type=int, default=2048)
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--decode", choices=["hbm", "gemm"], default="hbm")
+    ap.add_argument("--gemm", type=int, default=8192, help="M = N = K of one decode-step GEMM (bf16)")
+    ap.add_argument("--images", default="host,host_sm,self")
+    ap.add_argument("--caps", default="0", help="comma-separated SM caps for the self-lender swap (0 = all SMs)")
     args = ap.parse_args()
     nblk = args.nblk
     layers = [torch.zeros(2 * NB * S, dtype=torch.uint8, device="cuda") for _ in range(L)]
-    w = torch.ones(int(args.weights_gb * 1e9) // 8, dtype=torch.int64, device="cuda")
-    out = torch.empty((), dtype=torch.int64, device="cuda")
+    if args.decode == "hbm":
+        w = torch.ones(int(args.weights_gb * 1e9) // 8, dtype=torch.int64, device="cuda")
+        out = torch.empty((), dtype=torch.int64, device="cuda")
+    else:
+        g = args.gemm
+        ga = torch.randn(g, g, device="cuda", dtype=torch.bfloat16)
+        gb = torch.randn(g, g, device="cuda", dtype=torch.bfloat16)
+        gc = torch.empty(g, g, device="cuda", dtype=torch.bfloat16)
     dec = torch.cuda.Stream()
     swp = torch.cuda.Stream()
     perm = block_permutation(NB, NB, seed=2).tolist()
 
-    for where in ("host", "host_sm", "self"):
+    runs = []
+    for where in args.images.split(","):
+        for cap in ([int(c) for c in args.caps.split(",")] if where == "self" else [0]):
+            runs.append((where, cap))
+    for where, cap in runs:
         ctx = aqua.Ctx(0, L, bs, H, D, 2, NB, [t.data_ptr() for t in layers])
+        if cap:
+            ctx.set_option(aqua.OPT_MAX_CTAS, cap)
         arena = None
         if where == "self":
             arena = torch.empty(nblk * U, dtype=torch.uint8, device="cuda")
@@ -69,7 +98,10 @@ def main():
         def decode(st, n):
             with torch.cuda.stream(st):
                 for _ in range(n):
-                    torch.sum(w, dim=0, out=out)
+                    if args.decode == "hbm":
+                        torch.sum(w, dim=0, out=out)
+                    else:
+                        torch.matmul(ga, gb, out=gc)
 
         def page(st):
             ctx.swap_out([7], st.cuda_stream)
@@ -115,7 +147,12 @@ def main():
         t_ser = timed(serial)
         t_con = timed(concurrent)
         hidden = (t_ser - t_con) / min(t_dec, t_page) if min(t_dec, t_page) > 0 else 0.0
-        print(json.dumps({"images": where, "decode_steps": n, "decode_ms": round(t_dec, 3),
+        extra = {}
+        if args.decode == "gemm":
+            extra["gemm_TFLOPs"] = round(2 * args.gemm ** 3 * n / (t_dec / 1e3) / 1e12, 1)
+        print(json.dumps({"images": where, "decode": args.decode, "swap_sm_cap": cap,
+                          "swap_ctas": _ctas(ctx), **extra,
+                          "decode_steps": n, "decode_ms": round(t_dec, 3),
                           "paging_ms": round(t_page, 3), "paging_GBps": round(2 * nblk * U / t_page / 1e6, 1),
                           "serial_ms": round(t_ser, 3), "concurrent_ms": round(t_con, 3),
                           "overlap_gain": round(t_ser / t_con, 3),
