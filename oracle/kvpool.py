@@ -278,14 +278,15 @@ class Pool:
         for pid in pids:
             p = self.prompts[pid]
             new = self._take_lowest(len(p.slots))
-            ar = self.arena(p.location)
-            if self.layers is not None and ar.data is not None:
+            ar = self.arena(p.location)      # None only for a 0-block image relocated by reclaim
+            if p.slots and self.layers is not None and ar.data is not None:
                 for j, (b, s) in enumerate(zip(new, p.slots)):
                     for l in range(lay.L):
                         for kv in (0, 1):
                             off = s * lay.U + (2 * l + kv) * lay.S
                             self.chunk(l, kv, b)[:] = ar.data[off:off + lay.S]
-            ar.free.update(p.slots)
+            if p.slots:
+                ar.free.update(p.slots)
             p.state, p.location, p.slots, p.blocks = RESIDENT, LOC_LOCAL, [], new
             out.append(list(new))
         return out
@@ -412,7 +413,7 @@ class Pool:
             raise AquaError(E_NOBLOCKS, "pool exhausted")
         new = self._take_lowest(len(f.slots))
         ar = self.arena(f.location)
-        if self.layers is not None and ar.data is not None:
+        if f.slots and self.layers is not None and ar.data is not None:
             for b, s in zip(new, f.slots):
                 for l in range(lay.L):
                     for kv in (0, 1):
@@ -427,7 +428,8 @@ class Pool:
         f = self.prefixes.pop(int(fid), None)
         if f is None:
             raise AquaError(E_STATE, "unknown prefix")
-        self.arena(f.location).free.update(f.slots)
+        if f.slots:
+            self.arena(f.location).free.update(f.slots)
 
     # ---------------------------------------------------------------- C-6
     def free_prompt(self, pid: int) -> None:
@@ -438,7 +440,7 @@ class Pool:
             raise AquaError(E_STATE, "unknown pid")
         if p.state == RESIDENT:
             self.free.update(p.blocks)
-        else:
+        elif p.slots:
             self.arena(p.location).free.update(p.slots)
         del self.prompts[int(pid)]
 

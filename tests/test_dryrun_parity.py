@@ -136,7 +136,8 @@ def lay_U(pool):
     return pool.lay.U
 
 
-@pytest.mark.parametrize("seed", range(60))
+# AQUA_DRY_FUZZ_SEEDS widens this for one-off long runs (profiles/r02_dry_fuzz_long.log)
+@pytest.mark.parametrize("seed", range(int(os.environ.get("AQUA_DRY_FUZZ_SEEDS", "60"))))
 def test_random_op_sequences_match_oracle(seed):
     rnd = random.Random(seed)
     NB = rnd.randint(1, 24)
@@ -193,6 +194,26 @@ def test_random_op_sequences_match_oracle(seed):
         for p, pr in pool.prompts.items():
             st, loc, n, ids = c.query(p, with_ids=True)
             assert (st, loc, ids) == (pr.state, pr.location, pr.blocks if pr.state == kp.RESIDENT else pr.slots)
+
+
+def test_zero_block_image_reclaimed_without_host_matches_oracle():
+    """The degenerate path the 3000-seed fuzz found in the oracle: 0-block
+    images reclaimed with no host arena relocate to the host location; the
+    library and the oracle agree on every later call."""
+    NB = 6
+    lay = kp.Layout(L=1, bs=16, H=1, D=8, e=2, NB=NB)
+    pool = kp.Pool(lay)
+    c = aqua.Ctx(aqua.DRYRUN, 1, 16, 1, 8, 2, NB, [FAKE])
+    pool.lend(kp.LOC_PEER, 2 * lay.U)
+    c.lend(0, FAKE * 2, 2 * lay.U)
+    ops = [("alloc", (1, 0)), ("alloc", (2, 0)), ("alloc", (3, 2)), ("pstore", (0, 3, 0)), ("out", [1, 2]),
+           ("reclaim", None), ("in", [1]), ("xchg", ([], [2])), ("out", [1]), ("free", 1), ("pload", (0, 3)),
+           ("pdrop", 0), ("relend", 4), ("out", [2, 3]), ("in", [3, 2])]
+    for op in ops:
+        a, b = _apply(pool, c, op)
+        assert a == b, (op, a, b)
+        pool.check_invariants()
+    assert c.counts() == (len(pool.free), len(pool.peer.free), -1)
 
 
 # ------------------------------------------------------------------ CFS

@@ -205,6 +205,33 @@ def test_zero_block_prompt():
     assert pool.query(5) == (kp.RESIDENT, kp.LOC_LOCAL, 0, [])
 
 
+def test_zero_block_image_relocated_without_host_arena():
+    """Reclaim moves every lender image to the host; a 0-block
+    image needs no host slots, so it relocates even when no host arena was
+    lent, and afterwards swap_in / free / prefix load+drop of such images
+    touch no arena (found by the 3000-seed dry-run fuzz, profiles/
+    r02_dry_fuzz_long.log).  Expected values hand-derived: nothing to copy,
+    no slot or block changes hands."""
+    pool = make_pool(L=2, NB=4)
+    U = pool.lay.U
+    pool.lend(kp.LOC_PEER, 2 * U, np.zeros(2 * U, np.uint8))
+    assert pool.alloc_blocks(5, 0) == [] and pool.alloc_blocks(6, 0) == [] and pool.alloc_blocks(7, 2) == [0, 1]
+    assert pool.prefix_store(3, 7, 0) == (kp.LOC_PEER, [])
+    assert pool.swap_out([5, 6]) == [(5, kp.LOC_PEER, []), (6, kp.LOC_PEER, [])]
+    before = planes(pool).copy()
+    assert pool.host is None
+    assert pool.reclaim() == [(5, []), (6, [])]                 # no host arena needed for 0 slots
+    assert pool.peer is None and pool.query(5) == (kp.SWAPPED, kp.LOC_HOST, 0, [])
+    assert (pool.prefixes[3].location, pool.prefixes[3].slots) == (kp.LOC_HOST, [])
+    assert pool.swap_in([5]) == [[]]
+    assert pool.query(5) == (kp.RESIDENT, kp.LOC_LOCAL, 0, [])
+    pool.free_prompt(6)
+    assert pool.prefix_load(3, 7) == []
+    pool.prefix_drop(3)
+    assert np.array_equal(planes(pool), before) and pool.free == {2, 3}
+    pool.check_invariants()
+
+
 # ---------------------------------------------------------------- brute force
 class TinyModel:
     """Independent array-scan model of the allocator and slot placement."""
