@@ -8,12 +8,13 @@
  * prompts with the least tokens generated, leftover d slots to the prefill
  * prompts, stop when memory is exhausted; reschedule every k iterations or
  * when a request completes, paging out the prompts not in the next batch and
- * paging in the prompts not on the GPU.  Readings R8-R18:
+ * paging in the prompts not on the GPU.  Readings R8-R18 and R21:
  * ties (arrival, id); memory test ceil((ctx + t) / bs) blocks per prompt
  * summed <= num_blocks; prefill filled before decode; a non-fitting prompt
  * stops its walk; extra reschedule when the plan's next iteration no longer
  * fits or has no work; literal eviction of every resident prompt not in the
- * plan; a preempted prefill keeps its partial KV.
+ * plan; a preempted prefill keeps its partial KV; with no prefill prompt
+ * chosen (p = 0) the spare decode slots walk the prefill prompts (R21).
  * FCFS is the no-preemption baseline.
  *
  * Iteration protocol (the caller owns the KV pool, via libaqua):

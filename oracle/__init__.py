@@ -11,7 +11,7 @@ of the method's arithmetic).
 Plain, slow, obviously-correct Python + NumPy.  Every function cites the
 passage it follows: ``P:n`` = line n of the paper text, ``S:n`` =
 line n of SPEC.md; the paper's section is named beside it.  Where the paper is
-silent, the reading taken is numbered R1..R18 in DESIGN.md ("Readings").
+silent, the reading taken is numbered R1..R21 in DESIGN.md ("Readings").
 
 Modules
   kvpool   -- paged KV pool, block allocator, lender/host arenas, swap_out,

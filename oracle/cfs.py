@@ -21,6 +21,9 @@ This follows those steps in order.  Readings:
        (S:325).
   R12  a prompt that does not fit stops that walk ("stops filling").
   R16  fill order: prefill first, then decode (the paper's sentence order).
+  R21  step 4 with no prompt chosen in step 2 (p = 0): the left-over decode
+       slots walk the prefill prompts as step 2 does ("empty plan
+       only if nothing runnable").
   The count C of step 1 walks prefill-order then decode-order with t = 1
   (each prompt's current KV plus its next token; a prompt with no KV still
   needs one block), stopping at the first that does not fit (R12).
@@ -115,6 +118,23 @@ def plan(rs: List[Req], b: int, NB: int, bs: int) -> Tuple[List[int], List[Tuple
 
     # (4) leftover decode slots -> extra tokens for the chosen prefill prompts
     left = d - len(D)
+    if not chosen and left > 0:
+        # R21: step 2 chose no prompt (p = b - d = 0 once >= b prompts fit),
+        # so "the remaining slots in d are allocated to prompts in p" means
+        # prefill prompts in prefill order, walked as in step 2 with the
+        # left-over slots -- otherwise >= b prefill-phase prompts and too few
+        # decode prompts would get an empty plan (SPEC partition_batch:
+        # "empty plan only if nothing runnable")
+        for r in pre:
+            if left == 0:
+                break
+            alloc = min(left, r.P - r.f)
+            n = need(r, alloc, bs)
+            if used + n > NB:
+                break
+            used += n
+            chosen.append([r, alloc])
+            left -= alloc
     for item in chosen:
         if left == 0:
             break

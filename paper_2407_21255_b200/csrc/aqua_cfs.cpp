@@ -120,6 +120,21 @@ Plan partition(const aqua_cfs* s) {
   }
   // leftover decode slots become extra prefill tokens (R10), still within memory
   int32_t spare = d - static_cast<int32_t>(pl.dec.size());
+  if (chosen.empty()) {
+    // R21: no prompt chosen above (p = b - d = 0 once >= b prompts fit): the
+    // spare decode slots go to prefill prompts in prefill order, walked as
+    // above, so a run set of prefill-phase prompts never gets an empty plan
+    for (const Req* r : pre) {
+      if (spare == 0) break;
+      const int32_t a = std::min(spare, r->P - r->f);
+      const int32_t n = blocks_for(s, *r, a);
+      if (mem + n > NB) break;
+      mem += n;
+      chosen.push_back(r);
+      alloc.push_back(a);
+      spare -= a;
+    }
+  }
   for (size_t i = 0; i < chosen.size() && spare > 0; ++i) {
     const Req* r = chosen[i];
     const int64_t base = mem - blocks_for(s, *r, alloc[i]);

@@ -456,6 +456,61 @@ def test_native_trace_runner_matches_oracle(exchange):
     assert log == o.log
 
 
+# AQUA_TRACE_FUZZ_SEEDS widens this for one-off long runs (profiles/r02_trace_fuzz_long.log)
+@pytest.mark.parametrize("seed", range(int(os.environ.get("AQUA_TRACE_FUZZ_SEEDS", "12"))))
+def test_random_trace_call_logs_match_oracle(seed):
+    """Random bursty traces and engine settings -- pool size, block size,
+    time-slice k, budget b, CFS or FCFS, lender and host capacities down to
+    none (so preemptions overflow to the host or stall), occasionally the
+    elastic reclaim / re-offer -- through the Python driver and the native
+    C++ trace runner, both over the native scheduler and the dry-run library:
+    the whole call log must equal the oracle's sim.run log."""
+    from paper_2407_21255_b200.cfs import run_trace_native
+    rnd = random.Random(seed)
+    bs = rnd.choice([4, 16])
+    maxP, maxO = rnd.choice([(200, 60), (600, 120), (900, 200)])
+    tr = burst_trace(seed=100 + seed, lam0=rnd.choice([1.5, 2.5, 6.0]), n_pre=rnd.randint(1, 25),
+                     burst_mult=rnd.choice([1.0, 2.0, 4.0]), burst_s=rnd.uniform(1.0, 8.0), tail_s=rnd.uniform(0.0, 3.0),
+                     prompt=(maxP // 3, 0.8, 1, maxP), output=(maxO // 4, 0.7, 1, maxO))
+    need = -(-(maxP + maxO) // bs)                     # blocks of the longest request
+    NB = need + rnd.randint(1, 4 * need)
+    k = rnd.choice([1, 2, 3, 8])
+    b = rnd.choice([64, 512])
+    policy = rnd.choice(["cfs", "cfs", "fcfs"])
+    # swap space never runs out (the paper's DRAM fallback is 1.5 TB, P:874; neither side defines a
+    # preemption with nowhere to go): the lender may be small or absent, the host then holds everything
+    total = len(tr) * need
+    lender = rnd.choice([0, NB // 4, NB, total])
+    host = total if lender < total else rnd.choice([0, total])
+    elastic = None
+    if lender and host and policy == "cfs" and rnd.random() < 0.25:
+        elastic = (rnd.uniform(0.2, 4.0), rnd.choice([rnd.uniform(4.0, 9.0), 1e9]))
+    cfg = osim.SimConfig(NB=NB, bs=bs, b=b, k=k, policy=policy, lender_slots=lender, host_slots=host,
+                         elastic=elastic, relend_slots=lender if elastic else 0)
+    o = osim.run(tr, cfg)
+    pol = POLICY_CFS if policy == "cfs" else POLICY_FCFS
+
+    def ctx():
+        c = aqua.Ctx(aqua.DRYRUN, 1, bs, 1, 8, 2, NB, [FAKE])
+        if lender:
+            c.lend(0, FAKE * 2, lender * c.U)
+        if host:
+            c.lend(aqua.HOST, FAKE * 3, host * c.U)
+        return c
+
+    kw = {}
+    if elastic:
+        c0 = ctx()
+        kw["elastic"] = {"t_reclaim": elastic[0], "t_relend": elastic[1], "relend": (0, FAKE * 5, lender * c0.U)}
+        c0.close()
+    log, st = run_trace(tr, ctx(), Scheduler(NB=NB, bs=bs, b=b, k=k, policy=pol), **kw)
+    assert st["iters"] == o.iters, (seed, cfg)
+    assert log == o.log, (seed, cfg)
+    if not elastic:                                    # the native runner has no elastic hooks
+        nlog, nst = run_trace_native(tr, ctx(), Scheduler(NB=NB, bs=bs, b=b, k=k, policy=pol))
+        assert nlog == o.log and nst["iters"] == o.iters, (seed, cfg)
+
+
 def test_create_validates_layout():
     """aqua_create rejects layouts the kernels cannot move exactly (S or a
     stride not a multiple of 16, overlapping chunks, misaligned bases)."""

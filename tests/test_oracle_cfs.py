@@ -81,6 +81,55 @@ def test_spec_degenerate_cases():
     assert cfs.plan(one, 512, 1000, 16) == ([], [(9, 100)])
 
 
+def test_r21_prefill_only_run_set_larger_than_b():
+    """R21: with >= b prompts fitting, d = b and p = 0; without
+    decode prompts the paper's "remaining slots in d are allocated to
+    prompts in p" must still schedule prefill, else the plan is empty and
+    the engine stalls (SPEC partition_batch: "empty plan only if nothing
+    runnable").  Hand-executed: C = 5 prompts fit, d = min(4, 5) = 4,
+    p = 0, D = [], the 4 spare slots walk the prefill order: prompt 0
+    (least f, earliest arrival) takes min(4, 10) = 4 tokens."""
+    rs = [Req(id=i, arrival=float(i), P=10, O=5) for i in range(5)]
+    assert cfs.plan(rs, 4, 100, 16) == ([], [(0, 4)])
+    # spare slots spill over prompts in prefill order: P = 3 each -> 3 + 1
+    rs = [Req(id=i, arrival=float(i), P=3, O=5) for i in range(6)]
+    assert cfs.plan(rs, 4, 100, 16) == ([], [(0, 3), (1, 1)])
+    # two decode prompts and six prefill ones, b = 4: d = 4, D = [10, 11], 2 spare slots -> prefill
+    dec = [Req(id=10 + i, arrival=float(i), P=16, O=9, f=16, g=1, ctx=16, phase=DECODE) for i in range(2)]
+    assert cfs.plan(dec + rs, 4, 100, 16) == ([10, 11], [(0, 2)])
+    # the memory test still applies: one block, a prompt with a 16-token KV cannot add tokens
+    full = [Req(id=0, arrival=0.0, P=40, O=5, f=16, ctx=16)] + [Req(id=i, arrival=float(i), P=40, O=5)
+                                                                  for i in range(1, 4)]
+    assert cfs.plan(full, 2, 2, 16) == ([], [(1, 2)])
+
+
+def test_plan_never_empty_while_a_prompt_fits():
+    """SPEC S:275 as a property over random states: if some runnable prompt's
+    KV plus one token fits the pool alone, the plan schedules something."""
+    import random
+    rnd = random.Random(5)
+    for _ in range(3000):
+        n = rnd.randint(1, 12)
+        bs = rnd.choice([1, 4, 16])
+        rs = []
+        for i in range(n):
+            P, O = rnd.randint(1, 200), rnd.randint(1, 40)
+            if rnd.random() < 0.6:
+                f = rnd.randint(0, P - 1)
+                rs.append(Req(id=i, arrival=float(rnd.randint(0, 4)), P=P, O=O, f=f, ctx=f))
+            else:
+                g = rnd.randint(1, O)
+                rs.append(Req(id=i, arrival=float(rnd.randint(0, 4)), P=P, O=O, f=P, g=g, ctx=P + g - 1,
+                              phase=DECODE))
+        b = rnd.choice([1, 2, 3, 8, 64])
+        NB = rnd.randint(1, 60)
+        D, PF = cfs.plan(rs, b, NB, bs)
+        order = sorted((r for r in rs if r.phase == PREFILL), key=lambda r: (r.f, r.arrival, r.id)) + \
+            sorted((r for r in rs if r.phase == DECODE), key=lambda r: (r.g, r.arrival, r.id))
+        if cfs.need(order[0], 1, bs) <= NB:
+            assert D or PF, (b, NB, bs, rs)
+
+
 def _rotation_windows(n, m, slices):
     q = collections.deque(range(n))
     out = []
