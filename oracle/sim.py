@@ -136,11 +136,11 @@ def run(trace: Sequence[Tuple[int, float, int, int]], cfg: SimConfig,
                 out.append((pid, min(a, r.P - r.f)))
         return out
 
-    def fits(work):
+    def fits(work, leaving=()):
         tok = dict(work)
         tot = 0
         for pid, p in pool.prompts.items():
-            if p.state == RESIDENT:
+            if p.state == RESIDENT and pid not in leaving:
                 tot += cfs.need(run_set[pid], tok.get(pid, 0), lay.bs)
         for pid, tt in work:
             if not resident(pid):
@@ -208,16 +208,21 @@ def run(trace: Sequence[Tuple[int, float, int, int]], cfg: SimConfig,
                 log.append(("swap_in", tuple(page_in), tuple(tuple(x) for x in res)))
             plan = cfs.fcfs_plan([run_set[x] for x in admitted_fcfs], cfg.b)
             work = this_iter_tokens(plan)
-            while work and not fits(work):
-                # overflow after a fallback: preempt the latest-arrived resident
+            leaving = []
+            while work and not fits(work, leaving):
+                # overflow after a fallback: preempt the latest-arrived
+                # resident until the iteration fits; the victims leave in one
+                # call, latest arrival first (R18)
                 victims = [x for x in admitted_fcfs if resident(x)]
                 victim = max(victims, key=lambda x: (run_set[x].arrival, x))
                 admitted_fcfs.remove(victim)
-                res = pool.swap_out([victim])
-                blocks_out += sum(len(s_) for _, _, s_ in res)
-                log.append(("swap_out", (victim,), tuple((loc, tuple(s_)) for _, loc, s_ in res)))
+                leaving.append(victim)
                 plan = cfs.fcfs_plan([run_set[x] for x in admitted_fcfs], cfg.b)
                 work = this_iter_tokens(plan)
+            if leaving:
+                res = pool.swap_out(leaving)
+                blocks_out += sum(len(s_) for _, _, s_ in res)
+                log.append(("swap_out", tuple(leaving), tuple((loc, tuple(s_)) for _, loc, s_ in res)))
             if not work:
                 raise RuntimeError("FCFS: the head-of-line prompt can never fit the pool")
         else:

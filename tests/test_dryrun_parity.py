@@ -457,7 +457,8 @@ def test_native_trace_runner_matches_oracle(exchange):
 
 
 # AQUA_TRACE_FUZZ_SEEDS widens this for one-off long runs (profiles/r02_trace_fuzz_long.log)
-@pytest.mark.parametrize("seed", range(int(os.environ.get("AQUA_TRACE_FUZZ_SEEDS", "12"))))
+# seed 2455: an FCFS fallback that overflows by two residents (R18: one call, latest arrival first)
+@pytest.mark.parametrize("seed", sorted(set(range(int(os.environ.get("AQUA_TRACE_FUZZ_SEEDS", "12")))) | {2455}))
 def test_random_trace_call_logs_match_oracle(seed):
     """Random bursty traces and engine settings -- pool size, block size,
     time-slice k, budget b, CFS or FCFS, lender and host capacities down to
@@ -483,7 +484,7 @@ def test_random_trace_call_logs_match_oracle(seed):
     lender = rnd.choice([0, NB // 4, NB, total])
     host = total if lender < total else rnd.choice([0, total])
     elastic = None
-    if lender and host and policy == "cfs" and rnd.random() < 0.25:
+    if lender and host and rnd.random() < 0.25:
         elastic = (rnd.uniform(0.2, 4.0), rnd.choice([rnd.uniform(4.0, 9.0), 1e9]))
     cfg = osim.SimConfig(NB=NB, bs=bs, b=b, k=k, policy=policy, lender_slots=lender, host_slots=host,
                          elastic=elastic, relend_slots=lender if elastic else 0)
@@ -502,12 +503,17 @@ def test_random_trace_call_logs_match_oracle(seed):
     if elastic:
         c0 = ctx()
         kw["elastic"] = {"t_reclaim": elastic[0], "t_relend": elastic[1], "relend": (0, FAKE * 5, lender * c0.U)}
+        kw["policy_after_relend"] = pol
         c0.close()
+    if rnd.random() < 0.3:                             # reschedules issued as aqua_swap_exchange
+        kw["exchange_stream"] = 0
+        kw["exchange_pieces"] = rnd.choice([1, 3, 16])
     log, st = run_trace(tr, ctx(), Scheduler(NB=NB, bs=bs, b=b, k=k, policy=pol), **kw)
-    assert st["iters"] == o.iters, (seed, cfg)
-    assert log == o.log, (seed, cfg)
+    assert st["iters"] == o.iters, (seed, cfg, kw)
+    assert log == o.log, (seed, cfg, kw)
     if not elastic:                                    # the native runner has no elastic hooks
-        nlog, nst = run_trace_native(tr, ctx(), Scheduler(NB=NB, bs=bs, b=b, k=k, policy=pol))
+        nlog, nst = run_trace_native(tr, ctx(), Scheduler(NB=NB, bs=bs, b=b, k=k, policy=pol),
+                                     swap_stream2=rnd.choice([0, 1]))
         assert nlog == o.log and nst["iters"] == o.iters, (seed, cfg)
 
 
