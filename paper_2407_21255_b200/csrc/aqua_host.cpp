@@ -127,7 +127,8 @@ struct aqua_ctx {
   uint64_t ce_tick[2] = {0, 0};
   bool poisoned = false;
   std::string err;
-  std::vector<int32_t> last_b, last_s, last_l;
+  std::vector<Desc> last_ds;    // the last call's descriptors (aqua_last_descriptors decodes them)
+  int32_t last_mig_dst = -1;    // >= 0: they were a migration to this location
   uint64_t launches = 0;
   // shape of the last copy-kernel launch (aqua_last_launch)
   int32_t last_grid = 0, last_threads = 0, last_stages = 0, last_engine = 0, last_variant = 0;
@@ -511,10 +512,20 @@ aqua_status run_copy(aqua_ctx* c, const std::vector<Desc>& ds, aqua::Dir dir, cu
   // AUTO: images in host DRAM go through the copy engines (full-duplex PCIe,
   // no SMs held for the transfer: profiles/r01_duplex2.jsonl); everything
   // else through the fused TMA kernel
+  // one pass over the descriptors: which arenas the call touches
+  // (for kMig the descriptor's `block` is the source slot, bit 31 = its arena)
+  bool img_all_host = true, img_any_host = false, src_any_gpu = false, each_touches_host = true;
+  for (const Desc& d : ds) {
+    const bool h = d.slot_arena & kArenaBit;
+    const bool src_host = static_cast<uint32_t>(d.block) & kArenaBit;
+    img_all_host = img_all_host && h;
+    img_any_host = img_any_host || h;
+    src_any_gpu = src_any_gpu || !src_host;
+    each_touches_host = each_touches_host && (h || (dir == aqua::kMig && src_host));
+  }
   int engine = c->kernel;
   if (engine == AQUA_KERNEL_AUTO) {
-    bool host_only = dir != aqua::kMig && !dev_desc;
-    for (const Desc& d : ds) host_only = host_only && (d.slot_arena & kArenaBit);
+    const bool host_only = dir != aqua::kMig && !dev_desc && img_all_host;
     engine = host_only ? AQUA_KERNEL_CE_HOST : AQUA_KERNEL_TMA;
   }
   if (dir == aqua::kMig && engine != AQUA_KERNEL_LDST) engine = AQUA_KERNEL_TMA;  // baselines do not migrate
@@ -528,9 +539,7 @@ aqua_status run_copy(aqua_ctx* c, const std::vector<Desc>& ds, aqua::Dir dir, cu
   };
 
   if (engine == AQUA_KERNEL_CE_HOST) {
-    bool all_host = dir != aqua::kMig;
-    for (const Desc& d : ds) all_host = all_host && (d.slot_arena & kArenaBit);
-    if (all_host && !dev_desc) return run_copy_ce_host(c, ds, dir, st, c0, nc);
+    if (dir != aqua::kMig && img_all_host && !dev_desc) return run_copy_ce_host(c, ds, dir, st, c0, nc);
     engine = AQUA_KERNEL_TMA;   // only host images go through the copy engines
   }
   if (engine == AQUA_KERNEL_TMA || engine == AQUA_KERNEL_LDST) {
@@ -584,24 +593,12 @@ aqua_status run_copy(aqua_ctx* c, const std::vector<Desc>& ds, aqua::Dir dir, cu
       const int want = std::max(1, (c->rate_gbps + kSwapGBpsPerSm - 1) / kSwapGBpsPerSm);
       if (cap == 0 || want < cap) cap = std::min(want, c->num_sms);
     }
-    bool all_host = true;
-    for (const Desc& d : ds)
-      all_host = all_host && ((d.slot_arena & kArenaBit) ||
-                              (dir == aqua::kMig && (static_cast<uint32_t>(d.block) & kArenaBit)));
+    const bool all_host = each_touches_host;
     if (all_host && (cap == 0 || cap > kHostCtas)) cap = kHostCtas;
     // A launch that touches a peer lender's arena is NVLink-bound: cap it at
     // peer_ctas (the rest of the SMs stay with decode), and serve it with
     // plain loads/stores if the lend-time probe saw bulk copies misbehave.
-    bool touches_peer = false;
-    if (c->gpu.present && c->gpu.peer)
-      for (const Desc& d : ds) {
-        const bool img_gpu = !(d.slot_arena & kArenaBit);
-        const bool src_gpu = dir == aqua::kMig && !(static_cast<uint32_t>(d.block) & kArenaBit);
-        if (img_gpu || src_gpu) {
-          touches_peer = true;
-          break;
-        }
-      }
+    const bool touches_peer = c->gpu.present && c->gpu.peer && (!img_all_host || (dir == aqua::kMig && src_any_gpu));
     if (touches_peer) {
       if (c->peer_ctas > 0 && (cap == 0 || cap > c->peer_ctas)) cap = c->peer_ctas;
       if ((c->gpu.probe & 6) != 6 && engine == AQUA_KERNEL_TMA) engine = AQUA_KERNEL_LDST;
@@ -617,9 +614,7 @@ aqua_status run_copy(aqua_ctx* c, const std::vector<Desc>& ds, aqua::Dir dir, cu
     bool small_auto = false;
     if (c->kernel == AQUA_KERNEL_AUTO && engine == AQUA_KERNEL_TMA && (cap == 0 || cap >= c->num_sms) &&
         !p.kv_merged && (S_eff == 512 || S_eff == 1024) && dir != aqua::kMig) {
-      bool any_host = false;
-      for (const Desc& d : ds) any_host = any_host || (d.slot_arena & kArenaBit);
-      if (!any_host) engine = AQUA_KERNEL_LDST, small_auto = true;
+      if (!img_any_host) engine = AQUA_KERNEL_LDST, small_auto = true;
     }
     if (engine == AQUA_KERNEL_TMA) {
       // stage = 32 KiB (or the option): one piece of a large chunk, or a
@@ -810,14 +805,8 @@ aqua_status precheck(aqua_ctx* c) {
 }
 
 void set_last(aqua_ctx* c, const std::vector<Desc>& ds) {
-  c->last_b.resize(ds.size());
-  c->last_s.resize(ds.size());
-  c->last_l.resize(ds.size());
-  for (size_t i = 0; i < ds.size(); ++i) {
-    c->last_b[i] = ds[i].block;
-    c->last_s[i] = static_cast<int32_t>(ds[i].slot_arena & ~kArenaBit);
-    c->last_l[i] = (ds[i].slot_arena & kArenaBit) ? AQUA_LOC_HOST : AQUA_LOC_PEER;
-  }
+  c->last_ds.assign(ds.begin(), ds.end());
+  c->last_mig_dst = -1;
 }
 
 Arena* arena_of(aqua_ctx* c, int loc) { return loc == AQUA_LOC_HOST ? &c->host : &c->gpu; }
@@ -832,17 +821,25 @@ aqua_status launch(aqua_ctx* c, const std::vector<Desc>& ds, aqua::Dir dir, cuda
   if (ds.empty()) return AQUA_OK;
   if (c->dry) return record(c, st, ticket);
   DevGuard g(c->device);
+  // the distinct tickets of the sources and destinations, collected in one
+  // pass (a call's blocks and slots mostly share one or two)
   std::vector<uint64_t> ts;
-  ts.reserve(2 * ds.size());
+  uint64_t last = 0;
+  auto note = [&](uint64_t t) {
+    if (t == 0 || t == last) return;
+    last = t;
+    if (std::find(ts.begin(), ts.end(), t) == ts.end()) ts.push_back(t);
+  };
+  const uint64_t* gt = c->gpu.tick.data();
+  const uint64_t* ht = c->host.tick.data();
   for (const Desc& d : ds) {
     if (dir == aqua::kMig) {
       const uint32_t sb = static_cast<uint32_t>(d.block);
-      ts.push_back(arena_of(c, (sb & kArenaBit) ? AQUA_LOC_HOST : AQUA_LOC_PEER)->tick[sb & ~kArenaBit]);
+      note(((sb & kArenaBit) ? ht : gt)[sb & ~kArenaBit]);
     } else {
-      ts.push_back(c->btick[d.block]);
+      note(c->btick[d.block]);
     }
-    ts.push_back(arena_of(c, (d.slot_arena & kArenaBit) ? AQUA_LOC_HOST : AQUA_LOC_PEER)
-                     ->tick[d.slot_arena & ~kArenaBit]);
+    note(((d.slot_arena & kArenaBit) ? ht : gt)[d.slot_arena & ~kArenaBit]);
   }
   if (aqua_status s = wait_all(c, ts, st)) return s;
   return enqueue_copy(c, ds, dir, st, layer_group, group_tickets, ticket);
@@ -1499,14 +1496,8 @@ static aqua_status move_images(aqua_ctx* c, const std::vector<Prompt*>& ps, int3
       ds.push_back(Desc{static_cast<int32_t>(static_cast<uint32_t>(so) | sbit), static_cast<uint32_t>(sn) | dbit});
     }
   }
-  c->last_b.clear();
-  c->last_s.clear();
-  c->last_l.clear();
-  for (const Desc& d : ds) {
-    c->last_b.push_back(static_cast<int32_t>(static_cast<uint32_t>(d.block) & ~kArenaBit));
-    c->last_s.push_back(static_cast<int32_t>(d.slot_arena & ~kArenaBit));
-    c->last_l.push_back(dst);
-  }
+  c->last_ds.assign(ds.begin(), ds.end());
+  c->last_mig_dst = dst;
   uint64_t ticket = 0;
   if (aqua_status s = launch(c, ds, aqua::kMig, st, &ticket)) return s;
   for (size_t i = 0; i < ps.size(); ++i) {
@@ -1917,13 +1908,16 @@ aqua_status aqua_get_option(aqua_ctx* c, int32_t opt, int64_t* v) {
 aqua_status aqua_last_descriptors(aqua_ctx* c, int32_t* blocks, int32_t* slots, int32_t* locs, int64_t cap,
                                   int64_t* n_out) {
   if (!c) return fail(nullptr, AQUA_E_INVAL, "null ctx");
-  const int64_t n = static_cast<int64_t>(c->last_b.size());
+  const int64_t n = static_cast<int64_t>(c->last_ds.size());
   if (n_out) *n_out = n;
   const int64_t m = std::min(n, cap);
+  const bool mig = c->last_mig_dst >= 0;
   for (int64_t i = 0; i < m; ++i) {
-    if (blocks) blocks[i] = c->last_b[i];
-    if (slots) slots[i] = c->last_s[i];
-    if (locs) locs[i] = c->last_l[i];
+    const Desc& d = c->last_ds[i];
+    // a migration's `block` is the source slot (bit 31 = its arena)
+    if (blocks) blocks[i] = mig ? static_cast<int32_t>(static_cast<uint32_t>(d.block) & ~kArenaBit) : d.block;
+    if (slots) slots[i] = static_cast<int32_t>(d.slot_arena & ~kArenaBit);
+    if (locs) locs[i] = mig ? c->last_mig_dst : ((d.slot_arena & kArenaBit) ? AQUA_LOC_HOST : AQUA_LOC_PEER);
   }
   return AQUA_OK;
 }
