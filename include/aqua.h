@@ -105,8 +105,8 @@ enum { AQUA_LOC_LOCAL = 0, AQUA_LOC_PEER = 1, AQUA_LOC_HOST = 2 };
  * (auto | tma | ldst | ce_host) sets a context's initial engine. */
 enum {
   AQUA_KERNEL_AUTO = 0,       /* product default: CE_HOST when every image of the call is in host DRAM; the LDST
-                                 small-chunk kernel for plane-major 512 B and 1 KiB chunks on the whole GPU; else TMA (picked
-                                 from measurements) */
+                                 small-chunk kernel for plane-major 512 B and 1 KiB chunks (capped launches on a peer arena
+                                 excepted); else TMA (picked from measurements) */
   AQUA_KERNEL_TMA = 1,        /* fused gather/scatter, cp.async.bulk smem ring (UBLKCP) */
   AQUA_KERNEL_LDST = 2,       /* fused gather/scatter, 16-byte LDG/STG register path */
   AQUA_BASE_PER_CHUNK = 3,    /* baseline: one cudaMemcpyAsync per chunk (vLLM-style) */
@@ -123,8 +123,8 @@ enum {
   AQUA_OPT_TIMING = 5,        /* 1: each swap also records a start event; aqua_ticket_elapsed gives its device time */
   AQUA_OPT_LDST_VARIANT = 6,  /* LDST engine flavour: 2 (default) grid-stride 4 KiB items, software-pipelined;
                                  3 the small-chunk kernel (chunks of 512 B .. 4 KiB moved whole, several per 4 KiB
-                                 register round; AUTO picks it for plane-major 512 B / 1 KiB chunks on the whole GPU; other
-                                 chunk sizes fall back to 2).  0 and 1 (round-1 experiments) were retired: E_INVAL */
+                                 register round, 2 CTAs of 8 warps per SM, or 16-warp CTAs under a CTA cap; AUTO picks it for
+                                 plane-major 512 B / 1 KiB chunks; other chunk sizes fall back to 2).  0 and 1 (round-1 experiments) were retired: E_INVAL */
   AQUA_OPT_TMA_VARIANT = 7,   /* TMA engine: 0 (default) one ring per CTA driven by one warp; 3 hybrid: the ring
                                  plus 8 warps copying claimed batches through registers.  1 and 2 (warp-specialised,
                                  two rings) reached the same HBM rate in round 1 and were retired: AQUA_E_INVAL */

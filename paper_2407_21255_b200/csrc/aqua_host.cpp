@@ -609,10 +609,14 @@ aqua_status run_copy(aqua_ctx* c, const std::vector<Desc>& ds, aqua::Dir dir, cu
     // r02_small_device.jsonl: 512 B 5.81 / 5.80 TB/s vs 4.61 / 5.11 for the
     // hybrid, 1 KiB 5.99 / 5.98 vs 5.80 / 5.85 for the ring).  Merged K+V
     // chunks of block-major layouts stay on the ring (1 KiB merged: 4.93 vs
-    // 5.31, r02_small_chunks_bm2.jsonl); an SM cap keeps the ring / hybrid
-    // (more per CTA); host images (zero-copy over PCIe) never take it.
+    // 5.31, r02_small_chunks_bm2.jsonl); host images (zero-copy over PCIe)
+    // never take it.  Under an SM cap it runs 16-warp CTAs
+    // (r02_small_caps.jsonl, per 1 GiB call: 512 B 52 vs 42 GB/s of read +
+    // write per SM for the hybrid, 1 KiB 63-66 vs 54-57; from 2 KiB the ring
+    // / hybrid stay ahead) -- except on a peer lender's arena, whose capped
+    // launches keep the ring / hybrid.
     bool small_auto = false;
-    if (c->kernel == AQUA_KERNEL_AUTO && engine == AQUA_KERNEL_TMA && (cap == 0 || cap >= c->num_sms) &&
+    if (c->kernel == AQUA_KERNEL_AUTO && engine == AQUA_KERNEL_TMA && (cap == 0 || cap >= c->num_sms || !touches_peer) &&
         !p.kv_merged && (S_eff == 512 || S_eff == 1024) && dir != aqua::kMig) {
       if (!img_any_host) engine = AQUA_KERNEL_LDST, small_auto = true;
     }

@@ -832,8 +832,8 @@ cudaError_t launch_tma_t(const P& p, Dir dir, int num_sms, int grid_cap, int sta
 // dealt grid-stride (static, like the probe's scattered copy that reaches
 // 6.3 / 6.4 TB/s at 512 B / 1 KiB).  The (descriptor, chunk) of slot 0 is
 // divided out once per round; the other slots step from it.
-template <Dir D, class P>
-__global__ void __launch_bounds__(256) swap_small_kernel(const __grid_constant__ P p) {
+template <Dir D, class P, int NT>
+__global__ void __launch_bounds__(NT) swap_small_kernel(const __grid_constant__ P p) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
@@ -913,15 +913,29 @@ cudaError_t launch_ldst_t(const P& p, Dir dir, int num_sms, int grid_cap, cudaSt
   constexpr int small_cps = 2;
   if (variant == 3) {                    // small chunks: rounds of whole chunks through registers
     const int k = 256 / static_cast<int>(p.S >> 4);
-    const int grid = grid_for<void>((p.nitems + k - 1) / k, 8, num_sms, small_cps, grid_cap);
-    if (dir == kOut)
-      swap_small_kernel<kOut, P><<<grid, 256, 0, s>>>(p);
-    else if (dir == kIn)
-      swap_small_kernel<kIn, P><<<grid, 256, 0, s>>>(p);
-    else
-      swap_small_kernel<kMig, P><<<grid, 256, 0, s>>>(p);
+    const int64_t rounds = (p.nitems + k - 1) / k;
+    // Under an SM cap (fewer CTAs than 2 per SM) each CTA gets the SM's
+    // whole register budget for warps: 16 warps (512 threads at 108
+    // registers) instead of 8, twice the 4 KiB rounds in flight per SM
+    const bool capped = grid_cap > 0 && grid_cap < num_sms * small_cps;
+    const int nt = capped ? 512 : 256;
+    const int grid = grid_for<void>(rounds, nt / 32, num_sms, capped ? 1 : small_cps, grid_cap);
+    if (capped) {
+      if (dir == kOut)
+        swap_small_kernel<kOut, P, 512><<<grid, 512, 0, s>>>(p);
+      else if (dir == kIn)
+        swap_small_kernel<kIn, P, 512><<<grid, 512, 0, s>>>(p);
+      else
+        swap_small_kernel<kMig, P, 512><<<grid, 512, 0, s>>>(p);
+    } else if (dir == kOut) {
+      swap_small_kernel<kOut, P, 256><<<grid, 256, 0, s>>>(p);
+    } else if (dir == kIn) {
+      swap_small_kernel<kIn, P, 256><<<grid, 256, 0, s>>>(p);
+    } else {
+      swap_small_kernel<kMig, P, 256><<<grid, 256, 0, s>>>(p);
+    }
     if (ctas_used) *ctas_used = grid;
-    if (info) *info = LaunchInfo{grid, 256, 0};
+    if (info) *info = LaunchInfo{grid, nt, 0};
     return cudaGetLastError();
   }
   // software pipelined, one 256-thread CTA per SM: 6,624 / 6,572 GB/s on C2

@@ -981,3 +981,37 @@ def ncu_small():
 
 if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "ncu_small":
     ncu_small()
+
+
+def small_caps():
+    """Sub-stage chunks under SM caps: AUTO (the hybrid ring + register warps)
+    vs the small-chunk register kernel (512-thread CTAs when capped), device
+    time per 1 GiB call behind a sleep kernel; S = AQUA_SWEEP_S, caps =
+    AQUA_SWEEP_CAPS."""
+    Ss = [int(x) for x in os.environ.get("AQUA_SWEEP_S", "512,1024,2048,4096,8192").split(",")]
+    caps = [int(x) for x in os.environ.get("AQUA_SWEEP_CAPS", "8,16,32,64,96").split(",")]
+    for S in Ss:
+        L, H, D = 32, 1, S // 32
+        U = 2 * L * S
+        nblk = (1 << 30) // U
+        ctx, layers, arena, _ = setup(L, 16, H, D, 2 * nblk, nblk)
+        s = torch.cuda.Stream()
+        for cap in caps:
+            for eng in ("auto", "small"):
+                ctx.set_option(aqua.OPT_KERNEL, aqua.KERNEL_AUTO if eng == "auto" else aqua.KERNEL_LDST)
+                ctx.set_option(aqua.OPT_LDST_VARIANT, 3 if eng == "small" else 2)
+                ctx.set_option(aqua.OPT_MAX_CTAS, cap)
+                o, i = time_tickets(ctx, 5, s)
+                ll = ctx.last_launch()
+                print(json.dumps({"S": S, "cap": cap, "engine": eng, "kernel": ll["engine"], "variant": ll["variant"],
+                                  "grid": ll["ctas"], "threads": ll["threads_per_cta"],
+                                  "out_GBps_rw": round(2 * nblk * U / o / 1e6, 1),
+                                  "in_GBps_rw": round(2 * nblk * U / i / 1e6, 1),
+                                  "per_sm_rw": round(2 * nblk * U / ((o + i) / 2) / 1e6 / cap, 1)}), flush=True)
+        ctx.close()
+        del layers, arena
+        torch.cuda.empty_cache()
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "small_caps":
+    small_caps()

@@ -756,8 +756,9 @@ def test_auto_policy_launch_shapes():
     """aqua_last_launch reports what AUTO chose: claimed
     2-unit batches with a 4-stage ring at one CTA per SM; static ranges for a
     small call; under an SM cap, static ranges for stage-sized chunks and the
-    hybrid ring + LDST warps for sub-stage chunks; at full grid the batch size
-    by chunk size, and the hybrid for 512 B chunks."""
+    hybrid ring + LDST warps for sub-stage chunks of 2 KiB and up, the
+    small-chunk kernel (16-warp CTAs) for 512 B / 1 KiB; at full grid the batch
+    size by chunk size, and the small-chunk kernel for 512 B / 1 KiB chunks."""
     def ctx_for(L, H, NB, nslots, D=128):
         S = 16 * H * D * 2
         layers = [torch.zeros(2 * NB * S, dtype=torch.uint8, device="cuda") for _ in range(L)]
@@ -816,6 +817,16 @@ def test_auto_policy_launch_shapes():
         assert s["engine"] == engine and s["variant"] == variant, (D, s)
         assert s["ctas"] == (sm if engine == "tma" else 2 * sm) and s["schedule"] == sched, (D, s)
         assert s["threads_per_cta"] == {(0, "tma"): 32, (3, "tma"): 288, (3, "ldst"): 256}[(variant, engine)]
+        c.swap_in([1])
+        # under an SM cap (r02_small_caps.jsonl): 512 B and 1 KiB -> the small-chunk kernel with 16-warp
+        # CTAs, one per allowed SM; 2 KiB -> the hybrid ring + register warps
+        c.set_option(aqua.OPT_MAX_CTAS, 24)
+        c.swap_out([1])
+        s = c.last_launch()
+        if D == 64:
+            assert (s["engine"], s["variant"], s["ctas"], s["threads_per_cta"]) == ("tma", 3, 24, 288), s
+        else:
+            assert (s["engine"], s["variant"], s["ctas"], s["threads_per_cta"]) == ("ldst", 3, 24, 512), s
         c.swap_in([1])
         c.close()
         del keep, arena
