@@ -101,6 +101,7 @@ struct aqua_ctx {
   uint8_t* h_stage = nullptr;
   uint8_t* d_stage = nullptr;
   size_t stage_cap = 0, stage_head = 0;
+  size_t stage_min = size_t(1) << 20;   // smallest staging ring (AQUA_STAGE_MIN_BYTES: a test hook)
   std::deque<StageRegion> stage_live;
   // tickets
   uint64_t next_ticket = 1;
@@ -304,7 +305,7 @@ aqua_status stage_upload(aqua_ctx* c, const void* src, size_t nbytes, cudaStream
     if (c->d_stage) cudaFree(c->d_stage);
     c->h_stage = nullptr;
     c->d_stage = nullptr;
-    size_t cap = std::max<size_t>(len * 2, size_t(1) << 20);
+    size_t cap = std::max<size_t>(len * 2, c->stage_min);
     CK(c, cudaHostAlloc(reinterpret_cast<void**>(&c->h_stage), cap, cudaHostAllocDefault));
     CK(c, cudaMalloc(reinterpret_cast<void**>(&c->d_stage), cap));
     c->stage_cap = cap;
@@ -897,6 +898,8 @@ aqua_status aqua_create(int device, const aqua_kv_layout* lay, aqua_ctx** out) {
   aqua_ctx* c = new aqua_ctx();
   if (const char* pk = std::getenv("AQUA_LDST_PACK")) c->pack_vec = std::atoi(pk);   // tuning experiments
   if (const char* hu = std::getenv("AQUA_HYBRID_LDST_UNITS")) c->hybrid_ldst_units = std::atoi(hu);
+  // a tiny staging ring makes tests wrap and regrow it within a few calls
+  if (const char* sm = std::getenv("AQUA_STAGE_MIN_BYTES")) c->stage_min = std::max<size_t>(256, std::strtoull(sm, nullptr, 10));
   // AQUA_KERNEL=auto|tma|ldst|ce_host overrides the default copy engine
   // (operational escape hatch; aqua_set_option still wins afterwards)
   if (const char* k = std::getenv("AQUA_KERNEL")) {

@@ -552,9 +552,9 @@ def test_host_staging_freed_by_destroy():
     assert free0 - free1 < (256 << 20), (free0, free1)
 
 
-@pytest.mark.parametrize("engine", ["auto", "tma_dyn1", "tma_hybrid"])
+@pytest.mark.parametrize("engine", ["auto", "tma_dyn1", "tma_hybrid", "auto_staged"])
 @pytest.mark.parametrize("seed", list(range(max(3, len(FUZZ_SEEDS)))))
-def test_multistream_fuzz_equals_sequential(seed, engine):
+def test_multistream_fuzz_equals_sequential(seed, engine, monkeypatch):
     """R7 end to end: random library ops (fills, swaps, migrations, prefix
     store/load, frees), each on a random one of three streams, must leave
     exactly the bytes of the oracle's sequential execution -- every reuse
@@ -562,9 +562,15 @@ def test_multistream_fuzz_equals_sequential(seed, engine):
     claimed batches, every reuse of a launch counter pair)."""
     from oracle import pattern as opat
     rnd = random.Random(100 + seed)
+    if engine == "auto_staged":
+        # every call's descriptors through the pinned staging ring, which starts at 256 B so that it wraps
+        # (host-waiting on the regions still in flight on other streams) and regrows within a few calls
+        monkeypatch.setenv("AQUA_STAGE_MIN_BYTES", "256")
     rig = Rig(L=3, bs=16, H=2, D=64, NB=64, lender_slots=24, host_slots=24, seed=seed)
     c, o = rig.ctx, rig.opool
-    if engine != "auto":
+    if engine == "auto_staged":
+        c.set_option(aqua.OPT_INLINE_MAX, 0)
+    elif engine != "auto":
         _engine(c, engine)
     streams = [torch.cuda.Stream() for _ in range(3)]
     ntok = {}
