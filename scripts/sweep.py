@@ -1015,3 +1015,4 @@ def small_caps():
 
 if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "small_caps":
     small_caps()
+
