@@ -435,15 +435,15 @@ def run_ours(args):
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             ctx.swap_out(PIDS, sw)
-            new, _ = ctx.swap_in(PIDS, sw)
+            new, _ = ctx.swap_in(PIDS, sw, as_arrays=True)
             with torch.cuda.stream(swap):
                 if len(new) == 1:
                     bt_np[:] = new[0]
-                    b = new[0][0]
+                    b = int(new[0][0])
                     probe_h[0].copy_(layers[0][b * S0:b * S0 + 16], non_blocking=True)
                 else:
                     bt_np[:] = np.concatenate(new)
-                    idx_np[:] = [ids[0] * (S0 // 16) for ids in new]
+                    idx_np[:] = [int(ids[0]) * (S0 // 16) for ids in new]
                     idx_d.copy_(idx_h, non_blocking=True)
                     probe_h.copy_(rows0.index_select(0, idx_d), non_blocking=True)
                 bt_d.copy_(bt_h, non_blocking=True)

@@ -203,14 +203,16 @@ class Ctx:
             self._cnt_a = self._cnt.ctypes.data
         return self._cnt_a
 
-    def _tables(self, n: int) -> List[List[int]]:
-        """The new block tables of an n-prompt swap-in from the scratch buffers."""
+    def _tables(self, n: int, as_arrays: bool = False):
+        """The new block tables of an n-prompt swap-in from the scratch buffers
+        (lists of ints, or int32 numpy copies with as_arrays)."""
+        conv = np.ndarray.copy if as_arrays else np.ndarray.tolist
         if n == 1:
-            return [self._ids[:int(self._cnt[0])].tolist()]
+            return [conv(self._ids[:int(self._cnt[0])])]
         ids, cnt = self._ids, self._cnt[:n].tolist()
         out, k = [], 0
         for c in cnt:
-            out.append(ids[k:k + c].tolist())
+            out.append(conv(ids[k:k + c]))
             k += c
         return out
 
@@ -244,7 +246,11 @@ class Ctx:
                 n += k.value
         return n
 
-    def swap_in(self, pids: Sequence[int], stream: int = 0, cap: int = -1) -> Tuple[List[List[int]], int]:
+    def swap_in(self, pids: Sequence[int], stream: int = 0, cap: int = -1,
+                as_arrays: bool = False) -> Tuple[list, int]:
+        """-> (the new block table of each pid -- a list of ints, or an int32
+        numpy array with as_arrays, which skips the per-id Python objects --,
+        the ticket)"""
         n = len(pids)
         if cap < 0:
             # the scratch holds NB ids, the most a pool can hand out; a call
@@ -253,7 +259,7 @@ class Ctx:
             st = lib.aqua_swap_in(self.h, n, self._pids_arg(pids), stream or None, self._ids_a, len(self._ids),
                                   self._counts_arg(n), self._tk_a)
             if st == OK:
-                return self._tables(n), self._tk[0]
+                return self._tables(n, as_arrays), self._tk[0]
             if st != E_INVAL or b"out_ids too small" not in (lib.aqua_last_error(self.h) or b""):
                 _check(st, self.h)
             cap = self._cap(pids)
@@ -263,7 +269,8 @@ class Ctx:
                                  counts.ctypes.data, self._tk_a))
         out, k = [], 0
         for i in range(n):
-            out.append(ids[k:k + counts[i]].tolist())
+            seg = ids[k:k + counts[i]]
+            out.append(seg.copy() if as_arrays else seg.tolist())
             k += counts[i]
         return out, self._tk[0]
 

@@ -82,3 +82,21 @@ def test_exchange_through_scratch():
     assert [len(x) for x in tables] == [7] and to > 0 and ti > 0
     assert c.query(1)[0] == aqua.SWAPPED and c.query(2)[0] == aqua.RESIDENT
     c.close()
+
+
+def test_swap_in_as_arrays_equals_lists():
+    import numpy as np
+    res = []
+    for as_arrays in (False, True):
+        c = _ctx(NB=60, slots=60)
+        for p in (1, 2, 3):
+            c.alloc_blocks(p, 3 + p)
+        c.swap_out([1, 2, 3])
+        c.alloc_blocks(9, 5)
+        tables, _ = c.swap_in([3, 1, 2], as_arrays=as_arrays)
+        if as_arrays:
+            assert all(isinstance(t, np.ndarray) and t.dtype == np.int32 for t in tables)
+            tables = [t.tolist() for t in tables]
+        res.append(tables)
+        c.close()
+    assert res[0] == res[1] and [len(t) for t in res[0]] == [6, 4, 5]
