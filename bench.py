@@ -273,8 +273,8 @@ def run_ours(args):
     ctx = aqua.Ctx(local, L, bs, H, D, e, NB, [t.data_ptr() for t in layers])
     if args.engine != "auto":
         ctx.set_option(aqua.OPT_KERNEL, {"tma": aqua.KERNEL_TMA, "ldst": aqua.KERNEL_LDST,
-                                         "per_chunk": aqua.BASE_PER_CHUNK, "gather_temp": aqua.BASE_GATHER_TEMP,
-                                         "batch": aqua.BASE_BATCH}[args.engine])
+                                         "per_chunk": aqua.BASE_PER_CHUNK,
+                                         "gather_temp": aqua.BASE_GATHER_TEMP}[args.engine])
     if args.max_ctas:
         ctx.set_option(aqua.OPT_MAX_CTAS, args.max_ctas)
     if args.piece:
@@ -660,8 +660,7 @@ def host_baselines(ctx_dev, layers, dev, aqua, args):
     res = {}
     for name, eng in (("tma_zero_copy", aqua.KERNEL_TMA), ("ldst_zero_copy", aqua.KERNEL_LDST),
                       ("ce_host_staged", aqua.KERNEL_CE_HOST),
-                      ("per_chunk_memcpy", aqua.BASE_PER_CHUNK), ("gather_temp_memcpy", aqua.BASE_GATHER_TEMP),
-                      ("memcpy_batch", aqua.BASE_BATCH)):
+                      ("per_chunk_memcpy", aqua.BASE_PER_CHUNK), ("gather_temp_memcpy", aqua.BASE_GATHER_TEMP)):
         ctx.set_option(aqua.OPT_KERNEL, eng)
         try:
             ctx.swap_out([9], s.cuda_stream)
@@ -713,7 +712,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="c2")
-    ap.add_argument("--engine", default="auto", choices=["auto", "tma", "ldst", "per_chunk", "gather_temp", "batch"])
+    ap.add_argument("--engine", default="auto", choices=["auto", "tma", "ldst", "per_chunk", "gather_temp"])
     ap.add_argument("--max-ctas", type=int, default=0)
     ap.add_argument("--piece", type=int, default=0)
     ap.add_argument("--inline-max", type=int, default=-1,

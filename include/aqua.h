@@ -100,8 +100,9 @@ enum { AQUA_ST_RESIDENT = 1, AQUA_ST_SWAPPED = 2 };
 enum { AQUA_LOC_LOCAL = 0, AQUA_LOC_PEER = 1, AQUA_LOC_HOST = 2 };
 
 /* Copy engines for aqua_set_option(AQUA_OPT_KERNEL).  AUTO, TMA, LDST and
- * CE_HOST are the product; PER_CHUNK, GATHER_TEMP and BATCH are baselines
- * kept for measurement only.  The environment variable AQUA_KERNEL
+ * CE_HOST are the product; PER_CHUNK and GATHER_TEMP are baselines kept for
+ * measurement only.  Value 5 (a batched-memcpy baseline in round 1) is
+ * retired and rejected with AQUA_E_INVAL.  The environment variable AQUA_KERNEL
  * (auto | tma | ldst | ce_host) sets a context's initial engine. */
 enum {
   AQUA_KERNEL_AUTO = 0,       /* product default: CE_HOST when every image of the call is in host DRAM; the LDST
@@ -111,7 +112,6 @@ enum {
   AQUA_KERNEL_LDST = 2,       /* fused gather/scatter, 16-byte LDG/STG register path */
   AQUA_BASE_PER_CHUNK = 3,    /* baseline: one cudaMemcpyAsync per chunk (vLLM-style) */
   AQUA_BASE_GATHER_TEMP = 4,  /* baseline: the paper's gather-to-temp + one copy */
-  AQUA_BASE_BATCH = 5,        /* baseline: cudaMemcpyBatchAsync over all chunks */
   AQUA_KERNEL_CE_HOST = 6     /* host images via a GPU staging buffer + DMA copy engines (full-duplex PCIe);
                                  GPU-lender images still use the TMA kernel */
 };

@@ -24,7 +24,7 @@ OK, E_INVAL, E_NOBLOCKS, E_NOSPACE, E_STATE, E_CUDA, E_PEER = 0, -1, -2, -3, -4,
 HOST, DRYRUN, MAPPED = -1, -2, -3
 RESIDENT, SWAPPED = 1, 2
 LOC_LOCAL, LOC_PEER, LOC_HOST = 0, 1, 2
-KERNEL_AUTO, KERNEL_TMA, KERNEL_LDST, BASE_PER_CHUNK, BASE_GATHER_TEMP, BASE_BATCH, KERNEL_CE_HOST = 0, 1, 2, 3, 4, 5, 6
+KERNEL_AUTO, KERNEL_TMA, KERNEL_LDST, BASE_PER_CHUNK, BASE_GATHER_TEMP, KERNEL_CE_HOST = 0, 1, 2, 3, 4, 6   # 5 retired
 (OPT_KERNEL, OPT_MAX_CTAS, OPT_TMA_PIECE, OPT_TMA_STAGES, OPT_TIMING, OPT_LDST_VARIANT, OPT_TMA_VARIANT,
  OPT_INLINE_MAX, OPT_TMA_SCHED, OPT_TMA_STATIC_PCT, OPT_RATE_GBPS, OPT_PEER_CTAS,
  OPT_PEER_TEST) = (1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13)

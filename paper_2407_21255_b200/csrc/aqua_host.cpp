@@ -684,24 +684,6 @@ aqua_status run_copy(aqua_ctx* c, const std::vector<Desc>& ds, aqua::Dir dir, cu
       }
     return AQUA_OK;
   }
-  if (engine == AQUA_BASE_BATCH) {
-    const size_t n = ds.size() * nc;
-    std::vector<void*> dsts(n), srcs(n);
-    std::vector<size_t> sizes(n, static_cast<size_t>(c->S));
-    size_t k = 0;
-    for (const Desc& d : ds)
-      for (int cc = c0; cc < c0 + nc; ++cc, ++k) {
-        uint8_t *pool, *img;
-        chunk_ptrs(d, cc, &pool, &img);
-        dsts[k] = dir == aqua::kOut ? img : pool;
-        srcs[k] = dir == aqua::kOut ? pool : img;
-      }
-    cudaMemcpyAttributes attr{};
-    attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-    size_t idx0 = 0, fail_idx = 0;
-    CK(c, cudaMemcpyBatchAsync(dsts.data(), srcs.data(), sizes.data(), n, &attr, &idx0, 1, &fail_idx, st));
-    return AQUA_OK;
-  }
   if (engine == AQUA_BASE_GATHER_TEMP) {
     // The paper's two-step path: gather into a temporary tensor
     // on this GPU, then one large copy per contiguous run of slots.
@@ -1837,7 +1819,7 @@ aqua_status aqua_set_option(aqua_ctx* c, int32_t opt, int64_t v) {
   if (!c) return fail(nullptr, AQUA_E_INVAL, "null ctx");
   switch (opt) {
     case AQUA_OPT_KERNEL:
-      if (v < AQUA_KERNEL_AUTO || v > AQUA_KERNEL_CE_HOST) return fail(c, AQUA_E_INVAL, "kernel");
+      if (v < AQUA_KERNEL_AUTO || v > AQUA_KERNEL_CE_HOST || v == 5) return fail(c, AQUA_E_INVAL, "kernel");
       c->kernel = static_cast<int>(v);
       return AQUA_OK;
     case AQUA_OPT_MAX_CTAS:

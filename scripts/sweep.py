@@ -20,7 +20,7 @@ from paper_2407_21255_b200 import aqua  # noqa: E402
 from workloads import block_permutation  # noqa: E402
 
 ENG = {"tma": aqua.KERNEL_TMA, "ldst": aqua.KERNEL_LDST, "gather_temp": aqua.BASE_GATHER_TEMP,
-       "batch": aqua.BASE_BATCH, "per_chunk": aqua.BASE_PER_CHUNK, "ce_host": aqua.KERNEL_CE_HOST}
+       "per_chunk": aqua.BASE_PER_CHUNK, "ce_host": aqua.KERNEL_CE_HOST}
 
 
 def setup(L, bs, H, D, NB, nblk, host=False, block_major=False):
@@ -89,7 +89,7 @@ def engines():
     nbytes = nblk * U
     grid = [("tma", p, c) for p in (4096, 8192, 16384, 32768) for c in (0, 148, 296, 444)]
     grid += [("ldst", 0, c) for c in (0, 148, 296, 592)]
-    grid += [("gather_temp", 0, 0), ("batch", 0, 0)]
+    grid += [("gather_temp", 0, 0)]
     for eng, piece, ctas in grid:
         ctx.set_option(aqua.OPT_KERNEL, ENG[eng])
         ctx.set_option(aqua.OPT_TMA_PIECE, piece)

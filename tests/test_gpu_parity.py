@@ -24,7 +24,7 @@ from gpu_util import Rig
 pytestmark = pytest.mark.gpu
 GOLD = os.path.join(os.path.dirname(__file__), "golden")
 ENGINES = {"tma": aqua.KERNEL_TMA, "ldst": aqua.KERNEL_LDST, "per_chunk": aqua.BASE_PER_CHUNK,
-           "gather_temp": aqua.BASE_GATHER_TEMP, "batch": aqua.BASE_BATCH, "ce_host": aqua.KERNEL_CE_HOST,
+           "gather_temp": aqua.BASE_GATHER_TEMP, "ce_host": aqua.KERNEL_CE_HOST,
            "tma_dyn": aqua.KERNEL_TMA, "tma_dyn1": aqua.KERNEL_TMA, "tma_static": aqua.KERNEL_TMA,
            "tma_hybrid": aqua.KERNEL_TMA, "ldst_small": aqua.KERNEL_LDST, "auto": aqua.KERNEL_AUTO}
 # the engines and schedules the library can run (round 1's AUTO-unused experiments were retired in round 2)
