@@ -461,3 +461,113 @@ def test_replay_bytes_keeps_every_prompt_closed_form():
 
     sim.replay_bytes(res.log, pool, 3, on_iter=check)
     assert len(checked) == res.iters
+
+
+# ------------------------------------------- pins added by the mutation check
+# Each case below is hand-executed from the paper / SPEC text (expected values
+# derived on paper, not by running the oracle).  They kill the mutants that
+# scripts/oracle_mutants.py found surviving the earlier pins.
+
+def test_step3_decode_walk_stops_at_the_first_prompt_that_does_not_fit():
+    """R12, "Aqua stops filling the batch if the GPU's memory is
+    exhausted".  NB=4, bs=16, b=20.  X prefill (P=40, nothing done); A decode
+    (g=1, ctx=32: needs ceil(33/16)=3 blocks); B decode (g=2, ctx=15: 1 block).
+    Step 1 walks X (1 block), A (3) -> 4 used, B does not fit: C=2, d=2,
+    p=18.  Step 2: X gets 18 tokens = 2 blocks.  Step 3 (least generated
+    first): A needs 3 more -> 5 > 4, the walk stops; B (which would fit) is
+    NOT taken.  Step 4: the 2 unused decode slots go to X: 20 tokens, still
+    2 blocks.  Plan: D = [], prefill [(X, 20)]."""
+    X = Req(0, 0.0, 40, 5, 0, 0, 0, PREFILL)
+    A = Req(1, 1.0, 16, 100, 16, 1, 32, DECODE)
+    B = Req(2, 2.0, 15, 100, 15, 2, 15, DECODE)
+    assert cfs.plan([X, A, B], 20, 4, 16) == ([], [(0, 20)])
+
+
+def test_fcfs_plan_decodes_at_most_b_prompts():
+    """SPEC fcfs_step: one decode token per admitted decode prompt
+    in arrival order, within the batch budget b; nothing left for prefill."""
+    rs = [Req(i, float(i), 8, 100, 8, 1, 8, DECODE) for i in (4, 2, 0, 3, 1)]
+    assert cfs.fcfs_plan(rs, 3) == ([0, 1, 2], [])
+    assert cfs.fcfs_plan(rs, 7) == ([0, 1, 2, 3, 4], [])
+
+
+def test_sim_reschedules_when_a_request_completes():
+    """P:836-837 "Aqua reschedules the batch every k iterations OR WHEN A
+    REQUEST COMPLETES".  Three decode-only prompts already paged out (8 tokens
+    of KV, bs=64: one block each), NB=2, k=1000 (no time-slice reschedule in
+    the horizon).  Prompt 0 has O=3: it is at g=1, decodes at iterations 0 and
+    1 and completes after iteration 1.  The plan made at iteration 0 holds
+    {0, 1} (all g=1, arrival order); at iteration 2 a reschedule must page in
+    prompt 2 (least generated, g=1) beside prompt 1 (g=3)."""
+    tr = [(0, -3.0, 8, 3), (1, -2.0, 8, 10 ** 6), (2, -1.0, 8, 10 ** 6)]
+    r = sim.run(tr, sim.SimConfig(NB=2, bs=64, b=512, k=1000, host_slots=64, max_iters=6), warm=[0, 1, 2])
+    plans = [(e[1], e[2]) for e in r.log if e[0] == "plan"]
+    assert plans == [(0, (0, 1)), (2, (2, 1))]
+    assert ("swap_in", (2,), ((0,),)) in r.log           # block 0, freed by prompt 0
+    iters = {e[1]: tuple(p for p, _, _ in e[2]) for e in r.log if e[0] == "iter"}
+    assert iters == {0: (0, 1), 1: (0, 1), 2: (2, 1), 3: (2, 1), 4: (2, 1), 5: (2, 1)}
+
+
+def test_sim_virtual_clock_closed_form():
+    """S:233 iteration time t = 20 ms + 40 us x tokens; R15 first token at the
+    end of prefill (g = 1), finish when g == O.  One request alone (P=100,
+    O=4, memory ample): iteration 0 prefills 100 tokens (24 ms) -> TTFT
+    0.024 s; then O-1 = 3 decode iterations of one token (20.04 ms each) ->
+    finish 0.024 + 3 x 0.02004 = 0.08412 s, 4 iterations in all."""
+    r = sim.run([(0, 0.0, 100, 4)], sim.SimConfig(NB=1000))
+    assert r.iters == 4
+    assert r.ttft[0] == pytest.approx(0.024, rel=1e-12)
+    assert r.finish[0] == pytest.approx(0.024 + 3 * 0.02004, rel=1e-12)
+
+
+def test_fcfs_admits_while_the_projection_fits_exactly():
+    """S:297-305 "admit ... while the sum of full projections ceil((P+O)/bs)
+    fits NB": two requests of P=16, O=16 (2 blocks each at bs=16) fill NB=4
+    exactly, so both run in iteration 0 (16 prefill tokens each)."""
+    r = sim.run([(0, 0.0, 16, 16), (1, 0.0, 16, 16)], sim.SimConfig(NB=4, bs=16, policy="fcfs"))
+    it0 = next(e for e in r.log if e[0] == "iter")
+    assert it0 == ("iter", 0, ((0, 0, 16), (1, 0, 16)))
+
+
+def test_reoffer_stops_at_the_first_image_that_does_not_fit():
+    """R22 (NEXT-1 re-offer): host images move back in ascending pid
+    WHILE they fit the re-offered lender -- the walk stops at the first that
+    does not (R12's rule applied to the re-offer), it does not skip ahead.
+    Scenario with unequal image sizes where the two readings differ: the host
+    holds pids 3, 4, 5, ... with 6, 11, ... blocks, the re-offer has 12 slots:
+    pid 3 moves (6 <= 12), pid 4 (11 > 6 left) stops the walk, so a later
+    6-block image that would fit stays on the host."""
+    Ps = (40, 200, 40, 40, 120, 40, 40, 40)
+    tr = [(i, 0.01 * i, Ps[i], 300) for i in range(8)]
+    r = sim.run(tr, sim.SimConfig(NB=40, b=64, lender_slots=400, host_slots=2000, elastic=(2.0, 3.0),
+                                  relend_slots=12))
+    kinds = [e[0] for e in r.log]
+    i_rel = kinds.index("relend")
+    host, sizes = {}, {}
+    for e in r.log[:i_rel]:
+        if e[0] == "swap_out":
+            for pid, (loc, sl) in zip(e[1], e[2]):
+                host[pid] = loc == 2
+                sizes[pid] = len(sl)
+        elif e[0] == "reclaim":
+            for pid, sl in e[2]:
+                host[pid] = True
+        elif e[0] == "swap_in":
+            for pid in e[1]:
+                host.pop(pid, None)
+        elif e[0] == "free":
+            host.pop(e[1], None)
+    on_host = sorted(p for p, h in host.items() if h)
+    stop, skip, room_a, room_b = [], [], 12, 12
+    for p in on_host:
+        if sizes[p] <= room_b:
+            skip.append(p)
+            room_b -= sizes[p]
+    for p in on_host:
+        if sizes[p] > room_a:
+            break
+        stop.append(p)
+        room_a -= sizes[p]
+    assert stop != skip, "the scenario must tell the two readings apart"
+    mig = next(e for e in r.log[i_rel:] if e[0] == "migrate")
+    assert list(mig[2]) == stop

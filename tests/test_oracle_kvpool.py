@@ -582,3 +582,44 @@ def test_prefix_cache_bytes():
     with pytest.raises(kp.AquaError) as e:
         pool.prefix_load(42, 200)
     assert e.value.code == kp.E_STATE
+
+
+# ------------------------------------------- pins added by the mutation check
+def test_lend_capacity_is_floor_of_bytes_over_U():
+    """SURVEY 8(b) / include/aqua.h aqua_lend: capacity in slots =
+    floor(bytes / U); a partial slot is not usable."""
+    lay = kp.Layout(L=2, bs=16, H=2, D=64, e=2, NB=8)          # U = 16384
+    pool = kp.Pool(lay)
+    assert pool.lend(kp.LOC_PEER, 3 * lay.U + lay.U // 2) == 3
+    assert pool.lend(kp.LOC_HOST, lay.U - 16) == 0
+    pool.alloc_blocks(1, 1)
+    with pytest.raises(kp.AquaError) as ei:                      # 0 host slots: no room
+        pool.alloc_blocks(2, 4)
+        pool.swap_out([2, 1])
+    assert ei.value.code == kp.E_NOSPACE
+
+
+def test_prefix_store_uses_a_lender_with_exactly_n_free_slots():
+    """R5 for prefixes ("both CFS and prefill caching share the same
+    swap space"): the lender is used when it has n free slots (>= n, not > n)."""
+    lay = kp.Layout(L=1, bs=16, H=1, D=8, e=2, NB=8)
+    pool = kp.Pool(lay)
+    pool.lend(kp.LOC_PEER, 2 * lay.U)
+    pool.lend(kp.LOC_HOST, 8 * lay.U)
+    pool.alloc_blocks(7, 3)
+    assert pool.prefix_store(1, 7, 2) == (kp.LOC_PEER, [0, 1])
+    assert pool.prefix_store(2, 7, 1) == (kp.LOC_HOST, [0])
+
+
+def test_query_reports_slots_of_a_swapped_prompt():
+    """P:855-857 "the serving engine can query AquaLib for the tensor
+    location": a swapped prompt reports (SWAPPED, location, n, its slots)."""
+    lay = kp.Layout(L=1, bs=16, H=1, D=8, e=2, NB=8)
+    pool = kp.Pool(lay)
+    pool.lend(kp.LOC_PEER, 8 * lay.U)
+    pool.alloc_blocks(9, 2)                                      # slots 0, 1 of a different prompt
+    pool.swap_out([9])
+    pool.alloc_blocks(4, 3)
+    assert pool.query(4) == (kp.RESIDENT, kp.LOC_LOCAL, 3, [0, 1, 2])
+    pool.swap_out([4])
+    assert pool.query(4) == (kp.SWAPPED, kp.LOC_PEER, 3, [2, 3, 4])

@@ -1,0 +1,21 @@
+"""The oracle mutation list (scripts/oracle_mutants.py) still applies.
+
+Each mutant is a plausible mistake in oracle/ that some oracle pin must
+catch; the script runs the pins against every mutant (results in
+profiles/r02_oracle_mutants.json).  This fast check only makes sure every
+mutant's text still occurs in the oracle as the list says, so the list
+cannot silently go stale when the oracle changes."""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, os.path.join(ROOT, "scripts"))
+
+import oracle_mutants  # noqa: E402
+
+
+def test_every_mutant_applies_to_the_current_oracle():
+    oracle_mutants.check_all_apply()
+    assert len(oracle_mutants.MUTANTS) >= 60
+    files = {m[1] for m in oracle_mutants.MUTANTS}
+    assert files == {"kvpool.py", "cfs.py", "sim.py", "pattern.py", "bwfit.py"}
