@@ -30,6 +30,11 @@ The driver emits the exact call log the GPU run must reproduce:
   ("reclaim", i, ((pid, slots), ...))   ("relend", i, nslots)
   ("migrate", i, pids, (slots, ...))    ("policy", i, "fcfs"|"cfs")
 
+NEXT-1 elasticity: reclaim moves every lender image
+to DRAM and FCFS takes over; a re-offer moves DRAM images back in ascending
+pid while they fit, stopping at the first that does not (R22), then CFS
+replans.
+
 FCFS (R18; SPEC fcfs_step S:297-305, fallback S:306-313): requests are
 admitted in (arrival, id) order while the sum of their full projections
 ceil((P+O)/bs) fits NB; a swapped prompt is paged in when admitted; the

@@ -1,0 +1,4 @@
+cd $GRAFT_REPO_ROOT
+timeout 3000 python scripts/product_mutants.py run --kind gpu --timeout 600 --out gpurun_out/r02_product_mutants_gpu.json > gpurun_out/r02_product_mutants_gpu.log 2>&1; echo "mutants rc $?"
+tail -14 gpurun_out/r02_product_mutants_gpu.log
+nvidia-smi --query-gpu=name,memory.used --format=csv

@@ -19,3 +19,13 @@ def test_every_mutant_applies_to_the_current_oracle():
     assert len(oracle_mutants.MUTANTS) >= 60
     files = {m[1] for m in oracle_mutants.MUTANTS}
     assert files == {"kvpool.py", "cfs.py", "sim.py", "pattern.py", "bwfit.py"}
+
+
+def test_every_product_mutant_applies_to_the_current_sources():
+    """scripts/product_mutants.py: one-line edits of libaqua's kernels, host
+    library and native scheduler that the parity tests must catch (results
+    in profiles/r02_product_mutants_{cpu,gpu}.json)."""
+    import product_mutants
+    product_mutants.check_all_apply()
+    kinds = {m[3] for m in product_mutants.MUTANTS}
+    assert kinds == {"cpu", "gpu"}
