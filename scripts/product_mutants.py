@@ -83,6 +83,29 @@ MUTANTS = [
     ("alloc_blocks reuses a block without waiting for the swap that read it (A4)", "aqua_host.cpp",
      [("  for (int32_t b : ids) ts.push_back(c->btick[b]);\n  if (aqua_status s = wait_all(c, ts, reinterpret_cast<cudaStream_t>(stream))) return s;",
        "  for (int32_t b : ids) ts.push_back(c->btick[b]);", None)], "gpu"),
+    ("launch: no wait for the last use of the call's blocks and slots (R7)", "aqua_host.cpp",
+     [("  if (aqua_status s = wait_all(c, ts, st)) return s;\n  return enqueue_copy(c, ds, dir, st, layer_group, group_tickets, ticket);",
+       "  return enqueue_copy(c, ds, dir, st, layer_group, group_tickets, ticket);", None)], "gpu"),
+    ("free: the caller's stream is not recorded on the freed blocks (R7)", "aqua_host.cpp",
+     [("      if (aqua_status s = record(c, st, &t)) return s;\n    }\n    for (int32_t b : p.ids) {",
+       "    }\n    for (int32_t b : p.ids) {", None)], "gpu"),
+    ("swap_in: the read slots are not tagged with its ticket (A7)", "aqua_host.cpp",
+     [("    a->free.insert_all(ps[i]->ids.data(), ps[i]->ids.size());\n    uint64_t* st_tick = a->tick.data();\n    for (int32_t s : ps[i]->ids) st_tick[s] = ticket;",
+       "    a->free.insert_all(ps[i]->ids.data(), ps[i]->ids.size());\n    uint64_t* st_tick = a->tick.data();\n    (void)st_tick;", None)], "gpu"),
+    ("copy-engine host path: the last slot of a contiguous run is not copied to DRAM", "aqua_host.cpp",
+     [("          CK(c, cudaMemcpy2DAsync(img, c->U, t, per, per, r, cudaMemcpyDefault, st));",
+       "          CK(c, cudaMemcpy2DAsync(img, c->U, t, per, per, r > 1 ? r - 1 : r, cudaMemcpyDefault, st));", None)], "gpu"),
+    ("copy-engine host path: the staging buffer is reused without waiting for its last user", "aqua_host.cpp",
+     [("  if (aqua_status s = wait_all(c, {c->ce_tick[di]}, st)) return s;   // the buffer's last user\n",
+       "", None)], "gpu"),
+    ("layer-wise swaps: each layer group misses its last chunk", "aqua_host.cpp",
+     [("    if (aqua_status s = run_copy(c, ds, dir, st, &regions, 2 * l0, 2 * (l1 - l0), dd)) return s;",
+       "    if (aqua_status s = run_copy(c, ds, dir, st, &regions, 2 * l0, 2 * (l1 - l0) - 1, dd)) return s;", None)], "gpu"),
+    ("migration kernel: the source image's arena bit is ignored", "aqua_kernels.cu",
+     [("    const uint64_t sbase = (sb >> 31) ? p.arena_base[1] : p.arena_base[0];",
+       "    const uint64_t sbase = p.arena_base[0];", None)], "gpu"),
+    ("migration: the source slots are not tagged with its ticket (R7)", "aqua_host.cpp",
+     [("      as->free.insert(so);\n      as->tick[so] = ticket;", "      as->free.insert(so);", None)], "gpu"),
     # ---- host library: bookkeeping (A1, A2, A5, A7; R4, R5) -- dry-run parity on CPU
     ("placement: lender needs strictly more than n_p free slots (R5)", "aqua_host.cpp",
      [("    if (gpu_left >= np) {", "    if (gpu_left > np) {", None)], "cpu"),
@@ -194,12 +217,16 @@ def main() -> None:
     ap.add_argument("--jobs", type=int, default=min(8, os.cpu_count() or 1))
     ap.add_argument("--timeout", type=int, default=900)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--only", default="", help="comma-separated mutant names (substring match) to run")
     args = ap.parse_args()
     check_all_apply()
     if args.cmd == "check":
         print(f"{len(MUTANTS)} mutants apply")
         return
     sel = [i for i, m in enumerate(MUTANTS) if args.kind in ("all", m[3])]
+    if args.only:
+        keys = [k.strip() for k in args.only.split(",") if k.strip()]
+        sel = [i for i in sel if any(k in MUTANTS[i][0] for k in keys)]
     if args.cmd == "prepare":
         with cf.ThreadPoolExecutor(args.jobs) as ex:
             for d in ex.map(prepare_one, sel):

@@ -229,6 +229,66 @@ def test_adversarial_reuse_on_other_streams():
     rig.assert_bytes_equal("adversarial")
 
 
+@pytest.mark.parametrize("late", ["swap_out", "scribble", "swap_in", "slot_reuse"])
+def test_adversarial_reuse_with_a_delayed_stream(late):
+    """R7 made deterministic: a ~20 ms sleep kernel queued on one stream makes
+    the operation that was ENQUEUED first run LAST unless the library orders
+    the later one after it.  Each case delays one step of a reuse chain:
+      swap_out   -- a swap_out reads blocks that alloc_blocks hands out again
+                    at once and the caller overwrites on another stream (A4);
+      scribble   -- the caller's writes to reused blocks are late; the
+                    swap_in that receives those blocks after aqua_free must
+                    wait for them (free records the caller's stream);
+      swap_in    -- a swap_in reads lender slots that a swap_out on another
+                    stream reuses right after (A7);
+      slot_reuse -- the swap_out into the reused slots is late relative to
+                    nothing (control: must still equal sequential execution).
+    Without the library's waits each case would read or overwrite the wrong
+    bytes; the result must equal the oracle's sequential run."""
+    L, bs, H, D, NB = 4, 16, 8, 128, 64          # S = 32 KiB, U = 256 KiB
+    rig = Rig(L=L, bs=bs, H=H, D=D, NB=NB, lender_slots=32, host_slots=0)
+    c, o = rig.ctx, rig.opool
+    s_swap, s_dec = torch.cuda.Stream(), torch.cuda.Stream()
+    delay = 40_000_000                            # ~20 ms at 1.9 GHz: longer than the host's enqueueing
+    for p in range(4):
+        assert c.alloc_blocks(p, 16, s_dec.cuda_stream) == o.alloc_blocks(p, 16)
+    torch.cuda.synchronize()
+    for rnd in range(3):
+        s_swap.wait_stream(s_dec)
+        if late == "swap_out":
+            with torch.cuda.stream(s_swap):
+                torch.cuda._sleep(delay)
+        c.swap_out([0, 1], s_swap.cuda_stream)
+        o.swap_out([0, 1])
+        ids = c.alloc_blocks(10 + rnd, 32, s_dec.cuda_stream)
+        assert ids == o.alloc_blocks(10 + rnd, 32)
+        with torch.cuda.stream(s_dec):
+            if late == "scribble":
+                torch.cuda._sleep(delay)
+            val = (rnd * 37 + 11) % 256
+            for l in range(L):
+                for kv in (0, 1):
+                    for b in ids:
+                        off = kv * rig.lay.P_kv + b * rig.lay.P_b
+                        rig.layers[l][off:off + rig.lay.S].fill_(val)
+                        o.chunk(l, kv, b)[:] = val
+        c.free(10 + rnd, s_dec.cuda_stream)
+        o.free_prompt(10 + rnd)
+        if late == "swap_in":
+            with torch.cuda.stream(s_swap):
+                torch.cuda._sleep(delay)
+        new, _ = c.swap_in([1, 0], s_swap.cuda_stream)
+        assert new == o.swap_in([1, 0])
+        if late == "slot_reuse":
+            with torch.cuda.stream(s_dec):
+                torch.cuda._sleep(delay)
+        c.swap_out([2], s_dec.cuda_stream)
+        o.swap_out([2])
+        new, _ = c.swap_in([2], s_swap.cuda_stream)
+        assert new == o.swap_in([2])
+    rig.assert_bytes_equal(f"adversarial, late {late}")
+
+
 def test_c2_full_size_sampled_and_restore():
     """BASELINE configs[1] in the bench's launch configuration: one 32K-token
     Llama-3-8B prompt (2048 blocks of U = 2 MiB) on a fragmented block table
@@ -836,3 +896,75 @@ def test_auto_policy_launch_shapes():
         c.swap_in([1])
         c.close()
         del keep, arena
+
+
+@pytest.mark.parametrize("shape", ["s512", "s1k"])
+@pytest.mark.parametrize("ctas", [3, 0])
+def test_hybrid_register_warps_packed_chunks_at_scale(shape, ctas):
+    """The hybrid's register warps pack whole 512 B / 1 KiB chunks into 4 KiB
+    rounds (AUTO runs this for capped launches on a peer arena).  The small
+    random sequences leave those warps little to claim, so this call is big
+    enough (6,000 blocks on a fragmented pool) that they claim most batches;
+    whole pool and arena equal the oracle after swap_out and after swap_in."""
+    L, bs, H, D = SHAPES[shape][:4]
+    NB = 8192
+    rig = Rig(L=L, bs=bs, H=H, D=D, NB=NB, lender_slots=6500, host_slots=0)
+    c, o = rig.ctx, rig.opool
+    _engine(c, "tma_hybrid")
+    c.set_option(aqua.OPT_MAX_CTAS, ctas)
+    perm = block_permutation(NB, NB, seed=29).tolist()
+    _ops(rig, [("adopt", (1, perm[:6000])), ("adopt", (2, perm[6000:6100])), ("out", [1]),
+               ("alloc", (3, 1500)), ("in", [1])])
+
+
+@pytest.mark.parametrize("late", ["migrate", "none"])
+def test_migration_source_slots_reused_on_another_stream(late):
+    """R7 for NEXT-1: a migration reads the image's old slots; they are free
+    the moment aqua_migrate returns, and a swap_out on another stream lands
+    in them (lowest free slots).  With the migration delayed by a ~20 ms sleep
+    on its stream, the swap_out must still wait for it (the freed slots carry
+    the migration's ticket).  Whole buffers must equal the oracle's
+    sequential run."""
+    L, bs, H, D, NB = 4, 16, 8, 128, 64          # U = 256 KiB
+    rig = Rig(L=L, bs=bs, H=H, D=D, NB=NB, lender_slots=24, host_slots=24)
+    c, o = rig.ctx, rig.opool
+    s_mig, s_out = torch.cuda.Stream(), torch.cuda.Stream()
+    for p in range(3):
+        assert c.alloc_blocks(p, 8) == o.alloc_blocks(p, 8)
+    _ops(rig, [("out", [0])])                     # image of 0 on lender slots 0..7
+    torch.cuda.synchronize()
+    if late == "migrate":
+        with torch.cuda.stream(s_mig):
+            torch.cuda._sleep(40_000_000)
+    c.migrate([0], aqua.LOC_HOST, s_mig.cuda_stream)
+    o.migrate([0], kp.LOC_HOST)
+    c.swap_out([1], s_out.cuda_stream)            # -> lender slots 0..7 again
+    o.swap_out([1])
+    rig.assert_bytes_equal(f"migration source reuse, late {late}")
+
+
+@pytest.mark.parametrize("engine", ["auto", "ce_host"])
+def test_copy_engine_staging_shared_by_two_streams(engine):
+    """The copy-engine host path stages every host-bound call through one GPU
+    buffer per direction.  A large swap_out (64 MiB: ~1.2 ms of PCIe DMA out
+    of the buffer) on one stream and a second swap_out right after on another
+    stream: the second call's gather into the buffer must wait until the
+    first call's DMA has read it.  Whole buffers equal the oracle's."""
+    L, bs, H, D, NB = 32, 16, 8, 128, 96         # U = 2 MiB (Llama-3-8B block)
+    rig = Rig(L=L, bs=bs, H=H, D=D, NB=NB, lender_slots=0, host_slots=80)
+    c, o = rig.ctx, rig.opool
+    _engine(c, engine)
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    assert c.alloc_blocks(1, 32) == o.alloc_blocks(1, 32)
+    assert c.alloc_blocks(2, 32) == o.alloc_blocks(2, 32)
+    torch.cuda.synchronize()
+    c.swap_out([1], s1.cuda_stream)
+    o.swap_out([1])
+    c.swap_out([2], s2.cuda_stream)
+    o.swap_out([2])
+    rig.assert_bytes_equal(f"two host swap_outs on two streams, {engine}")
+    new1, _ = c.swap_in([1], s1.cuda_stream)
+    assert new1 == o.swap_in([1])
+    new2, _ = c.swap_in([2], s2.cuda_stream)
+    assert new2 == o.swap_in([2])
+    rig.assert_bytes_equal(f"two host swap_ins on two streams, {engine}")
