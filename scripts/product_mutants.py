@@ -106,6 +106,15 @@ MUTANTS = [
        "    const uint64_t sbase = p.arena_base[0];", None)], "gpu"),
     ("migration: the source slots are not tagged with its ticket (R7)", "aqua_host.cpp",
      [("      as->free.insert(so);\n      as->tick[so] = ticket;", "      as->free.insert(so);", None)], "gpu"),
+    ("exchange: every resume piece waits only for the first preemption piece", "aqua_host.cpp",
+     [("    parts[f == freed_by.end() ? 0 : f->second].push_back(d);", "    parts[0].push_back(d); (void)f;", None)], "gpu"),
+    ("prefix_store: the source blocks are not tagged with its ticket (R7)", "aqua_host.cpp",
+     [("    c->btick[src.ids[j]] = ticket;     // last reader of the prompt's blocks\n", "", None)], "gpu"),
+    ("prefix_load: the image slots are not tagged with its ticket (R7)", "aqua_host.cpp",
+     [("    a->tick[img.ids[j]] = ticket;      // last reader of the image\n", "", None)], "gpu"),
+    ("prefix_store copies the LAST n blocks of the prompt", "aqua_host.cpp",
+     [("    ds.push_back(Desc{src.ids[j], static_cast<uint32_t>(sl) | bit});",
+       "    ds.push_back(Desc{src.ids[src.ids.size() - n + j], static_cast<uint32_t>(sl) | bit});", None)], "gpu"),
     # ---- host library: bookkeeping (A1, A2, A5, A7; R4, R5) -- dry-run parity on CPU
     ("placement: lender needs strictly more than n_p free slots (R5)", "aqua_host.cpp",
      [("    if (gpu_left >= np) {", "    if (gpu_left > np) {", None)], "cpu"),
@@ -133,6 +142,26 @@ MUTANTS = [
      [("    if (!seen.insert(pids[i]).second) return fail(c, AQUA_E_INVAL, \"duplicate pid\");\n  for (int32_t i = 0; i < n; ++i) {\n    auto it = c->prompts.find(pids[i]);\n    if (it == c->prompts.end() || it->second.state != AQUA_ST_RESIDENT)",
        "    seen.insert(pids[i]);\n  for (int32_t i = 0; i < n; ++i) {\n    auto it = c->prompts.find(pids[i]);\n    if (it == c->prompts.end() || it->second.state != AQUA_ST_RESIDENT)",
        None)], "cpu"),
+    ("exchange: the blocks the preemptions free are not counted for the resume (NOBLOCKS)", "aqua_host.cpp",
+     [("  if (need > static_cast<int64_t>(c->free_blocks.size()) + freed)",
+       "  if (need > static_cast<int64_t>(c->free_blocks.size()) + 0 * freed)", None)], "cpu"),
+    ("exchange: resume blocks planned before the preemption frees its blocks", "aqua_host.cpp",
+     [("  // ---- preemption bookkeeping\n  for (int32_t i = 0; i < n_out; ++i) {\n    Arena* a = arena_of(c, loc[i]);\n    for (int32_t sl : slots[i]) a->free.erase(sl);\n    for (int32_t b : po[i]->ids) c->free_blocks.insert(b);\n  }",
+       "  // ---- preemption bookkeeping\n  for (int32_t i = 0; i < n_out; ++i) {\n    Arena* a = arena_of(c, loc[i]);\n    for (int32_t sl : slots[i]) a->free.erase(sl);\n  }", None)], "cpu"),
+    ("migrate: capacity check off by one", "aqua_host.cpp",
+     [("  if (!ad->present || need > ad->free.size()) return fail(c, AQUA_E_NOSPACE, \"dst arena missing or full\");",
+       "  if (!ad->present || need >= ad->free.size()) return fail(c, AQUA_E_NOSPACE, \"dst arena missing or full\");", None)], "cpu"),
+    ("prefix_store: lender needs more than n free slots", "aqua_host.cpp",
+     [("  if (c->gpu.present && c->gpu.free.size() >= n)", "  if (c->gpu.present && c->gpu.free.size() > n)", None)], "cpu"),
+    ("prefix_load: capacity check off by one", "aqua_host.cpp",
+     [("  if (n > c->free_blocks.size()) return fail(c, AQUA_E_NOBLOCKS, \"pool exhausted\");",
+       "  if (n > 0 && n >= c->free_blocks.size()) return fail(c, AQUA_E_NOBLOCKS, \"pool exhausted\");", None)], "cpu"),
+    ("reclaim: host capacity check off by one", "aqua_host.cpp",
+     [("  if (need > 0 && (!c->host.present || need > c->host.free.size()))",
+       "  if (need > 0 && (!c->host.present || need >= c->host.free.size()))", None)], "cpu"),
+    ("reclaim moves cached prefixes before prompts", "aqua_host.cpp",
+     [("  for (uint64_t p : pids) ps.push_back(&c->prompts[p]);\n  for (uint64_t f : fids) ps.push_back(&c->prefixes[f]);",
+       "  for (uint64_t f : fids) ps.push_back(&c->prefixes[f]);\n  for (uint64_t p : pids) ps.push_back(&c->prompts[p]);", None)], "cpu"),
     # ---- native CFS scheduler (aqua_cfs.cpp, A0)
     ("CFS: reschedule every k+1 iterations (P:836)", "aqua_cfs.cpp",
      [("s->iter - s->last >= s->cfg.k", "s->iter - s->last > s->cfg.k", None)], "cpu"),

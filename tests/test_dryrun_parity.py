@@ -196,6 +196,98 @@ def test_random_op_sequences_match_oracle(seed):
             assert (st, loc, ids) == (pr.state, pr.location, pr.blocks if pr.state == kp.RESIDENT else pr.slots)
 
 
+@pytest.mark.parametrize("slack", [0, -1, 1])
+@pytest.mark.parametrize("op", ["out_peer", "out_host", "in", "mig_host", "mig_peer", "pstore", "pload", "xchg"])
+def test_capacity_boundaries_match_oracle(op, slack):
+    """Every capacity check at its boundary: the call needs n blocks / slots
+    and exactly n + slack are free (slack 0 must succeed, -1 must fail with
+    the oracle's code and change nothing, +1 succeeds).  Random sequences
+    rarely land on the exact fit, so each boundary is set up on purpose."""
+    n = 3
+    NB = 16
+    lay = kp.Layout(L=1, bs=16, H=1, D=8, e=2, NB=NB)
+    pool = kp.Pool(lay)
+    c = aqua.Ctx(aqua.DRYRUN, 1, 16, 1, 8, 2, NB, [FAKE])
+    room = n + slack
+
+    def both(o):
+        a, b = _apply(pool, c, o)
+        assert a == b, (op, slack, o, a, b)
+        return a
+
+    def lend(kind, slots):
+        if kind == "peer":
+            pool.lend(kp.LOC_PEER, slots * lay.U)
+            c.lend(0, FAKE * 2, slots * lay.U)
+        else:
+            pool.lend(kp.LOC_HOST, slots * lay.U)
+            c.lend(aqua.HOST, FAKE * 3, slots * lay.U)
+
+    if op in ("out_peer", "out_host"):
+        lend("peer" if op == "out_peer" else "host", room)
+        both(("alloc", (1, n)))
+        r = both(("out", [1]))
+    elif op == "in":
+        lend("peer", 8)
+        both(("alloc", (1, n)))
+        both(("out", [1]))
+        both(("alloc", (2, NB - room)))           # leave exactly `room` free blocks
+        r = both(("in", [1]))
+    elif op in ("mig_host", "mig_peer"):
+        src, dst = ("peer", "host") if op == "mig_host" else ("host", "peer")
+        lend(src, 8)
+        both(("alloc", (1, n)))
+        both(("out", [1]))                       # the only arena so far: the image lands in src
+        lend(dst, room)
+        r = both(("mig", ([1], kp.LOC_HOST if dst == "host" else kp.LOC_PEER)))
+    elif op == "pstore":
+        lend("peer", room)
+        both(("alloc", (1, n)))
+        r = both(("pstore", (7, 1, n)))
+    elif op == "pload":
+        lend("peer", 8)
+        both(("alloc", (1, n)))
+        both(("pstore", (7, 1, n)))
+        both(("alloc", (2, NB - n - room)))
+        r = both(("pload", (7, 3)))
+    else:                                        # exchange: the swap-outs free blocks for the resume
+        lend("peer", 8)
+        both(("alloc", (1, n)))
+        both(("out", [1]))
+        both(("alloc", (2, 2)))
+        both(("alloc", (3, NB - 2 - (room - 2))))  # free blocks = room - 2; prompt 2's 2 come back
+        r = both(("xchg", ([2], [1])))
+    assert (r[0] == "err") == (slack < 0), (op, slack, r)
+    pool.check_invariants()
+
+
+def test_reclaim_order_prompts_then_prefixes_matches_oracle():
+    """P:758-768 reclaim (reading in oracle.kvpool.Pool.reclaim): every image
+    on the lender moves to the host -- prompts in ascending pid, then cached
+    prefixes in ascending id -- into the lowest host slots in that order.
+    Images interleaved on the lender (prefix, prompt, prefix, prompt) so a
+    different order gives different host slots."""
+    NB = 32
+    lay = kp.Layout(L=1, bs=16, H=1, D=8, e=2, NB=NB)
+    pool = kp.Pool(lay)
+    c = aqua.Ctx(aqua.DRYRUN, 1, 16, 1, 8, 2, NB, [FAKE])
+    pool.lend(kp.LOC_PEER, 16 * lay.U)
+    c.lend(0, FAKE * 2, 16 * lay.U)
+    pool.lend(kp.LOC_HOST, 16 * lay.U)
+    c.lend(aqua.HOST, FAKE * 3, 16 * lay.U)
+    ops = [("alloc", (1, 3)), ("alloc", (2, 2)), ("alloc", (3, 4)),
+           ("pstore", (9, 3, 2)), ("out", [2]), ("pstore", (5, 3, 1)), ("out", [1]), ("reclaim", None)]
+    for op in ops:
+        a, b = _apply(pool, c, op)
+        assert a == b, (op, a, b)
+    for p in (1, 2):
+        st, loc, n, ids = c.query(p, with_ids=True)
+        assert (st, loc, ids) == (pool.prompts[p].state, pool.prompts[p].location, pool.prompts[p].slots)
+    for f in (5, 9):
+        assert c.prefix_query(f) == (pool.prefixes[f].location, pool.prefixes[f].slots)
+    assert pool.prompts[1].slots == [0, 1, 2] and pool.prompts[2].slots == [3, 4]
+
+
 def test_zero_block_image_reclaimed_without_host_matches_oracle():
     """The degenerate path the 3000-seed fuzz found in the oracle: 0-block
     images reclaimed with no host arena relocate to the host location; the

@@ -958,13 +958,92 @@ def test_copy_engine_staging_shared_by_two_streams(engine):
     assert c.alloc_blocks(1, 32) == o.alloc_blocks(1, 32)
     assert c.alloc_blocks(2, 32) == o.alloc_blocks(2, 32)
     torch.cuda.synchronize()
+    # the two library calls back to back (the oracle's copies would give the GPU time to finish the first)
     c.swap_out([1], s1.cuda_stream)
-    o.swap_out([1])
     c.swap_out([2], s2.cuda_stream)
+    o.swap_out([1])
     o.swap_out([2])
     rig.assert_bytes_equal(f"two host swap_outs on two streams, {engine}")
     new1, _ = c.swap_in([1], s1.cuda_stream)
-    assert new1 == o.swap_in([1])
     new2, _ = c.swap_in([2], s2.cuda_stream)
+    assert new1 == o.swap_in([1])
     assert new2 == o.swap_in([2])
     rig.assert_bytes_equal(f"two host swap_ins on two streams, {engine}")
+
+
+@pytest.mark.parametrize("late", ["store", "load"])
+def test_prefix_cache_reuse_with_a_delayed_stream(late):
+    """R7 for NEXT-2, made deterministic with a ~20 ms sleep:
+      store -- a delayed prefix_store reads the source prompt's blocks; the
+               prompt is freed and its blocks reallocated and overwritten on
+               another stream right away: the overwrite must wait for the
+               store (the blocks carry its ticket);
+      load  -- a delayed prefix_load reads the cached image; the prefix is
+               dropped and a swap_out on another stream lands in its slots:
+               the swap_out must wait for the load.
+    Whole buffers equal the oracle's sequential run."""
+    L, bs, H, D, NB = 4, 16, 8, 128, 64          # U = 256 KiB
+    rig = Rig(L=L, bs=bs, H=H, D=D, NB=NB, lender_slots=16, host_slots=0)
+    c, o = rig.ctx, rig.opool
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    assert c.alloc_blocks(5, 8) == o.alloc_blocks(5, 8)
+    assert c.alloc_blocks(8, 6) == o.alloc_blocks(8, 6)
+    torch.cuda.synchronize()
+    if late == "store":
+        with torch.cuda.stream(s1):
+            torch.cuda._sleep(40_000_000)
+    c.prefix_store(9, 5, 8, s1.cuda_stream)
+    o.prefix_store(9, 5, 8)
+    if late == "store":
+        c.free(5, s2.cuda_stream)
+        o.free_prompt(5)
+        ids = c.alloc_blocks(6, 8, s2.cuda_stream)
+        assert ids == o.alloc_blocks(6, 8)
+        with torch.cuda.stream(s2):
+            for l in range(L):
+                for kv in (0, 1):
+                    for b in ids:
+                        off = kv * rig.lay.P_kv + b * rig.lay.P_b
+                        rig.layers[l][off:off + rig.lay.S].fill_(0x5A)
+                        o.chunk(l, kv, b)[:] = 0x5A
+        torch.cuda.synchronize()
+        new, _ = c.prefix_load(9, 7)
+        assert new == o.prefix_load(9, 7)
+    else:
+        torch.cuda.synchronize()
+        with torch.cuda.stream(s1):
+            torch.cuda._sleep(40_000_000)
+        new, _ = c.prefix_load(9, 7, s1.cuda_stream)
+        assert new == o.prefix_load(9, 7)
+        c.prefix_drop(9)
+        o.prefix_drop(9)
+        c.swap_out([8], s2.cuda_stream)          # -> the dropped image's slots 0..5
+        o.swap_out([8])
+    rig.assert_bytes_equal(f"prefix reuse, late {late}")
+
+
+def test_exchange_resume_waits_for_the_piece_that_frees_its_blocks():
+    """aqua_swap_exchange pipelines the resume behind the preemption pieces:
+    each resume descriptor waits for the piece that reads the block it
+    reuses.  Deterministic setup: the preempted prompt A (48 x 2 MiB) goes to
+    host DRAM (PCIe: each of the 3 pieces takes ~0.6 ms) while the resumed
+    prompt B comes from the lender (HBM: microseconds); A's block table runs
+    from the highest ids down, so B's fresh blocks (lowest-first) are the
+    ones the LAST piece reads.  Resuming after the first piece only would
+    overwrite them before they reach DRAM.  Whole buffers equal the
+    oracle's swap_out-then-swap_in."""
+    L, bs, H, D, NB = 32, 16, 8, 128, 64         # U = 2 MiB
+    rig = Rig(L=L, bs=bs, H=H, D=D, NB=NB, lender_slots=16, host_slots=48)
+    c, o = rig.ctx, rig.opool
+    assert c.alloc_blocks(2, 16) == o.alloc_blocks(2, 16)      # B: blocks 0..15
+    a_ids = list(range(NB - 1, 15, -1))                          # A: 63 .. 16
+    c.adopt_blocks(1, a_ids)
+    o.adopt_blocks(1, a_ids)
+    _ops(rig, [("out", [2])])                                    # B -> the lender (now full)
+    _ops(rig, [("alloc", (3, 16))])                              # filler: no free block left
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    new, _, _ = c.swap_exchange([1], [2], s1.cuda_stream, s2.cuda_stream, pieces=3)
+    o.swap_out([1])
+    assert new == o.swap_in([2]) == [list(range(16, 32))]
+    assert c.query(1)[1] == aqua.LOC_HOST
+    rig.assert_bytes_equal("exchange, resume into the last piece's blocks")
