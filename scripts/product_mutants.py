@@ -169,6 +169,29 @@ MUTANTS = [
      [("s->iter - s->last >= s->cfg.k || s->finished_prev ||", "s->iter - s->last >= s->cfg.k ||", None)], "cpu"),
     ("CFS step 3: one decode prompt too many", "aqua_cfs.cpp",
      [("    if (static_cast<int32_t>(pl.dec.size()) >= d) break;", "    if (static_cast<int32_t>(pl.dec.size()) > d) break;", None)], "cpu"),
+    ("CFS order: decode prompts by most tokens generated", "aqua_cfs.cpp",
+     [("    if (a->g != b->g) return a->g < b->g;", "    if (a->g != b->g) return a->g > b->g;", None)], "cpu"),
+    ("CFS order: prefill prompts by arrival only", "aqua_cfs.cpp",
+     [("    if (a->f != b->f) return a->f < b->f;\n", "", None)], "cpu"),
+    ("CFS step 1: decode prompts counted before prefill (R16)", "aqua_cfs.cpp",
+     [("    for (const Req* r : pass == 0 ? pre : dec) {", "    for (const Req* r : pass == 0 ? dec : pre) {", None)], "cpu"),
+    ("CFS step 1: d = fit, not min(b, fit)", "aqua_cfs.cpp",
+     [("  const int32_t d = std::min(b, fit);", "  const int32_t d = fit;", None)], "cpu"),
+    ("CFS step 3: a decode prompt that does not fit is skipped (R12)", "aqua_cfs.cpp",
+     [("    const int32_t n = blocks_for(s, *r, 1);\n    if (mem + n > NB) break;\n    mem += n;\n    pl.dec.push_back(r->id);",
+       "    const int32_t n = blocks_for(s, *r, 1);\n    if (mem + n > NB) continue;\n    mem += n;\n    pl.dec.push_back(r->id);", None)], "cpu"),
+    ("CFS R21 branch dropped", "aqua_cfs.cpp",
+     [("  if (chosen.empty()) {", "  if (false) {", None)], "cpu"),
+    ("CFS step 5: extra prefill tokens ignore memory", "aqua_cfs.cpp",
+     [("    if (room_tokens < hi) hi = static_cast<int32_t>(std::max<int64_t>(room_tokens, 0));\n", "", None)], "cpu"),
+    ("FCFS admission off by one (projection must fit NB)", "aqua_cfs.cpp",
+     [("      if (proj + n > s->cfg.num_blocks) break;", "      if (proj + n >= s->cfg.num_blocks) break;", None)], "cpu"),
+    ("FCFS plan: decode list not capped at b", "aqua_cfs.cpp",
+     [("        if (r->phase == AQUA_PHASE_DECODE && static_cast<int32_t>(pl.dec.size()) < s->cfg.batch_tokens)",
+       "        if (r->phase == AQUA_PHASE_DECODE)", None)], "cpu"),
+    ("FCFS overflow evicts the earliest-arrived resident (R18)", "aqua_cfs.cpp",
+     [("        if (r.where == kResident && (!victim || by_arrival(victim, &r))) victim = &r;",
+       "        if (r.where == kResident && (!victim || by_arrival(&r, victim))) victim = &r;", None)], "cpu"),
     ("CFS: a prompt finishes one token late", "aqua_cfs.cpp",
      [("    if (r.phase == AQUA_PHASE_DECODE && r.g >= r.O) fin.push_back(r.id);",
        "    if (r.phase == AQUA_PHASE_DECODE && r.g > r.O) fin.push_back(r.id);", None)], "cpu"),

@@ -376,6 +376,24 @@ def _product_log(trace, NB, lender_slots, host_slots, policy=POLICY_CFS, k=8, b=
 
 
 @pytest.mark.parametrize("policy", ["cfs", "fcfs"])
+def test_more_decoding_prompts_than_the_batch_budget(policy):
+    """b = 4 tokens per iteration and 9 prompts decoding at once (restarted
+    prompts, R19; ample memory): FCFS decodes the 4 earliest arrivals per
+    iteration (SPEC fcfs_step S:297-305), CFS the 4 least served.  The call
+    logs (plans, iterations) equal the oracle's."""
+    tr = [(i, 0.001 * i, 8, 12) for i in range(9)]
+    warm = [i for i, *_ in tr]                   # R19: all nine arrive decoding, images paged out
+    o = osim.run(tr, osim.SimConfig(NB=64, bs=16, b=4, k=3, policy=policy, lender_slots=0, host_slots=64,
+                                    max_iters=40), warm=warm)
+    c = aqua.Ctx(aqua.DRYRUN, 1, 16, 1, 8, 2, 64, [FAKE])
+    c.lend(aqua.HOST, FAKE * 3, 64 * c.U)
+    s = Scheduler(NB=64, bs=16, b=4, k=3, policy=POLICY_CFS if policy == "cfs" else POLICY_FCFS)
+    log, _ = run_trace(tr, c, s, warm=warm, max_iters=40)
+    assert log == o.log
+    assert max(len(e[2]) for e in o.log if e[0] == "iter") == 4
+
+
+@pytest.mark.parametrize("policy", ["cfs", "fcfs"])
 @pytest.mark.parametrize("k", [1, 8])
 def test_small_trace_call_log_matches_oracle(policy, k):
     tr = burst_trace(seed=3, burst_s=8.0, tail_s=3.0, prompt=(300, 0.8, 1, 900), output=(40, 0.7, 1, 200))
