@@ -115,6 +115,17 @@ MUTANTS = [
     ("prefix_store copies the LAST n blocks of the prompt", "aqua_host.cpp",
      [("    ds.push_back(Desc{src.ids[j], static_cast<uint32_t>(sl) | bit});",
        "    ds.push_back(Desc{src.ids[src.ids.size() - n + j], static_cast<uint32_t>(sl) | bit});", None)], "gpu"),
+    ("descriptor ring: a region is rewritten without waiting for its last user", "aqua_host.cpp",
+     [("    const bool overlap = it->off < off + len && off < it->off + it->len;",
+       "    const bool overlap = false && it->off < off + len && off < it->off + it->len;", None)], "gpu"),
+    ("TMA ring: grouped pool-side STORES of a unit swapped pairwise (swap_in)", "aqua_kernels.cu",
+     [("      for (int t = lane; t < k; t += 32) {\n        item_addrs<D>(p, d, su.c + t, 0, src, dst, bytes);\n        bulk_s2g(dst, buf + size_t(t) * bytes, bytes, pol);",
+       "      for (int t = lane; t < k; t += 32) {\n        item_addrs<D>(p, d, su.c + ((t ^ 1) < k ? (t ^ 1) : t), 0, src, dst, bytes);\n        bulk_s2g(dst, buf + size_t(t) * bytes, bytes, pol);", None)], "gpu"),
+    ("small-chunk kernel: next layer's K plane of block 0 read from block 1", "aqua_kernels.cu",
+     [("        pool = reinterpret_cast<uint8_t*>(__ldg(p.layer_base + (p.kv_merged ? c : c >> 1))) + boff;",
+       "        pool = reinterpret_cast<uint8_t*>(__ldg(p.layer_base + (p.kv_merged ? c : c >> 1))) + (boff ? boff : p.P_b);", None)], "gpu"),
+    ("claimed batches: the counter pair is not reset for the next launch", "aqua_kernels.cu",
+     [("    ctr[0] = 0;\n    ctr[1] = 0;", "    ctr[1] = 0;", None)], "gpu"),
     # ---- host library: bookkeeping (A1, A2, A5, A7; R4, R5) -- dry-run parity on CPU
     ("placement: lender needs strictly more than n_p free slots (R5)", "aqua_host.cpp",
      [("    if (gpu_left >= np) {", "    if (gpu_left > np) {", None)], "cpu"),
@@ -284,6 +295,14 @@ def main() -> None:
             for d in ex.map(prepare_one, sel):
                 print("built", d)
         return
+    # the unmutated library must pass the same tests first (else every "kill" is meaningless)
+    for kind in sorted({MUTANTS[i][3] for i in sel}):
+        tests = CPU_TESTS if kind == "cpu" else GPU_TESTS
+        r = subprocess.run([sys.executable, "-m", "pytest", *tests, "-x", "-q", "-p", "no:cacheprovider"],
+                           cwd=ROOT, capture_output=True, text=True, timeout=args.timeout)
+        if r.returncode != 0:
+            raise SystemExit(f"baseline {kind} tests fail on the unmutated library:\n{r.stdout[-3000:]}")
+        print(f"baseline {kind}: {r.stdout.strip().splitlines()[-1]}")
     jobs = args.jobs if args.kind == "cpu" else 1            # one GPU: one mutant at a time
     with cf.ThreadPoolExecutor(jobs) as ex:
         res = list(ex.map(lambda i: run_one(i, args.timeout), sel))

@@ -1047,3 +1047,32 @@ def test_exchange_resume_waits_for_the_piece_that_frees_its_blocks():
     assert new == o.swap_in([2]) == [list(range(16, 32))]
     assert c.query(1)[1] == aqua.LOC_HOST
     rig.assert_bytes_equal("exchange, resume into the last piece's blocks")
+
+
+def test_descriptor_ring_reuse_with_a_delayed_stream(monkeypatch):
+    """Staged descriptors (inline tier off) through a ring of a few regions:
+    a swap_out on a stream held back by a ~20 ms sleep has its descriptor
+    upload still queued when a second call on another stream wraps the ring
+    onto the same region.  The library must wait (host) for the region's
+    last user before rewriting it; otherwise the delayed call would move the
+    second call's blocks.  Whole buffers equal the oracle's."""
+    monkeypatch.setenv("AQUA_STAGE_MIN_BYTES", "256")
+    L, bs, H, D, NB = 2, 16, 2, 64, 64          # S = 4 KiB
+    rig = Rig(L=L, bs=bs, H=H, D=D, NB=NB, lender_slots=64, host_slots=0)
+    c, o = rig.ctx, rig.opool
+    c.set_option(aqua.OPT_INLINE_MAX, 0)
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    perm = block_permutation(NB, NB, seed=5).tolist()
+    for pid in range(4):                          # 16 blocks each: 128 B of descriptors per call
+        ids = perm[16 * pid:16 * (pid + 1)]
+        c.adopt_blocks(pid, ids)
+        o.adopt_blocks(pid, ids)
+    torch.cuda.synchronize()
+    with torch.cuda.stream(s1):
+        torch.cuda._sleep(40_000_000)
+    c.swap_out([0], s1.cuda_stream)               # its upload waits behind the sleep
+    for pid in (1, 2, 3):                         # the ring (256 B: two regions) wraps onto its region
+        c.swap_out([pid], s2.cuda_stream)
+    for pid in range(4):
+        o.swap_out([pid])
+    rig.assert_bytes_equal("staged descriptors, delayed first call")
