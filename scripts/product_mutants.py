@@ -37,10 +37,10 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OUT_DIR = os.path.join(ROOT, "build", "mutants")
 PKG = "paper_2407_21255_b200"
 
-CPU_TESTS = ["tests/test_dryrun_parity.py", "-m", "not gpu"]
+CPU_TESTS = ["tests/test_dryrun_parity.py", "tests/test_multiproc.py", "-m", "not gpu"]
 GPU_TESTS = ["tests/test_gpu_parity.py", "-m", "gpu"]
 
-# (name, file under csrc/, [(old, new, occurrence)], kind)
+# (name, file under csrc/ (or a .py file of the package), [(old, new, occurrence)], kind)
 MUTANTS = [
     # ---- kernels (aqua_kernels.cu): address arithmetic of A3 / A6 (R1, R3)
     ("image side: piece offset dropped", "aqua_kernels.cu",
@@ -173,6 +173,15 @@ MUTANTS = [
     ("reclaim moves cached prefixes before prompts", "aqua_host.cpp",
      [("  for (uint64_t p : pids) ps.push_back(&c->prompts[p]);\n  for (uint64_t f : fids) ps.push_back(&c->prefixes[f]);",
        "  for (uint64_t f : fids) ps.push_back(&c->prefixes[f]);\n  for (uint64_t p : pids) ps.push_back(&c->prompts[p]);", None)], "cpu"),
+    # ---- Python side of the product: pairing and the trace driver
+    ("pairing: maximises the SUM instead of the minimum pair bandwidth", "pairing.py",
+     [("            key = (min(vals) if vals else float(\"inf\"), [-x for x in part])\n            if best_key is None or key > best_key:\n                best, best_key = list(part), key",
+       "            key = (sum(vals) if vals else float(\"inf\"), [-x for x in part])\n            if best_key is None or key > best_key:\n                best, best_key = list(part), key", None)], "cpu"),
+    ("pairing: a pair's bandwidth taken one way only", "pairing.py",
+     [("        vals = [min(bw[b][l], bw[l][b]) for b, l in zip(borrowers, perm)]",
+       "        vals = [bw[b][l] for b, l in zip(borrowers, perm)]", None)], "cpu"),
+    ("driver: the re-offer skips an image that does not fit instead of stopping (R22)", "driver.py",
+     [("                    if k > room:\n                        break", "                    if k > room:\n                        continue", None)], "cpu"),
     # ---- native CFS scheduler (aqua_cfs.cpp, A0)
     ("CFS: reschedule every k+1 iterations (P:836)", "aqua_cfs.cpp",
      [("s->iter - s->last >= s->cfg.k", "s->iter - s->last > s->cfg.k", None)], "cpu"),
@@ -226,9 +235,13 @@ def apply(text: str, edits) -> str:
     return text
 
 
+def _src(root: str, fname: str) -> str:
+    return os.path.join(root, PKG, fname) if fname.endswith(".py") else os.path.join(root, PKG, "csrc", fname)
+
+
 def check_all_apply() -> None:
     for name, fname, edits, _ in MUTANTS:
-        src = open(os.path.join(ROOT, PKG, "csrc", fname)).read()
+        src = open(_src(ROOT, fname)).read()
         assert apply(src, edits) != src, name
 
 
@@ -241,9 +254,12 @@ def prepare_one(i: int) -> str:
     d = _dir(i)
     shutil.rmtree(d, ignore_errors=True)
     ign = shutil.ignore_patterns("__pycache__", "*.so", "*.so.tmp")
-    for sub in (PKG, "include", "oracle", "workloads", "tests"):
+    for sub in (PKG, "include", "oracle", "workloads", "tests", "scripts"):
         shutil.copytree(os.path.join(ROOT, sub), os.path.join(d, sub), ignore=ign)
-    p = os.path.join(d, PKG, "csrc", fname)
+    for f in ("bench.py", "__graft_entry__.py", "MEASURED_PEAKS.json", "BASELINE.json"):
+        if os.path.exists(os.path.join(ROOT, f)):
+            shutil.copy(os.path.join(ROOT, f), os.path.join(d, f))
+    p = _src(d, fname)
     with open(p) as f:
         src = f.read()
     with open(p, "w") as f:
@@ -269,7 +285,7 @@ def run_one(i: int, timeout: int) -> dict:
         killed, first, summary = r.returncode != 0, (failed[0] if failed else None), (out[-1] if out else "")
     except subprocess.TimeoutExpired:
         killed, first, summary = True, None, f"timeout after {timeout} s"
-    return {"mutant": name, "file": f"{PKG}/csrc/{fname}", "kind": kind, "killed": killed,
+    return {"mutant": name, "file": os.path.relpath(_src(ROOT, fname), ROOT), "kind": kind, "killed": killed,
             "first_failing_test": first, "summary": summary, "seconds": round(time.time() - t0, 1)}
 
 

@@ -477,6 +477,25 @@ def test_scheduler_failed_calls_change_nothing():
     assert a.stats()[0] == 0
 
 
+def test_reoffer_with_unequal_images_matches_oracle():
+    """R22 through the product: the driver's re-offer moves host images back
+    in ascending pid while they fit and stops at the first that does not --
+    a scenario (unequal image sizes, 12 re-offered slots) where skipping
+    ahead would move a different set.  Call log equal to the oracle's."""
+    Ps = (40, 200, 40, 40, 120, 40, 40, 40)
+    tr = [(i, 0.01 * i, Ps[i], 300) for i in range(8)]
+    NB, lender, host = 40, 400, 2000
+    o = osim.run(tr, osim.SimConfig(NB=NB, b=64, lender_slots=lender, host_slots=host, elastic=(2.0, 3.0),
+                                    relend_slots=12))
+    c = aqua.Ctx(aqua.DRYRUN, 1, 16, 1, 8, 2, NB, [FAKE])
+    c.lend(0, FAKE * 2, lender * c.U)
+    c.lend(aqua.HOST, FAKE * 3, host * c.U)
+    s = Scheduler(NB=NB, bs=16, b=64, k=8)
+    log, _ = run_trace(tr, c, s, elastic={"t_reclaim": 2.0, "t_relend": 3.0, "relend": (0, FAKE * 5, 12 * c.U)})
+    assert any(e[0] == "migrate" for e in o.log)
+    assert log == o.log
+
+
 @pytest.mark.parametrize("window", [(4.0, 9.0), (2.0, 30.0), (6.0, 6.5)])
 def test_elastic_trace_call_log_matches_oracle(window):
     """NEXT-1 end to end in metadata mode: lender reclaim -> images to DRAM,

@@ -74,6 +74,56 @@ def test_best_matching_from_measured_matrix():
     assert best_matching(bw3) == [2, 1, 0]
 
 
+def _all_matchings(n):
+    """Every perfect matching of range(n) (odd n: one self-paired), as partner lists."""
+    def rec(free, part):
+        if not free:
+            yield list(part)
+            return
+        i, rest = free[0], free[1:]
+        if len(free) % 2 == 1:
+            part[i] = i
+            yield from rec(rest, part)
+        for k, j in enumerate(rest):
+            part[i], part[j] = j, i
+            yield from rec(rest[:k] + rest[k + 1:], part)
+        part[i] = -1
+    yield from rec(list(range(n)), [-1] * n)
+
+
+def test_pairing_objective_is_max_min_of_both_directions():
+    """the pairing maximises the slowest pair's link, a pair's
+    link being the slower of its two directions.  Brute force over every
+    matching / assignment on random ASYMMETRIC matrices; and a case where
+    maximising the total would pick a different matching."""
+    import itertools
+    import random
+    from paper_2407_21255_b200.pairing import best_bipartite, best_matching
+
+    def link(bw, i, j):
+        return min(bw[i][j], bw[j][i])
+
+    # the total (sum) would prefer {0-1, 2-3}: 2 x 200 + 2 x 10 = 420 > 400
+    bw = [[0, 200, 100, 0], [200, 0, 0, 100], [100, 0, 0, 10], [0, 100, 10, 0]]
+    assert best_matching(bw) == [2, 3, 0, 1]
+    for seed in range(20):
+        rnd = random.Random(seed)
+        n = rnd.choice([4, 5, 6])
+        bw = [[0 if i == j else rnd.choice([50.0, 300.0, 500.0, 770.0]) for j in range(n)] for i in range(n)]
+        m = best_matching(bw)
+        got = min((link(bw, i, m[i]) for i in range(n) if m[i] != i), default=float("inf"))
+        want = max(min((link(bw, i, q[i]) for i in range(n) if q[i] != i), default=float("inf"))
+                   for q in _all_matchings(n))
+        assert got == want, (seed, bw, m)
+        if n % 2 == 0:
+            half = n // 2
+            mb = best_bipartite(bw, list(range(half)), list(range(half, n)))
+            got = min(link(bw, b, mb[b]) for b in range(half))
+            want = max(min(link(bw, b, l) for b, l in zip(range(half), p))
+                       for p in itertools.permutations(range(half, n)))
+            assert got == want, (seed, bw, mb)
+
+
 def test_best_bipartite_split_roles():
     """configs[3]'s roles: borrowers 0-3 each page to one of lenders 4-7."""
     import itertools
