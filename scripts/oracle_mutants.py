@@ -107,6 +107,30 @@ MUTANTS = [
      [("if self.peer is not None and len(self.peer.free) >= n:", "if self.peer is not None and len(self.peer.free) > n:", None)]),
     ("query of a swapped prompt reports its (empty) block table", "kvpool.py",
      [("ids = p.blocks if p.state == RESIDENT else p.slots", "ids = p.blocks", None)]),
+    ("Pool accepts S not a multiple of 16 bytes", "kvpool.py",
+     [("        if layout.S % 16 != 0:\n            raise AquaError(E_INVAL, \"S must be a multiple of 16 bytes\")",
+       "        if False:\n            raise AquaError(E_INVAL, \"S must be a multiple of 16 bytes\")", None)]),
+    ("adopt_blocks accepts out-of-range ids", "kvpool.py",
+     [("or any(not (0 <= b < self.lay.NB) for b in ids) \\", "or False \\", None)],
+     "equivalent: an id outside [0, NB) is never in the free set, so the free-and-distinct test that follows "
+     "rejects it with the same code (E_INVAL) and no change"),
+    ("alloc_blocks accepts n < 0", "kvpool.py",
+     [("        if n < 0:\n            raise AquaError(E_INVAL, \"n < 0\")", "        if False:\n            pass", None)]),
+    ("swap_out of a swapped prompt allowed", "kvpool.py",
+     [("            if p is None or p.state != RESIDENT:\n                raise AquaError(E_STATE, f\"pid {pid} not resident\")",
+       "            if p is None:\n                raise AquaError(E_STATE, f\"pid {pid} not resident\")", None)]),
+    ("swap_in of a resident prompt allowed", "kvpool.py",
+     [("            if p is None or p.state != SWAPPED:\n                raise AquaError(E_STATE, f\"pid {pid} not swapped\")",
+       "            if p is None:\n                raise AquaError(E_STATE, f\"pid {pid} not swapped\")", None)]),
+    ("migrate to the arena the image is already in allowed", "kvpool.py",
+     [("if p is None or p.state != SWAPPED or p.location == dst:", "if p is None or p.state != SWAPPED:", None)]),
+    ("prefix_store reuses a prefix id in use", "kvpool.py",
+     [("        if int(fid) in self.prefixes:\n            raise AquaError(E_INVAL, \"prefix id in use\")",
+       "        if False:\n            raise AquaError(E_INVAL, \"prefix id in use\")", None)]),
+    ("prefix_load: capacity check off by one", "kvpool.py",
+     [("        if len(f.slots) > len(self.free):", "        if len(f.slots) >= len(self.free):", None)]),
+    ("reclaim: host capacity check off by one", "kvpool.py",
+     [("if need and (self.host is None or need > len(self.host.free)):", "if need and (self.host is None or need >= len(self.host.free)):", None)]),
     # ---- cfs.py: batch partitioning ---------------
     ("decode order: most tokens generated first (P:833)", "cfs.py",
      [("key=lambda r: (r.g, r.arrival, r.id)", "key=lambda r: (-r.g, r.arrival, r.id)", None)]),
@@ -191,6 +215,13 @@ MUTANTS = [
     ("write_tokens: token row ignores the head count", "pattern.py",
      [("row = i * lay.H * lay.D * 2\n                ch[row:row + lay.H * lay.D * 2] = w.reshape(-1).view(np.uint8)",
        "row = i * lay.D * 2\n                ch[row:row + lay.H * lay.D * 2] = w.reshape(-1).view(np.uint8)", None)]),
+    ("write_token_range: the run of rows in a block starts at the block's row 0", "pattern.py",
+     [("                ch[i * row:(i + n) * row] = w[tt - t0:tt - t0 + n].reshape(-1)",
+       "                ch[0:n * row] = w[tt - t0:tt - t0 + n].reshape(-1)", None)]),
+    ("splitmix64 (scalar): wrong increment", "pattern.py",
+     [("    z = (x + 0x9E3779B97F4A7C15) & M64", "    z = (x + 0x9E3779B97F4A7C16) & M64", None)]),
+    ("token_words keeps the high 16 bits", "pattern.py",
+     [("    return (z & np.uint64(0xFFFF)).astype(np.uint16)", "    return (z >> np.uint64(48)).astype(np.uint16)", None)]),
     # ---- bwfit.py: saturating bandwidth curve -------
     ("B(s) = peak*s/(s+half) with half added twice", "bwfit.py",
      [("return peak * s / (s + half)", "return peak * s / (s + 2 * half)", None)]),

@@ -623,3 +623,29 @@ def test_query_reports_slots_of_a_swapped_prompt():
     assert pool.query(4) == (kp.RESIDENT, kp.LOC_LOCAL, 3, [0, 1, 2])
     pool.swap_out([4])
     assert pool.query(4) == (kp.SWAPPED, kp.LOC_PEER, 3, [2, 3, 4])
+
+
+def test_layout_chunk_must_be_16_byte_multiple():
+    """SURVEY 8(a) A3 / include/aqua.h aqua_create: S = bs*H*D*e must be a
+    multiple of 16 bytes (16-byte vectors and bulk copies); else INVAL."""
+    with pytest.raises(kp.AquaError) as ei:
+        kp.Pool(kp.Layout(L=1, bs=1, H=1, D=3, e=2, NB=4))          # S = 6 B
+    assert ei.value.code == kp.E_INVAL
+    kp.Pool(kp.Layout(L=1, bs=1, H=1, D=8, e=2, NB=4))              # S = 16 B is fine
+
+
+def test_prefix_load_with_exactly_n_free_blocks():
+    """NEXT-2 prefix load needs n free blocks: exactly n is enough (lowest
+    first, R4), n - 1 is NOBLOCKS with nothing changed."""
+    lay = kp.Layout(L=1, bs=16, H=1, D=8, e=2, NB=8)
+    pool = kp.Pool(lay)
+    pool.lend(kp.LOC_PEER, 8 * lay.U)
+    pool.alloc_blocks(1, 3)                                      # blocks 0..2
+    pool.prefix_store(7, 1, 3)
+    pool.alloc_blocks(2, 2)                                      # 3..4: exactly 3 free (5, 6, 7)
+    assert pool.prefix_load(7, 3) == [5, 6, 7]
+    pool.free_prompt(3)
+    pool.alloc_blocks(4, 1)                                      # 5: only 2 free
+    with pytest.raises(kp.AquaError) as ei:
+        pool.prefix_load(7, 5)
+    assert ei.value.code == kp.E_NOBLOCKS and len(pool.free) == 2 and 5 not in pool.prompts
