@@ -101,7 +101,11 @@ struct aqua_ctx {
   uint8_t* h_stage = nullptr;
   uint8_t* d_stage = nullptr;
   size_t stage_cap = 0, stage_head = 0;
-  size_t stage_min = size_t(1) << 20;   // smallest staging ring (AQUA_STAGE_MIN_BYTES: a test hook)
+  // smallest staging ring (AQUA_STAGE_MIN_BYTES: a test hook).  16 MiB holds
+  // the descriptors of 64 calls of 32K blocks, so the host can queue that far
+  // ahead of the GPU: with 1 MiB (4 such calls) back-to-back 512 B-chunk calls
+  // ran at 5.1-5.6 TB/s instead of their 6.07 (profiles/r02_block_order_ring*.jsonl)
+  size_t stage_min = size_t(16) << 20;
   std::deque<StageRegion> stage_live;
   // tickets
   uint64_t next_ticket = 1;
@@ -795,6 +799,11 @@ void set_last(aqua_ctx* c, const std::vector<Desc>& ds) {
   c->last_ds.assign(ds.begin(), ds.end());
   c->last_mig_dst = -1;
 }
+// The same for a caller that no longer needs its descriptors: no copy.
+void set_last(aqua_ctx* c, std::vector<Desc>&& ds) {
+  c->last_ds.swap(ds);
+  c->last_mig_dst = -1;
+}
 
 Arena* arena_of(aqua_ctx* c, int loc) { return loc == AQUA_LOC_HOST ? &c->host : &c->gpu; }
 
@@ -1189,7 +1198,7 @@ static aqua_status swap_out_impl(aqua_ctx* c, int32_t n, const uint64_t* pids, a
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   uint64_t ticket = 0;
   if (aqua_status s = launch(c, ds, aqua::kOut, st, &ticket, layer_group, group_tickets)) return s;
-  set_last(c, ds);
+  set_last(c, std::move(ds));   // ds is not read below
   // commit bookkeeping
   for (int32_t i = 0; i < n; ++i) {
     Arena* a = arena_of(c, loc[i]);
@@ -1245,7 +1254,7 @@ static aqua_status swap_in_impl(aqua_ctx* c, int32_t n, const uint64_t* pids, aq
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   uint64_t ticket = 0;
   if (aqua_status s = launch(c, ds, aqua::kIn, st, &ticket, layer_group, group_tickets)) return s;
-  set_last(c, ds);
+  set_last(c, std::move(ds));   // ds is not read below
   c->free_blocks.erase_lowest(static_cast<int32_t>(need));
   int64_t k = 0;
   for (int32_t i = 0; i < n; ++i) {

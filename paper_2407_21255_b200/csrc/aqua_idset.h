@@ -75,19 +75,24 @@ class IdSet {
     return iterator(this, lo_);
   }
 
-  // Bulk insert / erase of n ids (same semantics as n single calls), with
-  // the counters kept in locals.
+  // Bulk insert / erase of n ids (same semantics as n single calls).  Ids
+  // are taken in runs that fall in one bitmap word (slots and fresh blocks
+  // come sorted, so runs are long): each run is one read-modify-write of its
+  // word and a popcount, not one dependent update per id.
   void insert_all(const int32_t* ids, size_t n) {
     uint64_t* w = w_.data();
     int32_t cnt = count_, lo = lo_;
-    for (size_t i = 0; i < n; ++i) {
-      const int32_t id = ids[i];
-      uint64_t& x = w[id >> 6];
-      const uint64_t b = uint64_t(1) << (id & 63);
-      if (!(x & b)) {
-        x |= b;
-        ++cnt;
-        if ((id >> 6) < lo) lo = id >> 6;
+    size_t i = 0;
+    while (i < n) {
+      const int32_t wd = ids[i] >> 6;
+      uint64_t m = 0;
+      do m |= uint64_t(1) << (ids[i] & 63);
+      while (++i < n && (ids[i] >> 6) == wd);
+      const uint64_t add = m & ~w[wd];
+      if (add) {
+        w[wd] |= add;
+        cnt += __builtin_popcountll(add);
+        if (wd < lo) lo = wd;
       }
     }
     count_ = cnt;
@@ -96,14 +101,15 @@ class IdSet {
   void erase_all(const int32_t* ids, size_t n) {
     uint64_t* w = w_.data();
     int32_t cnt = count_;
-    for (size_t i = 0; i < n; ++i) {
-      const int32_t id = ids[i];
-      uint64_t& x = w[id >> 6];
-      const uint64_t b = uint64_t(1) << (id & 63);
-      if (x & b) {
-        x &= ~b;
-        --cnt;
-      }
+    size_t i = 0;
+    while (i < n) {
+      const int32_t wd = ids[i] >> 6;
+      uint64_t m = 0;
+      do m |= uint64_t(1) << (ids[i] & 63);
+      while (++i < n && (ids[i] >> 6) == wd);
+      const uint64_t del = m & w[wd];
+      w[wd] &= ~del;
+      cnt -= __builtin_popcountll(del);
     }
     count_ = cnt;
   }
@@ -147,12 +153,19 @@ class IdSet {
     const int32_t nw = static_cast<int32_t>(w_.size());
     while (k > 0 && lo_ < nw) {
       uint64_t& x = w_[lo_];
-      while (x && k > 0) {
-        x &= x - 1;
-        --k;
-        --count_;
+      const int32_t pc = __builtin_popcountll(x);
+      if (pc <= k) {                 // the whole word goes
+        x = 0;
+        k -= pc;
+        count_ -= pc;
+        ++lo_;
+      } else {                       // the lowest k bits of this word
+        count_ -= k;
+        while (k > 0) {
+          x &= x - 1;
+          --k;
+        }
       }
-      if (!x) ++lo_;
     }
   }
 

@@ -37,7 +37,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OUT_DIR = os.path.join(ROOT, "build", "mutants")
 PKG = "paper_2407_21255_b200"
 
-CPU_TESTS = ["tests/test_dryrun_parity.py", "tests/test_multiproc.py", "-m", "not gpu"]
+CPU_TESTS = ["tests/test_dryrun_parity.py", "tests/test_multiproc.py", "tests/test_idset.py", "-m", "not gpu"]
 GPU_TESTS = ["tests/test_gpu_parity.py", "-m", "gpu"]
 
 # (name, file under csrc/ (or a .py file of the package), [(old, new, occurrence)], kind)
@@ -182,6 +182,13 @@ MUTANTS = [
        "        vals = [bw[b][l] for b, l in zip(borrowers, perm)]", None)], "cpu"),
     ("driver: the re-offer skips an image that does not fit instead of stopping (R22)", "driver.py",
      [("                    if k > room:\n                        break", "                    if k > room:\n                        continue", None)], "cpu"),
+    ("free-id bitmap: a bulk insert does not lower the scan start (lowest-first lost)", "aqua_idset.h",
+     [("        cnt += __builtin_popcountll(add);\n        if (wd < lo) lo = wd;", "        cnt += __builtin_popcountll(add);", None)], "cpu"),
+    ("free-id bitmap: a bulk erase counts every id, present or not", "aqua_idset.h",
+     [("      const uint64_t del = m & w[wd];\n      w[wd] &= ~del;\n      cnt -= __builtin_popcountll(del);",
+       "      const uint64_t del = m & w[wd];\n      w[wd] &= ~del;\n      cnt -= __builtin_popcountll(m);", None)], "cpu"),
+    ("free-id bitmap: erase_lowest takes a whole word when fewer bits are wanted", "aqua_idset.h",
+     [("      if (pc <= k) {                 // the whole word goes", "      if (pc <= k + 1) {             // the whole word goes", None)], "cpu"),
     # ---- native CFS scheduler (aqua_cfs.cpp, A0)
     ("CFS: reschedule every k+1 iterations (P:836)", "aqua_cfs.cpp",
      [("s->iter - s->last >= s->cfg.k", "s->iter - s->last > s->cfg.k", None)], "cpu"),

@@ -1016,3 +1016,44 @@ def small_caps():
 if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "small_caps":
     small_caps()
 
+
+
+def block_order():
+    """Does the order / locality of a prompt's blocks in the pool change the
+    copy rate of small chunks?  One prompt of 1 GiB (plane-major, S =
+    AQUA_SWEEP_S), AUTO, three block tables over the same pool: a random half
+    of the blocks in random order (the sweeps' default: a fragmented pool),
+    the same blocks sorted ascending, and one contiguous run.  Back-to-back
+    (queued) and per-call (behind a sleep) device time."""
+    Ss = [int(x) for x in os.environ.get("AQUA_SWEEP_S", "512,1024,2048,8192,32768").split(",")]
+    for S in Ss:
+        L = 32
+        H, D = (1, S // 32) if S <= 4096 else (S // 4096, 128)
+        U = 2 * L * S
+        nblk = (1 << 30) // U
+        NB = 2 * nblk
+        layers = [torch.zeros(2 * NB * S, dtype=torch.uint8, device="cuda") for _ in range(L)]
+        arena = torch.empty(nblk * U, dtype=torch.uint8, device="cuda")
+        perm = block_permutation(NB, NB, seed=2).tolist()
+        tables = {"random_half_random_order": perm[:nblk], "random_half_sorted": sorted(perm[:nblk]),
+                  "contiguous": list(range(nblk))}
+        s = torch.cuda.Stream()
+        for name, bt in tables.items():
+            ctx = aqua.Ctx(0, L, 16, H, D, 2, NB, [t.data_ptr() for t in layers])
+            ctx.lend(0, arena.data_ptr(), nblk * U)
+            rest = sorted(set(range(NB)) - set(bt))
+            ctx.adopt_blocks(1, rest)
+            ctx.adopt_blocks(7, bt)
+            pair = time_queued(ctx, s, K=10, reps=3)
+            o, i = time_tickets(ctx, 5, s)
+            print(json.dumps({"S": S, "blocks": name, "nblk": nblk, "engine": ctx.last_launch()["engine"],
+                              "queued_TBps_rw": round(4 * nblk * U / pair / 1e9, 3),
+                              "per_call_out_TBps_rw": round(2 * nblk * U / o / 1e9, 3),
+                              "per_call_in_TBps_rw": round(2 * nblk * U / i / 1e9, 3)}), flush=True)
+            ctx.close()
+        del layers, arena
+        torch.cuda.empty_cache()
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "block_order":
+    block_order()
