@@ -34,7 +34,7 @@ import sys
 import time
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-OUT_DIR = os.path.join(ROOT, "build", "mutants")
+OUT_DIR = os.environ.get("AQUA_MUTANT_DIR", os.path.join(ROOT, "build", "mutants"))
 PKG = "paper_2407_21255_b200"
 
 CPU_TESTS = ["tests/test_dryrun_parity.py", "tests/test_multiproc.py", "tests/test_idset.py", "-m", "not gpu"]
