@@ -29,3 +29,16 @@ def test_every_product_mutant_applies_to_the_current_sources():
     product_mutants.check_all_apply()
     kinds = {m[3] for m in product_mutants.MUTANTS}
     assert kinds == {"cpu", "gpu"}
+
+
+def test_a_sample_of_oracle_mutants_is_killed():
+    """Run four mutants for real (one per oracle module with arithmetic):
+    each must fail an oracle pin.  The whole list runs with
+    `python scripts/oracle_mutants.py` (results in profiles/)."""
+    names = {"U counts K or V only (U = L*S)", "decode order: most tokens generated first (P:833)",
+             "reschedule every k+1 iterations (P:836)", "splitmix64 (vectorised): wrong second shift"}
+    idx = [i for i, m in enumerate(oracle_mutants.MUTANTS) if m[0] in names]
+    assert len(idx) == len(names)
+    for i in idx:
+        r = oracle_mutants.run_one(i)
+        assert r["killed"], r
