@@ -34,11 +34,11 @@ import sys
 import time
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-OUT_DIR = os.environ.get("AQUA_MUTANT_DIR", os.path.join(ROOT, "build", "mutants"))
+OUT_DIR = os.environ.get("AQUA_MUTANT_DIR") or os.path.join(ROOT, "build", "mutants")
 PKG = "paper_2407_21255_b200"
 
 CPU_TESTS = ["tests/test_dryrun_parity.py", "tests/test_multiproc.py", "tests/test_idset.py", "-m", "not gpu"]
-GPU_TESTS = ["tests/test_gpu_parity.py", "-m", "gpu"]
+GPU_TESTS = ["tests/test_gpu_parity.py", "tests/test_gpu_peer.py", "-m", "gpu"]
 
 # (name, file under csrc/ (or a .py file of the package), [(old, new, occurrence)], kind)
 MUTANTS = [
@@ -126,6 +126,16 @@ MUTANTS = [
        "        pool = reinterpret_cast<uint8_t*>(__ldg(p.layer_base + (p.kv_merged ? c : c >> 1))) + (boff ? boff : p.P_b);", None)], "gpu"),
     ("claimed batches: the counter pair is not reset for the next launch", "aqua_kernels.cu",
      [("    ctr[0] = 0;\n    ctr[1] = 0;", "    ctr[1] = 0;", None)], "gpu"),
+    # ---- AUTO launch policy (DESIGN 5.1, section 8 peer cap, NEXT-4 rate budget): shapes, not bytes
+    ("AUTO: a launch touching a peer arena is not capped at AQUA_OPT_PEER_CTAS", "aqua_host.cpp",
+     [("      if (c->peer_ctas > 0 && (cap == 0 || cap > c->peer_ctas)) cap = c->peer_ctas;\n", "", None)], "gpu"),
+    ("AUTO: a peer arena whose bulk-copy probe failed still gets the TMA engine (R20)", "aqua_host.cpp",
+     [("      if ((c->gpu.probe & 6) != 6 && engine == AQUA_KERNEL_TMA) engine = AQUA_KERNEL_LDST;\n", "", None)], "gpu"),
+    ("AUTO: the paging budget maps to one SM too few (rounds down)", "aqua_host.cpp",
+     [("      const int want = std::max(1, (c->rate_gbps + kSwapGBpsPerSm - 1) / kSwapGBpsPerSm);",
+       "      const int want = std::max(1, c->rate_gbps / kSwapGBpsPerSm);", None)], "gpu"),
+    ("AUTO: host-only launches are not capped (PCIe-bound)", "aqua_host.cpp",
+     [("    if (all_host && (cap == 0 || cap > kHostCtas)) cap = kHostCtas;\n", "", None)], "gpu"),
     # ---- host library: bookkeeping (A1, A2, A5, A7; R4, R5) -- dry-run parity on CPU
     ("placement: lender needs strictly more than n_p free slots (R5)", "aqua_host.cpp",
      [("    if (gpu_left >= np) {", "    if (gpu_left > np) {", None)], "cpu"),

@@ -1076,3 +1076,21 @@ def test_descriptor_ring_reuse_with_a_delayed_stream(monkeypatch):
     for pid in range(4):
         o.swap_out([pid])
     rig.assert_bytes_equal("staged descriptors, delayed first call")
+
+
+@pytest.mark.parametrize("engine", ["tma", "ldst"])
+def test_zero_copy_host_launches_are_capped(engine):
+    """A zero-copy swap whose images all live in pinned host DRAM is bound by
+    PCIe (~55 GB/s), which 8 CTAs saturate; AUTO's policy caps such launches
+    at 8 CTAs and leaves the other SMs to decode (DESIGN 5.1).  A launch that
+    also touches HBM images is not capped."""
+    rig = Rig(L=4, bs=16, H=8, D=128, NB=64, lender_slots=8, host_slots=40)
+    c, o = rig.ctx, rig.opool
+    _engine(c, engine)
+    _ops(rig, [("alloc", (1, 8)), ("alloc", (2, 20)), ("out", [1]), ("out", [2])])   # 1 -> lender, 2 -> host
+    assert c.query(2)[1] == aqua.LOC_HOST
+    assert c.last_launch()["ctas"] <= 16                       # host-only launch: 8 CTAs (LDST: 2 x 8)
+    _ops(rig, [("in", [2])])
+    assert c.last_launch()["ctas"] <= 16
+    _ops(rig, [("in", [1])])
+    assert c.last_launch()["ctas"] > 16                        # lender images: the whole GPU
