@@ -807,7 +807,6 @@ void set_last(aqua_ctx* c, std::vector<Desc>&& ds) {
 
 Arena* arena_of(aqua_ctx* c, int loc) { return loc == AQUA_LOC_HOST ? &c->host : &c->gpu; }
 
-}
 // Orders `st` after the last library use of every block and slot the
 // descriptors touch (R7), then enqueues the copy; a dry context only draws a
 // ticket.  For kMig the descriptor's `block` field is the source slot.
@@ -841,7 +840,7 @@ aqua_status launch(aqua_ctx* c, const std::vector<Desc>& ds, aqua::Dir dir, cuda
   return enqueue_copy(c, ds, dir, st, layer_group, group_tickets, ticket);
 }
 
-  // namespace
+}  // namespace
 
 extern "C" {
 
