@@ -1094,3 +1094,53 @@ def test_zero_copy_host_launches_are_capped(engine):
     assert c.last_launch()["ctas"] <= 16
     _ops(rig, [("in", [1])])
     assert c.last_launch()["ctas"] > 16                        # lender images: the whole GPU
+
+
+@pytest.mark.parametrize("engine", ["auto", "tma", "tma_hybrid", "ldst", "ldst_small"])
+def test_degenerate_and_maximum_calls_bytes(engine):
+    """The method's degenerate and maximum cases in one context, whole pool
+    and both arenas compared with the oracle after every call (R4, R5):
+    empty calls; a prompt that owns no block; the whole pool paged out in ONE
+    call into a lender with exactly NB slots; the next whole-pool prompt
+    falling back to a host arena of exactly NB slots (lender full); a prompt
+    that fits nowhere (NOSPACE); resumes needing one block more than is free
+    (NOBLOCKS) and then exactly every free block.  A failed call must leave
+    every byte and the bookkeeping as they were, with the oracle's code."""
+    NB = 24
+    rig = Rig(L=3, bs=16, H=1, D=32, NB=NB, lender_slots=NB, host_slots=NB, seed=7)   # S = 1 KiB, U = 6 KiB
+    _engine(rig.ctx, engine)
+    c, o = rig.ctx, rig.opool
+
+    def fails(name, arg, code):
+        with pytest.raises(kp.AquaError) as eo:
+            {"alloc": lambda: o.alloc_blocks(*arg), "out": lambda: o.swap_out(arg),
+             "in": lambda: o.swap_in(arg)}[name]()
+        with pytest.raises(aqua.AquaError) as ec:
+            {"alloc": lambda: c.alloc_blocks(*arg), "out": lambda: c.swap_out(arg),
+             "in": lambda: c.swap_in(arg, cap=4 * NB)}[name]()
+        assert eo.value.code == ec.value.code == code, (name, arg, eo.value.code, ec.value.code)
+        assert c.counts() == (len(o.free), len(o.peer.free), len(o.host.free))
+        rig.assert_bytes_equal(f"after failed {name} {arg}")
+
+    n0 = c.launch_count()
+    _ops(rig, [("out", []), ("in", []), ("alloc", (9, 0)), ("out", [9]), ("in", [9]), ("free", 9)])
+    assert c.launch_count() == n0                       # nothing to copy: no launch
+    # three ragged prompts own the whole pool; one call pages all of it into the lender (exactly full)
+    _ops(rig, [("alloc", (1, 1)), ("alloc", (2, 7)), ("alloc", (3, NB - 8)), ("out", [3, 1, 2])])
+    assert c.counts() == (NB, 0, NB)
+    # a fourth whole-pool prompt: the lender is full, so its image goes to the host arena (exactly full)
+    _ops(rig, [("alloc", (4, NB)), ("out", [4])])
+    assert c.query(4)[1] == aqua.LOC_HOST and c.counts() == (NB, 0, 0)
+    _ops(rig, [("alloc", (5, 1))])
+    fails("out", [5], aqua.E_NOSPACE)                   # fits nowhere
+    fails("in", [4], aqua.E_NOBLOCKS)                   # needs NB blocks, NB - 1 are free
+    fails("in", [3, 1, 2], aqua.E_NOBLOCKS)             # the same, over three images in one call
+    _ops(rig, [("in", [3, 2])])                         # needs exactly every free block (NB - 1)
+    assert c.counts() == (0, NB - 1, 0)
+    _ops(rig, [("free", 5), ("in", [1])])               # the pool is full again
+    assert c.counts() == (0, NB, 0)
+    fails("alloc", (6, 1), aqua.E_NOBLOCKS)
+    _ops(rig, [("free", 3), ("free", 1), ("free", 2), ("in", [4]), ("out", [4])])
+    assert c.query(4)[1] == aqua.LOC_PEER and c.counts() == (NB, 0, NB)   # lowest arena with room (R5)
+    _ops(rig, [("in", [4])])
+    assert c.counts() == (0, NB, NB)
