@@ -531,6 +531,23 @@ aqua_status run_copy(aqua_ctx* c, const std::vector<Desc>& ds, aqua::Dir dir, cu
   int engine = c->kernel;
   if (engine == AQUA_KERNEL_AUTO) {
     const bool host_only = dir != aqua::kMig && !dev_desc && img_all_host;
+    if (!host_only && img_any_host && dir != aqua::kMig && !dev_desc) {
+      // A call with images in both arenas (the lender filled up, R5): one
+      // fused launch would hold every SM for as long as PCIe takes.  Split it:
+      // the GPU-arena images on the TMA kernel (HBM/NVLink speed), then the
+      // host images through the copy engines, which hold no SMs
+      // (profiles/r02_mixed_split.jsonl).  Same stream, disjoint destinations.
+      std::vector<Desc> dg, dh;
+      for (const Desc& d : ds) ((d.slot_arena & kArenaBit) ? dh : dg).push_back(d);
+      int rg = 0;
+      if (aqua_status s = run_copy(c, dg, dir, st, &rg, c0, nc, nullptr)) return s;
+      if (rg) {   // seal this part's staged descriptors before the copy engines stage theirs
+        uint64_t t;
+        if (aqua_status s = record(c, st, &t)) return s;
+        stage_seal(c, rg, t);
+      }
+      return run_copy_ce_host(c, dh, dir, st, c0, nc);
+    }
     engine = host_only ? AQUA_KERNEL_CE_HOST : AQUA_KERNEL_TMA;
   }
   if (dir == aqua::kMig && engine != AQUA_KERNEL_LDST) engine = AQUA_KERNEL_TMA;  // baselines do not migrate

@@ -15,7 +15,13 @@ out is not in the next batch).  Three placements of the images:
   host_sm   the same through the zero-copy TMA kernel (8 SMs);
   self      the same GPU's HBM (self-lender): both sides are HBM-bound, so
             overlap cannot beat the sum of the HBM traffic (what round 1's C3
-            runs measured: separate streams = one stream).
+            runs measured: separate streams = one stream);
+  mixed     half the blocks (one prompt) fill a self-lender arena exactly,
+            the other prompt falls back to pinned DRAM (R5), both paged in
+            ONE call: AUTO splits it (TMA kernel for the lender images, copy
+            engines for the host ones);
+  mixed_tma the same call as one fused TMA launch (AQUA_KERNEL_TMA; AUTO
+            before the split), which holds its SMs for the PCIe time.
 
 For each: decode alone, paging alone, both serialised on one stream, and both
 on separate streams; prints one JSON line per placement with the overlap
@@ -85,7 +91,16 @@ def main():
         if cap:
             ctx.set_option(aqua.OPT_MAX_CTAS, cap)
         arena = None
-        if where == "self":
+        pids = [7]
+        if where in ("mixed", "mixed_tma"):
+            half = nblk // 2
+            arena = torch.empty(half * U, dtype=torch.uint8, device="cuda")
+            ctx.lend(0, arena.data_ptr(), half * U)
+            ctx.lend(aqua.HOST, 0, (nblk - half) * U)
+            if where == "mixed_tma":
+                ctx.set_option(aqua.OPT_KERNEL, aqua.KERNEL_TMA)
+            pids = [7, 8]
+        elif where == "self":
             arena = torch.empty(nblk * U, dtype=torch.uint8, device="cuda")
             ctx.lend(0, arena.data_ptr(), nblk * U)
         else:
@@ -93,7 +108,15 @@ def main():
             if where == "host_sm":
                 ctx.set_option(aqua.OPT_KERNEL, aqua.KERNEL_TMA)
         ctx.adopt_blocks(1, perm[nblk:])
-        ctx.adopt_blocks(7, perm[:nblk])
+        if len(pids) == 1:
+            ctx.adopt_blocks(7, perm[:nblk])
+        else:
+            ctx.adopt_blocks(7, perm[:nblk // 2])
+            ctx.adopt_blocks(8, perm[nblk // 2:nblk])
+            ctx.swap_out(pids)                   # placement check: lender exactly full, then host (R5)
+            assert (ctx.query(7)[1], ctx.query(8)[1]) == (aqua.LOC_PEER, aqua.LOC_HOST)
+            ctx.swap_in(pids)
+            torch.cuda.synchronize()
 
         def decode(st, n):
             with torch.cuda.stream(st):
@@ -104,8 +127,8 @@ def main():
                         torch.matmul(ga, gb, out=gc)
 
         def page(st):
-            ctx.swap_out([7], st.cuda_stream)
-            ctx.swap_in([7], st.cuda_stream)
+            ctx.swap_out(pids, st.cuda_stream)
+            ctx.swap_in(pids, st.cuda_stream)
 
         def timed(fn):
             best = None

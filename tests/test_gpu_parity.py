@@ -1144,3 +1144,30 @@ def test_degenerate_and_maximum_calls_bytes(engine):
     assert c.query(4)[1] == aqua.LOC_PEER and c.counts() == (NB, 0, NB)   # lowest arena with room (R5)
     _ops(rig, [("in", [4])])
     assert c.counts() == (0, NB, NB)
+
+
+@pytest.mark.parametrize("nblk", [3, 300])
+def test_mixed_arena_call_split_bytes(nblk):
+    """AUTO splits a call whose images land in both arenas (the lender fills
+    up, R5): the lender images on the TMA kernel, the host ones through the
+    copy engines, on the same stream.  Whole buffers vs the oracle after the
+    mixed swap_out and the mixed swap_in; 300 blocks per prompt put the
+    descriptors of both parts beyond the inline tier (staged uploads)."""
+    NB = 4 * nblk + 8
+    rig = Rig(L=2, bs=16, H=1, D=64, NB=NB, lender_slots=nblk + 1, host_slots=2 * nblk, seed=3)
+    c = rig.ctx
+    c.set_option(aqua.OPT_INLINE_MAX, 256)
+    _ops(rig, [("alloc", (1, nblk)), ("alloc", (2, 1)), ("alloc", (3, nblk)), ("alloc", (4, 5))])
+    n0 = c.launch_count()
+    _ops(rig, [("out", [1, 3, 2])])
+    assert (c.query(1)[1], c.query(3)[1], c.query(2)[1]) == (aqua.LOC_PEER, aqua.LOC_HOST, aqua.LOC_PEER)
+    # two launches: the lender part on the TMA kernel, the copy engines' gather of the host part
+    # (one fused launch would hold every SM for the PCIe time: profiles/r02_mixed_split.jsonl)
+    assert c.launch_count() - n0 == 2
+    _ops(rig, [("in", [3, 1]), ("out", [3]), ("in", [2, 3]), ("free", 1), ("free", 4)])
+    assert c.query(3)[0] == aqua.RESIDENT
+    c.set_option(aqua.OPT_KERNEL, aqua.KERNEL_TMA)      # an explicit engine: one fused launch
+    _ops(rig, [("alloc", (5, nblk + 1)), ("out", [3, 5])])
+    n0 = c.launch_count()
+    _ops(rig, [("in", [5, 3])])
+    assert c.launch_count() - n0 == 1
