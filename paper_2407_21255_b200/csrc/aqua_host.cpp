@@ -780,7 +780,14 @@ aqua_status enqueue_copy(aqua_ctx* c, const std::vector<Desc>& ds, aqua::Dir dir
   }
   const Desc* dd = nullptr;
   int up = 0;
-  const bool fused = c->kernel == AQUA_KERNEL_AUTO || c->kernel == AQUA_KERNEL_TMA || c->kernel == AQUA_KERNEL_LDST;
+  bool fused = c->kernel == AQUA_KERNEL_AUTO || c->kernel == AQUA_KERNEL_TMA || c->kernel == AQUA_KERNEL_LDST;
+  if (c->kernel == AQUA_KERNEL_AUTO && dir != aqua::kMig) {
+    // images in both arenas: each group's run_copy splits the call (lender
+    // part on the TMA kernel, host part on the copy engines), so no shared upload
+    bool any_host = false, any_gpu = false;
+    for (const Desc& d : ds) ((d.slot_arena & kArenaBit) ? any_host : any_gpu) = true;
+    if (any_host && any_gpu) fused = false;
+  }
   if (fused && ds.size() > static_cast<size_t>(c->inline_max)) {
     void* d;
     if (aqua_status s = stage_upload(c, ds.data(), ds.size() * sizeof(Desc), st, &d)) return s;

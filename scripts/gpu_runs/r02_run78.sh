@@ -1,0 +1,2 @@
+cd $GRAFT_REPO_ROOT
+timeout 2400 python scripts/product_mutants.py run --kind gpu --only "AUTO: a call with images in both,AUTO: the split sends,AUTO: layer-wise mixed" --timeout 600 --out gpurun_out/r02_product_mutants_gpu_split.json > gpurun_out/r02_product_mutants_gpu_split.log 2>&1; echo "mutants rc $?"; tail -8 gpurun_out/r02_product_mutants_gpu_split.log

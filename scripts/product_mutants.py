@@ -136,6 +136,13 @@ MUTANTS = [
        "      const int want = std::max(1, c->rate_gbps / kSwapGBpsPerSm);", None)], "gpu"),
     ("AUTO: host-only launches are not capped (PCIe-bound)", "aqua_host.cpp",
      [("    if (all_host && (cap == 0 || cap > kHostCtas)) cap = kHostCtas;\n", "", None)], "gpu"),
+    ("AUTO: a call with images in both arenas runs as one fused launch (not split)", "aqua_host.cpp",
+     [("    if (!host_only && img_any_host && dir != aqua::kMig && !dev_desc) {",
+       "    if (false) {", None)], "gpu"),
+    ("AUTO: the split sends every image to the TMA kernel (host part lost)", "aqua_host.cpp",
+     [("      return run_copy_ce_host(c, dh, dir, st, c0, nc);", "      return AQUA_OK;", None)], "gpu"),
+    ("AUTO: layer-wise mixed calls keep the shared descriptor upload", "aqua_host.cpp",
+     [("    if (any_host && any_gpu) fused = false;", "    (void)any_host;", None)], "gpu"),
     # ---- host library: bookkeeping (A1, A2, A5, A7; R4, R5) -- dry-run parity on CPU
     ("placement: lender needs strictly more than n_p free slots (R5)", "aqua_host.cpp",
      [("    if (gpu_left >= np) {", "    if (gpu_left > np) {", None)], "cpu"),

@@ -1171,3 +1171,27 @@ def test_mixed_arena_call_split_bytes(nblk):
     n0 = c.launch_count()
     _ops(rig, [("in", [5, 3])])
     assert c.launch_count() - n0 == 1
+
+
+@pytest.mark.parametrize("layer_group", [1, 3])
+@pytest.mark.parametrize("nblk", [4, 300])
+def test_layerwise_mixed_arena_split_bytes(layer_group, nblk):
+    """NEXT-3 with a call whose images span lender and host: AUTO splits
+    every layer group (no shared descriptor upload), one ticket per group;
+    whole buffers vs the oracle."""
+    rig = Rig(L=4, bs=16, H=2, D=32, NB=3 * nblk + 8, lender_slots=nblk, host_slots=nblk, seed=5)
+    c, o = rig.ctx, rig.opool
+    c.set_option(aqua.OPT_INLINE_MAX, 256)
+    for pid in (1, 2):
+        assert c.alloc_blocks(pid, nblk) == o.alloc_blocks(pid, nblk)
+    n0 = c.launch_count()
+    tks = c.swap_out_layers([1, 2], layer_group)
+    o.swap_out([1, 2])
+    ng = -(-4 // layer_group)
+    assert len(tks) == ng and tks == sorted(tks) and c.launch_count() - n0 == 2 * ng
+    assert (c.query(1)[1], c.query(2)[1]) == (aqua.LOC_PEER, aqua.LOC_HOST)
+    rig.assert_bytes_equal("layered mixed swap_out")
+    assert c.alloc_blocks(3, 5) == o.alloc_blocks(3, 5)
+    new, tks = c.swap_in_layers([2, 1], layer_group)
+    assert new == o.swap_in([2, 1]) and len(tks) == ng
+    rig.assert_bytes_equal("layered mixed swap_in")

@@ -202,8 +202,11 @@ def test_random_sequences_peer_policy_one_gpu(shape, mode, seed):
         name, arg = op
         # does the call move an image to or from the (pretend) peer arena?
         on_peer = lambda ps: any(q in o.prompts and o.prompts[q].location == kp.LOC_PEER for q in ps)
+        # a call with images in both arenas is split (AUTO): its last launch is the copy engines' local gather
+        locs = lambda ps: {o.prompts[q].location for q in ps if q in o.prompts}
         try:
             touches = name == "mig" or (name == "in" and on_peer(arg))
+            mixed = name == "in" and {kp.LOC_PEER, kp.LOC_HOST} <= locs(arg)
             if name == "mig":
                 c.migrate(arg[0], arg[1])
                 o.migrate(arg[0], arg[1])
@@ -211,7 +214,8 @@ def test_random_sequences_peer_policy_one_gpu(shape, mode, seed):
             else:
                 _ops(rig, [op])
             touches = touches or (name == "out" and on_peer(arg))
-            if touches:
+            mixed = mixed or (name == "out" and {kp.LOC_PEER, kp.LOC_HOST} <= locs(arg))
+            if touches and not mixed:
                 launch = c.last_launch()
                 assert launch["ctas"] <= 32 and launch["engine"] == ("tma" if mode == 1 else "ldst"), launch
         except (kp.AquaError, aqua.AquaError) as err:
