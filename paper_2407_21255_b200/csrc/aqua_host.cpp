@@ -529,6 +529,29 @@ aqua_status run_copy(aqua_ctx* c, const std::vector<Desc>& ds, aqua::Dir dir, cu
     each_touches_host = each_touches_host && (h || (dir == aqua::kMig && src_host));
   }
   int engine = c->kernel;
+  if (engine == AQUA_KERNEL_AUTO && dir == aqua::kMig && !dev_desc) {
+    // Lender <-> host migration (NEXT-1): both images are slot-contiguous, so
+    // the copy engines move each run of consecutive source and destination
+    // slots as one DMA and hold no SMs (the zero-copy kernel needed 8 for the
+    // PCIe time; profiles/r02_migrate_ce.jsonl).
+    const int64_t off = int64_t(c0) * c->S, width = int64_t(nc) * c->S;
+    auto addr = [&](uint32_t sa) {
+      return ((sa & kArenaBit) ? c->host.base : c->gpu.base) + int64_t(sa & ~kArenaBit) * c->U + off;
+    };
+    size_t j = 0;
+    while (j < ds.size()) {
+      const uint32_t s0 = static_cast<uint32_t>(ds[j].block), d0 = ds[j].slot_arena;
+      size_t r = 1;
+      while (j + r < ds.size() && static_cast<uint32_t>(ds[j + r].block) == s0 + r && ds[j + r].slot_arena == d0 + r)
+        ++r;
+      if (width == c->U)
+        CK(c, cudaMemcpyAsync(addr(d0), addr(s0), r * c->U, cudaMemcpyDefault, st));
+      else
+        CK(c, cudaMemcpy2DAsync(addr(d0), c->U, addr(s0), c->U, width, r, cudaMemcpyDefault, st));
+      j += r;
+    }
+    return AQUA_OK;
+  }
   if (engine == AQUA_KERNEL_AUTO) {
     const bool host_only = dir != aqua::kMig && !dev_desc && img_all_host;
     if (!host_only && img_any_host && dir != aqua::kMig && !dev_desc) {

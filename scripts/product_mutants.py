@@ -143,6 +143,12 @@ MUTANTS = [
      [("      return run_copy_ce_host(c, dh, dir, st, c0, nc);", "      return AQUA_OK;", None)], "gpu"),
     ("AUTO: layer-wise mixed calls keep the shared descriptor upload", "aqua_host.cpp",
      [("    if (any_host && any_gpu) fused = false;", "    (void)any_host;", None)], "gpu"),
+    ("migration on the copy engines: a run ignores the destination slots", "aqua_host.cpp",
+     [("static_cast<uint32_t>(ds[j + r].block) == s0 + r && ds[j + r].slot_arena == d0 + r)",
+       "static_cast<uint32_t>(ds[j + r].block) == s0 + r)", None)], "gpu"),
+    ("migration on the copy engines: a run ignores the source slots", "aqua_host.cpp",
+     [("static_cast<uint32_t>(ds[j + r].block) == s0 + r && ds[j + r].slot_arena == d0 + r)",
+       "ds[j + r].slot_arena == d0 + r)", None)], "gpu"),
     # ---- host library: bookkeeping (A1, A2, A5, A7; R4, R5) -- dry-run parity on CPU
     ("placement: lender needs strictly more than n_p free slots (R5)", "aqua_host.cpp",
      [("    if (gpu_left >= np) {", "    if (gpu_left > np) {", None)], "cpu"),

@@ -142,8 +142,17 @@ def migrate():
     """NEXT-1 data path: a 4 GiB image moved lender -> host (reclaim) and
     host -> lender (re-offer), device time from the library's timing events."""
     L, bs, H, D, NB, nblk = 32, 16, 8, 128, 4096, 2048
+    for engine in ("auto", "tma"):
+        _migrate_one(engine, L, bs, H, D, NB, nblk)
+
+
+def _migrate_one(engine, L, bs, H, D, NB, nblk):
+    """AUTO moves the slot-contiguous images on the copy engines (no SMs);
+    "tma" forces the fused arena->arena kernel (8 CTAs, the round-1 path)."""
     ctx, layers, arena, U = setup(L, bs, H, D, NB, nblk)
     ctx.lend(aqua.HOST, 0, nblk * U)
+    if engine == "tma":
+        ctx.set_option(aqua.OPT_KERNEL, aqua.KERNEL_TMA)
     ctx.set_option(aqua.OPT_TIMING, 1)
     s = torch.cuda.Stream()
     ctx.kv_fill_pattern(7, 0, nblk * bs, 5)
@@ -163,10 +172,13 @@ def migrate():
     torch.cuda.synchronize()
     o = statistics.median(r[0] for r in res)
     i = statistics.median(r[1] for r in res)
-    print(json.dumps({"migrate_bytes": nblk * U, "to_host_ms": round(o, 3), "to_lender_ms": round(i, 3),
+    print(json.dumps({"engine": engine, "migrate_bytes": nblk * U, "to_host_ms": round(o, 3), "to_lender_ms": round(i, 3),
                       "to_host_GBps": round(nblk * U / o / 1e6, 2), "to_lender_GBps": round(nblk * U / i / 1e6, 2),
                       "reclaim_ms": round(rec, 3), "resume_from_host_ms": round(ctx.ticket_elapsed(t4), 3),
                       "verify_mismatches": int(cnt.item())}), flush=True)
+    ctx.close()
+    del layers, arena
+    torch.cuda.empty_cache()
 
 
 def prefix():

@@ -457,7 +457,8 @@ def test_ticket_timing():
 @pytest.mark.parametrize("engine", KERNEL_ENGINES)
 def test_migrate_reclaim_relend_bytes(engine):
     """NEXT-1 on the GPU: images move lender -> host (reclaim) and back
-    (re-offer) through the fused arena->arena kernel, byte for byte with the
+    (re-offer) -- AUTO on the copy engines, explicit engines through the fused
+    arena->arena kernel -- byte for byte with the
     oracle; resumes from either place restore the blocks."""
     import torch
     from workloads import kv_random_bytes
@@ -465,9 +466,12 @@ def test_migrate_reclaim_relend_bytes(engine):
     c, o = rig.ctx, rig.opool
     _engine(c, engine)
     _ops(rig, [("alloc", (1, 5)), ("alloc", (2, 3)), ("alloc", (3, 4)), ("out", [1, 3]), ("out", [2])])
+    n0 = c.launch_count()
     t = c.migrate([3], aqua.LOC_HOST)
     o.migrate([3], kp.LOC_HOST)
     rig.assert_bytes_equal("migrate 3 -> host")
+    # AUTO moves slot-contiguous images on the copy engines (no kernel); an explicit engine launches it
+    assert (c.launch_count() - n0) == (0 if engine == "auto" else 1)
     t = c.reclaim()
     moved = o.reclaim()
     assert [p for p, _ in moved] == [1, 2]

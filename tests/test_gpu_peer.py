@@ -205,7 +205,8 @@ def test_random_sequences_peer_policy_one_gpu(shape, mode, seed):
         # a call with images in both arenas is split (AUTO): its last launch is the copy engines' local gather
         locs = lambda ps: {o.prompts[q].location for q in ps if q in o.prompts}
         try:
-            touches = name == "mig" or (name == "in" and on_peer(arg))
+            touches = name == "in" and on_peer(arg)     # a migration runs on the copy engines: no launch
+            n0 = c.launch_count()
             mixed = name == "in" and {kp.LOC_PEER, kp.LOC_HOST} <= locs(arg)
             if name == "mig":
                 c.migrate(arg[0], arg[1])
@@ -215,6 +216,8 @@ def test_random_sequences_peer_policy_one_gpu(shape, mode, seed):
                 _ops(rig, [op])
             touches = touches or (name == "out" and on_peer(arg))
             mixed = mixed or (name == "out" and {kp.LOC_PEER, kp.LOC_HOST} <= locs(arg))
+            if name == "mig":
+                assert c.launch_count() == n0
             if touches and not mixed:
                 launch = c.last_launch()
                 assert launch["ctas"] <= 32 and launch["engine"] == ("tma" if mode == 1 else "ldst"), launch
