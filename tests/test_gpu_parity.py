@@ -1199,3 +1199,29 @@ def test_layerwise_mixed_arena_split_bytes(layer_group, nblk):
     new, tks = c.swap_in_layers([2, 1], layer_group)
     assert new == o.swap_in([2, 1]) and len(tks) == ng
     rig.assert_bytes_equal("layered mixed swap_in")
+
+
+@pytest.mark.parametrize("engine", ["auto", "tma"])
+def test_migration_runs_with_fragmented_slots_bytes(engine):
+    """NEXT-1 migration moves runs of slots that are consecutive on BOTH
+    sides as one copy (AUTO: one DMA): consecutive source slots whose lowest
+    free destination slots have a hole (and the reverse) must split into
+    runs.  Whole buffers vs the oracle after every call."""
+    rig = Rig(L=2, bs=16, H=2, D=64, NB=24, lender_slots=8, host_slots=8, seed=11)
+    c, o = rig.ctx, rig.opool
+    _engine(c, engine)
+
+    def mig(pids, dst):
+        c.migrate(pids, dst)
+        o.migrate(pids, {aqua.LOC_PEER: kp.LOC_PEER, aqua.LOC_HOST: kp.LOC_HOST}[dst])
+        rig.assert_bytes_equal(f"migrate {pids} -> {dst}")
+
+    _ops(rig, [("alloc", (1, 1)), ("alloc", (2, 1)), ("alloc", (3, 1)), ("alloc", (4, 4)), ("out", [1, 2, 3])])
+    mig([1, 2, 3], aqua.LOC_HOST)                       # lender 0..2 -> host 0..2
+    mig([2], aqua.LOC_PEER)                             # host slot 1 becomes a hole
+    _ops(rig, [("out", [4])])                           # lender 1..4
+    mig([4], aqua.LOC_HOST)                             # consecutive source -> host 1, 3, 4, 5
+    assert c.query(4, with_ids=True)[3] == [1, 3, 4, 5]
+    mig([1], aqua.LOC_PEER)                             # host slot 0 becomes a hole: lender 1
+    mig([4, 3], aqua.LOC_PEER)                          # host 1, 3, 4, 5 then 2 -> lender 2..6
+    _ops(rig, [("in", [4, 3, 2, 1])])
