@@ -105,9 +105,11 @@ enum { AQUA_LOC_LOCAL = 0, AQUA_LOC_PEER = 1, AQUA_LOC_HOST = 2 };
  * retired and rejected with AQUA_E_INVAL.  The environment variable AQUA_KERNEL
  * (auto | tma | ldst | ce_host) sets a context's initial engine. */
 enum {
-  AQUA_KERNEL_AUTO = 0,       /* product default: CE_HOST when every image of the call is in host DRAM; the LDST
+  AQUA_KERNEL_AUTO = 0,       /* product default: CE_HOST when every image of the call is in host DRAM; a call with
+                                 images in both arenas is split (GPU-arena images as below, host images CE_HOST);
+                                 migrations on the copy engines (one DMA per run of consecutive slots); the LDST
                                  small-chunk kernel for plane-major 512 B and 1 KiB chunks (capped launches on a peer arena
-                                 excepted); else TMA (picked from measurements, DESIGN.md 5.1) */
+                                 excepted); else TMA (picked from measurements, DESIGN.md 5.1, 5.5) */
   AQUA_KERNEL_TMA = 1,        /* fused gather/scatter, cp.async.bulk smem ring (UBLKCP) */
   AQUA_KERNEL_LDST = 2,       /* fused gather/scatter, 16-byte LDG/STG register path */
   AQUA_BASE_PER_CHUNK = 3,    /* baseline: one cudaMemcpyAsync per chunk (vLLM-style) */
@@ -257,8 +259,10 @@ AQUA_API aqua_status aqua_free(aqua_ctx* ctx, uint64_t pid, aqua_stream_t stream
  * (listed once, none already in dst) to arena dst_loc (AQUA_LOC_PEER or
  * AQUA_LOC_HOST), lowest free slots in call order (R4):
  *   dst[new_j*U : +U] = src[old_j*U : +U];  the old slots are freed.
- * All-or-nothing: AQUA_E_NOSPACE if dst is missing or too small.  One fused
- * kernel launch (arena -> arena) on `stream`. */
+ * All-or-nothing: AQUA_E_NOSPACE if dst is missing or too small.  On
+ * `stream`: under AQUA_KERNEL_AUTO the copy engines (one DMA per run of slots
+ * consecutive on both sides, no SM held); with an explicit TMA / LDST engine
+ * one fused kernel launch (arena -> arena). */
 AQUA_API aqua_status aqua_migrate(aqua_ctx* ctx, int32_t n, const uint64_t* pids, int32_t dst_loc,
                                   aqua_stream_t stream, uint64_t* out_ticket);
 /* The GPU lender takes its memory back: every image on it moves to the host
